@@ -1,0 +1,203 @@
+/*
+ * lfm.h -- C ABI of the B200-native light-field Richardson-Lucy hot path (AutoDeconJ, arXiv 2208.11422).
+ *
+ * Citations: "P:n" = the paper (PAPER.md line n); "S:n" = SPEC.md line n (interfaces only);
+ * "C1..C18" = the readings of silent / garbled passages listed in DESIGN.md §3.
+ *
+ * One iteration of the hot path (§1 "3D Richardson-Lucy (RL) deconvolution"; §2.2):
+ *     yhat = H x                      forward projection
+ *     r    = y / (max(yhat,0) + eps)  ratio image            (C3)
+ *     bp   = H^T r                    backward projection (exact adjoint, C6)
+ *     x    = x * bp / max(H^T 1, eps) multiplicative non-negative update (C1)
+ *     m    = max_z x                  z max-projection
+ *     E    = DCT entropy of m         Eqs. (1)-(12)
+ *     stop when E shows a decreasing trend, return argmax-E iterate (Fig. 2d; C14-C15)
+ * with  H x (s,t) = sum_z sum_{p,q} x(z,p,q) * psf[z][p mod N][q mod N](s-p+ch, t-q+cw),
+ *       ch = (kh-1)/2, cw = (kw-1)/2, zero outside kernel and image ("same" size; C4, C5).
+ *
+ * Conventions for every entry point
+ *   - Arrays are row-major fp32 unless stated.  Volumes are [nz][H][W]; images [H][W];
+ *     the PSF bank is [nz][N][N][kh][kw] (page (z*N + a)*N + b holds the kernel of input phase
+ *     (a,b) = (p mod N, q mod N) of plane z).
+ *   - "device" pointers must be CUDA device memory of the plan's device; "host" pointers are
+ *     ordinary (preferably pinned) host memory.  `stream` is a cudaStream_t (NULL = legacy default
+ *     stream); device work is ordered on it.  Calls that return host values synchronise `stream`.
+ *   - The caller owns every buffer it passes; the library never retains a caller pointer past
+ *     the call.  The plan owns its transfer matrices, workspaces and communicator.
+ *   - No call aborts or throws across the ABI.  Every call returns an lfm_status; on failure
+ *     lfm_last_error() (thread-local) names the argument / term that was violated and nothing
+ *     has been written to the caller's outputs unless stated.
+ *   - Multi-GPU (depth / phase sharding, §2.1 "divide the 3D layers ... evenly among
+ *     different GPUs"): one process per GPU.  The nz*N*N "units" u = z*N*N + a*N + b (plane z,
+ *     input phase (a,b)) are split into contiguous ranges, the first (nu mod world) ranks owning
+ *     one extra unit.  Volumes at the boundary are always the FULL [nz][H][W] on every rank; a rank
+ *     reads / writes only the voxels of its own units unless stated.
+ */
+#ifndef LFM_H_
+#define LFM_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lfm_plan_s* lfm_plan;
+
+typedef enum {
+    LFM_OK = 0,
+    LFM_EINVAL = 1,   /* invalid argument / policy / NULL pointer                         */
+    LFM_EDIM = 2,     /* H or W not divisible by N, even kernel or even N, size mismatch */
+    LFM_ENEG = 3,     /* negative PSF entry or negative measurement                */
+    LFM_EZERO = 4,    /* all-zero measurement or a PSF that projects nothing             */
+    LFM_ENOMEM = 5,   /* device memory budget exceeded; lfm_last_error names the limiting term */
+    LFM_ECUDA = 6,    /* CUDA runtime error                                                        */
+    LFM_ENCCL = 7,    /* NCCL error: any rank failure fails the whole run                  */
+    LFM_EUNSUPPORTED = 8 /* valid request this build does not implement (message says which)     */
+} lfm_status;
+
+/* Optics for the metric's cutoff region, Eqs. (7) and (11).  All fields > 0, na <= 1.6. */
+typedef struct {
+    double wavelength_um;   /* lambda, emission wavelength                    */
+    double na;              /* numerical aperture of the objective            */
+    double mla_pitch_um;    /* d_ML, microlens pitch                          */
+    double magnification;   /* Q, objective magnification                     */
+} lfm_optics;
+
+enum { LFM_MODE_FIXED = 0, LFM_MODE_AUTO = 1 };
+enum { LFM_REGION_TRIANGLE = 0, LFM_REGION_RECTANGLE = 1 };     /* C11 */
+enum { LFM_UPDATE_RL = 0, LFM_UPDATE_ISRA = 1 };                /* C1  */
+
+/* Iteration / stopping policy ("stop iteration when the DCT entropy value shows a decreasing
+ * trend"; reading C15).  Defaults: lfm_policy_default(). */
+typedef struct {
+    int mode;         /* LFM_MODE_FIXED: run n_iters; LFM_MODE_AUTO: stop at the first k >= min_iters
+                         after `patience` consecutive strict decreases of E, or at max_iters      */
+    int n_iters;      /* fixed mode iteration count (>= 1)                                         */
+    int max_iters;    /* auto mode cap (default 50, Fig. 2d sweeps 1..50)                  */
+    int min_iters;    /* default 2                                                                 */
+    int patience;     /* default 1                                                                 */
+    float eps;        /* division guard, default 1e-6 (C3)                                         */
+    int region;       /* LFM_REGION_TRIANGLE (default) or LFM_REGION_RECTANGLE (C11)               */
+    int init_from_x;  /* 0: x0 = c0 = sum(y) / sum(H^T 1) uniform (C2); 1: caller's x is x0 (resume) */
+    int update;       /* LFM_UPDATE_RL (default).  LFM_UPDATE_ISRA -> LFM_EUNSUPPORTED in this build */
+} lfm_policy;
+
+/* Distribution.  world == 1: single GPU, no communicator.  world > 1: nccl_id is the 128-byte
+ * ncclUniqueId produced by lfm_comm_unique_id() on rank 0 and broadcast by the caller (e.g. with
+ * torch.distributed); every rank passes the same id. */
+typedef struct {
+    int rank;
+    int world;
+    unsigned char nccl_id[128];
+} lfm_dist;
+
+/* lfm_plan_create flags */
+enum {
+    LFM_PLAN_NO_COMM = 1,   /* world > 1 without a communicator: the plan owns rank's units and all
+                               cross-rank reductions are skipped (outputs are this rank's partials).
+                               For testing the sharding on one device.                              */
+    LFM_PLAN_DIRECT = 2     /* spatial-domain projections (direct polyphase convolution) instead of
+                               the frequency-domain transfer matrices; for small PSFs.             */
+};
+
+/* Information about a plan. */
+typedef struct {
+    int nnum, nz, kh, kw, height, width;
+    int unit_begin, unit_end;       /* owned units [begin, end)                                   */
+    int fft_h, fft_w;               /* coarse transform sizes Lh, Lw (0 in direct mode)           */
+    int lc_min_h, lc_min_w;         /* alias-free minimum n + ceil(c/N)            */
+    int n_kappa;                    /* Lh * (Lw/2 + 1) coarse frequencies kept                     */
+    int units_padded;               /* row length of the transfer matrices (>= owned units)       */
+    int x_s, y_s;                   /* cutoff region (Eqs. 9-10)                                   */
+    int direct;                     /* 1 if LFM_PLAN_DIRECT                                        */
+    size_t transfer_bytes;          /* bytes of transfer matrices held by this rank               */
+    size_t device_bytes;            /* all device memory held by the plan                         */
+    double plan_ms;                 /* wall time of lfm_plan_create                                */
+} lfm_info;
+
+/* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */
+lfm_policy lfm_policy_default(void);
+
+/* Thread-local description of the last failure (empty string if none). */
+const char* lfm_last_error(void);
+
+/* Version string of the library (build identifier). */
+const char* lfm_version(void);
+
+/* Writes a fresh ncclUniqueId (128 bytes) into id_out (host).  Call on rank 0 only. */
+lfm_status lfm_comm_unique_id(unsigned char* id_out);
+
+/* Memory estimate before allocation (Fig. 1 "estimate the required memory size").
+ * Writes the bytes one rank needs into *bytes_per_gpu (host).  If budget_bytes > 0 and the estimate
+ * exceeds it, returns LFM_ENOMEM and writes the name of the largest term into limiting_term
+ * (host, len bytes, NUL-terminated). */
+lfm_status lfm_plan_estimate(int nnum, int nz, int kh, int kw, int height, int width, int world, int flags,
+                             size_t budget_bytes, size_t* bytes_per_gpu, char* limiting_term, size_t len);
+
+/* Create a plan (one-time; "the PSF is evenly distributed to each card ... used directly for
+ * the next reconstruction").
+ *   psf_host   : host [nz][N][N][kh][kw] fp32, >= 0 (LFM_ENEG otherwise).  Only this rank's units are
+ *                copied to the device.  Not retained.
+ *   psf_t_host : must be NULL (exact adjoint = rot180 of psf per phase, C6); a supplied transposed
+ *                PSF returns LFM_EUNSUPPORTED in this build.
+ *   nnum       : N, odd >= 1.  height, width divisible by N.  kh, kw odd.
+ *   optics     : for the metric region (may be NULL: lfm_quality / auto mode then return LFM_EINVAL).
+ *   dist       : NULL means single GPU.
+ * Builds the coarse transfer matrices (frequency mode), the normalizer H^T 1 and the region. */
+lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* psf_t_host,
+                           int nnum, int nz, int kh, int kw, int height, int width,
+                           const lfm_optics* optics, const lfm_dist* dist, int flags, void* stream);
+
+lfm_status lfm_plan_info(lfm_plan plan, lfm_info* info /* host */);
+
+/* Destroys the plan and frees its device memory / communicator.  NULL is a no-op. */
+void lfm_plan_destroy(lfm_plan plan);
+
+/* Forward projection yhat = H x.
+ *   x : device [nz][H][W] (only owned units read).   y : device [H][W] written; summed over ranks. */
+lfm_status lfm_forward(lfm_plan plan, const float* x, float* y, void* stream);
+
+/* Backward projection xhat = H^T y.
+ *   y : device [H][W].   x : device [nz][H][W]; voxels of owned units written, others untouched. */
+lfm_status lfm_backward(lfm_plan plan, const float* y, float* x, void* stream);
+
+/* Normalizer H^T 1 into x (device [nz][H][W], owned units written). */
+lfm_status lfm_normalizer(lfm_plan plan, float* x, void* stream);
+
+/* One RL iteration without the stop rule: x_out = x_in * H^T(y/(max(H x_in,0)+eps)) / max(H^T 1, eps),
+ * and, if entropy_host != NULL, the DCT entropy of max_z x_out (Eq. 12) into *entropy_host
+ * (synchronises).  x_in, x_out: device [nz][H][W] (owned units; may alias).  y: device [H][W].
+ * yhat_out: optional device [H][W] receiving H x_in (summed over ranks). */
+lfm_status lfm_rl_step(lfm_plan plan, const float* y, const float* x_in, float* x_out, float eps,
+                       int region, float* yhat_out, double* entropy_host, void* stream);
+
+/* The RL loop with the DCT-entropy stop rule.
+ *   y          : device [H][W], >= 0, not all zero.
+ *   x          : device [nz][H][W].  In: x0 if policy->init_from_x.  Out: the argmax-E iterate on ALL
+ *                voxels (gathered across ranks once at the end).
+ *   best_iter, stop_iter : host outputs (1-based).
+ *   series_host: host [max(n_iters, max_iters)] receiving E_1..E_stop.
+ *   ms_host    : optional host [same] receiving per-iteration device milliseconds.
+ * Auto mode reads one double per iteration to the host. */
+lfm_status lfm_rl_iterate(lfm_plan plan, const float* y, float* x, const lfm_policy* policy,
+                          int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
+
+/* End-to-end call with HOST buffers: copies y in (H2D), runs lfm_rl_iterate, copies the argmax-E
+ * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best). */
+lfm_status lfm_deconvolve_host(lfm_plan plan, const float* y_host, float* x_host, const lfm_policy* policy,
+                               int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
+
+/* DCT entropy of max_z x (P:63 + Eq. 12).  x: device [nz][H][W]; max-projection reduced over ranks.
+ * region: LFM_REGION_*.  *entropy: host. */
+lfm_status lfm_quality(lfm_plan plan, const float* x, int region, double* entropy, void* stream);
+
+/* Stand-alone DCT entropy of one image (Eq. 12 with Eqs. 1-11).  img: device [H][W] fp32.
+ * nnum: N for Eqs. (7), (11).  Outputs (host): entropy, region sizes x_s, y_s. */
+lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, const lfm_optics* optics,
+                           int region, double* entropy, int* x_s, int* y_s, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFM_H_ */

@@ -1,0 +1,262 @@
+// kernels_misc.cu -- layout conversion, fills, deterministic fp64 reductions and the fp64 DCT-entropy
+// metric (K8).
+//
+// Metric (§2.2): m = max_z x; F(u,v) = sum_{i,j} m(i,j) Cr[u][i] Cw[v][j] with the
+// orthonormal DCT-II basis of Eqs. (2)-(4), only on the cutoff corner u < Y_S, v < X_S;
+// ||F||_2 = ||m||_2 by Parseval (reading C13, pinned by the oracle's Parseval test);
+// E = 2/(X_S Y_S) * sum_{(u,v) in T} -w log2 w, w = |F(u,v)| / ||m||_2 (Eq. 12, readings C12/C13).
+// All reductions use fixed partitions and fixed shuffle trees, so E is bit-reproducible.
+#include "lfm_internal.cuh"
+
+namespace lfm {
+
+__global__ void fill_kernel(float* p, size_t n, float v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void fill_dev_kernel(float* p, size_t n, const double* num, const double* den) {
+    const float v = (float)(num[0] / den[0]);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+cudaError_t launch_fill(float* p, size_t n, float v, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    fill_kernel<<<1184, 256, 0, s>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double* den, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    fill_dev_kernel<<<1184, 256, 0, s>>>(p, n, num, den);
+    return cudaGetLastError();
+}
+
+// image-order threads: pixel (z, p, q) of plane z belongs to unit z*N^2 + (p%N)*N + q%N
+__global__ void poly_image_kernel(const float* __restrict__ src, float* __restrict__ dst, XformGeom g, int ub, int uc,
+                                  int to_image) {
+    const int N = g.N, N2 = N * N;
+    const int zb = ub / N2, ze = (ub + uc - 1) / N2;
+    const size_t plane = (size_t)g.H * g.W;
+    const size_t total = (size_t)(ze - zb + 1) * plane;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int z = zb + (int)(e / plane);
+        const int pix = (int)(e % plane);
+        const int p = pix / g.W, q = pix % g.W;
+        const int u = z * N2 + (p % N) * N + (q % N);
+        if (u < ub || u >= ub + uc) continue;
+        const size_t pi = ((size_t)(u - ub) * g.nh + p / N) * g.nw + q / N;
+        const size_t ii = (size_t)z * plane + pix;
+        if (to_image)
+            dst[ii] = src[pi];
+        else
+            dst[pi] = src[ii];
+    }
+}
+
+cudaError_t launch_poly_to_image(const float* xp, float* x, const XformGeom& g, int unit_begin, int unit_count,
+                                 cudaStream_t s) {
+    if (unit_count <= 0) return cudaSuccess;
+    poly_image_kernel<<<2368, 256, 0, s>>>(xp, x, g, unit_begin, unit_count, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_image_to_poly(const float* x, float* xp, const XformGeom& g, int unit_begin, int unit_count,
+                                 cudaStream_t s) {
+    if (unit_count <= 0) return cudaSuccess;
+    poly_image_kernel<<<2368, 256, 0, s>>>(x, xp, g, unit_begin, unit_count, 0);
+    return cudaGetLastError();
+}
+
+// z max-projection of the owned units of an image-layout volume (lfm_quality)
+__global__ void max_project_kernel(const float* __restrict__ x, unsigned* __restrict__ mproj, XformGeom g) {
+    const int N = g.N, N2 = N * N;
+    const size_t plane = (size_t)g.H * g.W;
+    const size_t total = (size_t)g.nz * plane;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int z = (int)(e / plane);
+        const int pix = (int)(e % plane);
+        const int p = pix / g.W, q = pix % g.W;
+        const int u = z * N2 + (p % N) * N + (q % N);
+        if (u < g.unit0 || u >= g.unit0 + g.nu) continue;
+        atomicMax(mproj + pix, __float_as_uint(fmaxf(x[e], 0.0f)));
+    }
+}
+
+cudaError_t launch_max_project(const float* x, unsigned* mproj, const XformGeom& g, cudaStream_t s) {
+    max_project_kernel<<<2368, 256, 0, s>>>(x, mproj, g);
+    return cudaGetLastError();
+}
+
+// ---- deterministic fp64 sum / min / max ----
+__global__ void stats_partial_kernel(const float* __restrict__ p, size_t n, double* __restrict__ partials) {
+    __shared__ double ss[32], smn[32], smx[32];
+    double s = 0.0, mn = 1e300, mx = -1e300;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double v = p[i];
+        s += v;
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        ss[w] = s;
+        smn[w] = mn;
+        smx[w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 1e300, c = -1e300;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            a += ss[k];
+            b = fmin(b, smn[k]);
+            c = fmax(c, smx[k]);
+        }
+        partials[3 * blockIdx.x] = a;
+        partials[3 * blockIdx.x + 1] = b;
+        partials[3 * blockIdx.x + 2] = c;
+    }
+}
+
+__global__ void stats_final_kernel(const double* __restrict__ partials, int nparts, double* out3) {
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 1e300, c = -1e300;
+        for (int k = 0; k < nparts; ++k) {
+            a += partials[3 * k];
+            b = fmin(b, partials[3 * k + 1]);
+            c = fmax(c, partials[3 * k + 2]);
+        }
+        out3[0] = a;
+        out3[1] = b;
+        out3[2] = c;
+    }
+}
+
+cudaError_t launch_sum_stats(const float* p, size_t n, double* partials, int nparts, double* out3, cudaStream_t s) {
+    stats_partial_kernel<<<nparts, 256, 0, s>>>(p, n, partials);
+    stats_final_kernel<<<1, 32, 0, s>>>(partials, nparts, out3);
+    return cudaGetLastError();
+}
+
+// ---- metric ----
+constexpr int kMetricRows = 4;
+
+// T1[i][v] = sum_j m[i][j] Cw[v][j] (v < xs) and rowsq[i] = sum_j m[i][j]^2, fp64, kMetricRows rows per CTA
+__global__ void __launch_bounds__(256) metric_rows_kernel(const unsigned* __restrict__ mbits, int H, int W, int xs,
+                                                          const double* __restrict__ Cw, double* __restrict__ T1,
+                                                          double* __restrict__ rowsq) {
+    extern __shared__ double mrow[];
+    const int i0 = blockIdx.x * kMetricRows;
+    const int nr = min(kMetricRows, H - i0);
+    for (int e = threadIdx.x; e < nr * W; e += blockDim.x)
+        mrow[e] = (double)__uint_as_float(mbits[(size_t)i0 * W + e]);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int task = warp; task < xs + 1; task += nw) {
+        double acc[kMetricRows];
+#pragma unroll
+        for (int r = 0; r < kMetricRows; ++r) acc[r] = 0.0;
+        if (task < xs) {
+            const double* c = Cw + (size_t)task * W;
+            for (int j = lane; j < W; j += 32) {
+                const double cv = c[j];
+#pragma unroll
+                for (int r = 0; r < kMetricRows; ++r)
+                    if (r < nr) acc[r] = fma(mrow[r * W + j], cv, acc[r]);
+            }
+        } else {
+            for (int j = lane; j < W; j += 32) {
+#pragma unroll
+                for (int r = 0; r < kMetricRows; ++r)
+                    if (r < nr) acc[r] = fma(mrow[r * W + j], mrow[r * W + j], acc[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kMetricRows; ++r)
+            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+        if (lane == 0) {
+            for (int r = 0; r < nr; ++r) {
+                if (task < xs)
+                    T1[(size_t)(i0 + r) * xs + task] = acc[r];
+                else
+                    rowsq[i0 + r] = acc[r];
+            }
+        }
+    }
+}
+
+// F on the region members, Parseval norm, entropy.  One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) metric_final_kernel(int H, int xs, int ys, const double* __restrict__ Cr,
+                                                            const double* __restrict__ T1,
+                                                            const double* __restrict__ rowsq, const int2* __restrict__ mem,
+                                                            int nmem, double* __restrict__ out) {
+    __shared__ double red[32];
+    __shared__ double s_norm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // ||m||^2: thread-strided partial sums, warp tree, then warp 0 over warps (fixed order)
+    double t = 0.0;
+    for (int i = threadIdx.x; i < H; i += blockDim.x) t += rowsq[i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp] = t;
+    __syncthreads();
+    if (warp == 0) {
+        double v = lane < nw ? red[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_norm = sqrt(v);
+    }
+    __syncthreads();
+    const double L = s_norm;
+    // each warp evaluates F for members warp, warp+nw, ... and accumulates its entropy terms
+    double wsum = 0.0;
+    for (int k = warp; k < nmem; k += nw) {
+        const int u = mem[k].x, v = mem[k].y;
+        const double* cr = Cr + (size_t)u * H;
+        double f = 0.0;
+        for (int i = lane; i < H; i += 32) f = fma(cr[i], T1[(size_t)i * xs + v], f);
+        for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+        if (L > 0.0) {
+            const double w = fabs(f) / L;
+            if (w > 0.0) wsum += -w * log2(w);
+        }
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+        double v = lane < nw ? red[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            out[0] = (L > 0.0) ? 2.0 / ((double)xs * (double)ys) * v : 0.0;
+            out[1] = L;
+        }
+    }
+}
+
+cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
+                          const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
+                          double* out, cudaStream_t s) {
+    const size_t smem = (size_t)kMetricRows * W * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(metric_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    metric_rows_kernel<<<(H + kMetricRows - 1) / kMetricRows, 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq);
+    metric_final_kernel<<<1, 1024, 0, s>>>(H, xs, ys, Cr, T1, rowsq, members, nmem, out);
+    return cudaGetLastError();
+}
+
+// ---- ratio image (direct path): r = y / (max(yhat,0) + eps) ----
+__global__ void ratio_kernel(const float* __restrict__ y, const float* __restrict__ yhat, float* __restrict__ r,
+                             size_t n, float eps) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        r[i] = y[i] / (fmaxf(yhat[i], 0.0f) + eps);
+}
+
+cudaError_t launch_ratio(const float* y, const float* yhat, float* r, size_t n, float eps, cudaStream_t s) {
+    ratio_kernel<<<1184, 256, 0, s>>>(y, yhat, r, n, eps);
+    return cudaGetLastError();
+}
+
+}  // namespace lfm

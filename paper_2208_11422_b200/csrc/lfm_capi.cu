@@ -1,0 +1,857 @@
+// lfm_capi.cu -- the C ABI declared in include/lfm.h: plan (transfer matrices, normalizer, region),
+// projections, the RL loop with the DCT-entropy stop rule, and depth/phase sharding over NCCL.
+// See DESIGN.md §2 (path and boundary) and §5 (kernels).
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "lfm_internal.cuh"
+
+using namespace lfm;
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+lfm_status fail(lfm_status st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(LFM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define NK(call)                                                                                  \
+    do {                                                                                          \
+        ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess) return fail(LFM_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+#define ST(call)                              \
+    do {                                      \
+        lfm_status s_ = (call);               \
+        if (s_ != LFM_OK) return s_;          \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+struct Region {
+    int xs = 0, ys = 0;
+    std::vector<int2> tri, rect;
+};
+
+// Eqs. (7), (11), (9)-(10), (6): P_u = d_ML/(Q N), d_psf = 1.22 lambda N / NA,
+// X_S = clamp(ceil(P_u W / d_psf), 1, W), Y_S likewise with H (reading C10); triangle u X_S + v Y_S < X_S Y_S
+// with u the height index < Y_S and v the width index < X_S (reading C11).
+lfm_status make_region(const lfm_optics* o, int nnum, int H, int W, Region* r) {
+    if (!o) return fail(LFM_EINVAL, "optics is NULL: the metric region needs Eqs. (7)-(11) inputs");
+    if (!(o->wavelength_um > 0) || !(o->na > 0) || !(o->mla_pitch_um > 0) || !(o->magnification > 0))
+        return fail(LFM_EINVAL, "optics fields must be > 0 (S:25)");
+    if (o->na > 1.6) return fail(LFM_EINVAL, "optics.na must be <= 1.6 (S:27)");
+    if (H < 2 || W < 2) return fail(LFM_EDIM, "image must be at least 2x2 for the metric (S:60)");
+    const double pu = o->mla_pitch_um / (o->magnification * nnum);
+    const double dpsf = 1.22 * o->wavelength_um * nnum / o->na;
+    long long xs = (long long)std::ceil(pu * W / dpsf), ys = (long long)std::ceil(pu * H / dpsf);
+    if (xs < 1) xs = 1;
+    if (xs > W) xs = W;
+    if (ys < 1) ys = 1;
+    if (ys > H) ys = H;
+    r->xs = (int)xs;
+    r->ys = (int)ys;
+    r->tri.clear();
+    r->rect.clear();
+    for (int u = 0; u < ys; ++u)
+        for (int v = 0; v < xs; ++v) {
+            r->rect.push_back(make_int2(u, v));
+            if ((long long)u * xs + (long long)v * ys < xs * ys) r->tri.push_back(make_int2(u, v));
+        }
+    return LFM_OK;
+}
+
+// orthonormal DCT-II basis rows, Eqs. (2)-(4): C[u][x] = c(u,Z) cos((2x+1) pi u / (2Z))
+void dct_rows(int Z, int count, std::vector<double>* out) {
+    out->resize((size_t)count * Z);
+    const double pi = 3.14159265358979323846;
+    for (int u = 0; u < count; ++u) {
+        const double c = (u == 0) ? 1.0 / std::sqrt((double)Z) : std::sqrt(2.0 / Z);
+        for (int x = 0; x < Z; ++x) (*out)[(size_t)u * Z + x] = c * std::cos((2.0 * x + 1.0) * pi * u / (2.0 * Z));
+    }
+}
+
+struct MetricDev {
+    int H = 0, W = 0, xs = 0, ys = 0;
+    double *Cr = nullptr, *Cw = nullptr, *T1 = nullptr, *rowsq = nullptr, *out = nullptr;
+    int2* mem[2] = {nullptr, nullptr};
+    int nmem[2] = {0, 0};
+};
+
+void metric_free(MetricDev* m) {
+    cudaFree(m->Cr);
+    cudaFree(m->Cw);
+    cudaFree(m->T1);
+    cudaFree(m->rowsq);
+    cudaFree(m->out);
+    cudaFree(m->mem[0]);
+    cudaFree(m->mem[1]);
+    *m = MetricDev();
+}
+
+lfm_status metric_alloc(MetricDev* m, const Region& r, int H, int W, cudaStream_t s, size_t* bytes) {
+    m->H = H;
+    m->W = W;
+    m->xs = r.xs;
+    m->ys = r.ys;
+    std::vector<double> cr, cw;
+    dct_rows(H, r.ys, &cr);
+    dct_rows(W, r.xs, &cw);
+    CK(cudaMalloc(&m->Cr, cr.size() * sizeof(double)));
+    CK(cudaMalloc(&m->Cw, cw.size() * sizeof(double)));
+    CK(cudaMalloc(&m->T1, (size_t)H * r.xs * sizeof(double)));
+    CK(cudaMalloc(&m->rowsq, (size_t)H * sizeof(double)));
+    CK(cudaMalloc(&m->out, 8 * sizeof(double)));
+    CK(cudaMalloc(&m->mem[0], r.tri.size() * sizeof(int2)));
+    CK(cudaMalloc(&m->mem[1], r.rect.size() * sizeof(int2)));
+    m->nmem[0] = (int)r.tri.size();
+    m->nmem[1] = (int)r.rect.size();
+    CK(cudaMemcpyAsync(m->Cr, cr.data(), cr.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(m->Cw, cw.data(), cw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(m->mem[0], r.tri.data(), r.tri.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(m->mem[1], r.rect.data(), r.rect.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));   // host vectors die here
+    if (bytes)
+        *bytes += (cr.size() + cw.size() + (size_t)H * r.xs + H + 8) * sizeof(double) +
+                  (r.tri.size() + r.rect.size()) * sizeof(int2);
+    return LFM_OK;
+}
+
+struct SizeTerms {
+    size_t transfer, spectra, volumes, images, staging, metric;
+    size_t total() const { return transfer + spectra + volumes + images + staging + metric; }
+};
+
+void unit_range(int nu_total, int world, int rank, int* b, int* e) {
+    const int base = nu_total / world, extra = nu_total % world;
+    *b = rank * base + (rank < extra ? rank : extra);
+    *e = *b + base + (rank < extra ? 1 : 0);
+}
+
+struct Geo {
+    int N, nz, kh, kw, H, W, nh, nw, ch, cw;
+    int lcmin_h, lcmin_w, Lh, Lw, nk2, nkappa;
+};
+
+lfm_status make_geo(int nnum, int nz, int kh, int kw, int H, int W, bool direct, Geo* g) {
+    if (nnum < 1 || nnum % 2 == 0) return fail(LFM_EDIM, "nnum=%d must be odd and >= 1 (S:26)", nnum);
+    if (nz < 1) return fail(LFM_EDIM, "nz=%d must be >= 1", nz);
+    if (kh < 1 || kw < 1 || kh % 2 == 0 || kw % 2 == 0) return fail(LFM_EDIM, "kernel %dx%d must have odd sides (S:192)", kh, kw);
+    if (H < 1 || W < 1 || H % nnum || W % nnum)
+        return fail(LFM_EDIM, "image %dx%d must be divisible by nnum=%d (S:188)", H, W, nnum);
+    g->N = nnum;
+    g->nz = nz;
+    g->kh = kh;
+    g->kw = kw;
+    g->H = H;
+    g->W = W;
+    g->nh = H / nnum;
+    g->nw = W / nnum;
+    g->ch = (kh - 1) / 2;
+    g->cw = (kw - 1) / 2;
+    // alias-free coarse transform size n + ceil(c / N), rounded up to a 5-smooth length
+    g->lcmin_h = g->nh + (g->ch + nnum - 1) / nnum;
+    g->lcmin_w = g->nw + (g->cw + nnum - 1) / nnum;
+    if (direct) {
+        g->Lh = g->Lw = g->nk2 = g->nkappa = 0;
+    } else {
+        g->Lh = next_smooth(g->lcmin_h < 2 ? 2 : g->lcmin_h);
+        g->Lw = next_smooth(g->lcmin_w < 2 ? 2 : g->lcmin_w);
+        g->nk2 = g->Lw / 2 + 1;
+        g->nkappa = g->Lh * g->nk2;
+    }
+    return LFM_OK;
+}
+
+SizeTerms size_terms(const Geo& g, int nu, int nu_total, int world, bool direct) {
+    SizeTerms t{};
+    const size_t N2 = (size_t)g.N * g.N;
+    const size_t nu_pad = round_up((size_t)nu, 16);
+    const size_t vol = (size_t)nu * g.nh * g.nw * sizeof(float);
+    if (direct) {
+        t.transfer = (size_t)nu * g.kh * g.kw * sizeof(float);
+        t.spectra = 0;
+        t.staging = 0;
+    } else {
+        t.transfer = (size_t)g.nkappa * N2 * nu_pad * sizeof(float2);
+        t.spectra = 2 * (size_t)g.nkappa * nu_pad * sizeof(float2) + 2 * (size_t)g.nkappa * N2 * sizeof(float2);
+        t.staging = (size_t)nu * g.kh * g.kw * sizeof(float);
+    }
+    t.volumes = 4 * vol + (world > 1 ? (size_t)nu_total * g.nh * g.nw * sizeof(float) : 0);
+    t.images = 3 * (size_t)g.H * g.W * sizeof(float);
+    t.metric = (size_t)g.H * 64 * sizeof(double) * 2 + (1 << 20);
+    return t;
+}
+
+}  // namespace
+
+struct lfm_plan_s {
+    Geo geo{};
+    XformGeom xg{};
+    FftDesc fh{}, fw{};
+    int rank = 0, world = 1;
+    bool comm = false, direct = false;
+    ncclComm_t nccl = nullptr;
+    int u0 = 0, u1 = 0, nu = 0, nu_pad = 0, nu_total = 0;
+    int num_sms = 148;
+    float2 *tw_h = nullptr, *tw_w = nullptr;
+    float2* M = nullptr;
+    float* psf = nullptr;       // owned PSF slice (direct mode)
+    float* norm = nullptr;
+    double* norm_sum = nullptr; // device scalar, summed over ranks
+    float* xb[3] = {nullptr, nullptr, nullptr};
+    float* xfull = nullptr;     // gather buffer (world > 1)
+    float2 *G = nullptr, *Xh = nullptr, *Y = nullptr, *R = nullptr;
+    float* yhat = nullptr;
+    float* rimg = nullptr;
+    unsigned* mproj = nullptr;
+    double* partials = nullptr; // 3 * kParts
+    double* stats = nullptr;    // 3
+    double* host = nullptr;     // pinned 8 doubles
+    float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool has_optics = false;
+    lfm_optics optics{};
+    Region region;
+    MetricDev met;
+    size_t transfer_bytes = 0, bytes = 0;
+    double plan_ms = 0.0;
+};
+
+namespace {
+
+constexpr int kParts = 296;
+
+void plan_free(lfm_plan p) {
+    if (!p) return;
+    if (p->nccl) ncclCommDestroy(p->nccl);
+    cudaFree(p->tw_h);
+    cudaFree(p->tw_w);
+    cudaFree(p->M);
+    cudaFree(p->psf);
+    cudaFree(p->norm);
+    cudaFree(p->norm_sum);
+    for (auto& x : p->xb) cudaFree(x);
+    cudaFree(p->xfull);
+    cudaFree(p->G);
+    cudaFree(p->Xh);
+    cudaFree(p->Y);
+    cudaFree(p->R);
+    cudaFree(p->yhat);
+    cudaFree(p->rimg);
+    cudaFree(p->mproj);
+    cudaFree(p->partials);
+    cudaFree(p->stats);
+    cudaFree(p->y_stage);
+    cudaFree(p->x_stage);
+    if (p->host) cudaFreeHost(p->host);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    metric_free(&p->met);
+    delete p;
+}
+
+template <typename T>
+lfm_status dalloc(lfm_plan p, T** ptr, size_t bytes, const char* what) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? LFM_ENOMEM : LFM_ECUDA, "cudaMalloc(%s, %zu bytes): %s", what,
+                    bytes, cudaGetErrorString(e));
+    }
+    p->bytes += bytes;
+    return LFM_OK;
+}
+
+lfm_status twiddles(int L, float2** out, lfm_plan p, cudaStream_t s) {
+    std::vector<float2> t(L);
+    const double pi = 3.14159265358979323846;
+    for (int k = 0; k < L; ++k) {
+        const double a = -2.0 * pi * k / L;
+        t[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    ST(dalloc(p, out, L * sizeof(float2), "twiddles"));
+    CK(cudaMemcpyAsync(*out, t.data(), L * sizeof(float2), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    return LFM_OK;
+}
+
+R2CArgs r2c_args(int src, const float* in, const float* in2, float eps, int ntrans, float2* out, long long ld) {
+    R2CArgs a{};
+    a.src = src;
+    a.in = in;
+    a.in2 = in2;
+    a.eps = eps;
+    a.ntrans = ntrans;
+    a.out = out;
+    a.out_ld = ld;
+    a.cdiv = INT_MAX;
+    a.cmul = 0;
+    return a;
+}
+
+lfm_status allreduce(lfm_plan p, void* buf, size_t n, ncclDataType_t t, ncclRedOp_t op, cudaStream_t s) {
+    if (!p->comm) return LFM_OK;
+    NK(ncclAllReduce(buf, buf, n, t, op, p->nccl, s));
+    return LFM_OK;
+}
+
+// yhat = H x (x polyphase, owned units) summed over ranks
+lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_t s) {
+    const int N2 = p->geo.N * p->geo.N;
+    if (p->direct) {
+        CK(launch_direct_fwd(xp, p->psf, yimg, p->xg, s));
+    } else {
+        CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(SRC_POLY, xp, nullptr, 0.f, p->nu, p->G, p->nu_pad), s));
+        CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_pad, p->num_sms, s));
+        C2RArgs c{};
+        c.dst = DST_IMAGE;
+        c.in = p->Y;
+        c.in_ld = N2;
+        c.ntrans = N2;
+        c.out = yimg;
+        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+    }
+    return allreduce(p, yimg, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
+}
+
+// backward projection of an image source into one of the C2R destinations
+//   src: SRC_RATIO (img = y, img2 = yhat), SRC_ONES, SRC_IMAGE2D (img)
+lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2, float eps, int dst, float* out,
+                       const float* xold, cudaStream_t s) {
+    const int N2 = p->geo.N * p->geo.N;
+    if (p->direct) {
+        const size_t n = (size_t)p->geo.H * p->geo.W;
+        const float* r = img;
+        if (src == SRC_RATIO) {
+            CK(launch_ratio(img, img2, p->rimg, n, eps, s));
+            r = p->rimg;
+        } else if (src == SRC_ONES) {
+            CK(launch_fill(p->rimg, n, 1.0f, s));
+            r = p->rimg;
+        }
+        CK(launch_direct_bwd(r, p->psf, out, dst, xold, p->norm, p->mproj, eps, p->xg, s));
+        return LFM_OK;
+    }
+    CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
+    CK(launch_bwd_mac(p->M, p->R, p->Xh, p->geo.nkappa, N2, p->nu_pad, s));
+    C2RArgs c{};
+    c.dst = dst;
+    c.in = p->Xh;
+    c.in_ld = p->nu_pad;
+    c.ntrans = p->nu;
+    c.out = out;
+    c.xold = xold;
+    c.norm = p->norm;
+    c.mproj = p->mproj;
+    c.eps = eps;
+    CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+    return LFM_OK;
+}
+
+lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
+    if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the DCT-entropy metric needs them");
+    const int ri = region == LFM_REGION_RECTANGLE ? 1 : 0;
+    ST(allreduce(p, p->mproj, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclMax, s));
+    CK(launch_metric(p->mproj, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
+                     p->met.nmem[ri], p->met.T1, p->met.rowsq, p->met.out, s));
+    return LFM_OK;
+}
+
+// one RL iteration on polyphase volumes: xn = xc * H^T(y/(max(H xc,0)+eps)) / max(norm,eps); metric -> met.out[0]
+lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float eps, int region, bool metric,
+                   cudaStream_t s) {
+    ST(op_forward_poly(p, xc, p->yhat, s));
+    CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
+    ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
+    if (metric) ST(op_metric(p, region, s));
+    return LFM_OK;
+}
+
+lfm_status check_policy(const lfm_policy* pol) {
+    if (!pol) return fail(LFM_EINVAL, "policy is NULL");
+    if (pol->mode != LFM_MODE_FIXED && pol->mode != LFM_MODE_AUTO) return fail(LFM_EINVAL, "policy.mode=%d", pol->mode);
+    if (pol->mode == LFM_MODE_FIXED && pol->n_iters < 1) return fail(LFM_EINVAL, "policy.n_iters must be >= 1");
+    if (pol->mode == LFM_MODE_AUTO && (pol->min_iters < 1 || pol->min_iters > pol->max_iters))
+        return fail(LFM_EINVAL, "policy: need 1 <= min_iters <= max_iters (S:254)");
+    if (pol->patience < 1) return fail(LFM_EINVAL, "policy.patience must be >= 1 (S:254)");
+    if (!(pol->eps > 0.0f)) return fail(LFM_EINVAL, "policy.eps must be > 0");
+    if (pol->region != LFM_REGION_TRIANGLE && pol->region != LFM_REGION_RECTANGLE)
+        return fail(LFM_EINVAL, "policy.region=%d", pol->region);
+    if (pol->update == LFM_UPDATE_ISRA) return fail(LFM_EUNSUPPORTED, "policy.update=ISRA is not implemented in this build");
+    if (pol->update != LFM_UPDATE_RL) return fail(LFM_EINVAL, "policy.update=%d", pol->update);
+    return LFM_OK;
+}
+
+// y validation -> sum(y) left in p->stats[0]
+lfm_status check_y(lfm_plan p, const float* y, cudaStream_t s) {
+    const size_t n = (size_t)p->geo.H * p->geo.W;
+    CK(launch_sum_stats(y, n, p->partials, kParts, p->stats, s));
+    CK(cudaMemcpyAsync(p->host, p->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!(p->host[1] >= 0.0)) return fail(LFM_ENEG, "measurement y has a negative (or NaN) entry: min=%g (S:270)", p->host[1]);
+    if (!(p->host[2] > 0.0)) return fail(LFM_EZERO, "measurement y is all zero (S:288)");
+    return LFM_OK;
+}
+
+lfm_status gather_to_image(lfm_plan p, const float* xp_local, float* x, cudaStream_t s) {
+    if (!p->comm) {
+        CK(launch_poly_to_image(xp_local, x, p->xg, p->u0, p->nu, s));
+        return LFM_OK;
+    }
+    const size_t per = (size_t)p->geo.nh * p->geo.nw;
+    NK(ncclGroupStart());
+    for (int r = 0; r < p->world; ++r) {
+        int b, e;
+        unit_range(p->nu_total, p->world, r, &b, &e);
+        if (e <= b) continue;
+        ncclResult_t rr = ncclBroadcast(r == p->rank ? (const void*)xp_local : nullptr, p->xfull + (size_t)b * per,
+                                        (size_t)(e - b) * per, ncclFloat, r, p->nccl, s);
+        if (rr != ncclSuccess) {
+            ncclGroupEnd();
+            return fail(LFM_ENCCL, "ncclBroadcast: %s", ncclGetErrorString(rr));
+        }
+    }
+    NK(ncclGroupEnd());
+    CK(launch_poly_to_image(p->xfull, x, p->xg, 0, p->nu_total, s));
+    return LFM_OK;
+}
+
+}  // namespace
+
+// ================================================================================================
+extern "C" {
+
+lfm_policy lfm_policy_default(void) {
+    lfm_policy p;
+    p.mode = LFM_MODE_AUTO;
+    p.n_iters = 10;
+    p.max_iters = 50;
+    p.min_iters = 2;
+    p.patience = 1;
+    p.eps = 1e-6f;
+    p.region = LFM_REGION_TRIANGLE;
+    p.init_from_x = 0;
+    p.update = LFM_UPDATE_RL;
+    return p;
+}
+
+const char* lfm_last_error(void) { return g_err; }
+
+const char* lfm_version(void) { return "lfm-b200 0.1 (sm_100a; frequency-domain polyphase RL + fp64 DCT entropy)"; }
+
+lfm_status lfm_comm_unique_id(unsigned char* id_out) {
+    if (!id_out) return fail(LFM_EINVAL, "id_out is NULL");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(id_out, &id, 128);
+    return LFM_OK;
+}
+
+lfm_status lfm_plan_estimate(int nnum, int nz, int kh, int kw, int height, int width, int world, int flags,
+                             size_t budget_bytes, size_t* bytes_per_gpu, char* limiting_term, size_t len) {
+    g_err[0] = 0;
+    if (!bytes_per_gpu) return fail(LFM_EINVAL, "bytes_per_gpu is NULL");
+    if (world < 1) return fail(LFM_EINVAL, "world=%d", world);
+    const bool direct = (flags & LFM_PLAN_DIRECT) != 0;
+    Geo g;
+    ST(make_geo(nnum, nz, kh, kw, height, width, direct, &g));
+    const int nu_total = nz * nnum * nnum;
+    int b, e;
+    unit_range(nu_total, world, 0, &b, &e);   // rank 0 owns the largest share
+    SizeTerms t = size_terms(g, e - b, nu_total, world, direct);
+    *bytes_per_gpu = t.total();
+    const char* names[6] = {"transfer matrices", "spectra workspaces", "volumes", "images", "PSF staging", "metric"};
+    const size_t vals[6] = {t.transfer, t.spectra, t.volumes, t.images, t.staging, t.metric};
+    int best = 0;
+    for (int i = 1; i < 6; ++i)
+        if (vals[i] > vals[best]) best = i;
+    if (limiting_term && len) snprintf(limiting_term, len, "%s (%zu bytes)", names[best], vals[best]);
+    if (budget_bytes > 0 && *bytes_per_gpu > budget_bytes)
+        return fail(LFM_ENOMEM, "estimate %zu bytes per GPU exceeds budget %zu; limiting term: %s (%zu bytes)",
+                    *bytes_per_gpu, budget_bytes, names[best], vals[best]);
+    return LFM_OK;
+}
+
+lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* psf_t_host, int nnum, int nz, int kh,
+                           int kw, int height, int width, const lfm_optics* optics, const lfm_dist* dist, int flags,
+                           void* stream) {
+    g_err[0] = 0;
+    const auto t_start = std::chrono::steady_clock::now();
+    if (!out) return fail(LFM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!psf_host) return fail(LFM_EINVAL, "psf_host is NULL");
+    if (psf_t_host)
+        return fail(LFM_EUNSUPPORTED, "a supplied transposed PSF is not supported in this build; pass NULL for the exact adjoint (C6)");
+    const bool direct = (flags & LFM_PLAN_DIRECT) != 0;
+    Geo g;
+    ST(make_geo(nnum, nz, kh, kw, height, width, direct, &g));
+    int rank = 0, world = 1;
+    if (dist) {
+        rank = dist->rank;
+        world = dist->world;
+        if (world < 1 || rank < 0 || rank >= world) return fail(LFM_EINVAL, "dist rank=%d world=%d", rank, world);
+    }
+    cudaStream_t s = as_stream(stream);
+    lfm_plan p = new lfm_plan_s();
+    auto guard = [&](lfm_status st) {
+        if (st != LFM_OK) plan_free(p);
+        return st;
+    };
+#define PG(call)                                  \
+    do {                                          \
+        lfm_status s__ = (call);                  \
+        if (s__ != LFM_OK) return guard(s__);     \
+    } while (0)
+#define CKG(call)                                                                                           \
+    do {                                                                                                    \
+        cudaError_t e_ = (call);                                                                            \
+        if (e_ != cudaSuccess)                                                                              \
+            return guard(fail(LFM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
+    } while (0)
+    p->geo = g;
+    p->direct = direct;
+    p->rank = rank;
+    p->world = world;
+    p->nu_total = nz * nnum * nnum;
+    unit_range(p->nu_total, world, rank, &p->u0, &p->u1);
+    p->nu = p->u1 - p->u0;
+    p->nu_pad = (int)round_up((size_t)(p->nu > 0 ? p->nu : 1), 16);
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // PSF validation over the owned slice
+    const size_t kk = (size_t)kh * kw;
+    const float* psf_own = psf_host + (size_t)p->u0 * kk;
+    for (size_t i = 0, n = (size_t)p->nu * kk; i < n; ++i)
+        if (!(psf_own[i] >= 0.0f)) return guard(fail(LFM_ENEG, "psf has a negative (or NaN) entry at unit %zu (S:192)", p->u0 + i / kk));
+    if (optics) {
+        PG(make_region(optics, nnum, height, width, &p->region));
+        p->has_optics = true;
+        p->optics = *optics;
+    }
+    // memory budget ("estimate the required memory size")
+    {
+        SizeTerms t = size_terms(g, p->nu, p->nu_total, world, direct);
+        size_t free_b = 0, total_b = 0;
+        CKG(cudaMemGetInfo(&free_b, &total_b));
+        if (t.total() > free_b) {
+            const char* names[6] = {"transfer matrices", "spectra workspaces", "volumes", "images", "PSF staging", "metric"};
+            const size_t vals[6] = {t.transfer, t.spectra, t.volumes, t.images, t.staging, t.metric};
+            int best = 0;
+            for (int i = 1; i < 6; ++i)
+                if (vals[i] > vals[best]) best = i;
+            return guard(fail(LFM_ENOMEM, "plan needs %zu bytes on this GPU, %zu free; limiting term: %s (%zu bytes)",
+                              t.total(), free_b, names[best], vals[best]));
+        }
+    }
+    if (world > 1 && !(flags & LFM_PLAN_NO_COMM)) {
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&p->nccl, world, id, rank);
+        if (r != ncclSuccess) return guard(fail(LFM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+        p->comm = true;
+    }
+    // geometry for the kernels
+    XformGeom& xg = p->xg;
+    xg.N = nnum;
+    xg.H = height;
+    xg.W = width;
+    xg.nh = g.nh;
+    xg.nw = g.nw;
+    xg.nz = nz;
+    xg.Lh = g.Lh;
+    xg.Lw = g.Lw;
+    xg.nk2 = g.nk2;
+    xg.nkappa = g.nkappa;
+    xg.unit0 = p->u0;
+    xg.nu = p->nu;
+    xg.nu_pad = p->nu_pad;
+    xg.kh = kh;
+    xg.kw = kw;
+    xg.ch = g.ch;
+    xg.cw = g.cw;
+    const int N2 = nnum * nnum;
+    const size_t HW = (size_t)height * width;
+    const size_t vol = (size_t)p->nu * g.nh * g.nw;
+    // buffers
+    for (auto& x : p->xb) PG(dalloc(p, &x, vol * sizeof(float), "volume"));
+    PG(dalloc(p, &p->norm, vol * sizeof(float), "normalizer"));
+    PG(dalloc(p, &p->norm_sum, 4 * sizeof(double), "norm_sum"));
+    if (p->comm) PG(dalloc(p, &p->xfull, (size_t)p->nu_total * g.nh * g.nw * sizeof(float), "gather volume"));
+    PG(dalloc(p, &p->yhat, HW * sizeof(float), "yhat"));
+    PG(dalloc(p, &p->rimg, HW * sizeof(float), "ratio image"));
+    PG(dalloc(p, &p->mproj, HW * sizeof(unsigned), "max projection"));
+    PG(dalloc(p, &p->partials, 3 * kParts * sizeof(double), "partials"));
+    PG(dalloc(p, &p->stats, 4 * sizeof(double), "stats"));
+    CKG(cudaMallocHost(&p->host, 16 * sizeof(double)));
+    CKG(cudaEventCreate(&p->ev0));
+    CKG(cudaEventCreate(&p->ev1));
+    // PSF slice of the owned units -> device ("the PSF is evenly distributed to each card")
+    PG(dalloc(p, &p->psf, (size_t)p->nu * kk * sizeof(float), "psf slice"));
+    if (p->nu > 0) CKG(cudaMemcpyAsync(p->psf, psf_own, (size_t)p->nu * kk * sizeof(float), cudaMemcpyHostToDevice, s));
+    if (!direct) {
+        if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
+            return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", g.Lh, g.Lw));
+        PG(twiddles(g.Lh, &p->tw_h, p, s));
+        PG(twiddles(g.Lw, &p->tw_w, p, s));
+        p->transfer_bytes = (size_t)g.nkappa * N2 * p->nu_pad * sizeof(float2);
+        PG(dalloc(p, &p->M, p->transfer_bytes, "transfer matrices"));
+        PG(dalloc(p, &p->G, (size_t)g.nkappa * p->nu_pad * sizeof(float2), "G spectra"));
+        PG(dalloc(p, &p->Xh, (size_t)g.nkappa * p->nu_pad * sizeof(float2), "Xh spectra"));
+        PG(dalloc(p, &p->Y, (size_t)g.nkappa * N2 * sizeof(float2), "Y spectra"));
+        PG(dalloc(p, &p->R, (size_t)g.nkappa * N2 * sizeof(float2), "R spectra"));
+        CKG(cudaMemsetAsync(p->M, 0, p->transfer_bytes, s));      // padding columns stay zero
+        CKG(cudaMemsetAsync(p->G, 0, (size_t)g.nkappa * p->nu_pad * sizeof(float2), s));
+        // K1: transfer matrices M[kappa][b'][u] = DFT_{Lh x Lw}(g_{u,b'}), g_{u,b'}[d] = h_u[b' - a + c + N d]
+        R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * p->nu, p->M, (long long)N2 * p->nu_pad);
+        a.cdiv = p->nu > 0 ? p->nu : 1;
+        a.cmul = p->nu_pad;
+        CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, a, s));
+        CKG(cudaStreamSynchronize(s));
+        cudaFree(p->psf);           // the transfer matrices replace the PSF
+        p->bytes -= (size_t)p->nu * kk * sizeof(float);
+        p->psf = nullptr;
+    } else {
+        p->transfer_bytes = (size_t)p->nu * kk * sizeof(float);
+    }
+    // normalizer H^T 1, polyphase, and its global sum (for c0 = sum y / sum H^T 1, reading C2)
+    PG(op_backward(p, SRC_ONES, nullptr, nullptr, 1.0f, DST_POLY, p->norm, nullptr, s));
+    CKG(launch_sum_stats(p->norm, vol, p->partials, kParts, p->stats, s));
+    CKG(cudaMemcpyAsync(p->norm_sum, p->stats, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    PG(allreduce(p, p->norm_sum, 1, ncclDouble, ncclSum, s));
+    if (p->has_optics) PG(metric_alloc(&p->met, p->region, height, width, s, &p->bytes));
+    CKG(cudaStreamSynchronize(s));
+    p->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    *out = p;
+    return LFM_OK;
+#undef PG
+#undef CKG
+}
+
+lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
+    if (!p || !info) return fail(LFM_EINVAL, "NULL argument");
+    info->nnum = p->geo.N;
+    info->nz = p->geo.nz;
+    info->kh = p->geo.kh;
+    info->kw = p->geo.kw;
+    info->height = p->geo.H;
+    info->width = p->geo.W;
+    info->unit_begin = p->u0;
+    info->unit_end = p->u1;
+    info->fft_h = p->geo.Lh;
+    info->fft_w = p->geo.Lw;
+    info->lc_min_h = p->geo.lcmin_h;
+    info->lc_min_w = p->geo.lcmin_w;
+    info->n_kappa = p->geo.nkappa;
+    info->units_padded = p->nu_pad;
+    info->x_s = p->region.xs;
+    info->y_s = p->region.ys;
+    info->direct = p->direct ? 1 : 0;
+    info->transfer_bytes = p->transfer_bytes;
+    info->device_bytes = p->bytes;
+    info->plan_ms = p->plan_ms;
+    return LFM_OK;
+}
+
+void lfm_plan_destroy(lfm_plan p) { plan_free(p); }
+
+lfm_status lfm_forward(lfm_plan p, const float* x, float* y, void* stream) {
+    g_err[0] = 0;
+    if (!p || !x || !y) return fail(LFM_EINVAL, "NULL argument");
+    cudaStream_t s = as_stream(stream);
+    if (p->direct) {
+        CK(launch_image_to_poly(x, p->xb[0], p->xg, p->u0, p->nu, s));
+        ST(op_forward_poly(p, p->xb[0], y, s));
+        return LFM_OK;
+    }
+    const int N2 = p->geo.N * p->geo.N;
+    CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(SRC_IMAGE, x, nullptr, 0.f, p->nu, p->G, p->nu_pad), s));
+    CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_pad, p->num_sms, s));
+    C2RArgs c{};
+    c.dst = DST_IMAGE;
+    c.in = p->Y;
+    c.in_ld = N2;
+    c.ntrans = N2;
+    c.out = y;
+    CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+    return allreduce(p, y, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
+}
+
+lfm_status lfm_backward(lfm_plan p, const float* y, float* x, void* stream) {
+    g_err[0] = 0;
+    if (!p || !x || !y) return fail(LFM_EINVAL, "NULL argument");
+    return op_backward(p, SRC_IMAGE2D, y, nullptr, 1.0f, DST_VOLIMAGE, x, nullptr, as_stream(stream));
+}
+
+lfm_status lfm_normalizer(lfm_plan p, float* x, void* stream) {
+    g_err[0] = 0;
+    if (!p || !x) return fail(LFM_EINVAL, "NULL argument");
+    CK(launch_poly_to_image(p->norm, x, p->xg, p->u0, p->nu, as_stream(stream)));
+    return LFM_OK;
+}
+
+lfm_status lfm_rl_step(lfm_plan p, const float* y, const float* x_in, float* x_out, float eps, int region,
+                       float* yhat_out, double* entropy_host, void* stream) {
+    g_err[0] = 0;
+    if (!p || !y || !x_in || !x_out) return fail(LFM_EINVAL, "NULL argument");
+    if (!(eps > 0.0f)) return fail(LFM_EINVAL, "eps must be > 0");
+    cudaStream_t s = as_stream(stream);
+    CK(launch_image_to_poly(x_in, p->xb[0], p->xg, p->u0, p->nu, s));
+    ST(op_step(p, y, p->xb[0], p->xb[1], eps, region, entropy_host != nullptr, s));
+    if (yhat_out) CK(cudaMemcpyAsync(yhat_out, p->yhat, (size_t)p->geo.H * p->geo.W * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    CK(launch_poly_to_image(p->xb[1], x_out, p->xg, p->u0, p->nu, s));
+    if (entropy_host) {
+        CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *entropy_host = p->host[0];
+    }
+    return LFM_OK;
+}
+
+lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy* pol, int* best_iter, int* stop_iter,
+                          double* series_host, float* ms_host, void* stream) {
+    g_err[0] = 0;
+    if (!p || !y || !x || !best_iter || !stop_iter || !series_host) return fail(LFM_EINVAL, "NULL argument");
+    ST(check_policy(pol));
+    if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the stop rule needs the DCT-entropy metric");
+    cudaStream_t s = as_stream(stream);
+    ST(check_y(p, y, s));
+    const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
+    int cur = 0, best = -1;
+    if (pol->init_from_x) {
+        CK(launch_image_to_poly(x, p->xb[cur], p->xg, p->u0, p->nu, s));
+    } else {
+        CK(launch_fill_dev(p->xb[cur], vol, p->stats, p->norm_sum, s));   // c0 = sum y / sum H^T 1
+    }
+    const int cap = pol->mode == LFM_MODE_FIXED ? pol->n_iters : pol->max_iters;
+    double best_e = -INFINITY, prev = 0.0;
+    int decreases = 0, k = 0, best_k = 0;
+    for (;;) {
+        ++k;
+        int nxt = 0;
+        while (nxt == cur || nxt == best) ++nxt;
+        if (ms_host) CK(cudaEventRecord(p->ev0, s));
+        ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s));
+        if (ms_host) CK(cudaEventRecord(p->ev1, s));
+        CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const double e = p->host[0];
+        series_host[k - 1] = e;
+        if (ms_host) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            ms_host[k - 1] = ms;
+        }
+        // stop rule (reading C15): strict decreases counted, argmax with ties -> smallest k
+        if (k > 1 && e < prev)
+            ++decreases;
+        else
+            decreases = 0;
+        prev = e;
+        if (e > best_e) {
+            best_e = e;
+            best_k = k;
+            best = nxt;
+        }
+        cur = nxt;
+        bool stop;
+        if (pol->mode == LFM_MODE_FIXED)
+            stop = k >= pol->n_iters;
+        else
+            stop = (k >= pol->min_iters && decreases >= pol->patience) || k >= cap;
+        if (stop) break;
+    }
+    if (best < 0) best = cur;
+    ST(gather_to_image(p, p->xb[best], x, s));
+    CK(cudaStreamSynchronize(s));
+    *best_iter = best_k;
+    *stop_iter = k;
+    return LFM_OK;
+}
+
+lfm_status lfm_deconvolve_host(lfm_plan p, const float* y_host, float* x_host, const lfm_policy* pol, int* best_iter,
+                               int* stop_iter, double* series_host, float* ms_host, void* stream) {
+    g_err[0] = 0;
+    if (!p || !y_host || !x_host) return fail(LFM_EINVAL, "NULL argument");
+    ST(check_policy(pol));
+    cudaStream_t s = as_stream(stream);
+    const size_t HW = (size_t)p->geo.H * p->geo.W;
+    const size_t V = (size_t)p->geo.nz * HW;
+    if (!p->y_stage) ST(dalloc(p, &p->y_stage, HW * sizeof(float), "y staging"));
+    if (!p->x_stage) ST(dalloc(p, &p->x_stage, V * sizeof(float), "x staging"));
+    CK(cudaMemcpyAsync(p->y_stage, y_host, HW * sizeof(float), cudaMemcpyHostToDevice, s));
+    if (pol->init_from_x) CK(cudaMemcpyAsync(p->x_stage, x_host, V * sizeof(float), cudaMemcpyHostToDevice, s));
+    ST(lfm_rl_iterate(p, p->y_stage, p->x_stage, pol, best_iter, stop_iter, series_host, ms_host, stream));
+    CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return LFM_OK;
+}
+
+lfm_status lfm_quality(lfm_plan p, const float* x, int region, double* entropy, void* stream) {
+    g_err[0] = 0;
+    if (!p || !x || !entropy) return fail(LFM_EINVAL, "NULL argument");
+    if (region != LFM_REGION_TRIANGLE && region != LFM_REGION_RECTANGLE) return fail(LFM_EINVAL, "region=%d", region);
+    cudaStream_t s = as_stream(stream);
+    CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
+    CK(launch_max_project(x, p->mproj, p->xg, s));
+    ST(op_metric(p, region, s));
+    CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *entropy = p->host[0];
+    return LFM_OK;
+}
+
+lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, const lfm_optics* optics, int region,
+                           double* entropy, int* x_s, int* y_s, void* stream) {
+    g_err[0] = 0;
+    if (!img || !entropy) return fail(LFM_EINVAL, "NULL argument");
+    if (nnum < 1) return fail(LFM_EINVAL, "nnum=%d", nnum);
+    if (region != LFM_REGION_TRIANGLE && region != LFM_REGION_RECTANGLE) return fail(LFM_EINVAL, "region=%d", region);
+    Region r;
+    ST(make_region(optics, nnum, height, width, &r));
+    cudaStream_t s = as_stream(stream);
+    MetricDev m;
+    lfm_status st = metric_alloc(&m, r, height, width, s, nullptr);
+    if (st != LFM_OK) {
+        metric_free(&m);
+        return st;
+    }
+    const int ri = region == LFM_REGION_RECTANGLE ? 1 : 0;
+    double h = 0.0;
+    cudaError_t e = launch_metric(reinterpret_cast<const unsigned*>(img), height, width, m.xs, m.ys, m.Cr, m.Cw, m.mem[ri],
+                                  m.nmem[ri], m.T1, m.rowsq, m.out, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, m.out, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    metric_free(&m);
+    if (e != cudaSuccess) return fail(LFM_ECUDA, "lfm_dct_entropy: %s", cudaGetErrorString(e));
+    *entropy = h;
+    if (x_s) *x_s = r.xs;
+    if (y_s) *y_s = r.ys;
+    return LFM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// lfm_internal.cuh -- internal declarations of the B200 light-field RL path (not part of the ABI).
+//
+// Notation: N = Nnum, (nh, nw) = (H/N, W/N) lenslets, unit u = z*N*N + a1*N + a2
+// (plane z, input phase a), output phase b' = b1*N + b2, coarse transform Lh x Lw, kappa = k1*nk2 + k2
+// with nk2 = Lw/2 + 1 (Hermitian half plane).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <cstddef>
+#include <cstdint>
+#include "../../include/lfm.h"
+
+namespace lfm {
+
+constexpr int kMaxStages = 16;
+
+struct FftDesc {
+    int L;
+    int nst;
+    int radix[kMaxStages];
+};
+
+bool fft_factor(int L, FftDesc* d);         // radices 4,2,3,5; false if L is not 5-smooth
+int next_smooth(int n);                     // smallest 5-smooth integer >= n
+
+// ---- source / sink modes of the coarse transforms ----
+enum R2CSrc : int {
+    SRC_POLY = 0,     // polyphase volume [nu][nh][nw]            -> transform t = local unit
+    SRC_IMAGE = 1,    // image-layout volume [nz][H][W]           -> transform t = local unit
+    SRC_RATIO = 2,    // r = y / (max(yhat,0)+eps) on [H][W]       -> transform t = output phase b'
+    SRC_ONES = 3,     // all-ones image                            -> transform t = output phase b'
+    SRC_KERNEL = 4,   // PSF coarse kernels (plan)                 -> transform t = b'*nu + local unit
+    SRC_IMAGE2D = 5   // plain image [H][W] (lfm_backward input)   -> transform t = output phase b'
+};
+enum C2RDst : int {
+    DST_IMAGE = 0,    // yhat image [H][W] at (b1 + N i, b2 + N j); t = output phase
+    DST_POLY = 1,     // polyphase volume; t = local unit
+    DST_VOLIMAGE = 2, // image-layout volume [nz][H][W]; t = local unit
+    DST_UPDATE = 3    // x_new = x_old * max(bp,0) / max(norm,eps) (poly) + atomic max-projection
+};
+
+struct XformGeom {
+    int N, H, W, nh, nw, nz;
+    int Lh, Lw, nk2, nkappa;
+    int unit0;              // first owned global unit
+    int nu, nu_pad;
+    int kh, kw, ch, cw;
+};
+
+struct R2CArgs {
+    int src;
+    const float* in;        // source array (see R2CSrc)
+    const float* in2;       // yhat for SRC_RATIO
+    float eps;
+    int ntrans;             // number of transforms
+    float2* out;            // out[kappa * out_ld + col(t)]
+    long long out_ld;
+    int cdiv, cmul;         // col(t) = (t / cdiv) * cmul + t % cdiv
+};
+
+struct C2RArgs {
+    int dst;
+    const float2* in;       // in[kappa * in_ld + t]
+    long long in_ld;
+    int ntrans;
+    float* out;             // see C2RDst
+    const float* xold;      // DST_UPDATE
+    const float* norm;      // DST_UPDATE
+    unsigned* mproj;        // DST_UPDATE (float bits of non-negative values, atomicMax)
+    float eps;
+};
+
+struct Plan;
+
+// launchers (kernels_fft.cu)
+cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
+                       const float2* tw_w, const R2CArgs& a, cudaStream_t s);
+cudaError_t launch_c2r(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
+                       const float2* tw_w, const C2RArgs& a, cudaStream_t s);
+// (kernels_mac.cu)
+cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad,
+                           int num_sms, cudaStream_t s);
+cudaError_t launch_bwd_mac(const float2* M, const float2* R, float2* Xh, int nkappa, int N2, int nu_pad,
+                           cudaStream_t s);
+// (kernels_misc.cu)
+cudaError_t launch_fill(float* p, size_t n, float v, cudaStream_t s);
+cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double* den, cudaStream_t s);
+cudaError_t launch_poly_to_image(const float* xp, float* x, const XformGeom& g, int unit_begin, int unit_count,
+                                 cudaStream_t s);
+cudaError_t launch_image_to_poly(const float* x, float* xp, const XformGeom& g, int unit_begin, int unit_count,
+                                 cudaStream_t s);
+cudaError_t launch_max_project(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s);
+cudaError_t launch_sum_stats(const float* p, size_t n, double* partials, int nparts, double* out3, cudaStream_t s);
+cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
+                          const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
+                          double* out, cudaStream_t s);
+// direct spatial path (kernels_direct.cu)
+cudaError_t launch_direct_fwd(const float* xp, const float* psf, float* yimg, const XformGeom& g, cudaStream_t s);
+cudaError_t launch_direct_bwd(const float* rimg, const float* psf, float* out, int dst, const float* xold,
+                              const float* norm, unsigned* mproj, float eps, const XformGeom& g, cudaStream_t s);
+cudaError_t launch_ratio(const float* y, const float* yhat, float* r, size_t n, float eps, cudaStream_t s);
+
+}  // namespace lfm

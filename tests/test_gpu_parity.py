@@ -1,0 +1,280 @@
+"""GPU parity (marked gpu): the CUDA path, called through the C ABI, against the fp64 oracle on the
+same seeded inputs.  Tolerances: operators rel-L2 <= 2e-6 and max-abs <= 1e-5 * max|ref|
+(fp32 FFT + fp32 MAC over nz N^2 terms, measured ~1e-7); RL rel-L2 <= 1e-4 after 1 iteration and
+<= 1e-3 after 30 (BASELINE.json north star); identical stop / best iteration unless the decision margin is
+within 10x the observed entropy error (reading C16)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from lfm_inputs import CONFIGS, OPTICS, Config, gen_psf, gen_volume, lf_like, poisson  # noqa: E402
+from oracle import lfm_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+OPT = O.Optics(nnum=0, **OPTICS)
+
+
+def L():
+    from paper_2208_11422_b200 import lfm
+    return lfm
+
+
+def dev(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def optics(nnum):
+    return L().make_optics(**OPTICS)
+
+
+def rand_case(seed, nz, N, H, W, kh, kw):
+    rng = np.random.default_rng(seed)
+    h = rng.uniform(0, 1, (nz, N, N, kh, kw)).astype(np.float32)
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    x = rng.uniform(0, 1, (nz, H, W)).astype(np.float32)
+    r = rng.uniform(0.5, 1.5, (H, W)).astype(np.float32)
+    return h, x, r
+
+
+OP_CASES = [  # (nz, N, H, W, kh, kw): tiny, ragged units, non-square, radix 2/3/5 mixes, N=1, kernel > image
+    (3, 3, 33, 33, 9, 9),
+    (2, 3, 27, 36, 7, 11),
+    (4, 5, 45, 45, 15, 15),
+    (2, 1, 20, 24, 5, 7),
+    (2, 3, 9, 9, 21, 21),
+    (5, 7, 63, 49, 29, 21),
+]
+
+
+@pytest.mark.parametrize("flags", [0, 2], ids=["fft", "direct"])
+@pytest.mark.parametrize("case", OP_CASES, ids=[str(c) for c in OP_CASES])
+def test_projections_match_oracle(case, flags):
+    nz, N, H, W, kh, kw = case
+    h, x, r = rand_case(sum(case), *case)
+    hd = h.astype(np.float64)
+    with L().Plan(h, N, H, W, optics=optics(N), flags=flags) as plan:
+        y_d = torch.zeros((H, W), device="cuda")
+        plan.forward(dev(x), y_d)
+        xb_d = torch.zeros((nz, H, W), device="cuda")
+        plan.backward(dev(r), xb_d)
+        nrm_d = torch.zeros((nz, H, W), device="cuda")
+        plan.normalizer(nrm_d)
+        torch.cuda.synchronize()
+        info = plan.info()
+    y_ref = O.forward_project(x.astype(np.float64), hd)
+    xb_ref = O.backward_project(r.astype(np.float64), hd)
+    nrm_ref = O.compute_normalizer(hd, H, W)
+    for got, ref in [(y_d, y_ref), (xb_d, xb_ref), (nrm_d, nrm_ref)]:
+        g = got.cpu().numpy()
+        assert rel(g, ref) <= 2e-6, (rel(g, ref), info)
+        assert np.abs(g - ref).max() <= 1e-5 * np.abs(ref).max()
+    if flags == 0:
+        assert info["fft_h"] >= info["lc_min_h"] and info["fft_w"] >= info["lc_min_w"]
+
+
+def test_adjoint_on_gpu():
+    """<Hx, y> = <x, H^T y> for the GPU operators (fp32: 1e-5 relative)."""
+    h, x, r = rand_case(7, 3, 5, 45, 45, 15, 15)
+    with L().Plan(h, 5, 45, 45, optics=optics(5)) as plan:
+        y_d = torch.zeros((45, 45), device="cuda")
+        plan.forward(dev(x), y_d)
+        xb_d = torch.zeros((3, 45, 45), device="cuda")
+        plan.backward(dev(r), xb_d)
+        torch.cuda.synchronize()
+    lhs = np.vdot(y_d.cpu().numpy().astype(np.float64), r)
+    rhs = np.vdot(x.astype(np.float64), xb_d.cpu().numpy())
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_c2_operators_match_oracle():
+    """BASELINE configs[1] geometry (N=11, 319^2, 21 planes, K=99): full-image operator parity."""
+    cfg = CONFIGS["c2"]
+    h = gen_psf(cfg, np.float32)
+    x = gen_volume(cfg, 1, np.float32)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+        plan.forward(dev(x), y_d)
+        torch.cuda.synchronize()
+        y_ref = O.forward_project(x.astype(np.float64), h.astype(np.float64))
+        assert rel(y_d.cpu().numpy(), y_ref) <= 2e-6
+        r = (y_ref + 1.0) / (y_ref.mean() + 1.0)
+        xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        plan.backward(dev(r), xb_d)
+        torch.cuda.synchronize()
+    xb_ref = O.backward_project(r.astype(np.float32).astype(np.float64), h.astype(np.float64))
+    assert rel(xb_d.cpu().numpy(), xb_ref) <= 2e-6
+
+
+def tiny_problem(name="tiny", seed=1):
+    cfg = CONFIGS[name]
+    h = gen_psf(cfg, np.float32)
+    hd = h.astype(np.float64)
+    xt = gen_volume(cfg, seed)
+    y = poisson(O.forward_project(xt, hd), 100 + seed)
+    return cfg, h, hd, y
+
+
+def oracle_iterates(y, hd, cfg, n):
+    norm = O.compute_normalizer(hd, cfg.height, cfg.width)
+    x = O.initial_volume(y, hd, cfg.nz, cfg.height, cfg.width)
+    reg = O.cutoff_region(O.Optics(nnum=cfg.nnum, **OPTICS), cfg.height, cfg.width)
+    out, es = [], []
+    for _ in range(n):
+        x, _ = O.rl_step(x, y, hd, norm)
+        out.append(x.copy())
+        es.append(O.evaluate_iteration(x, reg))
+    return out, es
+
+
+@pytest.mark.parametrize("flags", [0, 2], ids=["fft", "direct"])
+def test_rl_tiny_1_and_30_iterations(flags):
+    """North star: rel-L2 <= 1e-4 after 1 iteration, <= 1e-3 after 30; E_k within 1e-4 relative."""
+    cfg, h, hd, y = tiny_problem()
+    xs, es = oracle_iterates(y, hd, cfg, 30)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+        y_d = dev(y)
+        for n, tol in [(1, 1e-4), (10, 1e-3), (30, 1e-3)]:
+            x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            res = plan.rl_iterate(y_d, x_d, L().make_policy(mode="fixed", n_iters=n))
+            assert res["stop_iter"] == n
+            # fixed mode returns the argmax-E iterate; compare against the oracle's same iterate
+            assert res["best_iter"] == int(np.argmax(es[:n])) + 1
+            assert rel(x_d.cpu().numpy(), xs[res["best_iter"] - 1]) <= tol
+            np.testing.assert_allclose(res["series"], es[:n], rtol=1e-4)
+
+
+def test_rl_step_matches_oracle_step_by_step():
+    """lfm_rl_step: each GPU step from the oracle's own iterate stays within 1e-5 of the oracle's next."""
+    cfg, h, hd, y = tiny_problem(seed=2)
+    xs, es = oracle_iterates(y, hd, cfg, 5)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        y_d = dev(y)
+        for k in range(4):
+            xo = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            yh = torch.zeros((cfg.height, cfg.width), device="cuda")
+            e = plan.rl_step(y_d, dev(xs[k]), xo, yhat_out=yh)
+            assert rel(xo.cpu().numpy(), xs[k + 1]) <= 1e-5
+            assert abs(e - es[k + 1]) <= 1e-5 * abs(es[k + 1])
+            assert rel(yh.cpu().numpy(), O.forward_project(xs[k].astype(np.float32).astype(np.float64), hd)) <= 2e-6
+
+
+def stop_parity(cfg, h, hd, y, max_iters=50, flags=0):
+    res_o = O.deconvolve(y, hd, O.Optics(nnum=cfg.nnum, **OPTICS), O.Policy(mode="auto", max_iters=max_iters))
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+        x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="auto", max_iters=max_iters))
+        torch.cuda.synchronize()
+    n = min(len(res["series"]), len(res_o.series))
+    err = max(abs(a - b) / abs(b) for a, b in zip(res["series"][:n], res_o.series[:n]))
+    s = res_o.series
+    k = res_o.stop_iter
+    margin = min(abs(s[i] - s[i - 1]) / abs(s[i]) for i in range(1, k)) if k > 1 else 1.0
+    return res, res_o, err, margin, x_d
+
+
+@pytest.mark.parametrize("name,seed", [("tiny", 1), ("tiny", 3), ("s15", 1)])
+def test_auto_stop_identical(name, seed):
+    """Identical stop_iter and best_iter vs the oracle (P:99 stop rule) unless tie-ambiguous (C16)."""
+    cfg, h, hd, y = tiny_problem(name, seed)
+    res, res_o, err, margin, x_d = stop_parity(cfg, h, hd, y)
+    assert err <= 1e-4
+    if margin <= 10 * err:
+        pytest.skip(f"tie-ambiguous: decision margin {margin:.2e} <= 10 x entropy error {err:.2e} (C16)")
+    assert (res["stop_iter"], res["best_iter"]) == (res_o.stop_iter, res_o.best_iter)
+    assert rel(x_d.cpu().numpy(), res_o.volume) <= 1e-3
+
+
+def test_c2_rl_8_iterations():
+    """BASELINE configs[1]: N=11, 319^2, 21 planes, 8 RL iterations (fixed)."""
+    cfg, h, hd, y = tiny_problem("c2", 1)
+    xs, es = oracle_iterates(y, hd, cfg, 8)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=8))
+        torch.cuda.synchronize()
+    assert res["best_iter"] == int(np.argmax(es)) + 1
+    assert rel(x_d.cpu().numpy(), xs[res["best_iter"] - 1]) <= 1e-3
+    np.testing.assert_allclose(res["series"], es, rtol=1e-4)
+    x1 = xs[0]
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=1))
+        assert rel(x_d.cpu().numpy(), x1) <= 1e-4
+
+
+def test_dct_entropy_standalone():
+    """Eq. (12) on the GPU (fp64) vs the oracle on full-size images, triangle and rectangle."""
+    for (H, W, N) in [(1005, 1005, 15), (319, 319, 11), (33, 33, 3), (225, 300, 15)]:
+        img = lf_like(Config("t", N, H, W, 1, 1, 0, 1, 0, 0, 0, "beads", 0, 1, 1, 0), 5).astype(np.float32)
+        for shape, code in [("triangle", 0), ("rectangle", 1)]:
+            e, xs, ys = L().lfm_dct_entropy(dev(img), N, optics(N), code)
+            reg = O.cutoff_region(O.Optics(nnum=N, **OPTICS), H, W, shape)
+            assert (xs, ys) == (reg.x_s, reg.y_s)
+            assert e == pytest.approx(O.dct_entropy(img.astype(np.float64), reg), rel=1e-10)
+
+
+def test_virtual_shards_partition():
+    """S:352 depth/phase sharding: NO_COMM plans of rank r/world own contiguous unit ranges; their partial
+    forwards sum to the full forward and their backwards cover disjoint units (world 2, 3, 4)."""
+    L_ = L()
+    h, x, r = rand_case(11, 4, 3, 27, 27, 9, 9)
+    hd = h.astype(np.float64)
+    y_ref = O.forward_project(x.astype(np.float64), hd)
+    xb_ref = O.backward_project(r.astype(np.float64), hd)
+    for world in (2, 3, 4):
+        tot = np.zeros_like(y_ref)
+        cover = np.zeros((4, 27, 27))
+        xb_acc = np.zeros_like(xb_ref)
+        for rank in range(world):
+            with L_.Plan(h, 3, 27, 27, optics=optics(3), rank=rank, world=world, flags=L_.LFM_PLAN_NO_COMM) as plan:
+                info = plan.info()
+                y_d = torch.zeros((27, 27), device="cuda")
+                plan.forward(dev(x), y_d)
+                xb_d = torch.full((4, 27, 27), -1.0, device="cuda")
+                plan.backward(dev(r), xb_d)
+                torch.cuda.synchronize()
+                tot += y_d.cpu().numpy()
+                xb = xb_d.cpu().numpy()
+                own = xb != -1.0
+                cover += own
+                xb_acc[own] = xb[own]
+                nu = 4 * 9
+                assert info["unit_begin"] == rank * (nu // world) + min(rank, nu % world)
+        assert rel(tot, y_ref) <= 2e-6
+        assert (cover == 1).all()
+        assert rel(xb_acc, xb_ref) <= 2e-6
+
+
+def test_error_statuses():
+    L_ = L()
+    h, x, r = rand_case(1, 2, 3, 9, 9, 3, 3)
+    with pytest.raises(L_.LfmError) as e:
+        L_.Plan(h, 3, 10, 9)
+    assert e.value.status == L_.LFM_EDIM
+    hn = h.copy()
+    hn[0, 0, 0, 0, 0] = -1
+    with pytest.raises(L_.LfmError) as e:
+        L_.Plan(hn, 3, 9, 9)
+    assert e.value.status == L_.LFM_ENEG
+    with L_.Plan(h, 3, 9, 9, optics=optics(3)) as plan:
+        x_d = torch.zeros((2, 9, 9), device="cuda")
+        with pytest.raises(L_.LfmError) as e:
+            plan.rl_iterate(torch.zeros((9, 9), device="cuda"), x_d, L_.make_policy())
+        assert e.value.status == L_.LFM_EZERO
+        yneg = torch.ones((9, 9), device="cuda")
+        yneg[1, 1] = -2
+        with pytest.raises(L_.LfmError) as e:
+            plan.rl_iterate(yneg, x_d, L_.make_policy())
+        assert e.value.status == L_.LFM_ENEG
+        with pytest.raises(L_.LfmError) as e:
+            plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(min_iters=9, max_iters=3))
+        assert e.value.status == L_.LFM_EINVAL
+        with pytest.raises(L_.LfmError) as e:
+            plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(update="isra"))
+        assert e.value.status == L_.LFM_EUNSUPPORTED
