@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- RL iterations/s of the B200 light-field Richardson-Lucy hot path (AutoDeconJ, arXiv 2208.11422).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...      (depth/phase sharding over NCCL)
+
+A step is one RL iteration = every row of SURVEY §8(a) a2..a9 (forward projection, ratio, backward
+projection, multiplicative update, z max-projection, fp64 DCT entropy, stop-rule bookkeeping with the
+argmax snapshot), on the BASELINE config the metric is quoted on (c3: Nnum=15, 1005x1005, 51 planes).
+Timing: W untimed iterations, then exactly K iterations inside one lfm_rl_iterate call, bracketed by
+barrier + cudaDeviceSynchronize, measured with CUDA events on the launching stream, max over ranks.
+The dominant kernel's duration comes from the library's per-stage CUDA events over the same timed region.
+Inputs are larger than L2: every projection streams the 58.9 GB transfer matrices (L2 = 126 MB).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from lfm_inputs import CONFIGS, OPTICS, gen_psf, gen_volume, lf_like, plane_support, poisson  # noqa: E402
+
+METRIC = "RL iterations/s (Nnum=15 LFM, 1/2/4/8 B200) and % of HBM roofline"
+UNIT = "iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-calls", type=int, default=1)
+    ap.add_argument("--cpu-rows", type=int, default=96, help="rows of the oracle's bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flags", type=int, default=0, help="lfm_plan_create flags (2 = direct path)")
+    return ap.parse_args()
+
+
+def workload_desc(cfg):
+    ks = sorted({plane_support(cfg, z) for z in range(cfg.nz)})
+    return (f"{cfg.name}: Nnum={cfg.nnum}, {cfg.height}x{cfg.width} image, {cfg.nz} depth planes, "
+            f"Gaussian-parallax PSF K_max={cfg.k_max} (per-plane support {ks[0]}..{ks[-1]}), "
+            f"{cfg.phantom} phantom + Poisson noise, auto-stop policy (max 50)")
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks line")
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" == r[4 + i]})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the oracle, as it stands, on a bounded sample of the same workload
+# ------------------------------------------------------------------------------------------------
+def oracle_iteration_seconds(cfg, h64, x64, y64, rows):
+    """Times the oracle's forward projection on `rows` output rows and its backward projection on the
+    same rows of every plane (the two terms of one RL iteration), plus the full-size elementwise RL
+    update and metric, and extrapolates to one full iteration."""
+    from oracle import lfm_oracle as O
+    H = cfg.height
+    r0 = max(0, H // 2 - rows // 2)
+    r1 = min(H, r0 + rows)
+    t0 = time.perf_counter()
+    O.forward_project(x64, h64, rows=(r0, r1))
+    t_fwd = time.perf_counter() - t0
+    r = np.ones((cfg.height, cfg.width))
+    nz = cfg.nz
+    t_bwd = 0.0
+    import ctypes
+    lib = O._load()
+    out = np.zeros((nz, cfg.height, cfg.width))
+    kh = h64.shape[3]
+    for z in range(nz):
+        t0 = time.perf_counter()
+        lib.lfmo_backward(O._dp(r), O._dp(h64), nz, cfg.nnum, kh, kh, cfg.height, cfg.width, 0, nz * cfg.nnum ** 2,
+                          ctypes.c_long(z * H + r0), ctypes.c_long(z * H + r1), O._dp(out))
+        t_bwd += time.perf_counter() - t0
+    t0 = time.perf_counter()
+    xs = x64 * 1.0001 / np.maximum(x64, 1e-6)          # full-size elementwise update cost (same shapes)
+    reg = O.cutoff_region(O.Optics(nnum=cfg.nnum, **OPTICS), cfg.height, cfg.width)
+    O.evaluate_iteration(xs, reg)
+    O.ratio_image(y64, y64)
+    t_el = time.perf_counter() - t0
+    scale = H / (r1 - r0)
+    return (t_fwd + t_bwd) * scale + t_el, dict(t_fwd=t_fwd, t_bwd=t_bwd, t_elementwise=t_el, rows=r1 - r0)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the fp64 oracle (this tier's reference arm), each step a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import lfm_oracle as O
+    cfg = CONFIGS[args.config]
+    h64 = gen_psf(cfg, np.float32).astype(np.float64)
+    x64 = gen_volume(cfg, 1, np.float64)
+    y64 = lf_like(cfg, 7)
+    O.build()
+    rows = max(2, min(cfg.height, 12 if cfg.height > 500 else cfg.height))
+    for _ in range(args.warmup):
+        oracle_iteration_seconds(cfg, h64, x64, y64, rows)
+    ts = [oracle_iteration_seconds(cfg, h64, x64, y64, rows)[0] for _ in range(args.steps)]
+    sec = float(np.mean(ts))
+    value = 1.0 / sec
+    sample = (f"per step: oracle forward on {rows} of {cfg.height} output rows + backward on the same rows of all "
+              f"{cfg.nz} planes + full-size update/metric, extrapolated to one iteration")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2208_11422_b200 import lfm as L
+
+    cfg = CONFIGS[args.config]
+    t_setup = time.perf_counter()
+    h = gen_psf(cfg, np.float32)
+    xt = gen_volume(cfg, 1, np.float32)
+    nccl_id = None
+    if world > 1:
+        obj = [L.lfm_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), rank=rank, world=world,
+                  nccl_id=nccl_id, flags=args.flags)
+    info = plan.info()
+    del h
+    H, W, nz = cfg.height, cfg.width, cfg.nz
+    # measurement y = Poisson(H x_true) using the product's own forward projection
+    xt_d = torch.from_numpy(xt).cuda()
+    yh_d = torch.zeros((H, W), device="cuda")
+    plan.forward(xt_d, yh_d)
+    torch.cuda.synchronize()
+    y = poisson(np.maximum(yh_d.cpu().numpy().astype(np.float64), 0.0), 101).astype(np.float32)
+    del xt_d
+    y_d = torch.from_numpy(y).cuda()
+    x_d = torch.zeros((nz, H, W), device="cuda")
+    setup_s = time.perf_counter() - t_setup
+
+    # warm-up
+    plan.rl_iterate(y_d, x_d, L.make_policy(mode="fixed", n_iters=args.warmup))
+    torch.cuda.synchronize()
+
+    # timed region: exactly K iterations
+    plan.profile(True)
+    plan.profile_read(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    res = plan.rl_iterate(y_d, x_d, L.make_policy(mode="fixed", n_iters=args.steps, init_from_x=True))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    prof = plan.profile_read(reset=True)
+    plan.profile(False)
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (algorithmic bytes at the minimal alias-free transform size)
+    N2 = cfg.nnum ** 2
+    nu = info["unit_end"] - info["unit_begin"]
+    kap_min = info["lc_min_h"] * (info["lc_min_w"] // 2 + 1)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak = json.load(open(peaks_path))["hbm_gbs"]
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    stage_ms = {k: prof["ms"][k] / max(1, prof["count"][k]) for k in prof["ms"]}
+    alg = {
+        "fwd_mac": kap_min * N2 * nu * 8 + kap_min * nu * 8 + kap_min * N2 * 8,   # M + G + Y
+        "bwd_mac": kap_min * N2 * nu * 8 + kap_min * N2 * 8 + kap_min * nu * 8,   # M + R + Xh
+    }
+    if info["direct"]:
+        dom = max(("fwd_mac", "bwd_mac", "c2r_update"), key=lambda k: stage_ms[k])
+        roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
+                "traffic": None}
+    else:
+        dom = max(("fwd_mac", "bwd_mac"), key=lambda k: stage_ms[k])
+        achieved = alg[dom] / (stage_ms[dom] / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            traffic = tj.get(cfg.name, {}).get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": stage_ms[dom],
+                "both": {k: {"avg_ms": stage_ms[k], "achieved_gbs": alg[k] / (stage_ms[k] / 1e3) / 1e9,
+                             "frac": alg[k] / (stage_ms[k] / 1e3) / 1e9 / peak} for k in alg}}
+    share = {k: prof["ms"][k] / max(1e-9, sum(prof["ms"].values())) for k in prof["ms"]}
+
+    # e2e: the public host-buffer call, auto-stop deconvolution of the same measurement
+    y_host = torch.from_numpy(y).pin_memory()
+    x_host = torch.zeros((nz, H, W), dtype=torch.float32).pin_memory()
+    e2e_iters, e2e_s, auto = 0, 0.0, None
+    for _ in range(max(1, args.e2e_calls)):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = plan.deconvolve_host(y_host.numpy(), x_host.numpy(), L.make_policy(mode="auto", max_iters=50))
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        if dist:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s += float(tt.item())
+        e2e_iters += r["stop_iter"]
+        auto = r
+    s = auto["series"]
+    k = auto["stop_iter"]
+    margin = min(abs(s[i] - s[i - 1]) / abs(s[i]) for i in range(1, k)) if k > 1 else None
+    calls = max(1, args.e2e_calls)
+    e2e = {"value": e2e_iters / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(H * W * 4 * calls / e2e_iters),
+           "d2h_bytes_per_step": int((nz * H * W * 4 + 8) * calls / e2e_iters),
+           "step": "one RL iteration of an auto-stop lfm_deconvolve_host call (host y in, host argmax volume out); "
+                   f"{calls} call(s), {e2e_iters} iterations"}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            h64 = gen_psf(cfg, np.float32).astype(np.float64)
+            sec, det = oracle_iteration_seconds(cfg, h64, xt.astype(np.float64), y.astype(np.float64), args.cpu_rows)
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                   "sample": (f"oracle (fp64 direct conv, OpenMP) forward on {det['rows']} of {H} rows + backward on the "
+                              f"same rows of all {nz} planes + full-size update/metric, extrapolated to one iteration "
+                              f"({det['t_fwd'] + det['t_bwd'] + det['t_elementwise']:.1f} s measured)")}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": workload_desc(cfg),
+                "parallelism": f"depth/phase (z,a)-unit sharding over {world} GPU(s), NCCL allreduce sum+max per iteration"
+                if world > 1 else "single GPU",
+                "transform": f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})"
+                if not info["direct"] else "direct spatial",
+                "transfer_matrix_gb_per_gpu": info["transfer_bytes"] / 1e9,
+                "l2": "inputs larger than L2: each projection streams the transfer matrices (L2 126 MB)",
+                "plan_ms": info["plan_ms"], "setup_s": setup_s,
+                "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"],
+                              "decision_margin": margin, "series": s},
+                "stage_share": share, "stage_avg_ms": stage_ms,
+            },
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": prof["launches"],
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    plan.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

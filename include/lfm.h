@@ -197,6 +197,26 @@ lfm_status lfm_quality(lfm_plan plan, const float* x, int region, double* entrop
 lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, const lfm_optics* optics,
                            int region, double* entropy, int* x_s, int* y_s, void* stream);
 
+/* ---- live per-stage timing (CUDA events on the plan's calls' stream) ----
+ * Stages of one iteration: 0 r2c_x (a2), 1 fwd_mac (a3), 2 c2r_yhat (a4), 3 allreduce_sum (C1),
+ * 4 r2c_ratio (a5), 5 bwd_mac (a6), 6 c2r_update (a7), 7 allreduce_max (C2), 8 metric (a8).
+ * When enabled, lfm_rl_iterate records an event before each stage and after the last one and adds the
+ * elapsed times after its per-iteration synchronisation.  `launches` counts this library's kernels. */
+#define LFM_N_STAGES 9
+typedef struct {
+    double ms[LFM_N_STAGES];          /* summed device milliseconds per stage   */
+    long long count[LFM_N_STAGES];    /* number of timed executions per stage   */
+    long long launches;               /* kernels launched by the library so far */
+    long long iterations;             /* RL iterations executed so far          */
+} lfm_profile_t;
+
+/* enable != 0 turns per-stage event timing on.  Counters keep accumulating until read with reset. */
+lfm_status lfm_profile(lfm_plan plan, int enable);
+/* Copies the counters into *out (host); reset != 0 zeroes them afterwards. */
+lfm_status lfm_profile_read(lfm_plan plan, lfm_profile_t* out, int reset);
+/* Name of stage i (static string), or NULL. */
+const char* lfm_profile_stage_name(int i);
+
 #ifdef __cplusplus
 }
 #endif

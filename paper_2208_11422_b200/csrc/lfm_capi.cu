@@ -229,6 +229,9 @@ struct lfm_plan_s {
     double* host = nullptr;     // pinned 8 doubles
     float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool prof = false;
+    cudaEvent_t pev[LFM_N_STAGES + 1] = {};
+    lfm_profile_t pacc{};
     bool has_optics = false;
     lfm_optics optics{};
     Region region;
@@ -240,6 +243,16 @@ struct lfm_plan_s {
 namespace {
 
 constexpr int kParts = 296;
+
+const char* kStageNames[LFM_N_STAGES] = {"r2c_x", "fwd_mac", "c2r_yhat", "allreduce_sum", "r2c_ratio",
+                                         "bwd_mac", "c2r_update", "allreduce_max", "metric"};
+
+// records the start event of `stage` (stage == LFM_N_STAGES: end of the last stage) when profiling
+inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
+    if (!p->prof) return LFM_OK;
+    CK(cudaEventRecord(p->pev[stage], s));
+    return LFM_OK;
+}
 
 void plan_free(lfm_plan p) {
     if (!p) return;
@@ -266,6 +279,8 @@ void plan_free(lfm_plan p) {
     if (p->host) cudaFreeHost(p->host);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    for (auto& e : p->pev)
+        if (e) cudaEventDestroy(e);
     metric_free(&p->met);
     delete p;
 }
@@ -319,11 +334,17 @@ lfm_status allreduce(lfm_plan p, void* buf, size_t n, ncclDataType_t t, ncclRedO
 // yhat = H x (x polyphase, owned units) summed over ranks
 lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
+    ST(mark(p, 0, s));
     if (p->direct) {
+        ST(mark(p, 1, s));
         CK(launch_direct_fwd(xp, p->psf, yimg, p->xg, s));
+        p->pacc.launches += 1;
+        ST(mark(p, 2, s));
     } else {
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(SRC_POLY, xp, nullptr, 0.f, p->nu, p->G, p->nu_pad), s));
+        ST(mark(p, 1, s));
         CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_pad, p->num_sms, s));
+        ST(mark(p, 2, s));
         C2RArgs c{};
         c.dst = DST_IMAGE;
         c.in = p->Y;
@@ -331,7 +352,9 @@ lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_
         c.ntrans = N2;
         c.out = yimg;
         CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+        p->pacc.launches += 3;
     }
+    ST(mark(p, 3, s));
     return allreduce(p, yimg, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
 }
 
@@ -340,21 +363,31 @@ lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_
 lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2, float eps, int dst, float* out,
                        const float* xold, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
+    ST(mark(p, 4, s));
     if (p->direct) {
         const size_t n = (size_t)p->geo.H * p->geo.W;
         const float* r = img;
         if (src == SRC_RATIO) {
             CK(launch_ratio(img, img2, p->rimg, n, eps, s));
             r = p->rimg;
+            p->pacc.launches += 1;
         } else if (src == SRC_ONES) {
             CK(launch_fill(p->rimg, n, 1.0f, s));
             r = p->rimg;
+            p->pacc.launches += 1;
         }
+        ST(mark(p, 5, s));
+        ST(mark(p, 6, s));
         CK(launch_direct_bwd(r, p->psf, out, dst, xold, p->norm, p->mproj, eps, p->xg, s));
+        p->pacc.launches += 1;
+        ST(mark(p, 7, s));
         return LFM_OK;
     }
     CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
+    ST(mark(p, 5, s));
     CK(launch_bwd_mac(p->M, p->R, p->Xh, p->geo.nkappa, N2, p->nu_pad, s));
+    ST(mark(p, 6, s));
+    p->pacc.launches += 3;
     C2RArgs c{};
     c.dst = dst;
     c.in = p->Xh;
@@ -366,6 +399,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     c.mproj = p->mproj;
     c.eps = eps;
     CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+    ST(mark(p, 7, s));
     return LFM_OK;
 }
 
@@ -373,16 +407,19 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
     if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the DCT-entropy metric needs them");
     const int ri = region == LFM_REGION_RECTANGLE ? 1 : 0;
     ST(allreduce(p, p->mproj, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclMax, s));
+    ST(mark(p, 8, s));
     CK(launch_metric(p->mproj, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
                      p->met.nmem[ri], p->met.T1, p->met.rowsq, p->met.out, s));
+    p->pacc.launches += 2;
+    ST(mark(p, LFM_N_STAGES, s));
     return LFM_OK;
 }
 
 // one RL iteration on polyphase volumes: xn = xc * H^T(y/(max(H xc,0)+eps)) / max(norm,eps); metric -> met.out[0]
 lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float eps, int region, bool metric,
                    cudaStream_t s) {
-    ST(op_forward_poly(p, xc, p->yhat, s));
     CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
+    ST(op_forward_poly(p, xc, p->yhat, s));
     ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
     if (metric) ST(op_metric(p, region, s));
     return LFM_OK;
@@ -761,6 +798,15 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         CK(cudaStreamSynchronize(s));
         const double e = p->host[0];
         series_host[k - 1] = e;
+        p->pacc.iterations += 1;
+        if (p->prof) {
+            for (int st = 0; st < LFM_N_STAGES; ++st) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, p->pev[st], p->pev[st + 1]));
+                p->pacc.ms[st] += ms;
+                p->pacc.count[st] += 1;
+            }
+        }
         if (ms_host) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
@@ -853,5 +899,23 @@ lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, co
     if (y_s) *y_s = r.ys;
     return LFM_OK;
 }
+
+lfm_status lfm_profile(lfm_plan p, int enable) {
+    if (!p) return fail(LFM_EINVAL, "plan is NULL");
+    if (enable && !p->pev[0])
+        for (auto& e : p->pev) CK(cudaEventCreate(&e));
+    if (enable && !p->has_optics) return fail(LFM_EINVAL, "profiling times lfm_rl_iterate, which needs optics");
+    p->prof = enable != 0;
+    return LFM_OK;
+}
+
+lfm_status lfm_profile_read(lfm_plan p, lfm_profile_t* out, int reset) {
+    if (!p || !out) return fail(LFM_EINVAL, "NULL argument");
+    *out = p->pacc;
+    if (reset) p->pacc = lfm_profile_t{};
+    return LFM_OK;
+}
+
+const char* lfm_profile_stage_name(int i) { return (i >= 0 && i < LFM_N_STAGES) ? kStageNames[i] : nullptr; }
 
 }  // extern "C"

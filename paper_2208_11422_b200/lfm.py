@@ -98,9 +98,23 @@ _lib_deconvolve_host = _sig("lfm_deconvolve_host", _i, [_P, _P, _P, ctypes.POINT
 _lib_quality = _sig("lfm_quality", _i, [_P, _P, _i, _D, _P])
 _lib_dct_entropy = _sig("lfm_dct_entropy", _i, [_P, _i, _i, _i, ctypes.POINTER(lfm_optics), _i, _D, _I, _I, _P])
 
+LFM_N_STAGES = 9
+
+
+class lfm_profile_t(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * LFM_N_STAGES), ("count", ctypes.c_longlong * LFM_N_STAGES),
+                ("launches", ctypes.c_longlong), ("iterations", ctypes.c_longlong)]
+
+
+_lib_profile = _sig("lfm_profile", _i, [_P, _i])
+_lib_profile_read = _sig("lfm_profile_read", _i, [_P, ctypes.POINTER(lfm_profile_t), _i])
+_lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
+STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
+
 EXPORTED = ["lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
             "lfm_plan_create", "lfm_plan_info", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
-            "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy"]
+            "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
+            "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name"]
 
 
 def _check(st):
@@ -277,6 +291,17 @@ class Plan:
         if want_ms:
             out["ms"] = list(ms[:stop.value])
         return out
+
+    def profile(self, enable=True):
+        _check(_lib_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self, reset=False):
+        """Per-stage summed device ms / counts, kernel launches and iterations since the last reset."""
+        pr = lfm_profile_t()
+        _check(_lib_profile_read(self._h, ctypes.byref(pr), 1 if reset else 0))
+        return dict(ms={STAGE_NAMES[i]: pr.ms[i] for i in range(LFM_N_STAGES)},
+                    count={STAGE_NAMES[i]: pr.count[i] for i in range(LFM_N_STAGES)},
+                    launches=pr.launches, iterations=pr.iterations)
 
     def quality(self, x, region=LFM_REGION_TRIANGLE, stream=None):
         _check_dev(x, (self.nz, self.height, self.width), "x")
