@@ -128,6 +128,11 @@ const char* lfm_version(void);
 /* Writes a fresh ncclUniqueId (128 bytes) into id_out (host).  Call on rank 0 only. */
 lfm_status lfm_comm_unique_id(unsigned char* id_out);
 
+/* Host-only: the contiguous unit range [*unit_begin, *unit_end) that `rank` of `world` owns among the
+ * nz*N*N units (z-major u = z*N*N + a*N + b); the first (nu mod world) ranks own one extra unit
+ * (S:334's even split, refined from planes to (z,a) units). */
+lfm_status lfm_shard_units(int nz, int nnum, int world, int rank, int* unit_begin, int* unit_end);
+
 /* Memory estimate before allocation (Fig. 1 "estimate the required memory size").
  * Writes the bytes one rank needs into *bytes_per_gpu (host).  If budget_bytes > 0 and the estimate
  * exceeds it, returns LFM_ENOMEM and writes the name of the largest term into limiting_term

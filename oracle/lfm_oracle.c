@@ -101,7 +101,9 @@ int lfmo_backward(const double* r, const double* h, int nz, int N, int kh, int k
     if (H % N || W % N) return 2;
     const int ch = (kh - 1) / 2, cw = (kw - 1) / 2;
     int* sup = (int*)malloc(sizeof(int) * 4 * (size_t)nz);
-    for (int z = 0; z < nz; ++z) plane_support(h, z, N, kh, kw, sup + 4 * z, sup + 4 * z + 1, sup + 4 * z + 2, sup + 4 * z + 3);
+    const int zlo = zp1 > zp0 ? (int)(zp0 / H) : 0, zhi = zp1 > zp0 ? (int)((zp1 - 1) / H) : -1;
+    for (int z = zlo; z <= zhi; ++z)    /* only the planes this call visits */
+        plane_support(h, z, N, kh, kw, sup + 4 * z, sup + 4 * z + 1, sup + 4 * z + 2, sup + 4 * z + 3);
     #pragma omp parallel for schedule(dynamic, 1)
     for (long zp = zp0; zp < zp1; ++zp) {
         const int z = (int)(zp / H), p = (int)(zp % H);

@@ -506,6 +506,15 @@ lfm_status lfm_comm_unique_id(unsigned char* id_out) {
     return LFM_OK;
 }
 
+lfm_status lfm_shard_units(int nz, int nnum, int world, int rank, int* unit_begin, int* unit_end) {
+    g_err[0] = 0;
+    if (!unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");
+    if (nz < 1 || nnum < 1 || world < 1 || rank < 0 || rank >= world)
+        return fail(LFM_EINVAL, "nz=%d nnum=%d world=%d rank=%d", nz, nnum, world, rank);
+    unit_range(nz * nnum * nnum, world, rank, unit_begin, unit_end);
+    return LFM_OK;
+}
+
 lfm_status lfm_plan_estimate(int nnum, int nz, int kh, int kw, int height, int width, int world, int flags,
                              size_t budget_bytes, size_t* bytes_per_gpu, char* limiting_term, size_t len) {
     g_err[0] = 0;

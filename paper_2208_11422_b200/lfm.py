@@ -82,6 +82,7 @@ def _sig(name, res, args):
 _lib_policy_default = _sig("lfm_policy_default", lfm_policy, [])
 _lib_last_error = _sig("lfm_last_error", ctypes.c_char_p, [])
 _lib_version = _sig("lfm_version", ctypes.c_char_p, [])
+_lib_shard_units = _sig("lfm_shard_units", _i, [_i, _i, _i, _i, _I, _I])
 _lib_unique_id = _sig("lfm_comm_unique_id", _i, [ctypes.POINTER(ctypes.c_ubyte)])
 _lib_estimate = _sig("lfm_plan_estimate", _i, [_i, _i, _i, _i, _i, _i, _i, _i, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t])
@@ -111,7 +112,7 @@ _lib_profile_read = _sig("lfm_profile_read", _i, [_P, ctypes.POINTER(lfm_profile
 _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
-EXPORTED = ["lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
+EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
             "lfm_plan_create", "lfm_plan_info", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name"]
@@ -186,6 +187,12 @@ def lfm_comm_unique_id():
     buf = (ctypes.c_ubyte * 128)()
     _check(_lib_unique_id(buf))
     return bytes(buf)
+
+
+def lfm_shard_units(nz, nnum, world, rank):
+    b, e = ctypes.c_int(0), ctypes.c_int(0)
+    _check(_lib_shard_units(nz, nnum, world, rank, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
 
 
 def lfm_plan_estimate(nnum, nz, kh, kw, height, width, world=1, flags=0, budget_bytes=0):
