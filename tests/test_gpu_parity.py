@@ -278,3 +278,98 @@ def test_error_statuses():
         with pytest.raises(L_.LfmError) as e:
             plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(update="isra"))
         assert e.value.status == L_.LFM_EUNSUPPORTED
+
+
+def test_host_buffer_call_and_quality():
+    """lfm_deconvolve_host (the e2e call) equals lfm_rl_iterate; lfm_quality equals the oracle's E."""
+    cfg, h, hd, y = tiny_problem(seed=4)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        pol = L().make_policy(mode="auto", max_iters=30)
+        x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        r1 = plan.rl_iterate(dev(y), x_d, pol)
+        xh = np.zeros((cfg.nz, cfg.height, cfg.width), np.float32)
+        r2 = plan.deconvolve_host(np.ascontiguousarray(y, np.float32), xh, pol)
+        assert (r1["stop_iter"], r1["best_iter"]) == (r2["stop_iter"], r2["best_iter"])
+        assert np.array_equal(xh, x_d.cpu().numpy())
+        e = plan.quality(x_d)
+    reg = O.cutoff_region(O.Optics(nnum=cfg.nnum, **OPTICS), cfg.height, cfg.width)
+    assert e == pytest.approx(O.evaluate_iteration(x_d.cpu().numpy().astype(np.float64), reg), rel=1e-10)
+    assert e == pytest.approx(r1["series"][r1["best_iter"] - 1], rel=1e-6)
+
+
+def _nonzero_rows(h, z):
+    nzr = np.nonzero(h[z].reshape(-1, h.shape[3], h.shape[4]).any(axis=(0, 2)))[0]
+    return int(nzr.min()), int(nzr.max())
+
+
+@pytest.fixture(scope="module")
+def c3_plan():
+    """The c3 workload in the launch configuration bench.py times (frequency path, 75x75, 1 GPU)."""
+    cfg = CONFIGS["c3"]
+    h = gen_psf(cfg, np.float32)
+    plan = L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum))
+    yield cfg, h, plan
+    plan.close()
+
+
+def test_c3_forward_backward_sampled(c3_plan):
+    """Full-size c3: forward at 64 sampled pixels and backward at 64 sampled voxels (corners, borders, interior,
+    all planes) against the oracle's one-output evaluators; |err| <= 1e-5 max|ref|."""
+    cfg, h, plan = c3_plan
+    hd = h.astype(np.float64)
+    rng = np.random.default_rng(0)
+    x = gen_volume(cfg, 2, np.float32)
+    y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+    plan.forward(dev(x), y_d)
+    torch.cuda.synchronize()
+    yg = y_d.cpu().numpy()
+    H, W = cfg.height, cfg.width
+    s = np.concatenate([[0, 0, H - 1, H - 1, 7, H // 2], rng.integers(0, H, 58)])
+    t = np.concatenate([[0, W - 1, 0, W - 1, W // 2, 3], rng.integers(0, W, 58)])
+    ref = O.forward_points(x.astype(np.float64), hd, s, t)
+    assert np.abs(yg[s, t] - ref).max() <= 1e-5 * np.abs(yg).max()
+    r = (lf_like(cfg, 3) + 1.0).astype(np.float32)
+    r /= r.mean()
+    xb_d = torch.zeros((cfg.nz, H, W), device="cuda")
+    plan.backward(dev(r), xb_d)
+    torch.cuda.synchronize()
+    z = np.concatenate([[0, cfg.nz - 1, cfg.nz // 2, 10], rng.integers(0, cfg.nz, 60)])
+    p = np.concatenate([[0, H - 1, 500, 14], rng.integers(0, H, 60)])
+    q = np.concatenate([[0, W - 1, 501, 1004], rng.integers(0, W, 60)])
+    refb = O.backward_points(r.astype(np.float64), hd, z, p, q)
+    got = xb_d[torch.from_numpy(z).cuda(), torch.from_numpy(p).cuda(), torch.from_numpy(q).cuda()].cpu().numpy()
+    assert np.abs(got - refb).max() <= 1e-5 * np.abs(refb).max()
+
+
+def test_c3_one_rl_step_sampled(c3_plan):
+    """Full-size c3, one RL step from a random positive x0 (init_from_x): x1 at 12 sampled voxels of the
+    near-focus planes computed by the oracle from its own forward / backward evaluators; 1e-5 relative."""
+    cfg, h, plan = c3_plan
+    hd = h.astype(np.float64)
+    H, W = cfg.height, cfg.width
+    rng = np.random.default_rng(5)
+    y = lf_like(cfg, 9).astype(np.float32)
+    x0 = (rng.uniform(0.5, 1.5, (cfg.nz, H, W)) * (y.mean() / cfg.nz)).astype(np.float32)
+    x1_d = torch.zeros((cfg.nz, H, W), device="cuda")
+    e = plan.rl_step(dev(y), dev(x0), x1_d)
+    torch.cuda.synchronize()
+    x1 = x1_d.cpu().numpy()
+    x0d = x0.astype(np.float64)
+    yd = y.astype(np.float64)
+    ch = cfg.k_max // 2
+    ones = np.ones((H, W))
+    for z in (25, 24, 26, 21):
+        i0, i1 = _nonzero_rows(hd, z)
+        for _ in range(3):
+            p, q = int(rng.integers(0, H)), int(rng.integers(0, W))
+            ss = [p + i - ch for i in range(i0, i1 + 1) if 0 <= p + i - ch < H]
+            tt = [q + j - ch for j in range(i0, i1 + 1) if 0 <= q + j - ch < W]
+            S, T = np.meshgrid(ss, tt, indexing="ij")
+            yhat = O.forward_points(x0d, hd, S.ravel(), T.ravel())
+            rimg = np.zeros((H, W))
+            rimg[S.ravel(), T.ravel()] = yd[S.ravel(), T.ravel()] / (np.maximum(yhat, 0) + O.EPS)
+            bp = O.backward_points(rimg, hd, [z], [p], [q])[0]
+            nrm = O.backward_points(ones, hd, [z], [p], [q])[0]
+            ref = x0d[z, p, q] * bp / max(nrm, O.EPS)
+            assert abs(x1[z, p, q] - ref) <= 1e-5 * abs(ref), (z, p, q, x1[z, p, q], ref)
+    assert e > 0
