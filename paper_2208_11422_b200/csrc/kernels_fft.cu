@@ -247,9 +247,13 @@ static cudaError_t set_smem(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+static bool g_fast = true;
+void set_fast_fft_enabled(bool on) { g_fast = on; }
+
 cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
                        const float2* tw_w, const R2CArgs& a, cudaStream_t s) {
     if (a.ntrans <= 0) return cudaSuccess;
+    if (g_fast && fast_fft_size(g.Lh, g.Lw)) return launch_r2c_fast(g, tw_h, a, s);
     const int S = xform_S(g);
     size_t smem;
     const int UB = xform_UB(g, S, &smem);
@@ -278,6 +282,7 @@ cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw,
 cudaError_t launch_c2r(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
                        const float2* tw_w, const C2RArgs& a, cudaStream_t s) {
     if (a.ntrans <= 0) return cudaSuccess;
+    if (g_fast && fast_fft_size(g.Lh, g.Lw)) return launch_c2r_fast(g, tw_h, a, s);
     const int S = xform_S(g);
     size_t smem;
     const int UB = xform_UB(g, S, &smem);

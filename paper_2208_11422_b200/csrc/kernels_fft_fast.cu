@@ -1,0 +1,405 @@
+// kernels_fft_fast.cu -- compile-time-specialised coarse transforms for the square sizes the BASELINE
+// configs use (Lc = 15, 16, 36, 75, 144).  Same mathematics as kernels_fft.cu (K2/K4/K5/K7),
+// re-organised for throughput:
+//   * one warp owns one 1-D transform; radix stages run in place with __syncwarp only (every lane loads
+//     its butterflies' inputs into registers, syncs, writes outputs), so warps never wait on each other
+//     between stages and all index arithmetic is compile-time (no runtime integer division);
+//   * one shared buffer per image: rows of odd stride RHO (>= Lw/2+1, conflict-light column access) and
+//     packed row pairs at stride 2*RHO, so the real-row packing / Hermitian split is done in place by the
+//     warp that transformed the row (no transpose buffer, half the shared memory of the generic path);
+//   * the C2R fuses rebuild-row -> inverse row FFT -> crop/scale -> epilogue per warp.
+#include "fft_smem.cuh"
+
+#ifndef LFM_FFT_MINB
+#define LFM_FFT_MINB 2   // resident CTAs per SM the register budget targets
+#endif
+
+namespace lfm {
+
+struct Radices {
+    int n;
+    int r[12];
+};
+
+constexpr Radices factorize(int L) {
+    Radices f{0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
+    int x = L;
+    const int order[4] = {4, 2, 3, 5};
+    for (int i = 0; i < 4; ++i)
+        while (x % order[i] == 0) {
+            f.r[f.n++] = order[i];
+            x /= order[i];
+        }
+    return f;
+}
+
+template <int L, int R, int NS, bool INV>
+__device__ __forceinline__ void warp_stage(float2* base, int stride, const float2* __restrict__ tw, int lane) {
+    constexpr int LR = L / R;
+    constexpr int NB = (LR + 31) / 32;
+    constexpr int TWS = L / (NS * R);
+    float2 v[NB][R];
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+        const int j = lane + 32 * t;
+        if (j < LR) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[t][q] = base[(j + q * LR) * stride];
+            if constexpr (NS > 1) {
+                const int k = j % NS;
+#pragma unroll
+                for (int q = 1; q < R; ++q) {
+                    float2 w = tw[q * k * TWS];
+                    if (INV) w.y = -w.y;
+                    v[t][q] = c_mul(v[t][q], w);
+                }
+            }
+            small_dft<R, INV>(v[t]);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+        const int j = lane + 32 * t;
+        if (j < LR) {
+            const int k = j % NS;
+            const int o = (j - k) * R + k;
+#pragma unroll
+            for (int q = 0; q < R; ++q) base[(o + q * NS) * stride] = v[t][q];
+        }
+    }
+    __syncwarp();
+}
+
+template <int L, int S, int NS, bool INV>
+__device__ __forceinline__ void warp_fft(float2* base, int stride, const float2* __restrict__ tw, int lane) {
+    constexpr Radices F = factorize(L);
+    if constexpr (S < F.n) {
+        constexpr int R = F.r[S];
+        warp_stage<L, R, NS, INV>(base, stride, tw, lane);
+        warp_fft<L, S + 1, NS * R, INV>(base, stride, tw, lane);
+    }
+}
+
+template <int L>
+struct FastGeom {
+    static constexpr int NK2 = L / 2 + 1;
+    static constexpr int RHO = (NK2 % 2) ? NK2 : NK2 + 1;   // odd row stride, 2*RHO >= L
+    static constexpr int S = (L + 1) * RHO;                 // complex per image (packed rows of an odd L fit)
+    static constexpr int NBL = (L + 31) / 32;
+};
+
+template <int SRC>
+__device__ __forceinline__ float src_value(const XformGeom& g, const R2CArgs& a, int t, int i, int j) {
+    if constexpr (SRC == SRC_POLY) {
+        return a.in[((size_t)t * g.nh + i) * g.nw + j];
+    } else if constexpr (SRC == SRC_IMAGE) {
+        const int u = g.unit0 + t;
+        const int N2 = g.N * g.N;
+        const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+        return a.in[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j];
+    } else if constexpr (SRC == SRC_RATIO) {
+        const int b1 = t / g.N, b2 = t % g.N;
+        const size_t pix = (size_t)(b1 + g.N * i) * g.W + b2 + g.N * j;
+        return a.in[pix] / (fmaxf(a.in2[pix], 0.0f) + a.eps);
+    } else if constexpr (SRC == SRC_ONES) {
+        return 1.0f;
+    } else if constexpr (SRC == SRC_IMAGE2D) {
+        const int b1 = t / g.N, b2 = t % g.N;
+        return a.in[(size_t)(b1 + g.N * i) * g.W + b2 + g.N * j];
+    } else {
+        const int bp = t / g.nu, uu = t - bp * g.nu;
+        const int b1 = bp / g.N, b2 = bp % g.N;
+        const int u = g.unit0 + uu;
+        const int a1 = (u / g.N) % g.N, a2 = u % g.N;
+        const float* ker = a.in + (size_t)uu * g.kh * g.kw;
+        float v = 0.0f;
+        for (int w1 = 0; w1 < 2; ++w1) {
+            const int k1 = b1 - a1 + g.ch + g.N * (w1 ? i - g.Lh : i);
+            if (k1 < 0 || k1 >= g.kh) continue;
+            for (int w2 = 0; w2 < 2; ++w2) {
+                const int k2 = b2 - a2 + g.cw + g.N * (w2 ? j - g.Lw : j);
+                if (k2 < 0 || k2 >= g.kw) continue;
+                v += ker[(size_t)k1 * g.kw + k2];
+            }
+        }
+        return v;
+    }
+
+}
+
+template <int L, int SRC>
+__global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g, const float2* __restrict__ twg, R2CArgs a,
+                                                          int UB) {
+    using FG = FastGeom<L>;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* buf = sm + L + (L & 1);   // keep 16-byte alignment
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
+    const int t0 = blockIdx.x * UB;
+    const int nt = min(UB, a.ntrans - t0);
+    constexpr bool full = (SRC == SRC_KERNEL);
+    const int nrows = full ? L : g.nh;
+    const int ncols = full ? L : g.nw;
+    const int P = (nrows + 1) / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+
+    // 1. packed rows (row 2pr in re, 2pr+1 in im) at buf[ui*S + pr*2*RHO + col]; unpacked rows >= 2P are zero
+    const int nload = nt * P * L;
+    for (int idx = threadIdx.x; idx < nload; idx += blockDim.x) {
+        const int ui = idx / (P * L);
+        const int rem = idx - ui * P * L;
+        const int pr = rem / L;
+        const int col = rem - pr * L;
+        float re = 0.0f, im = 0.0f;
+        if (col < ncols) {
+            re = src_value<SRC>(g, a, t0 + ui, 2 * pr, col);
+            if (2 * pr + 1 < nrows) im = src_value<SRC>(g, a, t0 + ui, 2 * pr + 1, col);
+        }
+        buf[ui * S + pr * 2 * RHO + col] = make_float2(re, im);
+    }
+    const int zr = L - 2 * P;
+    if (zr > 0) {
+        const int per = zr * NK2;
+        const int nz_ = nt * per;
+        for (int idx = threadIdx.x; idx < nz_; idx += blockDim.x) {
+            const int ui = idx / (per > 0 ? per : 1);
+            const int rem = idx - ui * per;
+            const int r = rem / NK2;
+            const int k = rem - r * NK2;
+            buf[ui * S + (2 * P + r) * RHO + k] = make_float2(0.0f, 0.0f);
+        }
+    }
+    __syncthreads();
+    // 2. per warp: row FFT of a packed pair, then the Hermitian split in place into rows 2pr, 2pr+1
+    for (int tr = warp; tr < nt * P; tr += nwarps) {
+        const int ui = tr / P, pr = tr - ui * P;
+        float2* row = buf + ui * S + pr * 2 * RHO;
+        warp_fft<L, 0, 1, false>(row, 1, tw, lane);
+        float2 Z[NBL], Q[NBL];
+#pragma unroll
+        for (int t = 0; t < NBL; ++t) {
+            const int k = lane + 32 * t;
+            if (k < NK2) {
+                Z[t] = row[k];
+                Q[t] = row[k == 0 ? 0 : L - k];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < NBL; ++t) {
+            const int k = lane + 32 * t;
+            if (k < NK2) {
+                const float2 q = make_float2(Q[t].x, -Q[t].y);   // conj(Z[-k])
+                row[k] = make_float2(0.5f * (Z[t].x + q.x), 0.5f * (Z[t].y + q.y));
+                if (2 * pr + 1 < L) row[RHO + k] = make_float2(0.5f * (Z[t].y - q.y), -0.5f * (Z[t].x - q.x));
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // 3. column FFTs (stride RHO)
+    for (int tr = warp; tr < nt * NK2; tr += nwarps) {
+        const int ui = tr / NK2, k2 = tr - ui * NK2;
+        warp_fft<L, 0, 1, false>(buf + ui * S + k2, RHO, tw, lane);
+    }
+    __syncthreads();
+    // 4. kappa-major store, UB units contiguous per kappa
+    constexpr int NKAP = L * NK2;
+    const int nst = NKAP * nt;
+    for (int idx = threadIdx.x; idx < nst; idx += blockDim.x) {
+        const int kap = idx / nt;
+        const int ui = idx - kap * nt;
+        const int k1 = kap / NK2;
+        const int k2 = kap - k1 * NK2;
+        const int t = t0 + ui;
+        const int q = t / a.cdiv;
+        const long long col = (long long)q * a.cmul + (t - q * a.cdiv);
+        a.out[(long long)kap * a.out_ld + col] = buf[ui * S + k1 * RHO + k2];
+    }
+}
+
+template <int L, int DST>
+__global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g, const float2* __restrict__ twg, C2RArgs a,
+                                                          int UB) {
+    using FG = FastGeom<L>;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* buf = sm + L + (L & 1);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
+    const int t0 = blockIdx.x * UB;
+    const int nt = min(UB, a.ntrans - t0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    constexpr int NKAP = L * NK2;
+    // 1. gather spectra into rows k1 (stride RHO)
+    const int nld = NKAP * nt;
+    for (int idx = threadIdx.x; idx < nld; idx += blockDim.x) {
+        const int kap = idx / nt;
+        const int ui = idx - kap * nt;
+        const int k1 = kap / NK2;
+        const int k2 = kap - k1 * NK2;
+        buf[ui * S + k1 * RHO + k2] = a.in[(long long)kap * a.in_ld + t0 + ui];
+    }
+    __syncthreads();
+    // 2. inverse column FFTs
+    for (int tr = warp; tr < nt * NK2; tr += nwarps) {
+        const int ui = tr / NK2, k2 = tr - ui * NK2;
+        warp_fft<L, 0, 1, true>(buf + ui * S + k2, RHO, tw, lane);
+    }
+    __syncthreads();
+    // 3. per warp and packed row pair: Hermitian row rebuild, inverse row FFT, crop / scale / epilogue
+    const int nh = g.nh, nw = g.nw;
+    const int P = (nh + 1) / 2;
+    const float scale = 1.0f / (float)(L * L);
+    for (int tr = warp; tr < nt * P; tr += nwarps) {
+        const int ui = tr / P, pr = tr - ui * P;
+        float2* row = buf + ui * S + pr * 2 * RHO;
+        const bool has1 = (2 * pr + 1 < nh);
+        float2 Z[NBL];
+#pragma unroll
+        for (int t = 0; t < NBL; ++t) {
+            const int k = lane + 32 * t;
+            if (k < L) {
+                const bool mirror = (k >= NK2);
+                const int kk = mirror ? L - k : k;
+                float2 A0 = row[kk];
+                float2 A1 = has1 ? row[RHO + kk] : make_float2(0.0f, 0.0f);
+                if (mirror) {
+                    A0.y = -A0.y;
+                    A1.y = -A1.y;
+                }
+                if (k == 0 || 2 * k == L) {
+                    A0.y = 0.0f;
+                    A1.y = 0.0f;
+                }
+                Z[t] = make_float2(A0.x - A1.y, A0.y + A1.x);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < NBL; ++t) {
+            const int k = lane + 32 * t;
+            if (k < L) row[k] = Z[t];
+        }
+        __syncwarp();
+        warp_fft<L, 0, 1, true>(row, 1, tw, lane);
+        const int t = t0 + ui;
+        for (int j = lane; j < nw; j += 32) {
+            const float2 zz = row[j];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !has1) break;
+                const int i = 2 * pr + h;
+                const float v = (h ? zz.y : zz.x) * scale;
+                if constexpr (DST == DST_IMAGE) {
+                    const int b1 = t / g.N, b2 = t % g.N;
+                    a.out[(size_t)(b1 + g.N * i) * g.W + b2 + g.N * j] = v;
+                } else if constexpr (DST == DST_POLY) {
+                    a.out[((size_t)t * nh + i) * nw + j] = v;
+                } else {
+                    const int u = g.unit0 + t;
+                    const int N2 = g.N * g.N;
+                    const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+                    if constexpr (DST == DST_VOLIMAGE) {
+                        a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
+                    } else {
+                        const size_t pidx = ((size_t)t * nh + i) * nw + j;
+                        const float xn = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
+                        a.out[pidx] = xn;
+                        atomicMax(a.mproj + (size_t)(a1 + g.N * i) * g.W + a2 + g.N * j, __float_as_uint(xn));
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int L>
+static int fast_ub(size_t* smem) {
+    const size_t per = (size_t)FastGeom<L>::S * sizeof(float2);
+    const size_t fixed = (size_t)(L + 1) * sizeof(float2);
+    const size_t budget = per <= 50 * 1024 ? 100 * 1024 : 200 * 1024;
+    int ub = (int)((budget - fixed) / per);
+    if (ub > 8) ub = 8;
+    if (ub < 1) ub = 1;
+    *smem = fixed + (size_t)ub * per;
+    return ub;
+}
+
+template <int L>
+static cudaError_t r2c_fast_L(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s) {
+    size_t smem;
+    const int UB = fast_ub<L>(&smem);
+    const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
+    cudaError_t e = cudaSuccess;
+#define LFM_FAST_R2C(SRCV)                                                                               \
+    case SRCV:                                                                                           \
+        e = cudaFuncSetAttribute(r2c_fast_kernel<L, SRCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                  \
+        r2c_fast_kernel<L, SRCV><<<grid, 512, smem, s>>>(g, tw, a, UB);                                  \
+        break;
+    switch (a.src) {
+        LFM_FAST_R2C(SRC_POLY)
+        LFM_FAST_R2C(SRC_IMAGE)
+        LFM_FAST_R2C(SRC_RATIO)
+        LFM_FAST_R2C(SRC_ONES)
+        LFM_FAST_R2C(SRC_KERNEL)
+        LFM_FAST_R2C(SRC_IMAGE2D)
+        default: return cudaErrorInvalidValue;
+    }
+#undef LFM_FAST_R2C
+    return cudaGetLastError();
+}
+
+template <int L>
+static cudaError_t c2r_fast_L(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s) {
+    size_t smem;
+    const int UB = fast_ub<L>(&smem);
+    const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
+    cudaError_t e = cudaSuccess;
+#define LFM_FAST_C2R(DSTV)                                                                               \
+    case DSTV:                                                                                           \
+        e = cudaFuncSetAttribute(c2r_fast_kernel<L, DSTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                  \
+        c2r_fast_kernel<L, DSTV><<<grid, 512, smem, s>>>(g, tw, a, UB);                                  \
+        break;
+    switch (a.dst) {
+        LFM_FAST_C2R(DST_IMAGE)
+        LFM_FAST_C2R(DST_POLY)
+        LFM_FAST_C2R(DST_VOLIMAGE)
+        LFM_FAST_C2R(DST_UPDATE)
+        default: return cudaErrorInvalidValue;
+    }
+#undef LFM_FAST_C2R
+    return cudaGetLastError();
+}
+
+bool fast_fft_size(int Lh, int Lw) {
+    return Lh == Lw && (Lh == 15 || Lh == 16 || Lh == 36 || Lh == 75 || Lh == 144);
+}
+
+cudaError_t launch_r2c_fast(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s) {
+    switch (g.Lh) {
+        case 15: return r2c_fast_L<15>(g, tw, a, s);
+        case 16: return r2c_fast_L<16>(g, tw, a, s);
+        case 36: return r2c_fast_L<36>(g, tw, a, s);
+        case 75: return r2c_fast_L<75>(g, tw, a, s);
+        case 144: return r2c_fast_L<144>(g, tw, a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_fast(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s) {
+    switch (g.Lh) {
+        case 15: return c2r_fast_L<15>(g, tw, a, s);
+        case 16: return c2r_fast_L<16>(g, tw, a, s);
+        case 36: return c2r_fast_L<36>(g, tw, a, s);
+        case 75: return c2r_fast_L<75>(g, tw, a, s);
+        case 144: return c2r_fast_L<144>(g, tw, a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace lfm

@@ -77,6 +77,11 @@ cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw,
                        const float2* tw_w, const R2CArgs& a, cudaStream_t s);
 cudaError_t launch_c2r(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
                        const float2* tw_w, const C2RArgs& a, cudaStream_t s);
+// (kernels_fft_fast.cu) compile-time-specialised square sizes; used by launch_r2c / launch_c2r when available
+bool fast_fft_size(int Lh, int Lw);
+cudaError_t launch_r2c_fast(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s);
+cudaError_t launch_c2r_fast(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s);
+void set_fast_fft_enabled(bool on);
 // (kernels_mac.cu)
 cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad,
                            int num_sms, cudaStream_t s);
