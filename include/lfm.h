@@ -204,7 +204,7 @@ lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, co
 
 /* ---- live per-stage timing (CUDA events on the plan's calls' stream) ----
  * Stages of one iteration: 0 r2c_x (a2), 1 fwd_mac (a3), 2 c2r_yhat (a4), 3 allreduce_sum (C1),
- * 4 r2c_ratio (a5), 5 bwd_mac (a6), 6 c2r_update (a7), 7 allreduce_max (C2), 8 metric (a8).
+ * 4 r2c_ratio (a5), 5 bwd_mac (a6), 6 c2r_update (a7), 7 maxproj_allreduce (a7 z-max + C2), 8 metric (a8).
  * When enabled, lfm_rl_iterate records an event before each stage and after the last one and adds the
  * elapsed times after its per-iteration synchronisation.  `launches` counts this library's kernels. */
 #define LFM_N_STAGES 9

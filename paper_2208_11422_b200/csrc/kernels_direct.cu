@@ -94,9 +94,7 @@ __global__ void __launch_bounds__(256) direct_bwd_kernel(const float* __restrict
         } else if (dst == DST_VOLIMAGE) {
             out[((size_t)z * g.H + p) * g.W + q] = acc;
         } else {  // DST_UPDATE
-            const float xn = xold[pidx] * fmaxf(acc, 0.0f) / fmaxf(norm[pidx], eps);
-            out[pidx] = xn;
-            atomicMax(mproj + (size_t)p * g.W + q, __float_as_uint(xn));
+            out[pidx] = xold[pidx] * fmaxf(acc, 0.0f) / fmaxf(norm[pidx], eps);
         }
     }
 }

@@ -7,7 +7,7 @@
 //   columns: nk2 complex FFTs of length Lh.
 // c2r_kernel: the inverse (columns, then packed row pairs), cropped to the nh x nw coarse grid,
 //   scaled by 1/(Lh Lw), followed by a fused epilogue (image scatter, polyphase store, or the RL
-//   multiplicative update + z max-projection).
+//   multiplicative update; the z max-projection is a separate deterministic pass, kernels_misc.cu).
 //
 // Polyphase facts used: with p = a + N m and s = b' + N m',
 //   (H x)(b' + N m') = sum_a sum_m x_a[m] g_{a,b'}[m' - m],  g_{a,b'}[d] = h_a[b' - a + c + N d],
@@ -218,9 +218,7 @@ __global__ void __launch_bounds__(512) c2r_kernel(XformGeom g, FftDesc fh, FftDe
                 a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
             } else {  // DST_UPDATE
                 const size_t pidx = ((size_t)t * nh + i) * nw + j;
-                const float xn = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
-                a.out[pidx] = xn;
-                atomicMax(a.mproj + (size_t)(a1 + g.N * i) * g.W + a2 + g.N * j, __float_as_uint(xn));
+                a.out[pidx] = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
             }
         }
     }

@@ -87,6 +87,11 @@ struct FastGeom {
     static constexpr int RHO = (NK2 % 2) ? NK2 : NK2 + 1;   // odd row stride, 2*RHO >= L
     static constexpr int S = (L + 1) * RHO;                 // complex per image (packed rows of an odd L fit)
     static constexpr int NBL = (L + 31) / 32;
+    // images per CTA: ~100 KB of shared memory (two CTAs per SM) unless one image needs more
+    static constexpr size_t PER = (size_t)S * 8;
+    static constexpr int UBR = (int)((PER <= 50 * 1024 ? 100 * 1024 : 200 * 1024) / PER);
+    static constexpr int UB = UBR > 8 ? 8 : (UBR < 1 ? 1 : UBR);
+    static constexpr size_t SMEM = (size_t)(L + 1) * 8 + (size_t)UB * PER;
 };
 
 template <int SRC>
@@ -129,10 +134,9 @@ __device__ __forceinline__ float src_value(const XformGeom& g, const R2CArgs& a,
 }
 
 template <int L, int SRC>
-__global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g, const float2* __restrict__ twg, R2CArgs a,
-                                                          int UB) {
+__global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g, const float2* __restrict__ twg, R2CArgs a) {
     using FG = FastGeom<L>;
-    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = FG::UB;
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);   // keep 16-byte alignment
@@ -145,19 +149,21 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g
     const int P = (nrows + 1) / 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
 
-    // 1. packed rows (row 2pr in re, 2pr+1 in im) at buf[ui*S + pr*2*RHO + col]; unpacked rows >= 2P are zero
-    const int nload = nt * P * L;
-    for (int idx = threadIdx.x; idx < nload; idx += blockDim.x) {
-        const int ui = idx / (P * L);
-        const int rem = idx - ui * P * L;
-        const int pr = rem / L;
-        const int col = rem - pr * L;
-        float re = 0.0f, im = 0.0f;
-        if (col < ncols) {
-            re = src_value<SRC>(g, a, t0 + ui, 2 * pr, col);
-            if (2 * pr + 1 < nrows) im = src_value<SRC>(g, a, t0 + ui, 2 * pr + 1, col);
+    // 1. packed rows (row 2pr in re, 2pr+1 in im) at buf[ui*S + pr*2*RHO + col]; unpacked rows >= 2P are zero.
+    //    One warp per packed row: one division per row, coalesced loads along the row.
+    for (int row = warp; row < nt * P; row += nwarps) {
+        const int ui = row / P;
+        const int pr = row - ui * P;
+        float2* dst = buf + ui * S + pr * 2 * RHO;
+        const bool two = (2 * pr + 1 < nrows);
+        for (int col = lane; col < L; col += 32) {
+            float re = 0.0f, im = 0.0f;
+            if (col < ncols) {
+                re = src_value<SRC>(g, a, t0 + ui, 2 * pr, col);
+                if (two) im = src_value<SRC>(g, a, t0 + ui, 2 * pr + 1, col);
+            }
+            dst[col] = make_float2(re, im);
         }
-        buf[ui * S + pr * 2 * RHO + col] = make_float2(re, im);
     }
     const int zr = L - 2 * P;
     if (zr > 0) {
@@ -205,26 +211,29 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g
         warp_fft<L, 0, 1, false>(buf + ui * S + k2, RHO, tw, lane);
     }
     __syncthreads();
-    // 4. kappa-major store, UB units contiguous per kappa
+    // 4. kappa-major store, UB units contiguous per kappa (UB compile-time: no run-time division)
+    __shared__ long long s_col[UB];
+    if (threadIdx.x < UB) {
+        const int t = t0 + threadIdx.x;
+        const int q = t / a.cdiv;
+        s_col[threadIdx.x] = (long long)q * a.cmul + (t - q * a.cdiv);
+    }
+    __syncthreads();
     constexpr int NKAP = L * NK2;
-    const int nst = NKAP * nt;
-    for (int idx = threadIdx.x; idx < nst; idx += blockDim.x) {
-        const int kap = idx / nt;
-        const int ui = idx - kap * nt;
+    for (int idx = threadIdx.x; idx < NKAP * UB; idx += blockDim.x) {
+        const int kap = idx / UB;
+        const int ui = idx - kap * UB;
+        if (ui >= nt) continue;
         const int k1 = kap / NK2;
         const int k2 = kap - k1 * NK2;
-        const int t = t0 + ui;
-        const int q = t / a.cdiv;
-        const long long col = (long long)q * a.cmul + (t - q * a.cdiv);
-        a.out[(long long)kap * a.out_ld + col] = buf[ui * S + k1 * RHO + k2];
+        a.out[(long long)kap * a.out_ld + s_col[ui]] = buf[ui * S + k1 * RHO + k2];
     }
 }
 
 template <int L, int DST>
-__global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g, const float2* __restrict__ twg, C2RArgs a,
-                                                          int UB) {
+__global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g, const float2* __restrict__ twg, C2RArgs a) {
     using FG = FastGeom<L>;
-    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = FG::UB;
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);
@@ -233,11 +242,11 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
     const int nt = min(UB, a.ntrans - t0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     constexpr int NKAP = L * NK2;
-    // 1. gather spectra into rows k1 (stride RHO)
-    const int nld = NKAP * nt;
-    for (int idx = threadIdx.x; idx < nld; idx += blockDim.x) {
-        const int kap = idx / nt;
-        const int ui = idx - kap * nt;
+    // 1. gather spectra into rows k1 (stride RHO); UB consecutive units per kappa
+    for (int idx = threadIdx.x; idx < NKAP * UB; idx += blockDim.x) {
+        const int kap = idx / UB;
+        const int ui = idx - kap * UB;
+        if (ui >= nt) continue;
         const int k1 = kap / NK2;
         const int k2 = kap - k1 * NK2;
         buf[ui * S + k1 * RHO + k2] = a.in[(long long)kap * a.in_ld + t0 + ui];
@@ -306,9 +315,7 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
                         a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
                     } else {
                         const size_t pidx = ((size_t)t * nh + i) * nw + j;
-                        const float xn = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
-                        a.out[pidx] = xn;
-                        atomicMax(a.mproj + (size_t)(a1 + g.N * i) * g.W + a2 + g.N * j, __float_as_uint(xn));
+                        a.out[pidx] = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
                     }
                 }
             }
@@ -317,28 +324,16 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
 }
 
 template <int L>
-static int fast_ub(size_t* smem) {
-    const size_t per = (size_t)FastGeom<L>::S * sizeof(float2);
-    const size_t fixed = (size_t)(L + 1) * sizeof(float2);
-    const size_t budget = per <= 50 * 1024 ? 100 * 1024 : 200 * 1024;
-    int ub = (int)((budget - fixed) / per);
-    if (ub > 8) ub = 8;
-    if (ub < 1) ub = 1;
-    *smem = fixed + (size_t)ub * per;
-    return ub;
-}
-
-template <int L>
 static cudaError_t r2c_fast_L(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s) {
-    size_t smem;
-    const int UB = fast_ub<L>(&smem);
+    const size_t smem = FastGeom<L>::SMEM;
+    constexpr int UB = FastGeom<L>::UB;
     const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
     cudaError_t e = cudaSuccess;
 #define LFM_FAST_R2C(SRCV)                                                                               \
     case SRCV:                                                                                           \
         e = cudaFuncSetAttribute(r2c_fast_kernel<L, SRCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                  \
-        r2c_fast_kernel<L, SRCV><<<grid, 512, smem, s>>>(g, tw, a, UB);                                  \
+        r2c_fast_kernel<L, SRCV><<<grid, 512, smem, s>>>(g, tw, a);                                  \
         break;
     switch (a.src) {
         LFM_FAST_R2C(SRC_POLY)
@@ -355,15 +350,15 @@ static cudaError_t r2c_fast_L(const XformGeom& g, const float2* tw, const R2CArg
 
 template <int L>
 static cudaError_t c2r_fast_L(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s) {
-    size_t smem;
-    const int UB = fast_ub<L>(&smem);
+    const size_t smem = FastGeom<L>::SMEM;
+    constexpr int UB = FastGeom<L>::UB;
     const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
     cudaError_t e = cudaSuccess;
 #define LFM_FAST_C2R(DSTV)                                                                               \
     case DSTV:                                                                                           \
         e = cudaFuncSetAttribute(c2r_fast_kernel<L, DSTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                  \
-        c2r_fast_kernel<L, DSTV><<<grid, 512, smem, s>>>(g, tw, a, UB);                                  \
+        c2r_fast_kernel<L, DSTV><<<grid, 512, smem, s>>>(g, tw, a);                                  \
         break;
     switch (a.dst) {
         LFM_FAST_C2R(DST_IMAGE)

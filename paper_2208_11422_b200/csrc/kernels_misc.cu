@@ -82,6 +82,36 @@ __global__ void max_project_kernel(const float* __restrict__ x, unsigned* __rest
     }
 }
 
+// z max-projection of the owned units of a POLYPHASE volume, deterministic and atomic-free:
+// one thread per (input phase a, coarse pixel m) reads x[(z*N^2 + a) - unit0][m] for every owned plane z
+// (coalesced along m) and writes max_z once to pixel (a1 + N m1, a2 + N m2); pixels whose phase this rank
+// owns in no plane get 0 (the identity of the cross-rank max, x >= 0).
+__global__ void max_project_poly_kernel(const float* __restrict__ xp, unsigned* __restrict__ mproj, XformGeom g) {
+    const int N = g.N, N2 = N * N;
+    const int per = g.nh * g.nw;
+    const size_t total = (size_t)N2 * per;
+    const int zb = g.unit0 / N2, ze = (g.unit0 + g.nu - 1) / N2;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e / per);
+        const int m = (int)(e - (size_t)a * per);
+        float v = 0.0f;
+        for (int z = zb; z <= ze; ++z) {
+            const int u = z * N2 + a;
+            if (u >= g.unit0 && u < g.unit0 + g.nu) v = fmaxf(v, xp[(size_t)(u - g.unit0) * per + m]);
+        }
+        const int m1 = m / g.nw, m2 = m - m1 * g.nw;
+        const int a1 = a / N, a2 = a - a1 * N;
+        mproj[(size_t)(a1 + N * m1) * g.W + a2 + N * m2] = __float_as_uint(v);
+    }
+}
+
+cudaError_t launch_max_project_poly(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s) {
+    const size_t total = (size_t)g.N * g.N * g.nh * g.nw;
+    const unsigned blocks = (unsigned)((total + 255) / 256 < 4736 ? (total + 255) / 256 : 4736);
+    max_project_poly_kernel<<<blocks, 256, 0, s>>>(xp, mproj, g);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_max_project(const float* x, unsigned* mproj, const XformGeom& g, cudaStream_t s) {
     max_project_kernel<<<2368, 256, 0, s>>>(x, mproj, g);
     return cudaGetLastError();

@@ -245,7 +245,7 @@ namespace {
 constexpr int kParts = 296;
 
 const char* kStageNames[LFM_N_STAGES] = {"r2c_x", "fwd_mac", "c2r_yhat", "allreduce_sum", "r2c_ratio",
-                                         "bwd_mac", "c2r_update", "allreduce_max", "metric"};
+                                         "bwd_mac", "c2r_update", "maxproj_allreduce", "metric"};
 
 // records the start event of `stage` (stage == LFM_N_STAGES: end of the last stage) when profiling
 inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
@@ -396,7 +396,6 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     c.out = out;
     c.xold = xold;
     c.norm = p->norm;
-    c.mproj = p->mproj;
     c.eps = eps;
     CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
     ST(mark(p, 7, s));
@@ -418,9 +417,10 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
 // one RL iteration on polyphase volumes: xn = xc * H^T(y/(max(H xc,0)+eps)) / max(norm,eps); metric -> met.out[0]
 lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float eps, int region, bool metric,
                    cudaStream_t s) {
-    CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
     ST(op_forward_poly(p, xc, p->yhat, s));
     ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
+    CK(launch_max_project_poly(xn, p->mproj, p->xg, s));     // a7: z max-projection, every pixel written
+    p->pacc.launches += 1;
     if (metric) ST(op_metric(p, region, s));
     return LFM_OK;
 }

@@ -36,7 +36,7 @@ enum C2RDst : int {
     DST_IMAGE = 0,    // yhat image [H][W] at (b1 + N i, b2 + N j); t = output phase
     DST_POLY = 1,     // polyphase volume; t = local unit
     DST_VOLIMAGE = 2, // image-layout volume [nz][H][W]; t = local unit
-    DST_UPDATE = 3    // x_new = x_old * max(bp,0) / max(norm,eps) (poly) + atomic max-projection
+    DST_UPDATE = 3    // x_new = x_old * max(bp,0) / max(norm,eps) (poly)
 };
 
 struct XformGeom {
@@ -66,7 +66,6 @@ struct C2RArgs {
     float* out;             // see C2RDst
     const float* xold;      // DST_UPDATE
     const float* norm;      // DST_UPDATE
-    unsigned* mproj;        // DST_UPDATE (float bits of non-negative values, atomicMax)
     float eps;
 };
 
@@ -94,7 +93,8 @@ cudaError_t launch_poly_to_image(const float* xp, float* x, const XformGeom& g, 
                                  cudaStream_t s);
 cudaError_t launch_image_to_poly(const float* x, float* xp, const XformGeom& g, int unit_begin, int unit_count,
                                  cudaStream_t s);
-cudaError_t launch_max_project(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s);
+cudaError_t launch_max_project(const float* x, unsigned* mproj, const XformGeom& g, cudaStream_t s);
+cudaError_t launch_max_project_poly(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s);
 cudaError_t launch_sum_stats(const float* p, size_t n, double* partials, int nparts, double* out3, cudaStream_t s);
 cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
                           const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
