@@ -245,7 +245,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (algorithmic bytes at the minimal alias-free transform size)
     N2 = cfg.nnum ** 2
-    nu = info["unit_end"] - info["unit_begin"]
+    nu = info["fft_units"]            # units streamed by the MAC kernels (hybrid plan: frequency-path units)
     kap_min = info["lc_min_h"] * (info["lc_min_w"] // 2 + 1)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
@@ -258,8 +258,8 @@ def run_ours(args):
         "fwd_mac": kap_min * N2 * nu * 8 + kap_min * nu * 8 + kap_min * N2 * 8,   # M + G + Y
         "bwd_mac": kap_min * N2 * nu * 8 + kap_min * N2 * 8 + kap_min * nu * 8,   # M + R + Xh
     }
-    if info["direct"]:
-        dom = max(("fwd_mac", "bwd_mac", "c2r_update"), key=lambda k: stage_ms[k])
+    if info["fft_units"] == 0:
+        dom = max(("dir_fwd", "dir_bwd"), key=lambda k: stage_ms[k])
         roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
                 "traffic": None}
     else:
@@ -325,6 +325,7 @@ def run_ours(args):
                 "transform": f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})"
                 if not info["direct"] else "direct spatial",
                 "transfer_matrix_gb_per_gpu": info["transfer_bytes"] / 1e9,
+                "hybrid": {"direct_planes": info["direct_planes"], "fft_units": info["fft_units"]},
                 "l2": "inputs larger than L2: each projection streams the transfer matrices (L2 126 MB)",
                 "plan_ms": info["plan_ms"], "setup_s": setup_s,
                 "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"],

@@ -97,8 +97,9 @@ enum {
     LFM_PLAN_NO_COMM = 1,   /* world > 1 without a communicator: the plan owns rank's units and all
                                cross-rank reductions are skipped (outputs are this rank's partials).
                                For testing the sharding on one device.                              */
-    LFM_PLAN_DIRECT = 2     /* spatial-domain projections (direct polyphase convolution) instead of
-                               the frequency-domain transfer matrices; for small PSFs.             */
+    LFM_PLAN_DIRECT = 2,    /* every plane on the spatial (direct polyphase convolution) path         */
+    LFM_PLAN_FFT_ONLY = 4   /* every plane on the frequency path.  Default (neither flag): hybrid --
+                               per plane, the cheaper of the two by the cost model of DESIGN.md §5   */
 };
 
 /* Information about a plan. */
@@ -110,10 +111,12 @@ typedef struct {
     int n_kappa;                    /* Lh * (Lw/2 + 1) coarse frequencies kept                     */
     int units_padded;               /* row length of the transfer matrices (>= owned units)       */
     int x_s, y_s;                   /* cutoff region (Eqs. 9-10)                                   */
-    int direct;                     /* 1 if LFM_PLAN_DIRECT                                        */
-    size_t transfer_bytes;          /* bytes of transfer matrices held by this rank               */
+    int direct;                     /* 1 if no owned unit is on the frequency path                 */
+    size_t transfer_bytes;          /* bytes of transfer matrices + direct taps held by this rank  */
     size_t device_bytes;            /* all device memory held by the plan                         */
     double plan_ms;                 /* wall time of lfm_plan_create                                */
+    int direct_planes;              /* planes (touching owned units) on the direct path            */
+    int fft_units;                  /* owned units on the frequency path                            */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */
@@ -203,11 +206,12 @@ lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, co
                            int region, double* entropy, int* x_s, int* y_s, void* stream);
 
 /* ---- live per-stage timing (CUDA events on the plan's calls' stream) ----
- * Stages of one iteration: 0 r2c_x (a2), 1 fwd_mac (a3), 2 c2r_yhat (a4), 3 allreduce_sum (C1),
- * 4 r2c_ratio (a5), 5 bwd_mac (a6), 6 c2r_update (a7), 7 maxproj_allreduce (a7 z-max + C2), 8 metric (a8).
+ * Stages of one iteration: 0 r2c_x (a2), 1 fwd_mac (a3), 2 c2r_yhat (a4), 3 dir_fwd (direct planes, K9),
+ * 4 allreduce_sum (C1), 5 r2c_ratio (a5), 6 bwd_mac (a6), 7 c2r_update (a7), 8 dir_bwd (direct planes + update),
+ * 9 maxproj_allreduce (a7 z-max + C2), 10 metric (a8).
  * When enabled, lfm_rl_iterate records an event before each stage and after the last one and adds the
  * elapsed times after its per-iteration synchronisation.  `launches` counts this library's kernels. */
-#define LFM_N_STAGES 9
+#define LFM_N_STAGES 11
 typedef struct {
     double ms[LFM_N_STAGES];          /* summed device milliseconds per stage   */
     long long count[LFM_N_STAGES];    /* number of timed executions per stage   */

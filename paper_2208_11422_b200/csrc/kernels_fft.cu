@@ -20,9 +20,10 @@ namespace lfm {
 template <int SRC>
 __device__ __forceinline__ float src_val(const XformGeom& g, const R2CArgs& a, int t, int i, int j) {
     if constexpr (SRC == SRC_POLY) {
-        return a.in[((size_t)t * g.nh + i) * g.nw + j];
+        const int lu = g.umap ? g.umap[t] : t;
+        return a.in[((size_t)lu * g.nh + i) * g.nw + j];
     } else if constexpr (SRC == SRC_IMAGE) {
-        const int u = g.unit0 + t;
+        const int u = g.unit0 + (g.umap ? g.umap[t] : t);
         const int N2 = g.N * g.N;
         const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
         return a.in[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j];
@@ -38,9 +39,10 @@ __device__ __forceinline__ float src_val(const XformGeom& g, const R2CArgs& a, i
     } else {  // SRC_KERNEL: t = b' * nu + uu ; wrapped coarse kernel g_{a,b'} at circular index (i, j)
         const int bp = t / g.nu, uu = t - bp * g.nu;
         const int b1 = bp / g.N, b2 = bp % g.N;
-        const int u = g.unit0 + uu;
+        const int lu = g.umap ? g.umap[uu] : uu;
+        const int u = g.unit0 + lu;
         const int a1 = (u / g.N) % g.N, a2 = u % g.N;
-        const float* ker = a.in + (size_t)uu * g.kh * g.kw;
+        const float* ker = a.in + (size_t)lu * g.kh * g.kw;
         float v = 0.0f;
 #pragma unroll
         for (int w1 = 0; w1 < 2; ++w1) {
@@ -209,15 +211,16 @@ __global__ void __launch_bounds__(512) c2r_kernel(XformGeom g, FftDesc fh, FftDe
             const int b1 = t / g.N, b2 = t % g.N;
             a.out[(size_t)(b1 + g.N * i) * g.W + b2 + g.N * j] = v;
         } else if constexpr (DST == DST_POLY) {
-            a.out[((size_t)t * nh + i) * nw + j] = v;
+            a.out[((size_t)(g.umap ? g.umap[t] : t) * nh + i) * nw + j] = v;
         } else {
-            const int u = g.unit0 + t;
+            const int lu = g.umap ? g.umap[t] : t;
+            const int u = g.unit0 + lu;
             const int N2 = g.N * g.N;
             const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
             if constexpr (DST == DST_VOLIMAGE) {
                 a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
             } else {  // DST_UPDATE
-                const size_t pidx = ((size_t)t * nh + i) * nw + j;
+                const size_t pidx = ((size_t)lu * nh + i) * nw + j;
                 a.out[pidx] = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
             }
         }

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "lfm_internal.cuh"
@@ -206,12 +207,20 @@ SizeTerms size_terms(const Geo& g, int nu, int nu_total, int world, bool direct)
 
 struct lfm_plan_s {
     Geo geo{};
-    XformGeom xg{};
+    XformGeom xg{};     // frequency-path transforms (nu = FFT units, umap)
+    XformGeom xall{};   // every owned unit (layout conversion, max-projection, generic direct path)
     FftDesc fh{}, fw{};
     int rank = 0, world = 1;
     bool comm = false, direct = false;
     ncclComm_t nccl = nullptr;
     int u0 = 0, u1 = 0, nu = 0, nu_pad = 0, nu_total = 0;
+    // hybrid plan: FFT units (frequency path) and direct planes (spatial path)
+    int nu_fft = 0, nu_fft_pad = 16;
+    int* umap = nullptr;        // [nu_fft] local unit index of FFT transform t
+    std::vector<DirArgs> dgroups;   // direct planes grouped by tap-box size D (one launch per group)
+    std::vector<void*> dallocs;     // device arrays owned by the direct groups
+    int n_direct_planes = 0;
+    float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
     int num_sms = 148;
     float2 *tw_h = nullptr, *tw_w = nullptr;
     float2* M = nullptr;
@@ -244,8 +253,11 @@ namespace {
 
 constexpr int kParts = 296;
 
-const char* kStageNames[LFM_N_STAGES] = {"r2c_x", "fwd_mac", "c2r_yhat", "allreduce_sum", "r2c_ratio",
-                                         "bwd_mac", "c2r_update", "maxproj_allreduce", "metric"};
+const char* kStageNames[LFM_N_STAGES] = {"r2c_x",      "fwd_mac",    "c2r_yhat", "dir_fwd",
+                                         "allreduce_sum", "r2c_ratio", "bwd_mac", "c2r_update",
+                                         "dir_bwd",    "maxproj_allreduce", "metric"};
+enum { ST_R2C_X = 0, ST_FWD_MAC, ST_C2R_YHAT, ST_DIR_FWD, ST_ALLRED_SUM, ST_R2C_RATIO, ST_BWD_MAC, ST_C2R_UPD,
+       ST_DIR_BWD, ST_MAXPROJ, ST_METRIC };
 
 // records the start event of `stage` (stage == LFM_N_STAGES: end of the last stage) when profiling
 inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
@@ -259,6 +271,9 @@ void plan_free(lfm_plan p) {
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
+    cudaFree(p->umap);
+    for (void* q : p->dallocs) cudaFree(q);
+    cudaFree(p->dpart);
     cudaFree(p->M);
     cudaFree(p->psf);
     cudaFree(p->norm);
@@ -332,30 +347,55 @@ lfm_status allreduce(lfm_plan p, void* buf, size_t n, ncclDataType_t t, ncclRedO
 }
 
 // yhat = H x (x polyphase, owned units) summed over ranks
-lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_t s) {
+// yhat = H x summed over ranks; x polyphase (owned units) or image layout [nz][H][W]
+lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
-    ST(mark(p, 0, s));
+    ST(mark(p, ST_R2C_X, s));
     if (p->direct) {
-        ST(mark(p, 1, s));
-        CK(launch_direct_fwd(xp, p->psf, yimg, p->xg, s));
+        const float* xp = x;
+        if (image) {
+            CK(launch_image_to_poly(x, p->xb[0], p->xall, p->u0, p->nu, s));
+            xp = p->xb[0];
+        }
+        ST(mark(p, ST_FWD_MAC, s));
+        ST(mark(p, ST_C2R_YHAT, s));
+        ST(mark(p, ST_DIR_FWD, s));
+        CK(launch_direct_fwd(xp, p->psf, yimg, p->xall, s));
         p->pacc.launches += 1;
-        ST(mark(p, 2, s));
     } else {
-        CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(SRC_POLY, xp, nullptr, 0.f, p->nu, p->G, p->nu_pad), s));
-        ST(mark(p, 1, s));
-        CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_pad, p->num_sms, s));
-        ST(mark(p, 2, s));
-        C2RArgs c{};
-        c.dst = DST_IMAGE;
-        c.in = p->Y;
-        c.in_ld = N2;
-        c.ntrans = N2;
-        c.out = yimg;
-        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
-        p->pacc.launches += 3;
+        if (p->nu_fft > 0) {
+            CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
+                          r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), s));
+            ST(mark(p, ST_FWD_MAC, s));
+            CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, p->num_sms, s));
+            ST(mark(p, ST_C2R_YHAT, s));
+            C2RArgs c{};
+            c.dst = DST_IMAGE;
+            c.in = p->Y;
+            c.in_ld = N2;
+            c.ntrans = N2;
+            c.out = yimg;
+            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+            p->pacc.launches += 3;
+        } else {
+            ST(mark(p, ST_FWD_MAC, s));
+            ST(mark(p, ST_C2R_YHAT, s));
+        }
+        ST(mark(p, ST_DIR_FWD, s));
+        bool acc = p->nu_fft > 0;
+        for (const DirArgs& dg : p->dgroups) {
+            CK(launch_dir_fwd(dg, x, image ? 1 : 0, p->dpart, yimg, acc ? 1 : 0, s));
+            p->pacc.launches += 2;
+            acc = true;
+        }
+        if (!acc) CK(cudaMemsetAsync(yimg, 0, (size_t)p->geo.H * p->geo.W * sizeof(float), s));
     }
-    ST(mark(p, 3, s));
+    ST(mark(p, ST_ALLRED_SUM, s));
     return allreduce(p, yimg, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
+}
+
+lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_t s) {
+    return op_forward_src(p, xp, /*image=*/false, yimg, s);
 }
 
 // backward projection of an image source into one of the C2R destinations
@@ -363,7 +403,7 @@ lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_
 lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2, float eps, int dst, float* out,
                        const float* xold, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
-    ST(mark(p, 4, s));
+    ST(mark(p, ST_R2C_RATIO, s));
     if (p->direct) {
         const size_t n = (size_t)p->geo.H * p->geo.W;
         const float* r = img;
@@ -376,29 +416,40 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
             r = p->rimg;
             p->pacc.launches += 1;
         }
-        ST(mark(p, 5, s));
-        ST(mark(p, 6, s));
-        CK(launch_direct_bwd(r, p->psf, out, dst, xold, p->norm, p->mproj, eps, p->xg, s));
+        ST(mark(p, ST_BWD_MAC, s));
+        ST(mark(p, ST_C2R_UPD, s));
+        ST(mark(p, ST_DIR_BWD, s));
+        CK(launch_direct_bwd(r, p->psf, out, dst, xold, p->norm, p->mproj, eps, p->xall, s));
         p->pacc.launches += 1;
-        ST(mark(p, 7, s));
+        ST(mark(p, ST_MAXPROJ, s));
         return LFM_OK;
     }
-    CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
-    ST(mark(p, 5, s));
-    CK(launch_bwd_mac(p->M, p->R, p->Xh, p->geo.nkappa, N2, p->nu_pad, s));
-    ST(mark(p, 6, s));
-    p->pacc.launches += 3;
-    C2RArgs c{};
-    c.dst = dst;
-    c.in = p->Xh;
-    c.in_ld = p->nu_pad;
-    c.ntrans = p->nu;
-    c.out = out;
-    c.xold = xold;
-    c.norm = p->norm;
-    c.eps = eps;
-    CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
-    ST(mark(p, 7, s));
+    if (p->nu_fft > 0) {
+        CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
+        ST(mark(p, ST_BWD_MAC, s));
+        CK(launch_bwd_mac(p->M, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, s));
+        ST(mark(p, ST_C2R_UPD, s));
+        C2RArgs c{};
+        c.dst = dst;
+        c.in = p->Xh;
+        c.in_ld = p->nu_fft_pad;
+        c.ntrans = p->nu_fft;
+        c.out = out;
+        c.xold = xold;
+        c.norm = p->norm;
+        c.eps = eps;
+        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+        p->pacc.launches += 3;
+    } else {
+        ST(mark(p, ST_BWD_MAC, s));
+        ST(mark(p, ST_C2R_UPD, s));
+    }
+    ST(mark(p, ST_DIR_BWD, s));
+    for (const DirArgs& dg : p->dgroups) {
+        CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, p->norm, s));
+        p->pacc.launches += 1;
+    }
+    ST(mark(p, ST_MAXPROJ, s));
     return LFM_OK;
 }
 
@@ -406,7 +457,7 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
     if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the DCT-entropy metric needs them");
     const int ri = region == LFM_REGION_RECTANGLE ? 1 : 0;
     ST(allreduce(p, p->mproj, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclMax, s));
-    ST(mark(p, 8, s));
+    ST(mark(p, ST_METRIC, s));
     CK(launch_metric(p->mproj, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
                      p->met.nmem[ri], p->met.T1, p->met.rowsq, p->met.out, s));
     p->pacc.launches += 2;
@@ -419,7 +470,7 @@ lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float
                    cudaStream_t s) {
     ST(op_forward_poly(p, xc, p->yhat, s));
     ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
-    CK(launch_max_project_poly(xn, p->mproj, p->xg, s));     // a7: z max-projection, every pixel written
+    CK(launch_max_project_poly(xn, p->mproj, p->xall, s));     // a7: z max-projection, every pixel written
     p->pacc.launches += 1;
     if (metric) ST(op_metric(p, region, s));
     return LFM_OK;
@@ -453,7 +504,7 @@ lfm_status check_y(lfm_plan p, const float* y, cudaStream_t s) {
 
 lfm_status gather_to_image(lfm_plan p, const float* xp_local, float* x, cudaStream_t s) {
     if (!p->comm) {
-        CK(launch_poly_to_image(xp_local, x, p->xg, p->u0, p->nu, s));
+        CK(launch_poly_to_image(xp_local, x, p->xall, p->u0, p->nu, s));
         return LFM_OK;
     }
     const size_t per = (size_t)p->geo.nh * p->geo.nw;
@@ -470,9 +521,42 @@ lfm_status gather_to_image(lfm_plan p, const float* xp_local, float* x, cudaStre
         }
     }
     NK(ncclGroupEnd());
-    CK(launch_poly_to_image(p->xfull, x, p->xg, 0, p->nu_total, s));
+    CK(launch_poly_to_image(p->xfull, x, p->xall, 0, p->nu_total, s));
     return LFM_OK;
 }
+
+
+inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+inline int ceildiv(int a, int b) { return -floordiv(-a, b); }
+
+// Tap box of the coarse kernels of one plane along one axis: for input phase a and output phase b the
+// coarse taps d with PSF index k = b - a + c + N d inside the plane's non-zero support [k0, k1].
+struct AxisBox {
+    int D = 0, dmin = 0, dmax = 0;
+    std::vector<int> dlo;   // [a][b]
+};
+AxisBox axis_box(int N, int c, int k0, int k1) {
+    AxisBox bx;
+    bx.dlo.assign((size_t)N * N, 0);
+    bx.dmin = 1 << 30;
+    bx.dmax = -(1 << 30);
+    for (int a = 0; a < N; ++a)
+        for (int b = 0; b < N; ++b) {
+            const int lo = ceildiv(k0 - c - (b - a), N), hi = floordiv(k1 - c - (b - a), N);
+            bx.dlo[(size_t)a * N + b] = lo;
+            bx.D = std::max(bx.D, hi - lo + 1);
+            bx.dmin = std::min(bx.dmin, lo);
+            bx.dmax = std::max(bx.dmax, lo);
+        }
+    return bx;
+}
+
+// Planning constants of the hybrid cost model (per iteration, both projections):
+//   frequency path  2 * units * N^2 * n_kappa * 8 B at kHbmBps, plus the coarse transforms;
+//   direct path     2 * units * N^2 * D^2 * nh * nw * 2 flop at kDirFlops[D].
+constexpr double kHbmBps = 7.0e12;
+constexpr double kXformPerUnit = 9.0e-8;
+const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 28.0e12};
 
 }  // namespace
 
@@ -550,9 +634,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     if (!psf_host) return fail(LFM_EINVAL, "psf_host is NULL");
     if (psf_t_host)
         return fail(LFM_EUNSUPPORTED, "a supplied transposed PSF is not supported in this build; pass NULL for the exact adjoint (C6)");
-    const bool direct = (flags & LFM_PLAN_DIRECT) != 0;
     Geo g;
-    ST(make_geo(nnum, nz, kh, kw, height, width, direct, &g));
+    ST(make_geo(nnum, nz, kh, kw, height, width, /*direct=*/false, &g));
     int rank = 0, world = 1;
     if (dist) {
         rank = dist->rank;
@@ -577,7 +660,6 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             return guard(fail(LFM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
     } while (0)
     p->geo = g;
-    p->direct = direct;
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
@@ -601,7 +683,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     }
     // memory budget ("estimate the required memory size")
     {
-        SizeTerms t = size_terms(g, p->nu, p->nu_total, world, direct);
+        SizeTerms t = size_terms(g, p->nu, p->nu_total, world, (flags & LFM_PLAN_DIRECT) != 0);
         size_t free_b = 0, total_b = 0;
         CKG(cudaMemGetInfo(&free_b, &total_b));
         if (t.total() > free_b) {
@@ -640,6 +722,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     xg.kw = kw;
     xg.ch = g.ch;
     xg.cw = g.cw;
+    xg.umap = nullptr;
+    p->xall = xg;
     const int N2 = nnum * nnum;
     const size_t HW = (size_t)height * width;
     const size_t vol = (size_t)p->nu * g.nh * g.nw;
@@ -659,26 +743,167 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     // PSF slice of the owned units -> device ("the PSF is evenly distributed to each card")
     PG(dalloc(p, &p->psf, (size_t)p->nu * kk * sizeof(float), "psf slice"));
     if (p->nu > 0) CKG(cudaMemcpyAsync(p->psf, psf_own, (size_t)p->nu * kk * sizeof(float), cudaMemcpyHostToDevice, s));
-    if (!direct) {
-        if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
-            return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", g.Lh, g.Lw));
-        PG(twiddles(g.Lh, &p->tw_h, p, s));
-        PG(twiddles(g.Lw, &p->tw_w, p, s));
-        p->transfer_bytes = (size_t)g.nkappa * N2 * p->nu_pad * sizeof(float2);
-        PG(dalloc(p, &p->M, p->transfer_bytes, "transfer matrices"));
-        PG(dalloc(p, &p->G, (size_t)g.nkappa * p->nu_pad * sizeof(float2), "G spectra"));
-        PG(dalloc(p, &p->Xh, (size_t)g.nkappa * p->nu_pad * sizeof(float2), "Xh spectra"));
-        PG(dalloc(p, &p->Y, (size_t)g.nkappa * N2 * sizeof(float2), "Y spectra"));
-        PG(dalloc(p, &p->R, (size_t)g.nkappa * N2 * sizeof(float2), "R spectra"));
-        CKG(cudaMemsetAsync(p->M, 0, p->transfer_bytes, s));      // padding columns stay zero
-        CKG(cudaMemsetAsync(p->G, 0, (size_t)g.nkappa * p->nu_pad * sizeof(float2), s));
-        // K1: transfer matrices M[kappa][b'][u] = DFT_{Lh x Lw}(g_{u,b'}), g_{u,b'}[d] = h_u[b' - a + c + N d]
-        R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * p->nu, p->M, (long long)N2 * p->nu_pad);
-        a.cdiv = p->nu > 0 ? p->nu : 1;
-        a.cmul = p->nu_pad;
-        CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, a, s));
+
+    // ---- hybrid plan: per plane, the tap box of its coarse kernels and a cost model pick the
+    //      direct path (D x D taps per phase pair) or the frequency path (streamed transfer matrices)
+    std::vector<int> plane_direct(nz, 0), plane_D(nz, 0);
+    std::vector<AxisBox> box1(nz), box2(nz);
+    const int zb = p->nu > 0 ? p->u0 / N2 : 0, ze = p->nu > 0 ? (p->u1 - 1) / N2 : -1;
+    bool too_big = false;
+    for (int z = zb; z <= ze; ++z) {
+        int k0 = kh, k1 = -1, j0 = kw, j1 = -1;
+        const int ub = std::max(p->u0, z * N2), ue = std::min(p->u1, (z + 1) * N2);
+        for (int u = ub; u < ue; ++u) {
+            const float* ker = psf_host + (size_t)u * kk;
+            for (int i = 0; i < kh; ++i)
+                for (int j = 0; j < kw; ++j)
+                    if (ker[(size_t)i * kw + j] != 0.0f) {
+                        k0 = std::min(k0, i);
+                        k1 = std::max(k1, i);
+                        j0 = std::min(j0, j);
+                        j1 = std::max(j1, j);
+                    }
+        }
+        if (k1 < 0) {   // all-zero owned kernels: a single (zero) tap
+            k0 = k1 = g.ch;
+            j0 = j1 = g.cw;
+        }
+        box1[z] = axis_box(nnum, g.ch, k0, k1);
+        box2[z] = axis_box(nnum, g.cw, j0, j1);
+        const int D = std::max(box1[z].D, box2[z].D);
+        plane_D[z] = D;
+        const double units = ue - ub;
+        const double t_fft = 2.0 * units * N2 * g.nkappa * 8.0 / kHbmBps + kXformPerUnit * units;
+        const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
+        if (flags & LFM_PLAN_FFT_ONLY)
+            plane_direct[z] = 0;
+        else if (flags & LFM_PLAN_DIRECT)
+            plane_direct[z] = 1;
+        else
+            plane_direct[z] = t_dir < t_fft ? 1 : 0;
+        if (plane_direct[z] && D > kDirMaxD) too_big = true;
+    }
+    p->direct = too_big;   // all-direct request with boxes beyond kDirMaxD: the generic spatial kernels
+    if (!p->direct) {
+        // FFT units through a unit map (z-major order kept)
+        std::vector<int> umap;
+        for (int u = p->u0; u < p->u1; ++u)
+            if (!plane_direct[u / N2]) umap.push_back(u - p->u0);
+        p->nu_fft = (int)umap.size();
+        p->nu_fft_pad = (int)round_up((size_t)std::max(p->nu_fft, 1), 16);
+        if (p->nu_fft > 0) {
+            PG(dalloc(p, &p->umap, umap.size() * sizeof(int), "unit map"));
+            CKG(cudaMemcpyAsync(p->umap, umap.data(), umap.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+        }
+        xg.nu = p->nu_fft;
+        xg.nu_pad = p->nu_fft_pad;
+        xg.umap = p->umap;
+        // direct planes grouped by box size; taps g_z[b'][a][e] = h_{z,a}[b - a + c + N (dlo + e)] (both layouts)
+        size_t coef_bytes = 0;
+        for (int D = 1; D <= kDirMaxD; ++D) {
+            std::vector<int> zl;
+            for (int z = zb; z <= ze; ++z)
+                if (plane_direct[z] && plane_D[z] == D) zl.push_back(z);
+            if (zl.empty()) continue;
+            const int nzd = (int)zl.size(), DD = D * D;
+            std::vector<float> cf((size_t)nzd * N2 * DD * N2, 0.0f), cb((size_t)nzd * N2 * DD * N2, 0.0f);
+            std::vector<int> dl((size_t)nzd * 2 * N2);
+            DirArgs da{};
+            da.dmin1 = da.dmin2 = 1 << 30;
+            da.dmax1 = da.dmax2 = -(1 << 30);
+            for (int zi = 0; zi < nzd; ++zi) {
+                const int z = zl[zi];
+                const AxisBox& B1 = box1[z];
+                const AxisBox& B2 = box2[z];
+                da.dmin1 = std::min(da.dmin1, B1.dmin);
+                da.dmax1 = std::max(da.dmax1, B1.dmax);
+                da.dmin2 = std::min(da.dmin2, B2.dmin);
+                da.dmax2 = std::max(da.dmax2, B2.dmax);
+                for (int q = 0; q < N2; ++q) {
+                    dl[((size_t)zi * 2 + 0) * N2 + q] = B1.dlo[q];
+                    dl[((size_t)zi * 2 + 1) * N2 + q] = B2.dlo[q];
+                }
+                for (int a = 0; a < N2; ++a) {
+                    const int u = z * N2 + a;
+                    if (u < p->u0 || u >= p->u1) continue;
+                    const int a1 = a / nnum, a2 = a % nnum;
+                    const float* ker = psf_host + (size_t)u * kk;
+                    for (int bq = 0; bq < N2; ++bq) {
+                        const int b1 = bq / nnum, b2 = bq % nnum;
+                        const int o1 = B1.dlo[(size_t)a1 * nnum + b1], o2 = B2.dlo[(size_t)a2 * nnum + b2];
+                        for (int e1 = 0; e1 < D; ++e1) {
+                            const int k1 = b1 - a1 + g.ch + nnum * (o1 + e1);
+                            if (k1 < 0 || k1 >= kh) continue;
+                            for (int e2 = 0; e2 < D; ++e2) {
+                                const int k2 = b2 - a2 + g.cw + nnum * (o2 + e2);
+                                if (k2 < 0 || k2 >= kw) continue;
+                                const float v = ker[(size_t)k1 * kw + k2];
+                                cf[(((size_t)zi * N2 + a) * DD + e1 * D + e2) * N2 + bq] = v;
+                                cb[(((size_t)zi * N2 + bq) * DD + e1 * D + e2) * N2 + a] = v;
+                            }
+                        }
+                    }
+                }
+            }
+            int* dz = nullptr;
+            float *dcf = nullptr, *dcb = nullptr;
+            int* ddl = nullptr;
+            PG(dalloc(p, &dz, zl.size() * sizeof(int), "direct plane list"));
+            p->dallocs.push_back(dz);
+            PG(dalloc(p, &dcf, cf.size() * sizeof(float), "direct taps (forward layout)"));
+            p->dallocs.push_back(dcf);
+            PG(dalloc(p, &dcb, cb.size() * sizeof(float), "direct taps (backward layout)"));
+            p->dallocs.push_back(dcb);
+            PG(dalloc(p, &ddl, dl.size() * sizeof(int), "direct box origins"));
+            p->dallocs.push_back(ddl);
+            CKG(cudaMemcpyAsync(dz, zl.data(), zl.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+            CKG(cudaMemcpyAsync(dcf, cf.data(), cf.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+            CKG(cudaMemcpyAsync(dcb, cb.data(), cb.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+            CKG(cudaMemcpyAsync(ddl, dl.data(), dl.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+            CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
+            da.N = nnum;
+            da.H = height;
+            da.W = width;
+            da.nh = g.nh;
+            da.nw = g.nw;
+            da.unit0 = p->u0;
+            da.nu = p->nu;
+            da.nzd = nzd;
+            da.zlist = dz;
+            da.D = D;
+            da.coef_f = dcf;
+            da.coef_b = dcb;
+            da.dlo = ddl;
+            p->dgroups.push_back(da);
+            p->n_direct_planes += nzd;
+            coef_bytes += 2 * cf.size() * sizeof(float);
+        }
+        p->transfer_bytes = coef_bytes;
+        int maxg = 0;
+        for (const DirArgs& dg : p->dgroups) maxg = std::max(maxg, dg.nzd);
+        if (maxg > 0) PG(dalloc(p, &p->dpart, (size_t)maxg * HW * sizeof(float), "direct forward partials"));
+        if (p->nu_fft > 0) {
+            if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
+                return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", g.Lh, g.Lw));
+            PG(twiddles(g.Lh, &p->tw_h, p, s));
+            PG(twiddles(g.Lw, &p->tw_w, p, s));
+            const size_t mbytes = (size_t)g.nkappa * N2 * p->nu_fft_pad * sizeof(float2);
+            p->transfer_bytes += mbytes;
+            PG(dalloc(p, &p->M, mbytes, "transfer matrices"));
+            PG(dalloc(p, &p->G, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), "G spectra"));
+            PG(dalloc(p, &p->Xh, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
+            PG(dalloc(p, &p->Y, (size_t)g.nkappa * N2 * sizeof(float2), "Y spectra"));
+            PG(dalloc(p, &p->R, (size_t)g.nkappa * N2 * sizeof(float2), "R spectra"));
+            CKG(cudaMemsetAsync(p->M, 0, mbytes, s));      // padding columns stay zero
+            CKG(cudaMemsetAsync(p->G, 0, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), s));
+            // K1: transfer matrices M[kappa][b'][t] = DFT_{Lh x Lw}(g_{u(t),b'}), g_{u,b'}[d] = h_u[b' - a + c + N d]
+            R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * p->nu_fft, p->M, (long long)N2 * p->nu_fft_pad);
+            a.cdiv = p->nu_fft;
+            a.cmul = p->nu_fft_pad;
+            CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, a, s));
+        }
         CKG(cudaStreamSynchronize(s));
-        cudaFree(p->psf);           // the transfer matrices replace the PSF
+        cudaFree(p->psf);           // transfer matrices and direct taps replace the PSF
         p->bytes -= (size_t)p->nu * kk * sizeof(float);
         p->psf = nullptr;
     } else {
@@ -713,10 +938,12 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->lc_min_h = p->geo.lcmin_h;
     info->lc_min_w = p->geo.lcmin_w;
     info->n_kappa = p->geo.nkappa;
-    info->units_padded = p->nu_pad;
+    info->units_padded = p->nu_fft_pad;
     info->x_s = p->region.xs;
     info->y_s = p->region.ys;
-    info->direct = p->direct ? 1 : 0;
+    info->direct = p->direct ? 1 : (p->nu_fft == 0 ? 1 : 0);
+    info->direct_planes = p->direct ? p->geo.nz : p->n_direct_planes;
+    info->fft_units = p->direct ? 0 : p->nu_fft;
     info->transfer_bytes = p->transfer_bytes;
     info->device_bytes = p->bytes;
     info->plan_ms = p->plan_ms;
@@ -728,23 +955,7 @@ void lfm_plan_destroy(lfm_plan p) { plan_free(p); }
 lfm_status lfm_forward(lfm_plan p, const float* x, float* y, void* stream) {
     g_err[0] = 0;
     if (!p || !x || !y) return fail(LFM_EINVAL, "NULL argument");
-    cudaStream_t s = as_stream(stream);
-    if (p->direct) {
-        CK(launch_image_to_poly(x, p->xb[0], p->xg, p->u0, p->nu, s));
-        ST(op_forward_poly(p, p->xb[0], y, s));
-        return LFM_OK;
-    }
-    const int N2 = p->geo.N * p->geo.N;
-    CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(SRC_IMAGE, x, nullptr, 0.f, p->nu, p->G, p->nu_pad), s));
-    CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_pad, p->num_sms, s));
-    C2RArgs c{};
-    c.dst = DST_IMAGE;
-    c.in = p->Y;
-    c.in_ld = N2;
-    c.ntrans = N2;
-    c.out = y;
-    CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
-    return allreduce(p, y, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
+    return op_forward_src(p, x, /*image=*/true, y, as_stream(stream));
 }
 
 lfm_status lfm_backward(lfm_plan p, const float* y, float* x, void* stream) {
@@ -756,7 +967,7 @@ lfm_status lfm_backward(lfm_plan p, const float* y, float* x, void* stream) {
 lfm_status lfm_normalizer(lfm_plan p, float* x, void* stream) {
     g_err[0] = 0;
     if (!p || !x) return fail(LFM_EINVAL, "NULL argument");
-    CK(launch_poly_to_image(p->norm, x, p->xg, p->u0, p->nu, as_stream(stream)));
+    CK(launch_poly_to_image(p->norm, x, p->xall, p->u0, p->nu, as_stream(stream)));
     return LFM_OK;
 }
 
@@ -766,10 +977,10 @@ lfm_status lfm_rl_step(lfm_plan p, const float* y, const float* x_in, float* x_o
     if (!p || !y || !x_in || !x_out) return fail(LFM_EINVAL, "NULL argument");
     if (!(eps > 0.0f)) return fail(LFM_EINVAL, "eps must be > 0");
     cudaStream_t s = as_stream(stream);
-    CK(launch_image_to_poly(x_in, p->xb[0], p->xg, p->u0, p->nu, s));
+    CK(launch_image_to_poly(x_in, p->xb[0], p->xall, p->u0, p->nu, s));
     ST(op_step(p, y, p->xb[0], p->xb[1], eps, region, entropy_host != nullptr, s));
     if (yhat_out) CK(cudaMemcpyAsync(yhat_out, p->yhat, (size_t)p->geo.H * p->geo.W * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    CK(launch_poly_to_image(p->xb[1], x_out, p->xg, p->u0, p->nu, s));
+    CK(launch_poly_to_image(p->xb[1], x_out, p->xall, p->u0, p->nu, s));
     if (entropy_host) {
         CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -789,7 +1000,7 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
     const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
     int cur = 0, best = -1;
     if (pol->init_from_x) {
-        CK(launch_image_to_poly(x, p->xb[cur], p->xg, p->u0, p->nu, s));
+        CK(launch_image_to_poly(x, p->xb[cur], p->xall, p->u0, p->nu, s));
     } else {
         CK(launch_fill_dev(p->xb[cur], vol, p->stats, p->norm_sum, s));   // c0 = sum y / sum H^T 1
     }
@@ -872,7 +1083,7 @@ lfm_status lfm_quality(lfm_plan p, const float* x, int region, double* entropy, 
     if (region != LFM_REGION_TRIANGLE && region != LFM_REGION_RECTANGLE) return fail(LFM_EINVAL, "region=%d", region);
     cudaStream_t s = as_stream(stream);
     CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
-    CK(launch_max_project(x, p->mproj, p->xg, s));
+    CK(launch_max_project(x, p->mproj, p->xall, s));
     ST(op_metric(p, region, s));
     CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

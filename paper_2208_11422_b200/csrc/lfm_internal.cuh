@@ -43,7 +43,8 @@ struct XformGeom {
     int N, H, W, nh, nw, nz;
     int Lh, Lw, nk2, nkappa;
     int unit0;              // first owned global unit
-    int nu, nu_pad;
+    int nu, nu_pad;         // transforms over units (FFT units of the plan) and their padded row length
+    const int* umap;        // [nu] local unit index (u - unit0) of transform t; nullptr = identity
     int kh, kw, ch, cw;
 };
 
@@ -69,7 +70,23 @@ struct C2RArgs {
     float eps;
 };
 
-struct Plan;
+// hybrid-plan direct part (kernels_direct.cu)
+constexpr int kDirMaxD = 5;   // largest per-pair tap box handled by the register-blocked direct kernels
+struct DirArgs {
+    int N, H, W, nh, nw;
+    int unit0, nu;            // owned units
+    int nzd;                  // number of direct planes
+    const int* zlist;         // [nzd] global plane index
+    int D;                    // taps per dimension (box), coefficients zero-padded to D x D
+    int dmin1, dmax1, dmin2, dmax2;   // range of the box origins dlo over all pairs and direct planes
+    const float* coef_f;      // [nzd][a][D*D][b'] (forward: output phase fastest)
+    const float* coef_b;      // [nzd][b'][D*D][a] (backward: input phase fastest)
+    const int* dlo;           // [nzd][2][N][N]: dlo1[a1][b1], dlo2[a2][b2]
+};
+cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
+                           cudaStream_t s);  // part: [nzd][H][W] scratch
+cudaError_t launch_dir_bwd(const DirArgs& d, int src, const float* img, const float* img2, float eps, int dst, float* out,
+                           const float* xold, const float* norm, cudaStream_t s);
 
 // launchers (kernels_fft.cu)
 cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,

@@ -52,7 +52,7 @@ OP_CASES = [  # (nz, N, H, W, kh, kw): tiny, ragged units, non-square, radix 2/3
 ]
 
 
-@pytest.mark.parametrize("flags", [0, 2], ids=["fft", "direct"])
+@pytest.mark.parametrize("flags", [0, 2, 4], ids=["hybrid", "direct", "fft"])
 @pytest.mark.parametrize("case", OP_CASES, ids=[str(c) for c in OP_CASES])
 def test_projections_match_oracle(case, flags):
     nz, N, H, W, kh, kw = case
@@ -74,8 +74,11 @@ def test_projections_match_oracle(case, flags):
         g = got.cpu().numpy()
         assert rel(g, ref) <= 2e-6, (rel(g, ref), info)
         assert np.abs(g - ref).max() <= 1e-5 * np.abs(ref).max()
-    if flags == 0:
+    if flags == 4:
         assert info["fft_h"] >= info["lc_min_h"] and info["fft_w"] >= info["lc_min_w"]
+        assert info["direct_planes"] == 0 and info["fft_units"] == nz * N * N
+    if flags == 2:
+        assert info["direct_planes"] == nz and info["fft_units"] == 0
 
 
 def test_adjoint_on_gpu():
@@ -132,7 +135,7 @@ def oracle_iterates(y, hd, cfg, n):
     return out, es
 
 
-@pytest.mark.parametrize("flags", [0, 2], ids=["fft", "direct"])
+@pytest.mark.parametrize("flags", [0, 2, 4], ids=["hybrid", "direct", "fft"])
 def test_rl_tiny_1_and_30_iterations(flags):
     """North star: rel-L2 <= 1e-4 after 1 iteration, <= 1e-3 after 30; E_k within 1e-4 relative."""
     cfg, h, hd, y = tiny_problem()
