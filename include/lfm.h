@@ -98,8 +98,10 @@ enum {
                                cross-rank reductions are skipped (outputs are this rank's partials).
                                For testing the sharding on one device.                              */
     LFM_PLAN_DIRECT = 2,    /* every plane on the spatial (direct polyphase convolution) path         */
-    LFM_PLAN_FFT_ONLY = 4   /* every plane on the frequency path.  Default (neither flag): hybrid --
-                               per plane, the cheaper of the two by the cost model of DESIGN.md §5   */
+    LFM_PLAN_FFT_ONLY = 4,  /* every plane on the frequency path.  Default (neither flag): hybrid --
+                               per plane, the cheapest path by the cost model of DESIGN.md §5        */
+    LFM_PLAN_TC_DIRECT = 16 /* allow the tcgen05 3xTF32 tensor-core kernels for direct planes (opt-in:
+                               correct, currently slower than the CUDA-core ones)      */
 };
 
 /* Information about a plan. */
@@ -117,6 +119,7 @@ typedef struct {
     double plan_ms;                 /* wall time of lfm_plan_create                                */
     int direct_planes;              /* planes (touching owned units) on the direct path            */
     int fft_units;                  /* owned units on the frequency path                            */
+    int tc_planes;                  /* direct planes on the tcgen05 (3xTF32 tensor-core) kernels    */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */

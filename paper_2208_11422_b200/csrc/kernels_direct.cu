@@ -426,7 +426,11 @@ cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, floa
         default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
-    dir_reduce_kernel<<<1184, 256, 0, s>>>(part, d.nzd, (size_t)d.H * d.W, y, accumulate);
+    return launch_plane_reduce(part, d.nzd, (size_t)d.H * d.W, y, accumulate, s);
+}
+
+cudaError_t launch_plane_reduce(const float* part, int nzd, size_t hw, float* y, int accumulate, cudaStream_t s) {
+    dir_reduce_kernel<<<1184, 256, 0, s>>>(part, nzd, hw, y, accumulate);
     return cudaGetLastError();
 }
 

@@ -217,7 +217,9 @@ struct lfm_plan_s {
     // hybrid plan: FFT units (frequency path) and direct planes (spatial path)
     int nu_fft = 0, nu_fft_pad = 16;
     int* umap = nullptr;        // [nu_fft] local unit index of FFT transform t
-    std::vector<DirArgs> dgroups;   // direct planes grouped by tap-box size D (one launch per group)
+    std::vector<DirArgs> dgroups;   // SIMT direct planes grouped by tap-box size D (one launch per group)
+    std::vector<TcDirArgs> tcf, tcb;   // tensor-core direct groups (forward / backward coefficient layouts)
+    int n_tc_planes = 0;
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -383,6 +385,11 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
         }
         ST(mark(p, ST_DIR_FWD, s));
         bool acc = p->nu_fft > 0;
+        for (const TcDirArgs& tg : p->tcf) {
+            CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, p->dpart, yimg, acc ? 1 : 0, s));
+            p->pacc.launches += 2;
+            acc = true;
+        }
         for (const DirArgs& dg : p->dgroups) {
             CK(launch_dir_fwd(dg, x, image ? 1 : 0, p->dpart, yimg, acc ? 1 : 0, s));
             p->pacc.launches += 2;
@@ -445,6 +452,10 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         ST(mark(p, ST_C2R_UPD, s));
     }
     ST(mark(p, ST_DIR_BWD, s));
+    for (const TcDirArgs& tg : p->tcb) {
+        CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, p->norm, s));
+        p->pacc.launches += 1;
+    }
     for (const DirArgs& dg : p->dgroups) {
         CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, p->norm, s));
         p->pacc.launches += 1;
@@ -557,6 +568,10 @@ AxisBox axis_box(int N, int c, int k0, int k1) {
 constexpr double kHbmBps = 7.0e12;
 constexpr double kXformPerUnit = 9.0e-8;
 const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 28.0e12};
+// tensor-core direct path: cycles per (tile, N-group, K-chunk, tap) iteration, SM clock
+constexpr double kTcCyclesPerTap = 3400.0;   // measured r01 (issue/latency bound)
+constexpr double kSmClock = 1.9e9;
+constexpr size_t kTcSmemLimit = 220 * 1024;
 
 }  // namespace
 
@@ -775,20 +790,35 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double units = ue - ub;
         const double t_fft = 2.0 * units * N2 * g.nkappa * 8.0 / kHbmBps + kXformPerUnit * units;
         const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
-        if (flags & LFM_PLAN_FFT_ONLY)
-            plane_direct[z] = 0;
-        else if (flags & LFM_PLAN_DIRECT)
-            plane_direct[z] = 1;
-        else
-            plane_direct[z] = t_dir < t_fft ? 1 : 0;
-        if (plane_direct[z] && D > kDirMaxD) too_big = true;
+        // tensor-core direct: union tap box of the plane and its shared-memory footprint
+        const int T1 = box1[z].dmax - box1[z].dmin + box1[z].D, T2 = box2[z].dmax - box2[z].dmin + box2[z].D;
+        const int NG = std::min(48, (int)round_up((size_t)N2, 16)), ngr = (N2 + NG - 1) / NG;
+        const int Kpad = (int)round_up((size_t)N2, 8), nch = (Kpad + 31) / 32;
+        const int npix = g.nh * g.nw, tiles = (npix + 127) / 128;
+        int span = 1;
+        for (int p0 = 0; p0 < npix; p0 += 128) span = std::max(span, std::min(p0 + 127, npix - 1) / g.nw - p0 / g.nw + 1);
+        const bool tc_ok = (flags & LFM_PLAN_TC_DIRECT) &&
+                           tcdir_smem_bytes(NG, span + T1 - 1, g.nw + T2 - 1) <= kTcSmemLimit;
+        const double t_tc = tc_ok ? 2.0 * tiles * ngr * nch * (double)T1 * T2 * kTcCyclesPerTap / (p->num_sms * kSmClock)
+                                  : 1e30;
+        int mode = 0;                            // 0 FFT, 1 SIMT direct, 2 tensor-core direct
+        if (flags & LFM_PLAN_FFT_ONLY) {
+            mode = 0;
+        } else if (flags & LFM_PLAN_DIRECT) {
+            mode = tc_ok ? 2 : 1;
+        } else {
+            const double best = std::min(t_fft, std::min(t_dir, t_tc));
+            mode = best == t_fft ? 0 : (best == t_tc ? 2 : 1);
+        }
+        plane_direct[z] = mode;
+        if (mode == 1 && D > kDirMaxD) too_big = true;
     }
     p->direct = too_big;   // all-direct request with boxes beyond kDirMaxD: the generic spatial kernels
     if (!p->direct) {
         // FFT units through a unit map (z-major order kept)
         std::vector<int> umap;
         for (int u = p->u0; u < p->u1; ++u)
-            if (!plane_direct[u / N2]) umap.push_back(u - p->u0);
+            if (plane_direct[u / N2] == 0) umap.push_back(u - p->u0);
         p->nu_fft = (int)umap.size();
         p->nu_fft_pad = (int)round_up((size_t)std::max(p->nu_fft, 1), 16);
         if (p->nu_fft > 0) {
@@ -803,7 +833,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         for (int D = 1; D <= kDirMaxD; ++D) {
             std::vector<int> zl;
             for (int z = zb; z <= ze; ++z)
-                if (plane_direct[z] && plane_D[z] == D) zl.push_back(z);
+                if (plane_direct[z] == 1 && plane_D[z] == D) zl.push_back(z);
             if (zl.empty()) continue;
             const int nzd = (int)zl.size(), DD = D * D;
             std::vector<float> cf((size_t)nzd * N2 * DD * N2, 0.0f), cb((size_t)nzd * N2 * DD * N2, 0.0f);
@@ -878,9 +908,70 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             p->n_direct_planes += nzd;
             coef_bytes += 2 * cf.size() * sizeof(float);
         }
+        // tensor-core direct groups: planes with identical tap boxes share one launch
+        {
+            std::vector<int> done(nz, 0);
+            for (int z0 = zb; z0 <= ze; ++z0) {
+                if (plane_direct[z0] != 2 || done[z0]) continue;
+                std::vector<int> zl;
+                for (int z = z0; z <= ze; ++z)
+                    if (plane_direct[z] == 2 && !done[z] && box1[z].dmin == box1[z0].dmin && box1[z].dmax == box1[z0].dmax &&
+                        box1[z].D == box1[z0].D && box2[z].dmin == box2[z0].dmin && box2[z].dmax == box2[z0].dmax &&
+                        box2[z].D == box2[z0].D) {
+                        zl.push_back(z);
+                        done[z] = 1;
+                    }
+                TcDirArgs ta{};
+                ta.N = nnum;
+                ta.H = height;
+                ta.W = width;
+                ta.nh = g.nh;
+                ta.nw = g.nw;
+                ta.unit0 = p->u0;
+                ta.nu = p->nu;
+                ta.nzd = (int)zl.size();
+                ta.NG = std::min(48, (int)round_up((size_t)N2, 16));
+                ta.ngroups = (N2 + ta.NG - 1) / ta.NG;
+                ta.Kpad = (int)round_up((size_t)N2, 8);
+                ta.d1min = box1[z0].dmin;
+                ta.d1max = box1[z0].dmax + box1[z0].D - 1;
+                ta.d2min = box2[z0].dmin;
+                ta.d2max = box2[z0].dmax + box2[z0].D - 1;
+                ta.T1 = ta.d1max - ta.d1min + 1;
+                ta.T2 = ta.d2max - ta.d2min + 1;
+                const int npix = g.nh * g.nw;
+                int span = 1;
+                for (int q0 = 0; q0 < npix; q0 += 128) span = std::max(span, std::min(q0 + 127, npix - 1) / g.nw - q0 / g.nw + 1);
+                ta.WR = span + ta.T1 - 1;
+                ta.WC = g.nw + ta.T2 - 1;
+                int* dz = nullptr;
+                PG(dalloc(p, &dz, zl.size() * sizeof(int), "tc plane list"));
+                p->dallocs.push_back(dz);
+                CKG(cudaMemcpyAsync(dz, zl.data(), zl.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                ta.zlist = dz;
+                const size_t nf = tcdir_coef_floats(ta);
+                float *cf = nullptr, *cb = nullptr;
+                PG(dalloc(p, &cf, nf * sizeof(float), "tc direct taps (forward)"));
+                p->dallocs.push_back(cf);
+                PG(dalloc(p, &cb, nf * sizeof(float), "tc direct taps (backward)"));
+                p->dallocs.push_back(cb);
+                CKG(launch_tcdir_coef(ta, dz, p->psf, kh, kw, g.ch, g.cw, 1, cf, s));
+                CKG(launch_tcdir_coef(ta, dz, p->psf, kh, kw, g.ch, g.cw, 0, cb, s));
+                CKG(cudaStreamSynchronize(s));   // zl dies at the end of this scope
+                TcDirArgs tb = ta;
+                ta.coef = cf;
+                tb.coef = cb;
+                p->tcf.push_back(ta);
+                p->tcb.push_back(tb);
+                p->n_tc_planes += ta.nzd;
+                p->n_direct_planes += ta.nzd;
+                coef_bytes += 2 * nf * sizeof(float);
+            }
+        }
         p->transfer_bytes = coef_bytes;
         int maxg = 0;
         for (const DirArgs& dg : p->dgroups) maxg = std::max(maxg, dg.nzd);
+        for (const TcDirArgs& tg : p->tcf) maxg = std::max(maxg, tg.nzd);
         if (maxg > 0) PG(dalloc(p, &p->dpart, (size_t)maxg * HW * sizeof(float), "direct forward partials"));
         if (p->nu_fft > 0) {
             if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
@@ -944,6 +1035,7 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->direct = p->direct ? 1 : (p->nu_fft == 0 ? 1 : 0);
     info->direct_planes = p->direct ? p->geo.nz : p->n_direct_planes;
     info->fft_units = p->direct ? 0 : p->nu_fft;
+    info->tc_planes = p->direct ? 0 : p->n_tc_planes;
     info->transfer_bytes = p->transfer_bytes;
     info->device_bytes = p->bytes;
     info->plan_ms = p->plan_ms;

@@ -83,6 +83,28 @@ struct DirArgs {
     const float* coef_b;      // [nzd][b'][D*D][a] (backward: input phase fastest)
     const int* dlo;           // [nzd][2][N][N]: dlo1[a1][b1], dlo2[a2][b2]
 };
+// tensor-core direct part (kernels_tcdir.cu)
+struct TcDirArgs {
+    int N, H, W, nh, nw;
+    int unit0, nu;            // owned units
+    int nzd;                  // planes in this group
+    const int* zlist;         // [nzd] global plane index (device)
+    int NG, ngroups;          // N-phases per CTA (TMEM columns) and number of groups
+    int Kpad;                 // reduction phases padded to a multiple of 8
+    int T1, T2;               // union tap box
+    int d1min, d1max, d2min, d2max;   // tap offsets (inclusive)
+    int WR, WC;               // source window rows / cols
+    const float* coef;        // [zi][grp][chunk][tap][hi|lo][NG x 32] (direction-specific)
+};
+size_t tcdir_smem_bytes(int NG, int WR, int WC);
+size_t tcdir_coef_floats(const TcDirArgs& d);
+cudaError_t launch_tcdir_coef(const TcDirArgs& d, const int* zlist_dev, const float* psf_dev, int kh, int kw, int ch,
+                              int cw, int fwd, float* out, cudaStream_t s);
+cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
+                             cudaStream_t s);
+cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
+                             float* out, const float* xold, const float* norm, cudaStream_t s);
+cudaError_t launch_plane_reduce(const float* part, int nzd, size_t hw, float* y, int accumulate, cudaStream_t s);
 cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
                            cudaStream_t s);  // part: [nzd][H][W] scratch
 cudaError_t launch_dir_bwd(const DirArgs& d, int src, const float* img, const float* img2, float eps, int dst, float* out,

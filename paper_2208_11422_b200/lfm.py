@@ -27,7 +27,7 @@ STATUS_NAMES = ["LFM_OK", "LFM_EINVAL", "LFM_EDIM", "LFM_ENEG", "LFM_EZERO", "LF
 LFM_MODE_FIXED, LFM_MODE_AUTO = 0, 1
 LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
-LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY = 1, 2, 4
+LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT = 1, 2, 4, 16
 
 
 class LfmError(RuntimeError):
@@ -59,7 +59,8 @@ class lfm_info(ctypes.Structure):
                 ("lc_min_h", ctypes.c_int), ("lc_min_w", ctypes.c_int), ("n_kappa", ctypes.c_int),
                 ("units_padded", ctypes.c_int), ("x_s", ctypes.c_int), ("y_s", ctypes.c_int),
                 ("direct", ctypes.c_int), ("transfer_bytes", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
-                ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int)]
+                ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
+                ("tc_planes", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -1,6 +1,8 @@
 """GPU parity (marked gpu): the CUDA path, called through the C ABI, against the fp64 oracle on the
-same seeded inputs.  Tolerances: operators rel-L2 <= 2e-6 and max-abs <= 1e-5 * max|ref|
-(fp32 FFT + fp32 MAC over nz N^2 terms, measured ~1e-7); RL rel-L2 <= 1e-4 after 1 iteration and
+same seeded inputs.  Tolerances: operators rel-L2 <= 2e-6 and max-abs <= 1e-5 * max|ref| on
+the CUDA-core paths (fp32 FFT + fp32 MAC over nz N^2 terms, measured ~1e-7); <= 1e-5 rel-L2 / 2e-5 max-abs
+when planes run on the tcgen05 3xTF32 path (its fp32 accumulation truncates: measured bias 3e-6..7e-6
+relative over ~250 chained MMAs); RL rel-L2 <= 1e-4 after 1 iteration and
 <= 1e-3 after 30 (BASELINE.json north star); identical stop / best iteration unless the decision margin is
 within 10x the observed entropy error (reading C16)."""
 import numpy as np
@@ -33,6 +35,11 @@ def optics(nnum):
     return L().make_optics(**OPTICS)
 
 
+def op_tol(info):
+    """(rel-L2, max-abs/max) operator tolerance: CUDA-core paths 2e-6 / 1e-5; tcgen05 3xTF32 planes 1e-5 / 2e-5."""
+    return (1e-5, 2e-5) if info.get("tc_planes", 0) > 0 else (2e-6, 1e-5)
+
+
 def rand_case(seed, nz, N, H, W, kh, kw):
     rng = np.random.default_rng(seed)
     h = rng.uniform(0, 1, (nz, N, N, kh, kw)).astype(np.float32)
@@ -52,7 +59,7 @@ OP_CASES = [  # (nz, N, H, W, kh, kw): tiny, ragged units, non-square, radix 2/3
 ]
 
 
-@pytest.mark.parametrize("flags", [0, 2, 4], ids=["hybrid", "direct", "fft"])
+@pytest.mark.parametrize("flags", [0, 2, 4, 18, 16], ids=["hybrid", "direct", "fft", "direct-tc", "hybrid-tc"])
 @pytest.mark.parametrize("case", OP_CASES, ids=[str(c) for c in OP_CASES])
 def test_projections_match_oracle(case, flags):
     nz, N, H, W, kh, kw = case
@@ -70,14 +77,15 @@ def test_projections_match_oracle(case, flags):
     y_ref = O.forward_project(x.astype(np.float64), hd)
     xb_ref = O.backward_project(r.astype(np.float64), hd)
     nrm_ref = O.compute_normalizer(hd, H, W)
+    tol, mtol = op_tol(info)
     for got, ref in [(y_d, y_ref), (xb_d, xb_ref), (nrm_d, nrm_ref)]:
         g = got.cpu().numpy()
-        assert rel(g, ref) <= 2e-6, (rel(g, ref), info)
-        assert np.abs(g - ref).max() <= 1e-5 * np.abs(ref).max()
+        assert rel(g, ref) <= tol, (rel(g, ref), info)
+        assert np.abs(g - ref).max() <= mtol * np.abs(ref).max()
     if flags == 4:
         assert info["fft_h"] >= info["lc_min_h"] and info["fft_w"] >= info["lc_min_w"]
         assert info["direct_planes"] == 0 and info["fft_units"] == nz * N * N
-    if flags == 2:
+    if flags & 2:
         assert info["direct_planes"] == nz and info["fft_units"] == 0
 
 
@@ -95,23 +103,25 @@ def test_adjoint_on_gpu():
     assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
 
 
-def test_c2_operators_match_oracle():
+@pytest.mark.parametrize("flags", [0, 18], ids=["hybrid", "direct-tc"])
+def test_c2_operators_match_oracle(flags):
     """BASELINE configs[1] geometry (N=11, 319^2, 21 planes, K=99): full-image operator parity."""
     cfg = CONFIGS["c2"]
     h = gen_psf(cfg, np.float32)
     x = gen_volume(cfg, 1, np.float32)
-    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+        tol = op_tol(plan.info())[0]
         y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
         plan.forward(dev(x), y_d)
         torch.cuda.synchronize()
         y_ref = O.forward_project(x.astype(np.float64), h.astype(np.float64))
-        assert rel(y_d.cpu().numpy(), y_ref) <= 2e-6
+        assert rel(y_d.cpu().numpy(), y_ref) <= tol
         r = (y_ref + 1.0) / (y_ref.mean() + 1.0)
         xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
         plan.backward(dev(r), xb_d)
         torch.cuda.synchronize()
     xb_ref = O.backward_project(r.astype(np.float32).astype(np.float64), h.astype(np.float64))
-    assert rel(xb_d.cpu().numpy(), xb_ref) <= 2e-6
+    assert rel(xb_d.cpu().numpy(), xb_ref) <= tol
 
 
 def tiny_problem(name="tiny", seed=1):
@@ -135,7 +145,7 @@ def oracle_iterates(y, hd, cfg, n):
     return out, es
 
 
-@pytest.mark.parametrize("flags", [0, 2, 4], ids=["hybrid", "direct", "fft"])
+@pytest.mark.parametrize("flags", [0, 2, 4, 18], ids=["hybrid", "direct", "fft", "direct-tc"])
 def test_rl_tiny_1_and_30_iterations(flags):
     """North star: rel-L2 <= 1e-4 after 1 iteration, <= 1e-3 after 30; E_k within 1e-4 relative."""
     cfg, h, hd, y = tiny_problem()
@@ -181,11 +191,11 @@ def stop_parity(cfg, h, hd, y, max_iters=50, flags=0):
     return res, res_o, err, margin, x_d
 
 
-@pytest.mark.parametrize("name,seed", [("tiny", 1), ("tiny", 3), ("s15", 1)])
-def test_auto_stop_identical(name, seed):
+@pytest.mark.parametrize("name,seed,flags", [("tiny", 1, 0), ("tiny", 3, 0), ("s15", 1, 0), ("s15", 1, 18)])
+def test_auto_stop_identical(name, seed, flags):
     """Identical stop_iter and best_iter vs the oracle (P:99 stop rule) unless tie-ambiguous (C16)."""
     cfg, h, hd, y = tiny_problem(name, seed)
-    res, res_o, err, margin, x_d = stop_parity(cfg, h, hd, y)
+    res, res_o, err, margin, x_d = stop_parity(cfg, h, hd, y, flags=flags)
     assert err <= 1e-4
     if margin <= 10 * err:
         pytest.skip(f"tie-ambiguous: decision margin {margin:.2e} <= 10 x entropy error {err:.2e} (C16)")
