@@ -80,7 +80,8 @@ typedef struct {
     float eps;        /* division guard, default 1e-6 (C3)                                         */
     int region;       /* LFM_REGION_TRIANGLE (default) or LFM_REGION_RECTANGLE (C11)               */
     int init_from_x;  /* 0: x0 = c0 = sum(y) / sum(H^T 1) uniform (C2); 1: caller's x is x0 (resume) */
-    int update;       /* LFM_UPDATE_RL (default).  LFM_UPDATE_ISRA -> LFM_EUNSUPPORTED in this build */
+    int update;       /* LFM_UPDATE_RL (default) or LFM_UPDATE_ISRA (MATLAB-lineage x * H^T y / H^T H x, x0 = H^T y unless
+                         init_from_x; reading C1)                                          */
 } lfm_policy;
 
 /* Distribution.  world == 1: single GPU, no communicator.  world > 1: nccl_id is the 128-byte

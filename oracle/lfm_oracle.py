@@ -379,8 +379,9 @@ class DeconvResult:
 
 
 def deconvolve(y, h, optics: Optics, policy: Policy, x0=None, region_shape="triangle",
-               keep_iterates=False):
-    """RL loop with the DCT-entropy stop rule.  Rejects all-zero y."""
+               keep_iterates=False, update="rl"):
+    """RL loop with the DCT-entropy stop rule.  Rejects all-zero y.
+    update="isra": the MATLAB-lineage form x * H^T y / H^T H x starting from x0 = H^T y (reading C1)."""
     y = np.asarray(y, dtype=np.float64)
     if np.any(y < 0):
         raise ValueError("negative measurement")
@@ -389,13 +390,20 @@ def deconvolve(y, h, optics: Optics, policy: Policy, x0=None, region_shape="tria
     nz, N, kh, kw = _psf_dims(np.asarray(h))
     H, W = y.shape
     region = cutoff_region(optics, H, W, region_shape)
-    norm = compute_normalizer(h, H, W)
-    x = initial_volume(y, h, nz, H, W) if x0 is None else np.array(x0, dtype=np.float64)
+    if update == "isra":
+        hty = backward_project(y, h)
+        x = hty.copy() if x0 is None else np.array(x0, dtype=np.float64)
+    else:
+        norm = compute_normalizer(h, H, W)
+        x = initial_volume(y, h, nz, H, W) if x0 is None else np.array(x0, dtype=np.float64)
     rule = StopRule(policy)
     best = x.copy()
     iterates = []
     while True:
-        x, _ = rl_step(x, y, h, norm, policy.eps)
+        if update == "isra":
+            x, _ = isra_step(x, y, h, hty, policy.eps)
+        else:
+            x, _ = rl_step(x, y, h, norm, policy.eps)
         if keep_iterates:
             iterates.append(x.copy())
         improved, stop = rule.update(evaluate_iteration(x, region))

@@ -93,8 +93,10 @@ __global__ void __launch_bounds__(256) direct_bwd_kernel(const float* __restrict
             out[pidx] = acc;
         } else if (dst == DST_VOLIMAGE) {
             out[((size_t)z * g.H + p) * g.W + q] = acc;
+        } else if (dst == DST_ISRA) {
+            out[pidx] = update_value<DST_ISRA>(xold[pidx], norm[pidx], acc, eps);
         } else {  // DST_UPDATE
-            out[pidx] = xold[pidx] * fmaxf(acc, 0.0f) / fmaxf(norm[pidx], eps);
+            out[pidx] = update_value<DST_UPDATE>(xold[pidx], norm[pidx], acc, eps);
         }
     }
 }
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(DirCfg<D>::THREADS) dir_bwd_kernel(DirArgs d, 
                         } else if constexpr (DST == DST_VOLIMAGE) {
                             out[((size_t)z * d.H + a1 + N * m1) * d.W + a2 + N * m2] = v;
                         } else {
-                            out[pidx] = xold[pidx] * fmaxf(v, 0.0f) / fmaxf(norm[pidx], eps);
+                            out[pidx] = update_value<DST>(xold[pidx], norm[pidx], v, eps);
                         }
                     }
                 }
@@ -405,6 +407,7 @@ static cudaError_t dir_bwd_D(const DirArgs& d, int src, const float* img, const 
 #define LFM_DIR_B(SRCV, DSTV) \
     if (src == SRCV && dst == DSTV) return dir_bwd_DSD<D, SRCV, DSTV>(d, img, img2, eps, out, xold, norm, s);
     LFM_DIR_B(SRC_RATIO, DST_UPDATE)
+    LFM_DIR_B(SRC_IMAGE2D, DST_ISRA)
     LFM_DIR_B(SRC_ONES, DST_POLY)
     LFM_DIR_B(SRC_IMAGE2D, DST_VOLIMAGE)
     LFM_DIR_B(SRC_IMAGE2D, DST_POLY)

@@ -219,9 +219,9 @@ __global__ void __launch_bounds__(512) c2r_kernel(XformGeom g, FftDesc fh, FftDe
             const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
             if constexpr (DST == DST_VOLIMAGE) {
                 a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
-            } else {  // DST_UPDATE
+            } else {  // DST_UPDATE / DST_ISRA
                 const size_t pidx = ((size_t)lu * nh + i) * nw + j;
-                a.out[pidx] = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
+                a.out[pidx] = update_value<DST>(a.xold[pidx], a.norm[pidx], v, a.eps);
             }
         }
     }
@@ -301,6 +301,7 @@ cudaError_t launch_c2r(const XformGeom& g, const FftDesc& fh, const FftDesc& fw,
         LFM_C2R_CASE(DST_POLY)
         LFM_C2R_CASE(DST_VOLIMAGE)
         LFM_C2R_CASE(DST_UPDATE)
+        LFM_C2R_CASE(DST_ISRA)
         default: return cudaErrorInvalidValue;
     }
 #undef LFM_C2R_CASE

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
                         a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
                     } else {
                         const size_t pidx = ((size_t)lu * nh + i) * nw + j;
-                        a.out[pidx] = a.xold[pidx] * fmaxf(v, 0.0f) / fmaxf(a.norm[pidx], a.eps);
+                        a.out[pidx] = update_value<DST>(a.xold[pidx], a.norm[pidx], v, a.eps);
                     }
                 }
             }
@@ -368,6 +368,7 @@ static cudaError_t c2r_fast_L(const XformGeom& g, const float2* tw, const C2RArg
         LFM_FAST_C2R(DST_POLY)
         LFM_FAST_C2R(DST_VOLIMAGE)
         LFM_FAST_C2R(DST_UPDATE)
+        LFM_FAST_C2R(DST_ISRA)
         default: return cudaErrorInvalidValue;
     }
 #undef LFM_FAST_C2R

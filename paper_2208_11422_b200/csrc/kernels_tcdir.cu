@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcdir_kernel(TcDirArgs d, const
                         const int a1 = n / N, a2 = n - (n / N) * N;
                         out[((size_t)z * d.H + a1 + N * m1) * d.W + a2 + N * m2] = acc[i];
                     } else {
-                        out[pidx] = xold[pidx] * fmaxf(acc[i], 0.0f) / fmaxf(norm[pidx], eps);
+                        out[pidx] = update_value<DST>(xold[pidx], norm[pidx], acc[i], eps);
                     }
                 }
             }
@@ -331,6 +331,7 @@ cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, cons
 #define LFM_TCB(SRCV, DSTV) \
     if (src == SRCV && dst == DSTV) return tcdir_launch<false, SRCV, DSTV>(d, img, img2, eps, out, xold, norm, s);
     LFM_TCB(SRC_RATIO, DST_UPDATE)
+    LFM_TCB(SRC_IMAGE2D, DST_ISRA)
     LFM_TCB(SRC_ONES, DST_POLY)
     LFM_TCB(SRC_IMAGE2D, DST_VOLIMAGE)
     LFM_TCB(SRC_IMAGE2D, DST_POLY)

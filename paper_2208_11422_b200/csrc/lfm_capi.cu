@@ -228,6 +228,7 @@ struct lfm_plan_s {
     float2* M = nullptr;
     float* psf = nullptr;       // owned PSF slice (direct mode)
     float* norm = nullptr;
+    float* hty = nullptr;       // H^T y (ISRA), allocated on first use
     double* norm_sum = nullptr; // device scalar, summed over ranks
     float* xb[3] = {nullptr, nullptr, nullptr};
     float* xfull = nullptr;     // gather buffer (world > 1)
@@ -279,6 +280,7 @@ void plan_free(lfm_plan p) {
     cudaFree(p->M);
     cudaFree(p->psf);
     cudaFree(p->norm);
+    cudaFree(p->hty);
     cudaFree(p->norm_sum);
     for (auto& x : p->xb) cudaFree(x);
     cudaFree(p->xfull);
@@ -407,9 +409,11 @@ lfm_status op_forward_poly(lfm_plan p, const float* xp, float* yimg, cudaStream_
 
 // backward projection of an image source into one of the C2R destinations
 //   src: SRC_RATIO (img = y, img2 = yhat), SRC_ONES, SRC_IMAGE2D (img)
+// aux: the update's second volume (nullptr -> the normalizer H^T 1; ISRA passes H^T y)
 lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2, float eps, int dst, float* out,
-                       const float* xold, cudaStream_t s) {
+                       const float* xold, cudaStream_t s, const float* aux = nullptr) {
     const int N2 = p->geo.N * p->geo.N;
+    if (!aux) aux = p->norm;
     ST(mark(p, ST_R2C_RATIO, s));
     if (p->direct) {
         const size_t n = (size_t)p->geo.H * p->geo.W;
@@ -426,7 +430,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         ST(mark(p, ST_BWD_MAC, s));
         ST(mark(p, ST_C2R_UPD, s));
         ST(mark(p, ST_DIR_BWD, s));
-        CK(launch_direct_bwd(r, p->psf, out, dst, xold, p->norm, p->mproj, eps, p->xall, s));
+        CK(launch_direct_bwd(r, p->psf, out, dst, xold, aux, p->mproj, eps, p->xall, s));
         p->pacc.launches += 1;
         ST(mark(p, ST_MAXPROJ, s));
         return LFM_OK;
@@ -443,7 +447,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         c.ntrans = p->nu_fft;
         c.out = out;
         c.xold = xold;
-        c.norm = p->norm;
+        c.norm = aux;
         c.eps = eps;
         CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
         p->pacc.launches += 3;
@@ -453,11 +457,11 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     }
     ST(mark(p, ST_DIR_BWD, s));
     for (const TcDirArgs& tg : p->tcb) {
-        CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, p->norm, s));
+        CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s));
         p->pacc.launches += 1;
     }
     for (const DirArgs& dg : p->dgroups) {
-        CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, p->norm, s));
+        CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, aux, s));
         p->pacc.launches += 1;
     }
     ST(mark(p, ST_MAXPROJ, s));
@@ -476,11 +480,16 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
     return LFM_OK;
 }
 
-// one RL iteration on polyphase volumes: xn = xc * H^T(y/(max(H xc,0)+eps)) / max(norm,eps); metric -> met.out[0]
+// one iteration on polyphase volumes, then the z max-projection and (optionally) the metric -> met.out[0]
+//   RL   (C1): xn = xc * H^T(y/(max(H xc,0)+eps)) / max(H^T 1, eps)
+//   ISRA (f3): xn = xc * H^T y / max(H^T H xc, eps)           (hty = H^T y, polyphase)
 lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float eps, int region, bool metric,
-                   cudaStream_t s) {
+                   cudaStream_t s, int update = LFM_UPDATE_RL, const float* hty = nullptr) {
     ST(op_forward_poly(p, xc, p->yhat, s));
-    ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
+    if (update == LFM_UPDATE_ISRA)
+        ST(op_backward(p, SRC_IMAGE2D, p->yhat, nullptr, eps, DST_ISRA, xn, xc, s, hty));
+    else
+        ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
     CK(launch_max_project_poly(xn, p->mproj, p->xall, s));     // a7: z max-projection, every pixel written
     p->pacc.launches += 1;
     if (metric) ST(op_metric(p, region, s));
@@ -497,8 +506,7 @@ lfm_status check_policy(const lfm_policy* pol) {
     if (!(pol->eps > 0.0f)) return fail(LFM_EINVAL, "policy.eps must be > 0");
     if (pol->region != LFM_REGION_TRIANGLE && pol->region != LFM_REGION_RECTANGLE)
         return fail(LFM_EINVAL, "policy.region=%d", pol->region);
-    if (pol->update == LFM_UPDATE_ISRA) return fail(LFM_EUNSUPPORTED, "policy.update=ISRA is not implemented in this build");
-    if (pol->update != LFM_UPDATE_RL) return fail(LFM_EINVAL, "policy.update=%d", pol->update);
+    if (pol->update != LFM_UPDATE_RL && pol->update != LFM_UPDATE_ISRA) return fail(LFM_EINVAL, "policy.update=%d", pol->update);
     return LFM_OK;
 }
 
@@ -1091,8 +1099,15 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
     ST(check_y(p, y, s));
     const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
     int cur = 0, best = -1;
+    const bool isra = pol->update == LFM_UPDATE_ISRA;
+    if (isra) {   // H^T y once per call (polyphase, owned units)
+        if (!p->hty) ST(dalloc(p, &p->hty, vol * sizeof(float), "H^T y"));
+        ST(op_backward(p, SRC_IMAGE2D, y, nullptr, 1.0f, DST_POLY, p->hty, nullptr, s));
+    }
     if (pol->init_from_x) {
         CK(launch_image_to_poly(x, p->xb[cur], p->xall, p->u0, p->nu, s));
+    } else if (isra) {
+        CK(cudaMemcpyAsync(p->xb[cur], p->hty, vol * sizeof(float), cudaMemcpyDeviceToDevice, s));   // x0 = H^T y
     } else {
         CK(launch_fill_dev(p->xb[cur], vol, p->stats, p->norm_sum, s));   // c0 = sum y / sum H^T 1
     }
@@ -1104,7 +1119,7 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         int nxt = 0;
         while (nxt == cur || nxt == best) ++nxt;
         if (ms_host) CK(cudaEventRecord(p->ev0, s));
-        ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s));
+        ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty));
         if (ms_host) CK(cudaEventRecord(p->ev1, s));
         CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -36,8 +36,18 @@ enum C2RDst : int {
     DST_IMAGE = 0,    // yhat image [H][W] at (b1 + N i, b2 + N j); t = output phase
     DST_POLY = 1,     // polyphase volume; t = local unit
     DST_VOLIMAGE = 2, // image-layout volume [nz][H][W]; t = local unit
-    DST_UPDATE = 3    // x_new = x_old * max(bp,0) / max(norm,eps) (poly)
+    DST_UPDATE = 3,   // RL:   x_new = x_old * max(bp,0) / max(norm,eps) (poly)
+    DST_ISRA = 4      // ISRA: x_new = x_old * max(aux,0) / max(bp,eps), aux = H^T y, bp = H^T H x (poly)
 };
+
+// multiplicative update epilogues (aux = normalizer H^T 1 for RL, H^T y for ISRA)
+template <int DST>
+__device__ __forceinline__ float update_value(float xold, float aux, float bp, float eps) {
+    if constexpr (DST == DST_ISRA)
+        return xold * fmaxf(aux, 0.0f) / fmaxf(bp, eps);
+    else
+        return xold * fmaxf(bp, 0.0f) / fmaxf(aux, eps);
+}
 
 struct XformGeom {
     int N, H, W, nh, nw, nz;
@@ -66,7 +76,7 @@ struct C2RArgs {
     int ntrans;
     float* out;             // see C2RDst
     const float* xold;      // DST_UPDATE
-    const float* norm;      // DST_UPDATE
+    const float* norm;      // DST_UPDATE: H^T 1; DST_ISRA: H^T y
     float eps;
 };
 

@@ -289,8 +289,8 @@ def test_error_statuses():
             plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(min_iters=9, max_iters=3))
         assert e.value.status == L_.LFM_EINVAL
         with pytest.raises(L_.LfmError) as e:
-            plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(update="isra"))
-        assert e.value.status == L_.LFM_EUNSUPPORTED
+            plan.rl_iterate(torch.ones((9, 9), device="cuda"), x_d, L_.make_policy(eps=0.0))
+        assert e.value.status == L_.LFM_EINVAL
 
 
 def test_host_buffer_call_and_quality():
@@ -386,3 +386,19 @@ def test_c3_one_rl_step_sampled(c3_plan):
             ref = x0d[z, p, q] * bp / max(nrm, O.EPS)
             assert abs(x1[z, p, q] - ref) <= 1e-5 * abs(ref), (z, p, q, x1[z, p, q], ref)
     assert e > 0
+
+
+@pytest.mark.parametrize("flags", [0, 2, 4, 18], ids=["hybrid", "direct", "fft", "direct-tc"])
+def test_isra_matches_oracle(flags):
+    """MATLAB-lineage ISRA update x * H^T y / H^T H x from x0 = H^T y; 1 and 10 iterations."""
+    cfg, h, hd, y = tiny_problem(seed=5)
+    for n, tol in [(1, 1e-4), (10, 1e-3)]:
+        ref = O.deconvolve(y, hd, O.Optics(nnum=cfg.nnum, **OPTICS), O.Policy(mode="fixed", n_iters=n),
+                           update="isra", keep_iterates=True)
+        with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+            x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=n, update="isra"))
+            torch.cuda.synchronize()
+        assert res["best_iter"] == ref.best_iter
+        assert rel(x_d.cpu().numpy(), ref.iterates[res["best_iter"] - 1]) <= tol
+        np.testing.assert_allclose(res["series"], ref.series, rtol=1e-4)
