@@ -151,8 +151,10 @@ lfm_status lfm_plan_estimate(int nnum, int nz, int kh, int kw, int height, int w
  * the next reconstruction").
  *   psf_host   : host [nz][N][N][kh][kw] fp32, >= 0 (LFM_ENEG otherwise).  Only this rank's units are
  *                copied to the device.  Not retained.
- *   psf_t_host : must be NULL (exact adjoint = rot180 of psf per phase, C6); a supplied transposed
- *                PSF returns LFM_EUNSUPPORTED in this build.
+ *   psf_t_host : NULL -> backward = exact adjoint of psf (C6).  Else host [nz][N][N][kh][kw] >= 0, the MATLAB
+ *                lineage "Ht": backward(r)(z,p,q) = sum_{s,t} r(s,t) Ht[z][p%N][q%N](p-s+ch, q-t+cw), which
+ *                equals the exact adjoint when Ht = rot180(psf) per kernel.  Not retained; costs a
+ *                second set of transfer matrices / direct taps.
  *   nnum       : N, odd >= 1.  height, width divisible by N.  kh, kw odd.
  *   optics     : for the metric region (may be NULL: lfm_quality / auto mode then return LFM_EINVAL).
  *   dist       : NULL means single GPU.

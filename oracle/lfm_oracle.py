@@ -152,6 +152,13 @@ def backward_points(r, h, z_idx, p_idx, q_idx):
     return out
 
 
+def backward_project_ht(r, ht):
+    """MATLAB-lineage backward with a supplied transposed PSF (reading C6):
+    xhat(z,p,q) = sum_{s,t} r(s,t) Ht[z][p%N][q%N](p-s+ch, q-t+cw).  Since Ht(p-s+c) = rot180(Ht)(s-p+c), this is
+    the adjoint formula of S:208 evaluated with the kernel bank rot180(Ht)."""
+    return backward_project(r, np.ascontiguousarray(np.asarray(ht, dtype=np.float64)[:, :, :, ::-1, ::-1]))
+
+
 def compute_normalizer(h, H, W, units=None):
     """H^T 1: backward projection of the all-ones image; the RL denominator."""
     return backward_project(np.ones((H, W)), h, units=units)

@@ -226,7 +226,9 @@ struct lfm_plan_s {
     int num_sms = 148;
     float2 *tw_h = nullptr, *tw_w = nullptr;
     float2* M = nullptr;
-    float* psf = nullptr;       // owned PSF slice (direct mode)
+    float* psf = nullptr;       // owned PSF slice (generic direct mode)
+    float* psfb = nullptr;      // owned backward PSF slice = rot180(supplied Ht), or == psf (exact adjoint)
+    float2* Mb = nullptr;       // backward transfer matrices (== M unless Ht is supplied)
     float* norm = nullptr;
     float* hty = nullptr;       // H^T y (ISRA), allocated on first use
     double* norm_sum = nullptr; // device scalar, summed over ranks
@@ -277,7 +279,9 @@ void plan_free(lfm_plan p) {
     cudaFree(p->umap);
     for (void* q : p->dallocs) cudaFree(q);
     cudaFree(p->dpart);
+    if (p->Mb && p->Mb != p->M) cudaFree(p->Mb);
     cudaFree(p->M);
+    if (p->psfb && p->psfb != p->psf) cudaFree(p->psfb);
     cudaFree(p->psf);
     cudaFree(p->norm);
     cudaFree(p->hty);
@@ -430,7 +434,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         ST(mark(p, ST_BWD_MAC, s));
         ST(mark(p, ST_C2R_UPD, s));
         ST(mark(p, ST_DIR_BWD, s));
-        CK(launch_direct_bwd(r, p->psf, out, dst, xold, aux, p->mproj, eps, p->xall, s));
+        CK(launch_direct_bwd(r, p->psfb, out, dst, xold, aux, p->mproj, eps, p->xall, s));
         p->pacc.launches += 1;
         ST(mark(p, ST_MAXPROJ, s));
         return LFM_OK;
@@ -438,7 +442,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     if (p->nu_fft > 0) {
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
         ST(mark(p, ST_BWD_MAC, s));
-        CK(launch_bwd_mac(p->M, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, s));
+        CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, s));
         ST(mark(p, ST_C2R_UPD, s));
         C2RArgs c{};
         c.dst = dst;
@@ -655,8 +659,6 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     if (!out) return fail(LFM_EINVAL, "out is NULL");
     *out = nullptr;
     if (!psf_host) return fail(LFM_EINVAL, "psf_host is NULL");
-    if (psf_t_host)
-        return fail(LFM_EUNSUPPORTED, "a supplied transposed PSF is not supported in this build; pass NULL for the exact adjoint (C6)");
     Geo g;
     ST(make_geo(nnum, nz, kh, kw, height, width, /*direct=*/false, &g));
     int rank = 0, world = 1;
@@ -699,6 +701,22 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     const float* psf_own = psf_host + (size_t)p->u0 * kk;
     for (size_t i = 0, n = (size_t)p->nu * kk; i < n; ++i)
         if (!(psf_own[i] >= 0.0f)) return guard(fail(LFM_ENEG, "psf has a negative (or NaN) entry at unit %zu (S:192)", p->u0 + i / kk));
+    // backward kernels: the exact adjoint uses psf itself (C6); a supplied Ht enters as rot180(Ht) so that
+    // H^T r (z,p,q) = sum_s r(s) Ht[z][p%N][q%N](p - s + c) runs through the same adjoint machinery
+    std::vector<float> psfb_host;
+    const float* psfb_own = psf_own;
+    if (psf_t_host) {
+        psfb_host.resize((size_t)p->nu * kk);
+        const float* ht_own = psf_t_host + (size_t)p->u0 * kk;
+        for (size_t uu = 0; uu < (size_t)p->nu; ++uu)
+            for (int i = 0; i < kh; ++i)
+                for (int j = 0; j < kw; ++j) {
+                    const float v = ht_own[uu * kk + (size_t)(kh - 1 - i) * kw + (kw - 1 - j)];
+                    if (!(v >= 0.0f)) return guard(fail(LFM_ENEG, "psf_t has a negative (or NaN) entry at unit %zu", p->u0 + uu));
+                    psfb_host[uu * kk + (size_t)i * kw + j] = v;
+                }
+        psfb_own = psfb_host.data();
+    }
     if (optics) {
         PG(make_region(optics, nnum, height, width, &p->region));
         p->has_optics = true;
@@ -707,6 +725,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     // memory budget ("estimate the required memory size")
     {
         SizeTerms t = size_terms(g, p->nu, p->nu_total, world, (flags & LFM_PLAN_DIRECT) != 0);
+        if (psf_t_host) t.transfer *= 2;   // a second set of transfer matrices for Ht
         size_t free_b = 0, total_b = 0;
         CKG(cudaMemGetInfo(&free_b, &total_b));
         if (t.total() > free_b) {
@@ -766,6 +785,13 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     // PSF slice of the owned units -> device ("the PSF is evenly distributed to each card")
     PG(dalloc(p, &p->psf, (size_t)p->nu * kk * sizeof(float), "psf slice"));
     if (p->nu > 0) CKG(cudaMemcpyAsync(p->psf, psf_own, (size_t)p->nu * kk * sizeof(float), cudaMemcpyHostToDevice, s));
+    p->psfb = p->psf;
+    if (psf_t_host) {
+        PG(dalloc(p, &p->psfb, (size_t)p->nu * kk * sizeof(float), "backward psf slice"));
+        if (p->nu > 0)
+            CKG(cudaMemcpyAsync(p->psfb, psfb_own, (size_t)p->nu * kk * sizeof(float), cudaMemcpyHostToDevice, s));
+        CKG(cudaStreamSynchronize(s));   // psfb_host is read by the copy
+    }
 
     // ---- hybrid plan: per plane, the tap box of its coarse kernels and a cost model pick the
     //      direct path (D x D taps per phase pair) or the frequency path (streamed transfer matrices)
@@ -776,17 +802,18 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     for (int z = zb; z <= ze; ++z) {
         int k0 = kh, k1 = -1, j0 = kw, j1 = -1;
         const int ub = std::max(p->u0, z * N2), ue = std::min(p->u1, (z + 1) * N2);
-        for (int u = ub; u < ue; ++u) {
-            const float* ker = psf_host + (size_t)u * kk;
-            for (int i = 0; i < kh; ++i)
-                for (int j = 0; j < kw; ++j)
-                    if (ker[(size_t)i * kw + j] != 0.0f) {
-                        k0 = std::min(k0, i);
-                        k1 = std::max(k1, i);
-                        j0 = std::min(j0, j);
-                        j1 = std::max(j1, j);
-                    }
-        }
+        for (int u = ub; u < ue; ++u)
+            for (int w = 0; w < (psf_t_host ? 2 : 1); ++w) {
+                const float* ker = (w ? psfb_own : psf_own) + (size_t)(u - p->u0) * kk;
+                for (int i = 0; i < kh; ++i)
+                    for (int j = 0; j < kw; ++j)
+                        if (ker[(size_t)i * kw + j] != 0.0f) {
+                            k0 = std::min(k0, i);
+                            k1 = std::max(k1, i);
+                            j0 = std::min(j0, j);
+                            j1 = std::max(j1, j);
+                        }
+            }
         if (k1 < 0) {   // all-zero owned kernels: a single (zero) tap
             k0 = k1 = g.ch;
             j0 = j1 = g.cw;
@@ -866,6 +893,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     if (u < p->u0 || u >= p->u1) continue;
                     const int a1 = a / nnum, a2 = a % nnum;
                     const float* ker = psf_host + (size_t)u * kk;
+                    const float* kerb = psfb_own + (size_t)(u - p->u0) * kk;
                     for (int bq = 0; bq < N2; ++bq) {
                         const int b1 = bq / nnum, b2 = bq % nnum;
                         const int o1 = B1.dlo[(size_t)a1 * nnum + b1], o2 = B2.dlo[(size_t)a2 * nnum + b2];
@@ -875,9 +903,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                             for (int e2 = 0; e2 < D; ++e2) {
                                 const int k2 = b2 - a2 + g.cw + nnum * (o2 + e2);
                                 if (k2 < 0 || k2 >= kw) continue;
-                                const float v = ker[(size_t)k1 * kw + k2];
-                                cf[(((size_t)zi * N2 + a) * DD + e1 * D + e2) * N2 + bq] = v;
-                                cb[(((size_t)zi * N2 + bq) * DD + e1 * D + e2) * N2 + a] = v;
+                                cf[(((size_t)zi * N2 + a) * DD + e1 * D + e2) * N2 + bq] = ker[(size_t)k1 * kw + k2];
+                                cb[(((size_t)zi * N2 + bq) * DD + e1 * D + e2) * N2 + a] = kerb[(size_t)k1 * kw + k2];
                             }
                         }
                     }
@@ -964,7 +991,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 PG(dalloc(p, &cb, nf * sizeof(float), "tc direct taps (backward)"));
                 p->dallocs.push_back(cb);
                 CKG(launch_tcdir_coef(ta, dz, p->psf, kh, kw, g.ch, g.cw, 1, cf, s));
-                CKG(launch_tcdir_coef(ta, dz, p->psf, kh, kw, g.ch, g.cw, 0, cb, s));
+                CKG(launch_tcdir_coef(ta, dz, p->psfb, kh, kw, g.ch, g.cw, 0, cb, s));
                 CKG(cudaStreamSynchronize(s));   // zl dies at the end of this scope
                 TcDirArgs tb = ta;
                 ta.coef = cf;
@@ -1000,11 +1027,26 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             a.cdiv = p->nu_fft;
             a.cmul = p->nu_fft_pad;
             CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, a, s));
+            p->Mb = p->M;
+            if (psf_t_host) {   // second set of transfer matrices from rot180(Ht)
+                p->transfer_bytes += mbytes;
+                PG(dalloc(p, &p->Mb, mbytes, "backward transfer matrices"));
+                CKG(cudaMemsetAsync(p->Mb, 0, mbytes, s));
+                R2CArgs ab = r2c_args(SRC_KERNEL, p->psfb, nullptr, 0.f, N2 * p->nu_fft, p->Mb, (long long)N2 * p->nu_fft_pad);
+                ab.cdiv = p->nu_fft;
+                ab.cmul = p->nu_fft_pad;
+                CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, ab, s));
+            }
         }
         CKG(cudaStreamSynchronize(s));
+        if (p->psfb != p->psf) {
+            cudaFree(p->psfb);
+            p->bytes -= (size_t)p->nu * kk * sizeof(float);
+        }
         cudaFree(p->psf);           // transfer matrices and direct taps replace the PSF
         p->bytes -= (size_t)p->nu * kk * sizeof(float);
         p->psf = nullptr;
+        p->psfb = nullptr;
     } else {
         p->transfer_bytes = (size_t)p->nu * kk * sizeof(float);
     }

@@ -206,8 +206,12 @@ def lfm_plan_estimate(nnum, nz, kh, kw, height, width, world=1, flags=0, budget_
 class Plan:
     """Owns an lfm_plan (C handle).  Methods map one to one to the ABI calls."""
 
-    def __init__(self, psf, nnum, height, width, optics=None, rank=0, world=1, nccl_id=None, flags=0, stream=None):
+    def __init__(self, psf, nnum, height, width, optics=None, rank=0, world=1, nccl_id=None, flags=0, stream=None,
+                 psf_t=None):
         psf = np.ascontiguousarray(psf, dtype=np.float32)
+        psf_t = None if psf_t is None else np.ascontiguousarray(psf_t, dtype=np.float32)
+        if psf_t is not None and psf_t.shape != psf.shape:
+            raise ValueError("psf_t must have the shape of psf")
         if psf.ndim != 5 or psf.shape[1] != nnum or psf.shape[2] != nnum:
             raise ValueError("psf must be [nz][N][N][kh][kw]")
         nz, _, _, kh, kw = psf.shape
@@ -220,7 +224,7 @@ class Plan:
                 ctypes.memmove(dist.nccl_id, bytes(nccl_id), 128)
         h = _P()
         opt = optics if (optics is None or isinstance(optics, lfm_optics)) else lfm_optics(*optics)
-        _check(_lib_create(ctypes.byref(h), _ptr(psf), None, nnum, nz, kh, kw, height, width,
+        _check(_lib_create(ctypes.byref(h), _ptr(psf), _ptr(psf_t), nnum, nz, kh, kw, height, width,
                            ctypes.byref(opt) if opt is not None else None,
                            ctypes.byref(dist) if dist is not None else None, flags, _stream(stream)))
         self._h = h

@@ -402,3 +402,32 @@ def test_isra_matches_oracle(flags):
         assert res["best_iter"] == ref.best_iter
         assert rel(x_d.cpu().numpy(), ref.iterates[res["best_iter"] - 1]) <= tol
         np.testing.assert_allclose(res["series"], ref.series, rtol=1e-4)
+
+
+@pytest.mark.parametrize("flags", [0, 2, 4, 18], ids=["hybrid", "direct", "fft", "direct-tc"])
+def test_supplied_ht(flags):
+    """f3: a supplied transposed PSF Ht drives the backward (and normalizer); Ht = rot180(H) reproduces the
+    exact-adjoint plan; an unrelated Ht matches the oracle's Ht backward."""
+    h, x, r = rand_case(21, 3, 3, 27, 33, 9, 9)
+    rng = np.random.default_rng(22)
+    ht = rng.uniform(0, 1, h.shape).astype(np.float32)
+    with L().Plan(h, 3, 27, 33, optics=optics(3), flags=flags, psf_t=ht) as plan:
+        xb_d = torch.zeros((3, 27, 33), device="cuda")
+        plan.backward(dev(r), xb_d)
+        nrm_d = torch.zeros((3, 27, 33), device="cuda")
+        plan.normalizer(nrm_d)
+        y_d = torch.zeros((27, 33), device="cuda")
+        plan.forward(dev(x), y_d)
+        torch.cuda.synchronize()
+        tol = op_tol(plan.info())[0]
+    assert rel(xb_d.cpu().numpy(), O.backward_project_ht(r.astype(np.float64), ht.astype(np.float64))) <= tol
+    assert rel(nrm_d.cpu().numpy(), O.backward_project_ht(np.ones((27, 33)), ht.astype(np.float64))) <= tol
+    assert rel(y_d.cpu().numpy(), O.forward_project(x.astype(np.float64), h.astype(np.float64))) <= tol
+    with L().Plan(h, 3, 27, 33, optics=optics(3), flags=flags, psf_t=np.ascontiguousarray(h[:, :, :, ::-1, ::-1])) as p1, \
+            L().Plan(h, 3, 27, 33, optics=optics(3), flags=flags) as p0:
+        a_d = torch.zeros((3, 27, 33), device="cuda")
+        b_d = torch.zeros((3, 27, 33), device="cuda")
+        p1.backward(dev(r), a_d)
+        p0.backward(dev(r), b_d)
+        torch.cuda.synchronize()
+        assert rel(a_d.cpu().numpy(), b_d.cpu().numpy().astype(np.float64)) <= 1e-6

@@ -205,3 +205,28 @@ def test_rejects_bad_dims():
         O.forward_project(np.ones((1, 10, 9)), h)       # H not divisible by N
     with pytest.raises(ValueError):
         O.forward_project(np.ones((1, 9, 9)), np.ones((1, 3, 3, 4, 3)))   # even kernel
+
+
+def test_ht_backward_bruteforce():
+    """f3: the Ht backward equals the operator built entry by entry from its definition
+    xhat(z,p,q) = sum_{s,t} r(s,t) Ht[z][p%N][q%N](p-s+ch, q-t+cw); with Ht = rot180(h) it is the exact adjoint."""
+    rng = np.random.default_rng(12)
+    nz, N, H, W, kh, kw = 2, 3, 9, 12, 5, 3
+    ht = rng.uniform(0, 1, (nz, N, N, kh, kw))
+    ch, cw = kh // 2, kw // 2
+    B = np.zeros((nz * H * W, H * W))
+    for z in range(nz):
+        for p in range(H):
+            for q in range(W):
+                for s in range(H):
+                    i = p - s + ch
+                    if not 0 <= i < kh:
+                        continue
+                    for t in range(W):
+                        j = q - t + cw
+                        if 0 <= j < kw:
+                            B[(z * H + p) * W + q, s * W + t] = ht[z, p % N, q % N, i, j]
+    r = rng.uniform(0, 1, (H, W))
+    np.testing.assert_allclose(O.backward_project_ht(r, ht).ravel(), B @ r.ravel(), rtol=1e-12, atol=1e-13)
+    h = rng.uniform(0, 1, (nz, N, N, kh, kw))
+    np.testing.assert_allclose(O.backward_project_ht(r, h[:, :, :, ::-1, ::-1]), O.backward_project(r, h), rtol=1e-13)
