@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=96, help="rows of the oracle's bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="lfm_plan_create flags (2 = direct path)")
+    ap.add_argument("--frames", type=int, default=8, help="c5: frames per lockstep batch (2/4/8/16)")
     return ap.parse_args()
 
 
@@ -346,10 +347,65 @@ def run_ours(args):
     return 0
 
 
+def run_c5(args):
+    """c5 (BASELINE configs[4]): time-lapse of c3-geometry frames, frame-batched lockstep RL.
+    value = frame-iterations/s over K lockstep iterations of one batch of F frames (fixed mode)."""
+    import torch
+    from paper_2208_11422_b200 import lfm as L
+    from lfm_inputs import gen_somata
+    cfg = CONFIGS["c3"]
+    F = args.frames
+    h = gen_psf(cfg, np.float32)
+    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), flags=args.flags or 4)
+    info = plan.info()
+    del h
+    H, W, nz = cfg.height, cfg.width, cfg.nz
+    rng = np.random.default_rng(7)
+    phase = rng.uniform(0, 2 * np.pi, cfg.n_objects)
+    ys = []
+    for f in range(F):   # soma intensities 1 + 0.5 sin(2 pi f / 64 + phi_i) (SURVEY §8(d)), noise seed 1000 + f
+        xt = torch.from_numpy(gen_somata(cfg, 1, np.float32, modulation=1 + 0.5 * np.sin(2 * np.pi * f / 64 + phase))).cuda()
+        yh = torch.zeros((H, W), device="cuda")
+        plan.forward(xt, yh)
+        torch.cuda.synchronize()
+        ys.append(poisson(np.maximum(yh.cpu().numpy().astype(np.float64), 0), 1000 + f).astype(np.float32))
+        del xt
+    yb = torch.from_numpy(np.stack(ys)).cuda()
+    xb = torch.zeros((F, nz, H, W), device="cuda")
+    plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.warmup))
+    plan.profile_read(reset=True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.steps, init_from_x=True))
+    ev1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    prof = plan.profile_read(reset=True)
+    auto = plan.rl_iterate_batch(yb, xb, L.make_policy(mode="auto", max_iters=50))
+    line = {"metric": "frame-iterations/s (c5 time-lapse, frame-batched lockstep RL)", "value": F * args.steps / (ms / 1e3),
+            "unit": "frame-iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"c5: batch of {F} time-lapse frames of the c3 geometry (Nnum=15, 1005x1005, 51 planes)",
+                       "frames_per_batch": F, "plan_flags": args.flags or 4, "fft_units": info["fft_units"],
+                       "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"]}},
+            "gpu_launches": prof["launches"], "clocks": clk}
+    print(json.dumps(line), flush=True)
+    plan.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c5":
+        return run_c5(args)
     return run_ours(args)
 
 

@@ -197,6 +197,15 @@ lfm_status lfm_rl_step(lfm_plan plan, const float* y, const float* x_in, float* 
 lfm_status lfm_rl_iterate(lfm_plan plan, const float* y, float* x, const lfm_policy* policy,
                           int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
+/* Frame-batched lockstep RL for time-lapse data: F in {2,4,8,16} independent frames share every
+ * pass over the transfer matrices (a (N^2 x units) x (units x F) complex GEMM per coarse frequency), each frame
+ * with its own stop rule and argmax snapshot; frames that stop early are frozen.
+ *   y : device [F][H][W];  x : device [F][nz][H][W] (in: x0 if policy->init_from_x; out: each frame's argmax iterate)
+ *   best_iter, stop_iter : host [F];  series_host : host [F][max(n_iters, max_iters)];
+ *   ms_host : optional host [max(...)] device ms per lockstep iteration.  RL update only. */
+lfm_status lfm_rl_iterate_batch(lfm_plan plan, int frames, const float* y, float* x, const lfm_policy* policy,
+                                int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
+
 /* End-to-end call with HOST buffers: copies y in (H2D), runs lfm_rl_iterate, copies the argmax-E
  * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best). */
 lfm_status lfm_deconvolve_host(lfm_plan plan, const float* y_host, float* x_host, const lfm_policy* policy,

@@ -144,6 +144,172 @@ __global__ void __launch_bounds__(128) bwd_mac_kernel(const float2* __restrict__
     o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
 }
 
+// ================================================================================================
+// Frame-batched (lockstep time-lapse) versions: one pass over M serves F frames, turning each
+// per-kappa GEMV into a (N2 x nu) x (nu x F) complex GEMM; arithmetic intensity rises from 1 to F flop/byte.
+// ================================================================================================
+constexpr int kBatchKT = 16;   // u (reduction) tile of the batched forward
+
+// CTA per kappa, thread per output phase b' (N2 <= 256); M tile [k][b'] and G tile [k][f] staged in shared
+// memory (double buffered through registers), F complex accumulators per thread.
+template <int F>
+__global__ void __launch_bounds__(256) fwd_mac_batch_kernel(const float2* __restrict__ M, const float2* __restrict__ G,
+                                                            long long g_fstride, float2* __restrict__ Y,
+                                                            long long y_fstride, int N2, int nu_pad) {
+    extern __shared__ float4 smb[];
+    auto ms = reinterpret_cast<float2 (*)[kBatchKT][257]>(smb);                                  // [2][KT][257]
+    auto gs = reinterpret_cast<float4 (*)[kBatchKT][F / 2]>(smb + (2 * kBatchKT * 257 + 1) / 2);   // [2][KT][F/2]
+    const long long kap = blockIdx.x;
+    const int tid = threadIdx.x;
+    const float2* Mk = M + kap * N2 * (long long)nu_pad;
+    const int ntiles = nu_pad / kBatchKT;
+    // staging assignment: 8 threads x float4 (2 complex) per row segment of 16 complex
+    const int seg_row0 = tid >> 3, seg_q = tid & 7;    // rows seg_row0 + 32*i
+    float4 mreg[8];
+    float4 greg;
+    auto load_tile = [&](int t) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int row = seg_row0 + 32 * i;
+            mreg[i] = row < N2 ? __ldcs(reinterpret_cast<const float4*>(Mk + (long long)row * nu_pad + t * kBatchKT) + seg_q)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (tid < kBatchKT * F / 2) {   // G: F frames x 16 complex, as float4 pairs of frames
+            const int k = tid / (F / 2), fp = tid - (tid / (F / 2)) * (F / 2);
+            const float2 g0 = G[2 * fp * g_fstride + kap * nu_pad + t * kBatchKT + k];
+            const float2 g1 = G[(2 * fp + 1) * g_fstride + kap * nu_pad + t * kBatchKT + k];
+            greg = make_float4(g0.x, g0.y, g1.x, g1.y);
+        }
+    };
+    auto store_tile = [&](int b) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int row = seg_row0 + 32 * i;
+            ms[b][2 * seg_q][row] = make_float2(mreg[i].x, mreg[i].y);
+            ms[b][2 * seg_q + 1][row] = make_float2(mreg[i].z, mreg[i].w);
+        }
+        if (tid < kBatchKT * F / 2) {
+            const int k = tid / (F / 2), fp = tid - (tid / (F / 2)) * (F / 2);
+            gs[b][k][fp] = greg;
+        }
+    };
+    float accr[F], acci[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) accr[f] = acci[f] = 0.f;
+    load_tile(0);
+    store_tile(0);
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+        const int b = t & 1;
+        if (t + 1 < ntiles) load_tile(t + 1);
+#pragma unroll
+        for (int k = 0; k < kBatchKT; ++k) {
+            const float2 m = ms[b][k][tid];
+#pragma unroll
+            for (int fp = 0; fp < F / 2; ++fp) {
+                const float4 g = gs[b][k][fp];
+                accr[2 * fp] = fmaf(m.x, g.x, accr[2 * fp]);
+                accr[2 * fp] = fmaf(-m.y, g.y, accr[2 * fp]);
+                acci[2 * fp] = fmaf(m.x, g.y, acci[2 * fp]);
+                acci[2 * fp] = fmaf(m.y, g.x, acci[2 * fp]);
+                accr[2 * fp + 1] = fmaf(m.x, g.z, accr[2 * fp + 1]);
+                accr[2 * fp + 1] = fmaf(-m.y, g.w, accr[2 * fp + 1]);
+                acci[2 * fp + 1] = fmaf(m.x, g.w, acci[2 * fp + 1]);
+                acci[2 * fp + 1] = fmaf(m.y, g.z, acci[2 * fp + 1]);
+            }
+        }
+        if (t + 1 < ntiles) store_tile(b ^ 1);
+        __syncthreads();
+    }
+    if (tid < N2) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) Y[f * y_fstride + kap * N2 + tid] = make_float2(accr[f], acci[f]);
+    }
+}
+
+// thread per 4 consecutive units, walks the N2 rows of M[kappa] once for all F frames; R[f][kappa][b'] in smem
+template <int F>
+__global__ void __launch_bounds__(128) bwd_mac_batch_kernel(const float2* __restrict__ M, const float2* __restrict__ R,
+                                                            long long r_fstride, float2* __restrict__ Xh,
+                                                            long long x_fstride, int N2, int nu_pad) {
+    extern __shared__ float2 rsb[];   // [b'][f]
+    const long long kap = blockIdx.y;
+    for (int e = threadIdx.x; e < N2 * F; e += blockDim.x) {
+        const int bq = e / F, f = e - (e / F) * F;
+        rsb[e] = R[f * r_fstride + kap * N2 + bq];
+    }
+    __syncthreads();
+    const int nv = nu_pad >> 2;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const f8* base = reinterpret_cast<const f8*>(M + kap * N2 * (long long)nu_pad) + v;
+    const long long stride = nv;
+    float acc[F][8];
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[f][i] = 0.f;
+    int b = 0;
+    for (; b + 3 < N2; b += 4) {
+        f8 m[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m[q] = ld_stream8(base + (b + q) * stride);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int f = 0; f < F; ++f) cjmac4(m[q], rsb[(b + q) * F + f], acc[f]);
+    }
+    for (; b < N2; ++b) {
+        const f8 m = ld_stream8(base + b * stride);
+#pragma unroll
+        for (int f = 0; f < F; ++f) cjmac4(m, rsb[b * F + f], acc[f]);
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        float4* o = reinterpret_cast<float4*>(Xh + f * x_fstride + kap * nu_pad) + 2 * v;
+        o[0] = make_float4(acc[f][0], acc[f][1], acc[f][2], acc[f][3]);
+        o[1] = make_float4(acc[f][4], acc[f][5], acc[f][6], acc[f][7]);
+    }
+}
+
+cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_fstride, float2* Y, long long y_fstride,
+                                 int F, int nkappa, int N2, int nu_pad, cudaStream_t s) {
+    if (N2 > 256 || nu_pad % kBatchKT) return cudaErrorInvalidValue;
+    const size_t smem = ((2 * kBatchKT * 257 + 1) / 2) * sizeof(float4) + 2 * kBatchKT * (F / 2) * sizeof(float4);
+    cudaError_t e = cudaSuccess;
+#define LFM_FB(FV)                                                                                              \
+    case FV:                                                                                                    \
+        e = cudaFuncSetAttribute(fwd_mac_batch_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                         \
+        fwd_mac_batch_kernel<FV><<<nkappa, 256, smem, s>>>(M, G, g_fstride, Y, y_fstride, N2, nu_pad);          \
+        break;
+    switch (F) {
+        LFM_FB(2)
+        LFM_FB(4)
+        LFM_FB(8)
+        LFM_FB(16)
+        default: return cudaErrorInvalidValue;
+    }
+#undef LFM_FB
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_fstride, float2* Xh, long long x_fstride,
+                                 int F, int nkappa, int N2, int nu_pad, cudaStream_t s) {
+    const int threads = 128;
+    const int nv = nu_pad / 4;
+    dim3 grid((nv + threads - 1) / threads, nkappa);
+    const size_t smem = (size_t)N2 * F * sizeof(float2);
+    switch (F) {
+        case 2: bwd_mac_batch_kernel<2><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
+        case 4: bwd_mac_batch_kernel<4><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
+        case 8: bwd_mac_batch_kernel<8><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
+        case 16: bwd_mac_batch_kernel<16><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
                            cudaStream_t s) {
     const size_t smem = (size_t)nu_pad * sizeof(float2);

@@ -242,6 +242,12 @@ struct lfm_plan_s {
     double* stats = nullptr;    // 3
     double* host = nullptr;     // pinned 8 doubles
     float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
+    // frame-batched lockstep buffers (lfm_rl_iterate_batch), capacity bcap frames
+    int bcap = 0;
+    float2 *bG = nullptr, *bXh = nullptr, *bY = nullptr, *bR = nullptr;
+    float *bx = nullptr, *byhat = nullptr;
+    unsigned* bmproj = nullptr;
+    double *bent = nullptr, *bhost = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool prof = false;
     cudaEvent_t pev[LFM_N_STAGES + 1] = {};
@@ -299,6 +305,15 @@ void plan_free(lfm_plan p) {
     cudaFree(p->stats);
     cudaFree(p->y_stage);
     cudaFree(p->x_stage);
+    cudaFree(p->bG);
+    cudaFree(p->bXh);
+    cudaFree(p->bY);
+    cudaFree(p->bR);
+    cudaFree(p->bx);
+    cudaFree(p->byhat);
+    cudaFree(p->bmproj);
+    cudaFree(p->bent);
+    if (p->bhost) cudaFreeHost(p->bhost);
     if (p->host) cudaFreeHost(p->host);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
@@ -1266,6 +1281,176 @@ lfm_status lfm_dct_entropy(const float* img, int height, int width, int nnum, co
     *entropy = h;
     if (x_s) *x_s = r.xs;
     if (y_s) *y_s = r.ys;
+    return LFM_OK;
+}
+
+lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x, const lfm_policy* pol, int* best_iter,
+                                int* stop_iter, double* series_host, float* ms_host, void* stream) {
+    g_err[0] = 0;
+    if (!p || !y || !x || !best_iter || !stop_iter || !series_host) return fail(LFM_EINVAL, "NULL argument");
+    if (frames != 2 && frames != 4 && frames != 8 && frames != 16)
+        return fail(LFM_EINVAL, "frames=%d: the batched path takes 2, 4, 8 or 16 frames (one frame: lfm_rl_iterate)", frames);
+    ST(check_policy(pol));
+    if (pol->update != LFM_UPDATE_RL) return fail(LFM_EUNSUPPORTED, "the batched path runs the RL update only");
+    if (p->direct) return fail(LFM_EUNSUPPORTED, "the batched path needs a frequency / hybrid plan");
+    if (p->geo.N * p->geo.N > 256) return fail(LFM_EUNSUPPORTED, "the batched forward MAC handles N^2 <= 256");
+    if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the stop rule needs the metric");
+    cudaStream_t s = as_stream(stream);
+    const int F = frames, N2 = p->geo.N * p->geo.N;
+    const size_t HW = (size_t)p->geo.H * p->geo.W;
+    const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
+    const long long sG = (long long)p->geo.nkappa * p->nu_fft_pad, sY = (long long)p->geo.nkappa * N2;
+    if (p->bcap < F) {   // (re)allocate the per-frame state
+        cudaFree(p->bG); cudaFree(p->bXh); cudaFree(p->bY); cudaFree(p->bR); cudaFree(p->bx); cudaFree(p->byhat);
+        cudaFree(p->bmproj); cudaFree(p->bent);
+        if (p->bhost) cudaFreeHost(p->bhost);
+        p->bG = p->bXh = p->bY = p->bR = nullptr;
+        p->bx = p->byhat = nullptr;
+        p->bmproj = nullptr;
+        p->bent = p->bhost = nullptr;
+        p->bcap = 0;
+        if (p->nu_fft > 0) {
+            ST(dalloc(p, &p->bG, (size_t)F * sG * sizeof(float2), "batch G spectra"));
+            ST(dalloc(p, &p->bXh, (size_t)F * sG * sizeof(float2), "batch Xh spectra"));
+            ST(dalloc(p, &p->bY, (size_t)F * sY * sizeof(float2), "batch Y spectra"));
+            ST(dalloc(p, &p->bR, (size_t)F * sY * sizeof(float2), "batch R spectra"));
+            CK(cudaMemsetAsync(p->bG, 0, (size_t)F * sG * sizeof(float2), s));   // padding columns stay zero
+        }
+        ST(dalloc(p, &p->bx, (size_t)3 * F * vol * sizeof(float), "batch volumes"));
+        ST(dalloc(p, &p->byhat, (size_t)F * HW * sizeof(float), "batch yhat"));
+        ST(dalloc(p, &p->bmproj, (size_t)F * HW * sizeof(unsigned), "batch max projections"));
+        ST(dalloc(p, &p->bent, (size_t)2 * F * sizeof(double), "batch entropies"));
+        CK(cudaMallocHost(&p->bhost, (size_t)2 * F * sizeof(double)));
+        p->bcap = F;
+    }
+    auto xbuf = [&](int f, int b) { return p->bx + ((size_t)f * 3 + b) * vol; };
+    // validate every frame and initialise x0 (uniform c0_f = sum y_f / sum H^T 1, reading C2, or caller's x)
+    for (int f = 0; f < F; ++f) {
+        ST(check_y(p, y + (size_t)f * HW, s));
+        if (pol->init_from_x)
+            CK(launch_image_to_poly(x + (size_t)f * p->geo.nz * HW, xbuf(f, 0), p->xall, p->u0, p->nu, s));
+        else
+            CK(launch_fill_dev(xbuf(f, 0), vol, p->stats, p->norm_sum, s));
+    }
+    const int cap = pol->mode == LFM_MODE_FIXED ? pol->n_iters : pol->max_iters;
+    const int sstride = std::max(pol->n_iters, pol->max_iters);   // series_host row stride (lfm.h)
+    std::vector<int> cur(F, 0), best(F, -1), dec(F, 0), bestk(F, 0), stopped(F, 0);
+    std::vector<double> prev(F, 0.0), beste(F, -INFINITY);
+    int k = 0, active = F;
+    while (active > 0) {
+        ++k;
+        std::vector<int> nxt(F, 0);
+        for (int f = 0; f < F; ++f)
+            while (nxt[f] == cur[f] || nxt[f] == best[f]) ++nxt[f];
+        if (ms_host) CK(cudaEventRecord(p->ev0, s));
+        // ---- forward: coarse transforms per frame, one batched pass over M, inverse per frame ----
+        if (p->nu_fft > 0) {
+            for (int f = 0; f < F; ++f)
+                if (!stopped[f])
+                    CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
+                                  r2c_args(SRC_POLY, xbuf(f, cur[f]), nullptr, 0.f, p->nu_fft, p->bG + f * sG, p->nu_fft_pad), s));
+            CK(launch_fwd_mac_batch(p->M, p->bG, sG, p->bY, sY, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            p->pacc.launches += 1;
+        }
+        for (int f = 0; f < F; ++f) {
+            if (stopped[f]) continue;
+            float* yimg = p->byhat + f * HW;
+            bool acc = false;
+            if (p->nu_fft > 0) {
+                C2RArgs c{};
+                c.dst = DST_IMAGE;
+                c.in = p->bY + f * sY;
+                c.in_ld = N2;
+                c.ntrans = N2;
+                c.out = yimg;
+                CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+                p->pacc.launches += 2;
+                acc = true;
+            }
+            for (const TcDirArgs& tg : p->tcf) {
+                CK(launch_tcdir_fwd(tg, xbuf(f, cur[f]), 0, p->dpart, yimg, acc ? 1 : 0, s));
+                acc = true;
+            }
+            for (const DirArgs& dg : p->dgroups) {
+                CK(launch_dir_fwd(dg, xbuf(f, cur[f]), 0, p->dpart, yimg, acc ? 1 : 0, s));
+                acc = true;
+            }
+            ST(allreduce(p, yimg, HW, ncclFloat, ncclSum, s));
+            if (p->nu_fft > 0)
+                CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
+                              r2c_args(SRC_RATIO, y + f * HW, yimg, pol->eps, N2, p->bR + f * sY, N2), s));
+        }
+        // ---- backward: one batched pass over M^H, inverse + update per frame ----
+        if (p->nu_fft > 0) {
+            CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            p->pacc.launches += 1;
+        }
+        for (int f = 0; f < F; ++f) {
+            if (stopped[f]) continue;
+            float* xo = xbuf(f, cur[f]);
+            float* xn = xbuf(f, nxt[f]);
+            if (p->nu_fft > 0) {
+                C2RArgs c{};
+                c.dst = DST_UPDATE;
+                c.in = p->bXh + f * sG;
+                c.in_ld = p->nu_fft_pad;
+                c.ntrans = p->nu_fft;
+                c.out = xn;
+                c.xold = xo;
+                c.norm = p->norm;
+                c.eps = pol->eps;
+                CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+            }
+            for (const TcDirArgs& tg : p->tcb)
+                CK(launch_tcdir_bwd(tg, SRC_RATIO, y + f * HW, p->byhat + f * HW, pol->eps, DST_UPDATE, xn, xo, p->norm, s));
+            for (const DirArgs& dg : p->dgroups)
+                CK(launch_dir_bwd(dg, SRC_RATIO, y + f * HW, p->byhat + f * HW, pol->eps, DST_UPDATE, xn, xo, p->norm, s));
+            unsigned* mp = p->bmproj + f * HW;
+            CK(launch_max_project_poly(xn, mp, p->xall, s));
+            ST(allreduce(p, mp, HW, ncclFloat, ncclMax, s));
+            const int ri = pol->region == LFM_REGION_RECTANGLE ? 1 : 0;
+            CK(launch_metric(mp, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
+                             p->met.nmem[ri], p->met.T1, p->met.rowsq, p->bent + 2 * f, s));
+            p->pacc.launches += 4;
+        }
+        if (ms_host) CK(cudaEventRecord(p->ev1, s));
+        CK(cudaMemcpyAsync(p->bhost, p->bent, 2 * F * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ms_host) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            ms_host[k - 1] = ms;
+        }
+        p->pacc.iterations += active;
+        for (int f = 0; f < F; ++f) {
+            if (stopped[f]) continue;
+            const double e = p->bhost[2 * f];
+            series_host[(size_t)f * sstride + k - 1] = e;
+            if (k > 1 && e < prev[f])
+                ++dec[f];
+            else
+                dec[f] = 0;
+            prev[f] = e;
+            if (e > beste[f]) {
+                beste[f] = e;
+                bestk[f] = k;
+                best[f] = nxt[f];
+            }
+            cur[f] = nxt[f];
+            const bool stop = pol->mode == LFM_MODE_FIXED
+                                  ? k >= pol->n_iters
+                                  : ((k >= pol->min_iters && dec[f] >= pol->patience) || k >= cap);
+            if (stop) {
+                stopped[f] = 1;
+                stop_iter[f] = k;
+                best_iter[f] = bestk[f];
+                --active;
+            }
+        }
+    }
+    for (int f = 0; f < F; ++f)
+        ST(gather_to_image(p, xbuf(f, best[f] < 0 ? cur[f] : best[f]), x + (size_t)f * p->geo.nz * HW, s));
+    CK(cudaStreamSynchronize(s));
     return LFM_OK;
 }
 

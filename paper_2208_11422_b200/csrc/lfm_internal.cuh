@@ -135,6 +135,10 @@ cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkap
                            int num_sms, cudaStream_t s);
 cudaError_t launch_bwd_mac(const float2* M, const float2* R, float2* Xh, int nkappa, int N2, int nu_pad,
                            cudaStream_t s);
+cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_fstride, float2* Y, long long y_fstride,
+                                 int F, int nkappa, int N2, int nu_pad, cudaStream_t s);   // F in {2,4,8,16}
+cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_fstride, float2* Xh, long long x_fstride,
+                                 int F, int nkappa, int N2, int nu_pad, cudaStream_t s);
 // (kernels_misc.cu)
 cudaError_t launch_fill(float* p, size_t n, float v, cudaStream_t s);
 cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double* den, cudaStream_t s);

@@ -98,6 +98,8 @@ _lib_rl_step = _sig("lfm_rl_step", _i, [_P, _P, _P, _P, ctypes.c_float, _i, _P, 
 _lib_rl_iterate = _sig("lfm_rl_iterate", _i, [_P, _P, _P, ctypes.POINTER(lfm_policy), _I, _I, _D, _F, _P])
 _lib_deconvolve_host = _sig("lfm_deconvolve_host", _i, [_P, _P, _P, ctypes.POINTER(lfm_policy), _I, _I, _D, _F, _P])
 _lib_quality = _sig("lfm_quality", _i, [_P, _P, _i, _D, _P])
+_lib_rl_iterate_batch = _sig("lfm_rl_iterate_batch", _i, [_P, _i, _P, _P, ctypes.POINTER(lfm_policy), _I, _I, _D, _F,
+                                                          _P])
 _lib_dct_entropy = _sig("lfm_dct_entropy", _i, [_P, _i, _i, _i, ctypes.POINTER(lfm_optics), _i, _D, _I, _I, _P])
 
 LFM_N_STAGES = 11
@@ -116,7 +118,7 @@ STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
             "lfm_plan_create", "lfm_plan_info", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
-            "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name"]
+            "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
 
 
 def _check(st):
@@ -289,6 +291,23 @@ class Plan:
         out = dict(best_iter=best.value, stop_iter=stop.value, series=list(series[:stop.value]))
         if want_ms:
             out["ms"] = list(ms[:stop.value])
+        return out
+
+    def rl_iterate_batch(self, y, x, policy, want_ms=False, stream=None):
+        """Lockstep RL over F frames (y [F,H,W], x [F,nz,H,W] CUDA tensors); per-frame results."""
+        F = y.shape[0]
+        _check_dev(y, (F, self.height, self.width), "y")
+        _check_dev(x, (F, self.nz, self.height, self.width), "x")
+        cap = max(policy.n_iters, policy.max_iters)
+        series = (ctypes.c_double * (cap * F))()
+        ms = (ctypes.c_float * cap)() if want_ms else None
+        best, stop = (ctypes.c_int * F)(), (ctypes.c_int * F)()
+        _check(_lib_rl_iterate_batch(self._h, F, _ptr(y), _ptr(x), ctypes.byref(policy), best, stop, series, ms,
+                                     _stream(stream)))
+        out = dict(best_iter=list(best), stop_iter=list(stop),
+                   series=[list(series[f * cap:f * cap + stop[f]]) for f in range(F)])
+        if want_ms:
+            out["ms"] = list(ms[:max(stop)])
         return out
 
     def deconvolve_host(self, y_host, x_host, policy, want_ms=False, stream=None):

@@ -431,3 +431,27 @@ def test_supplied_ht(flags):
         p0.backward(dev(r), b_d)
         torch.cuda.synchronize()
         assert rel(a_d.cpu().numpy(), b_d.cpu().numpy().astype(np.float64)) <= 1e-6
+
+
+@pytest.mark.parametrize("name,F,flags", [("tiny", 4, 0), ("tiny", 2, 4), ("c2", 4, 4), ("s15", 8, 0)])
+def test_batched_frames_match_single(name, F, flags):
+    """f1: lockstep frame batching -- each frame's iterate, series, best and stop equal the single-frame plan's
+    (and so the oracle's) within fp32 re-association (1e-5), in fixed and auto modes."""
+    cfg = CONFIGS[name]
+    h = gen_psf(cfg, np.float32)
+    hd = h.astype(np.float64)
+    ys = [poisson(O.forward_project(gen_volume(cfg, 1 + f % 3), hd) * (1.0 + 0.1 * f), 300 + f) for f in range(F)]
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+        for pol in (L().make_policy(mode="fixed", n_iters=3), L().make_policy(mode="auto", max_iters=25)):
+            yb = dev(np.stack(ys))
+            xb = torch.zeros((F, cfg.nz, cfg.height, cfg.width), device="cuda")
+            rb = plan.rl_iterate_batch(yb, xb, pol)
+            for f in range(F):
+                x1 = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                r1 = plan.rl_iterate(dev(ys[f]), x1, pol)
+                assert (rb["stop_iter"][f], rb["best_iter"][f]) == (r1["stop_iter"], r1["best_iter"])
+                np.testing.assert_allclose(rb["series"][f], r1["series"], rtol=1e-5)
+                assert rel(xb[f].cpu().numpy(), x1.cpu().numpy().astype(np.float64)) <= 1e-5
+    if name == "tiny":   # and the oracle, for one frame
+        ref = O.deconvolve(ys[0], hd, O.Optics(nnum=cfg.nnum, **OPTICS), O.Policy(mode="auto", max_iters=25))
+        assert (rb["stop_iter"][0], rb["best_iter"][0]) == (ref.stop_iter, ref.best_iter)
