@@ -190,6 +190,8 @@ def run_ours(args):
 
     cfg = CONFIGS[args.config]
     t_setup = time.perf_counter()
+    side = torch.cuda.Stream()          # a real stream: CUDA-graph replay (LFM_PLAN_GRAPHS) cannot use the legacy one
+    torch.cuda.set_stream(side)
     h = gen_psf(cfg, np.float32)
     xt = gen_volume(cfg, 1, np.float32)
     nccl_id = None

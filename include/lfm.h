@@ -101,8 +101,10 @@ enum {
     LFM_PLAN_DIRECT = 2,    /* every plane on the spatial (direct polyphase convolution) path         */
     LFM_PLAN_FFT_ONLY = 4,  /* every plane on the frequency path.  Default (neither flag): hybrid --
                                per plane, the cheapest path by the cost model of DESIGN.md §5        */
-    LFM_PLAN_TC_DIRECT = 16 /* allow the tcgen05 3xTF32 tensor-core kernels for direct planes (opt-in:
+    LFM_PLAN_TC_DIRECT = 16,/* allow the tcgen05 3xTF32 tensor-core kernels for direct planes (opt-in:
                                correct, currently slower than the CUDA-core ones)      */
+    LFM_PLAN_GRAPHS = 32    /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
+                               non-default stream; not combined with lfm_profile timing)             */
 };
 
 /* Information about a plan. */

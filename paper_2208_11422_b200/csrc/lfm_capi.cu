@@ -242,6 +242,16 @@ struct lfm_plan_s {
     double* stats = nullptr;    // 3
     double* host = nullptr;     // pinned 8 doubles
     float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
+    // CUDA-graph replay of one iteration (LFM_PLAN_GRAPHS): one graph per (cur, next) buffer pair,
+    // keyed also by the measurement pointer and the policy scalars baked into the captured launches
+    bool graphs = false;
+    struct GraphKey {
+        int cur, nxt, region, update;
+        const float* y;
+        float eps;
+    };
+    std::vector<GraphKey> gkeys;
+    std::vector<cudaGraphExec_t> gexec;
     // frame-batched lockstep buffers (lfm_rl_iterate_batch), capacity bcap frames
     int bcap = 0;
     float2 *bG = nullptr, *bXh = nullptr, *bY = nullptr, *bR = nullptr;
@@ -279,6 +289,7 @@ inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
 
 void plan_free(lfm_plan p) {
     if (!p) return;
+    for (cudaGraphExec_t g : p->gexec) cudaGraphExecDestroy(g);
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -515,6 +526,43 @@ lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float
     return LFM_OK;
 }
 
+// f4: the whole iteration (transforms, MACs, direct planes, collectives, metric and the 8-byte D2H of E) as
+// one CUDA graph, captured on first use for a (cur, next) buffer pair and replayed with a single launch.
+lfm_status step_graph(lfm_plan p, const float* y, int cur, int nxt, const lfm_policy* pol, cudaStream_t s) {
+    size_t gi = 0;
+    for (; gi < p->gkeys.size(); ++gi) {
+        const auto& k = p->gkeys[gi];
+        if (k.cur == cur && k.nxt == nxt && k.y == y && k.eps == pol->eps && k.region == pol->region &&
+            k.update == pol->update)
+            break;
+    }
+    if (gi == p->gkeys.size()) {
+        if (s == nullptr) return fail(LFM_EINVAL, "LFM_PLAN_GRAPHS needs a non-default stream (legacy stream cannot be captured)");
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        lfm_status st = op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty);
+        cudaError_t ce = cudaSuccess;
+        if (st == LFM_OK) ce = cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaError_t ee = cudaStreamEndCapture(s, &graph);
+        if (st != LFM_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce != cudaSuccess || ee != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            return fail(LFM_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce != cudaSuccess ? ce : ee));
+        }
+        cudaGraphExec_t exec = nullptr;
+        cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail(LFM_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+        p->gkeys.push_back({cur, nxt, pol->region, pol->update, y, pol->eps});
+        p->gexec.push_back(exec);
+    }
+    CK(cudaGraphLaunch(p->gexec[gi], s));
+    return LFM_OK;
+}
+
 lfm_status check_policy(const lfm_policy* pol) {
     if (!pol) return fail(LFM_EINVAL, "policy is NULL");
     if (pol->mode != LFM_MODE_FIXED && pol->mode != LFM_MODE_AUTO) return fail(LFM_EINVAL, "policy.mode=%d", pol->mode);
@@ -700,6 +748,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             return guard(fail(LFM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
     } while (0)
     p->geo = g;
+    p->graphs = (flags & LFM_PLAN_GRAPHS) != 0;
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
@@ -1176,9 +1225,13 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         int nxt = 0;
         while (nxt == cur || nxt == best) ++nxt;
         if (ms_host) CK(cudaEventRecord(p->ev0, s));
-        ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty));
+        if (p->graphs && !p->prof) {
+            ST(step_graph(p, y, cur, nxt, pol, s));
+        } else {
+            ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty));
+            CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
         if (ms_host) CK(cudaEventRecord(p->ev1, s));
-        CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const double e = p->host[0];
         series_host[k - 1] = e;

@@ -455,3 +455,23 @@ def test_batched_frames_match_single(name, F, flags):
     if name == "tiny":   # and the oracle, for one frame
         ref = O.deconvolve(ys[0], hd, O.Optics(nnum=cfg.nnum, **OPTICS), O.Policy(mode="auto", max_iters=25))
         assert (rb["stop_iter"][0], rb["best_iter"][0]) == (ref.stop_iter, ref.best_iter)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2"])
+def test_graph_replay_identical(name):
+    """f4: with LFM_PLAN_GRAPHS each iteration replays a captured CUDA graph; results are bit-identical to the
+    eager launches (same kernels, same order) and the replay is not slower."""
+    cfg, h, hd, y = tiny_problem(name, 2)
+    s = torch.cuda.Stream()
+    out = {}
+    with torch.cuda.stream(s):
+        for flags in (0, L().LFM_PLAN_GRAPHS):
+            with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+                x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=3), stream=s)   # warm / capture
+                r = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="auto", max_iters=30), want_ms=True, stream=s)
+                s.synchronize()
+                out[flags] = (r, x_d.cpu().numpy())
+    (r0, x0), (r1, x1) = out[0], out[L().LFM_PLAN_GRAPHS]
+    assert (r0["stop_iter"], r0["best_iter"]) == (r1["stop_iter"], r1["best_iter"])
+    assert r0["series"] == r1["series"] and np.array_equal(x0, x1)
