@@ -98,13 +98,15 @@ enum {
     LFM_PLAN_NO_COMM = 1,   /* world > 1 without a communicator: the plan owns rank's units and all
                                cross-rank reductions are skipped (outputs are this rank's partials).
                                For testing the sharding on one device.                              */
-    LFM_PLAN_DIRECT = 2,    /* every plane on the spatial (direct polyphase convolution) path         */
+    LFM_PLAN_DIRECT = 2,    /* every plane on the spatial (direct polyphase convolution) path, on the
+                               CUDA-core kernels (with LFM_PLAN_TC_DIRECT: on the tensor-core kernel) */
     LFM_PLAN_FFT_ONLY = 4,  /* every plane on the frequency path.  Default (neither flag): hybrid --
-                               per plane, the cheapest path by the cost model of DESIGN.md §5        */
-    LFM_PLAN_TC_DIRECT = 16,/* allow the tcgen05 3xTF32 tensor-core kernels for direct planes (opt-in:
-                               correct, currently slower than the CUDA-core ones)      */
-    LFM_PLAN_GRAPHS = 32    /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
+                               per plane, the cheapest of frequency / CUDA-core direct / tensor-core
+                               direct by the cost model of DESIGN.md §5                               */
+    LFM_PLAN_TC_DIRECT = 16,/* with LFM_PLAN_DIRECT: every plane on the tcgen05 3xTF32 kernel         */
+    LFM_PLAN_GRAPHS = 32,   /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
                                non-default stream; not combined with lfm_profile timing)             */
+    LFM_PLAN_NO_TC = 64     /* hybrid without the tensor-core direct kernel                          */
 };
 
 /* Information about a plan. */

@@ -1,105 +1,69 @@
 // kernels_tcdir.cu -- direct polyphase projections of near-focus planes on the 5th-generation tensor cores
-// (DESIGN.md §5, K9tc; SURVEY f2).  fp32-accurate through the 3xTF32 split (a*b ~ ah*bh + ah*bl + al*bh).
+// (DESIGN.md §5.3, K9tc; SURVEY f2).  fp32-accurate through the 3xTF32 split (a*b ~ ah*bh + ah*bl + al*bh).
 //
-// For one plane z the direct path is a sum over coarse tap offsets d of dense contractions over phases:
-//   forward : Y[p][b']  += sum_a  X_a[m(p) - d] * G_d[b'][a]      (K = input phases a,  N = output phases b')
-//   backward: Xh[p][a]   = sum_b' r_b'[m(p) + d] * G_d[b'][a]      (K = output phases b', N = input phases a)
-// with G_d[b'][a] = h_{z,a}[b' - a + c + N d] (zero outside the kernel).  A CTA owns 128 coarse
-// pixels (M, one TMEM lane each), one group of NG <= 48 N-phases (TMEM columns) and one plane, and loops over
-// K chunks of 32 phases x taps:
-//   * all 256 threads stage the chunk's source window (X planes or ratio-image phases, halo for every tap) in
-//     shared memory, then for each tap build the shifted A tile (128 x 32, hi and lo) in the canonical K-major
-//     core-matrix layout;
-//   * the tap's coefficient tile (NG x 32, hi and lo, precomputed in the same layout) arrives by one bulk copy,
-//     one iteration ahead, into a 3-deep ring;
-//   * one thread issues 3 tcgen05.mma.kind::tf32 per K-step into the TMEM accumulator and commits to an
-//     mbarrier; A tiles are double buffered so the next tap's tile is built while the tensor core works.
-// The epilogue reads TMEM (tcgen05.ld 32x32b) and writes per-plane forward partials (summed across planes in a
-// fixed order afterwards) or the backward result with the RL update / polyphase / image-layout epilogue.
+// For one plane z the direct path is a sum over coarse taps d of dense contractions over phases
+// (G_d[b'][a] = h_{z,a}[b1 - a1 + c + N d1][b2 - a2 + c + N d2], zero outside the kernel):
+//   forward : Y[m'][b']  = sum_d sum_a  X_a[m' - d] * G_d[b'][a]      (K = input phases a,  N = output phases b')
+//   backward: Xh[m][a]   = sum_d sum_b' r_b'[m + d] * G_d[b'][a]      (K = output phases b', N = input phases a)
+// Mapping onto tcgen05 (M = 128 coarse pixels = TMEM lanes, N = all phases <= 256 TMEM columns, K = 32-phase
+// chunks): every (tap, chunk) is one pipeline stage
+//   * A (128 pixels x 32 phases, hi and lo) is ONE 3-D TMA box each from a per-iteration staged copy of the
+//     source on a padded coarse grid -- a tap is only a row offset of the box, borders come from TMA's zero fill;
+//   * B (the tap's Ntile x 32 coefficient tile, hi and lo, pre-swizzled at plan time) is one 1-D bulk copy;
+//   * one thread issues 3 x ksteps tcgen05.mma.kind::tf32 (K = 8 each) into a fresh TMEM accumulator;
+//   * 8 drainer warps add the accumulator into fp32 registers with round-to-nearest after every stage
+//     (tcgen05's fp32 accumulation truncates; a 12-MMA chain keeps that bias below 1e-6 relative), while the
+//     tensor core fills the other accumulator.
+// One launch per direction covers every tensor-core plane: persistent CTAs walk a static LPT schedule of
+// (plane, pixel tile) items; forward items write per-plane partial images (summed over planes in a fixed order
+// afterwards -> deterministic), backward items write the plane's update epilogue directly.
+#include <algorithm>
+
 #include "lfm_internal.cuh"
 #include "tc_sm100.cuh"
 
 namespace lfm {
 
 namespace {
-constexpr int kTcM = 128;          // pixels per CTA (TMEM lanes)
-constexpr int kTcKC = 32;          // K phases per chunk (4 MMA K-steps)
-constexpr int kTcP = 4;            // taps per drain group (accumulation chain = kTcP/2 taps x 12 MMAs)
-constexpr int kTcBRing = 4;        // coefficient tiles in flight
-constexpr int kDrainWarps = 4;     // warps 0-3: TMEM lane quarters -> fp32 running sums, epilogue
-constexpr int kBuildWarps = 8;     // warps 4-11: window staging and A-tile builds
-constexpr int kTcThreads = 32 * (kDrainWarps + kBuildWarps + 1);   // + warp 12: MMA issuer / B producer
-constexpr uint32_t kTmemCols = 256;   // 2 regions x 2 accumulators x 64 columns (NG <= 48)
+constexpr int kM = 128;            // pixels per tile (TMEM lanes)
+constexpr int kKC = 32;            // phases per chunk (one 128-byte swizzle row)
+constexpr int kStages = 2;         // smem pipeline depth (A hi/lo + B hi/lo per stage)
+constexpr int kDrainWarps = 8;     // warps 2..9: two per TMEM lane quarter, half of the columns each
+constexpr int kThreads = 32 * (2 + kDrainWarps);
+constexpr int kMaxNh = 128;        // columns per drainer thread
+constexpr uint32_t kTmemCols = 512;   // 2 accumulators x 256 columns
+constexpr uint32_t kATile = kM * kKC * 4;   // 16 KB
+
+__host__ __device__ inline uint32_t stage_bytes(int Ntile) { return 2 * kATile + 2u * (uint32_t)Ntile * kKC * 4; }
 }  // namespace
 
-struct TcSmem {
-    uint32_t a[2];       // A tiles (hi then lo), 32 KB each
-    uint32_t b[kTcBRing];// B tiles (hi then lo), NG x 32 x 8 bytes
-    uint32_t win;        // source window [32][WR][WC]
-    uint32_t total;
-};
+size_t tcdir_smem_bytes(int Ntile) { return (size_t)kStages * stage_bytes(Ntile) + 1024; }
 
-__host__ __device__ inline TcSmem tc_smem_layout(int NG, int WR, int WC) {
-    TcSmem L{};
-    uint32_t o = 0;
-    const uint32_t atile = kTcM * kTcKC * 4 * 2;
-    const uint32_t btile = (uint32_t)NG * kTcKC * 4 * 2;
-    for (int i = 0; i < 2; ++i) {
-        L.a[i] = o;
-        o += atile;
-    }
-    for (int i = 0; i < kTcBRing; ++i) {
-        L.b[i] = o;
-        o += btile;
-    }
-    L.win = o;
-    o += (uint32_t)kTcKC * WR * WC * 4;
-    L.total = o;
-    return L;
-}
-
-__device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kBuildWarps) : "memory"); }
-
-// SRC (forward): 0 polyphase volume, 1 image-layout volume.  (backward): SRC_RATIO, SRC_ONES, SRC_IMAGE2D
-template <bool FWD, int SRC, int DST>
-__global__ void __launch_bounds__(kTcThreads, 1) tcdir_kernel(TcDirArgs d, const float* __restrict__ src,
-                                                              const float* __restrict__ src2, float eps,
-                                                              float* __restrict__ out, const float* __restrict__ xold,
-                                                              const float* __restrict__ norm) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    __shared__ uint64_t bar_afull[2], bar_aempty[2], bar_bfull[kTcBRing], bar_bempty[kTcBRing];
-    __shared__ uint64_t bar_mma[2], bar_tfree[2];
+// ------------------------------------------------------------------------------------------------
+template <bool FWD, int DST>
+__global__ void __launch_bounds__(kThreads, 1) tcdir_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ xold,
+                                                            const float* __restrict__ norm, float eps, float* __restrict__ out) {
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar_full[kStages], bar_empty[kStages], bar_acc[2], bar_tfree[2];
     __shared__ uint32_t tmem_base;
-    const int N = d.N, N2 = N * N;
-    const int NG = d.NG;
-    const int T2 = d.T2, NT = d.T1 * d.T2;
-    const int npix = d.nh * d.nw;
-    const int p0 = blockIdx.x * kTcM;
-    const int grp = blockIdx.y;
-    const int zi = blockIdx.z;
-    const int z = d.zlist[zi];
-    const int row0 = p0 / d.nw;
-    const int WR = d.WR, WC = d.WC, wsz = WR * WC;
-    const TcSmem L = tc_smem_layout(NG, WR, WC);
-    float* win = reinterpret_cast<float*>(smem + L.win);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nchunks = (d.Kpad + kTcKC - 1) / kTcKC;
-    const int total = nchunks * NT;
-    const int ngroups_drain = (total + kTcP - 1) / kTcP;
-    const uint32_t btile_bytes = (uint32_t)NG * kTcKC * 8;
+    const uint32_t raw = tc::smem_u32(smem_raw);
+    unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // SWIZZLE_128B tiles: 1024-byte aligned
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ib = d.item_off[blockIdx.x], ie = d.item_off[blockIdx.x + 1];
+    const uint32_t sbytes = stage_bytes(d.Ntile);
+    const uint32_t bbytes = 2u * (uint32_t)d.Ntile * kKC * 4;
 
-    if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            tc::mbar_init(&bar_afull[i], 32 * kBuildWarps);
-            tc::mbar_init(&bar_aempty[i], 1);
-            tc::mbar_init(&bar_mma[i], 1);
-            tc::mbar_init(&bar_tfree[i], 32 * kDrainWarps);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            tc::mbar_init(&bar_full[i], 1);
+            tc::mbar_init(&bar_empty[i], 1);
         }
-        for (int i = 0; i < kTcBRing; ++i) {
-            tc::mbar_init(&bar_bfull[i], 1);
-            tc::mbar_init(&bar_bempty[i], 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bar_acc[i], 1);
+            tc::mbar_init(&bar_tfree[i], kDrainWarps);
         }
         tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&d.tmap);
     }
     if (warp == 0) tc::tmem_alloc(&tmem_base, kTmemCols);
     tc::fence_before();
@@ -107,194 +71,127 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcdir_kernel(TcDirArgs d, const
     tc::fence_after();
     const uint32_t tmem = tmem_base;
 
-    if (warp < kDrainWarps) {
-        // ===================== drainers: TMEM -> fp32 (round-to-nearest) running sums =====================
-        float acc[48];
-#pragma unroll
-        for (int i = 0; i < 48; ++i) acc[i] = 0.0f;
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
-        for (int g = 0; g < ngroups_drain; ++g) {
-            const int reg = g & 1;
-            tc::mbar_wait(&bar_mma[reg], (g >> 1) & 1);
-            tc::fence_after();
-            const int nacc = min(2, total - g * kTcP);
-            for (int j = 0; j < nacc; ++j) {
-#pragma unroll
-                for (int c0 = 0; c0 < 48; c0 += 16) {
-                    if (c0 < NG) {
-                        float v[16];
-                        tc::tmem_ld16(lane_base + (uint32_t)(reg * 128 + j * 64 + c0), v);
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
+    if (warp == 0) {
+        if (lane == 0) {
+            // ============================ producer: TMA (A) + bulk copy (B) ============================
+            int it = 0;
+            for (int i = ib; i < ie; ++i) {
+                const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
+                const TcPlane pl = d.planes[zi];
+                const unsigned char* coef = reinterpret_cast<const unsigned char*>(d.coef + pl.coef_off);
+                for (int c = 0; c < d.nch; ++c)
+                    for (int t = 0; t < pl.T1 * pl.T2; ++t, ++it) {
+                        const int s = it % kStages;
+                        if (it >= kStages) tc::mbar_wait(&bar_empty[s], ((it / kStages) - 1) & 1);
+                        unsigned char* st = smem + (size_t)s * sbytes;
+                        const int e1 = pl.e1min + t / pl.T2, e2 = pl.e2min + t % pl.T2;
+                        const int row = tile * kM + e1 * d.Wp + e2 - d.e2lo;
+                        const int slab_hi = FWD ? (zi * 2) * d.nch + c : c;
+                        const int slab_lo = FWD ? (zi * 2 + 1) * d.nch + c : d.nch + c;
+                        tc::mbar_arrive_expect_tx(&bar_full[s], sbytes);
+                        tc::tma_load_3d(st, &d.tmap, 0, row, slab_hi, &bar_full[s]);
+                        tc::tma_load_3d(st + kATile, &d.tmap, 0, row, slab_lo, &bar_full[s]);
+                        tc::bulk_g2s(st + 2 * kATile, coef + ((size_t)t * d.nch + c) * bbytes, bbytes, &bar_full[s]);
                     }
-                }
-            }
-            tc::fence_before();
-            tc::mbar_arrive(&bar_tfree[reg]);
-        }
-        // ---- epilogue ----
-        const int r = 32 * warp + lane;
-        const int p = p0 + r;
-        if (p < npix) {
-            const int m1 = p / d.nw, m2 = p - (p / d.nw) * d.nw;
-#pragma unroll
-            for (int i = 0; i < 48; ++i) {
-                const int n = grp * NG + i;
-                if (i >= NG || n >= N2) break;
-                if constexpr (FWD) {   // n = output phase b'
-                    const int b1 = n / N, b2 = n - (n / N) * N;
-                    out[(size_t)zi * d.H * d.W + (size_t)(b1 + N * m1) * d.W + b2 + N * m2] = acc[i];
-                } else {               // n = input phase a of plane z
-                    const int u = z * N2 + n;
-                    if (u < d.unit0 || u >= d.unit0 + d.nu) continue;
-                    const size_t pidx = ((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2;
-                    if constexpr (DST == DST_POLY) {
-                        out[pidx] = acc[i];
-                    } else if constexpr (DST == DST_VOLIMAGE) {
-                        const int a1 = n / N, a2 = n - (n / N) * N;
-                        out[((size_t)z * d.H + a1 + N * m1) * d.W + a2 + N * m2] = acc[i];
-                    } else {
-                        out[pidx] = update_value<DST>(xold[pidx], norm[pidx], acc[i], eps);
-                    }
-                }
             }
         }
-    } else if (warp < kDrainWarps + kBuildWarps) {
-        // ===================== builders: windows and shifted A tiles (hi, lo) =====================
-        const int bt = tid - 32 * kDrainWarps;           // 0..255
-        const int r = bt & (kTcM - 1);                    // pixel row of the A tile
-        const int kq0 = bt >> 7;                          // k-quads kq0, kq0+2, kq0+4, kq0+6
-        const int p = p0 + r;
-        const bool pv = p < npix;
-        const int m1 = pv ? p / d.nw : 0, m2 = pv ? p - (p / d.nw) * d.nw : 0;
-        // window offset of tap (0,0); a tap (td1, td2) moves it by -(td1*WC + td2) (fwd) or +(td1*WC + td2) (bwd)
-        const int base0 = FWD ? (m1 - row0 + d.d1max - d.d1min) * WC + (m2 + d.d2max - d.d2min) : (m1 - row0) * WC + m2;
-        const uint32_t aoff = (uint32_t)((r >> 3) * (kTcKC / 4) * 128 + (r & 7) * 16) / 4;   // + kq * 32 floats
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ============================ MMA issuer (one thread) ============================
+            const uint32_t idesc = tc::idesc_tf32(kM, d.Ntile);
+            int it = 0;
+            for (int i = ib; i < ie; ++i) {
+                const int zi = d.items[i] / d.tiles;
+                const int NT = d.planes[zi].T1 * d.planes[zi].T2;
+                for (int c = 0; c < d.nch; ++c) {
+                        const int ks = c == d.nch - 1 ? d.kst_last : kKC / 8;
+                    for (int t = 0; t < NT; ++t, ++it) {
+                            const int s = it % kStages, j = it & 1;
+                            tc::mbar_wait(&bar_full[s], (it / kStages) & 1);
+                            if (it >= 2) tc::mbar_wait(&bar_tfree[j], ((it >> 1) - 1) & 1);
+                            tc::fence_after();
+                            const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * sbytes), a_lo = a_hi + kATile;
+                            const uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + (uint32_t)d.Ntile * kKC * 4;
+                            const uint32_t acc = tmem + (uint32_t)(j * 256);
+                            for (int k = 0; k < ks; ++k) {
+                                const uint64_t ah = tc::sdesc_sw128(a_hi + 32 * k), al = tc::sdesc_sw128(a_lo + 32 * k);
+                                const uint64_t bh = tc::sdesc_sw128(b_hi + 32 * k), bl = tc::sdesc_sw128(b_lo + 32 * k);
+                                tc::mma_tf32(acc, ah, bh, idesc, k > 0 ? 1u : 0u);
+                                tc::mma_tf32(acc, ah, bl, idesc, 1u);
+                                tc::mma_tf32(acc, al, bh, idesc, 1u);
+                            }
+                            tc::mma_commit(&bar_empty[s]);
+                            tc::mma_commit(&bar_acc[j]);
+                        }
+                    }
+            }
+        }
+    } else {
+        // ============================ drainers: TMEM -> fp32 running sums, epilogue ============================
+        const int q = warp & 3;                       // TMEM lane quarter this warp may access
+        const int half = (warp - 2) >> 2;             // column half
+        const int Nh = d.Ntile >> 1;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(half * Nh);
+        const int r = 32 * q + lane;                  // tile row (pixel) of this thread
+        float acc[kMaxNh];
+#pragma unroll
+        for (int i = 0; i < kMaxNh; ++i) acc[i] = 0.0f;
         int it = 0;
-        for (int c = 0; c < nchunks; ++c) {
-            const int k0 = c * kTcKC;
-            builders_sync();   // every A build of the previous chunk has read the window
-            for (int row = bt >> 5; row < kTcKC * WR; row += kBuildWarps) {
-                const int kk = row / WR, wr = row - (row / WR) * WR;
-                const int k = k0 + kk;
-                float* wrow = win + (size_t)row * WC;
-                if (k >= N2) {
-                    for (int wc = lane; wc < WC; wc += 32) wrow[wc] = 0.0f;
-                    continue;
-                }
-                if constexpr (FWD) {
-                    const int mm1 = row0 - d.d1max + wr;
-                    const int u = z * N2 + k;
-                    const bool ok = mm1 >= 0 && mm1 < d.nh && u >= d.unit0 && u < d.unit0 + d.nu;
-                    const float* srow;
-                    if constexpr (SRC == 0) {
-                        srow = src + ((size_t)(u - d.unit0) * d.nh + mm1) * d.nw;
-                    }
-                    for (int wc = lane; wc < WC; wc += 32) {
-                        const int mm2 = wc - d.d2max;
-                        float v = 0.0f;
-                        if (ok && mm2 >= 0 && mm2 < d.nw) {
-                            if constexpr (SRC == 0) {
-                                v = srow[mm2];
-                            } else {
-                                const int a1 = k / N, a2 = k - (k / N) * N;
-                                v = src[((size_t)z * d.H + a1 + N * mm1) * d.W + a2 + N * mm2];
-                            }
-                        }
-                        wrow[wc] = v;
-                    }
-                } else {
-                    const int mm1 = row0 + d.d1min + wr;
-                    const bool ok = mm1 >= 0 && mm1 < d.nh;
-                    const int b1 = k / N, b2 = k - (k / N) * N;
-                    const size_t rbase = (size_t)(b1 + N * mm1) * d.W + b2;
-                    for (int wc = lane; wc < WC; wc += 32) {
-                        const int mm2 = d.d2min + wc;
-                        float v = 0.0f;
-                        if (ok && mm2 >= 0 && mm2 < d.nw) {
-                            if constexpr (SRC == SRC_ONES) {
-                                v = 1.0f;
-                            } else {
-                                const size_t pix = rbase + (size_t)N * mm2;
-                                if constexpr (SRC == SRC_RATIO)
-                                    v = src[pix] / (fmaxf(src2[pix], 0.0f) + eps);
-                                else
-                                    v = src[pix];
-                            }
-                        }
-                        wrow[wc] = v;
-                    }
-                }
-            }
-            builders_sync();
-            for (int t = 0; t < NT; ++t, ++it) {
-                const int sa = it & 1;
-                const int td1 = t / T2, td2 = t - (t / T2) * T2;
-                if (it >= 2) tc::mbar_wait(&bar_aempty[sa], ((it - 2) >> 1) & 1);
-                float* ahi = reinterpret_cast<float*>(smem + L.a[sa]);
-                float* alo = ahi + kTcM * kTcKC;
-                const int off = FWD ? base0 - td1 * WC - td2 : base0 + td1 * WC + td2;
+        for (int i = ib; i < ie; ++i) {
+            const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
+            const int nst = d.nch * d.planes[zi].T1 * d.planes[zi].T2;
+            for (int st = 0; st < nst; ++st, ++it) {
+                const int j = it & 1;
+                tc::mbar_wait(&bar_acc[j], (it >> 1) & 1);
+                tc::fence_after();
+                const uint32_t base = lane_base + (uint32_t)(j * 256);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int kq = kq0 + 2 * q;
-                    float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), lv = hv;
-                    if (pv) {
-                        const float* w0 = win + (size_t)(4 * kq) * wsz + off;
-                        tc::split_tf32(w0[0], hv.x, lv.x);
-                        tc::split_tf32(w0[wsz], hv.y, lv.y);
-                        tc::split_tf32(w0[2 * wsz], hv.z, lv.z);
-                        tc::split_tf32(w0[3 * wsz], hv.w, lv.w);
+                for (int c0 = 0; c0 < kMaxNh; c0 += 32) {
+                    if (c0 < Nh) {
+                        uint32_t v[32];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (c0 + 8 * u < Nh) tc::tmem_ld8_nowait(base + (uint32_t)(c0 + 8 * u), v + 8 * u);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u)
+                            if (c0 + u < Nh) acc[c0 + u] += __uint_as_float(v[u]);
                     }
-                    *reinterpret_cast<float4*>(ahi + aoff + kq * 32) = hv;
-                    *reinterpret_cast<float4*>(alo + aoff + kq * 32) = lv;
                 }
-                tc::fence_proxy_async();
-                tc::mbar_arrive(&bar_afull[sa]);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_tfree[j]);
             }
-        }
-    } else if (lane == 0) {
-        // ===================== MMA issuer + coefficient producer (one thread) =====================
-        const unsigned char* coef = reinterpret_cast<const unsigned char*>(d.coef) +
-                                    ((size_t)zi * d.ngroups + grp) * (size_t)total * btile_bytes;
-        const uint32_t idesc = tc::idesc_tf32(kTcM, NG);
-        const int pre = min(kTcBRing - 1, total);
-        for (int j = 0; j < pre; ++j) {
-            tc::mbar_arrive_expect_tx(&bar_bfull[j], btile_bytes);
-            tc::bulk_g2s(smem + L.b[j], coef + (size_t)j * btile_bytes, btile_bytes, &bar_bfull[j]);
-        }
-        for (int it = 0; it < total; ++it) {
-            const int c = it / NT;
-            const int ksteps = min(kTcKC, d.Kpad - c * kTcKC) / 8;
-            const int g = it / kTcP, reg = g & 1;
-            if (it % kTcP == 0 && g >= 2) tc::mbar_wait(&bar_tfree[reg], ((g - 2) >> 1) & 1);
-            const int sa = it & 1, sb = it % kTcBRing;
-            tc::mbar_wait(&bar_afull[sa], (it >> 1) & 1);
-            tc::mbar_wait(&bar_bfull[sb], (it / kTcBRing) & 1);
-            tc::fence_after();
-            const uint32_t a_hi = tc::smem_u32(smem + L.a[sa]), a_lo = a_hi + kTcM * kTcKC * 4;
-            const uint32_t b_hi = tc::smem_u32(smem + L.b[sb]), b_lo = b_hi + (uint32_t)NG * kTcKC * 4;
-            const uint32_t acc_t = tmem + (uint32_t)(reg * 128 + (it & 1) * 64);
-            const bool first = (it % kTcP) < 2;       // first use of this accumulator in the group
-            for (int s = 0; s < ksteps; ++s) {
-                const uint64_t ah = tc::sdesc(a_hi + s * 256, 128, (kTcKC / 4) * 128);
-                const uint64_t al = tc::sdesc(a_lo + s * 256, 128, (kTcKC / 4) * 128);
-                const uint64_t bh = tc::sdesc(b_hi + s * 256, 128, (kTcKC / 4) * 128);
-                const uint64_t bl = tc::sdesc(b_lo + s * 256, 128, (kTcKC / 4) * 128);
-                tc::mma_tf32(acc_t, ah, bh, idesc, (first && s == 0) ? 0u : 1u);
-                tc::mma_tf32(acc_t, ah, bl, idesc, 1u);
-                tc::mma_tf32(acc_t, al, bh, idesc, 1u);
+            // ---- epilogue of the item ----
+            const int L = tile * kM + r;
+            const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp;
+            if (m1 < d.nh && m2 < d.nw) {
+                const size_t HW = (size_t)d.H * d.W;
+#pragma unroll
+                for (int i = 0; i < kMaxNh; ++i) {
+                    const int n = half * Nh + i;
+                    if (i < Nh && n < d.N2) {
+                        const int n1 = n / d.N, n2 = n - (n / d.N) * d.N;
+                        if constexpr (FWD) {   // n = output phase b'
+                            d.part[(size_t)zi * HW + (size_t)(n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i];
+                        } else {               // n = input phase a of plane z
+                            const int z = d.zlist[zi];
+                            const int u = z * d.N2 + n;
+                            if (u >= d.unit0 && u < d.unit0 + d.nu) {
+                                const size_t pidx = ((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2;
+                                if constexpr (DST == DST_POLY)
+                                    out[pidx] = acc[i];
+                                else if constexpr (DST == DST_VOLIMAGE)
+                                    out[((size_t)z * d.H + n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i];
+                                else
+                                    out[pidx] = update_value<DST>(xold[pidx], norm[pidx], acc[i], eps);
+                            }
+                        }
+                    }
+                }
             }
-            tc::mma_commit(&bar_aempty[sa]);
-            tc::mma_commit(&bar_bempty[sb]);
-            if (it % kTcP == kTcP - 1 || it == total - 1) tc::mma_commit(&bar_mma[reg]);
-            // refill the B ring: tile it+kTcBRing-1 goes to the slot of tile it-1 (wait for its MMAs)
-            const int j = it + kTcBRing - 1;
-            if (j < total) {
-                const int sj = j % kTcBRing;
-                if (j >= kTcBRing) tc::mbar_wait(&bar_bempty[sj], ((j - kTcBRing) / kTcBRing) & 1);
-                tc::mbar_arrive_expect_tx(&bar_bfull[sj], btile_bytes);
-                tc::bulk_g2s(smem + L.b[sj], coef + (size_t)j * btile_bytes, btile_bytes, &bar_bfull[sj]);
-            }
+#pragma unroll
+            for (int i = 0; i < kMaxNh; ++i) acc[i] = 0.0f;
         }
     }
     tc::fence_before();
@@ -302,70 +199,79 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcdir_kernel(TcDirArgs d, const
     if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
-template <bool FWD, int SRC, int DST>
-static cudaError_t tcdir_launch(const TcDirArgs& d, const float* src, const float* src2, float eps, float* out,
-                                const float* xold, const float* norm, cudaStream_t s) {
-    const TcSmem L = tc_smem_layout(d.NG, d.WR, d.WC);
-    cudaError_t e = cudaFuncSetAttribute(tcdir_kernel<FWD, SRC, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L.total);
-    if (e != cudaSuccess) return e;
-    dim3 grid((d.nh * d.nw + kTcM - 1) / kTcM, d.ngroups, d.nzd);
-    tcdir_kernel<FWD, SRC, DST><<<grid, kTcThreads, L.total, s>>>(d, src, src2, eps, out, xold, norm);
-    return cudaGetLastError();
+// ------------------------------------------------------------------------------------------------
+// Source staging: slab rows L of the padded grid (m1 = L / Wp, m2 = L % Wp + e2lo), 32 phases per row,
+// hi = tf32(v), lo = tf32(v - hi).  A 32-row x 32-phase tile per block, transposed through shared memory.
+//   forward  (SRC 0 polyphase volume [nu][nh][nw], 1 image-layout volume [nz][H][W]): plane blockIdx.z
+//   backward (SRC_RATIO y / (max(yhat,0)+eps), SRC_ONES, SRC_IMAGE2D): one image
+template <bool FWD, int SRC>
+__global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ src,
+                                                       const float* __restrict__ src2, float eps) {
+    __shared__ float tile[kKC][33];
+    const int L0 = blockIdx.x * 32, c = blockIdx.y, zi = blockIdx.z;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    {
+        const int L = L0 + tx;
+        const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp + d.e2lo;
+        const bool pv = L < d.Lp && m1 < d.nh && m2 >= 0 && m2 < d.nw;
+        for (int k = ty; k < kKC; k += 8) {
+            const int ph = c * kKC + k;
+            float v = 0.0f;
+            if (pv && ph < d.N2) {
+                const int p1 = ph / d.N, p2 = ph - (ph / d.N) * d.N;
+                if constexpr (FWD) {
+                    const int z = d.zlist[zi];
+                    const int u = z * d.N2 + ph;
+                    if (u >= d.unit0 && u < d.unit0 + d.nu) {
+                        if constexpr (SRC == 0)
+                            v = src[((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2];
+                        else
+                            v = src[((size_t)z * d.H + p1 + d.N * m1) * d.W + p2 + d.N * m2];
+                    }
+                } else {
+                    const size_t pix = (size_t)(p1 + d.N * m1) * d.W + p2 + d.N * m2;
+                    if constexpr (SRC == SRC_ONES)
+                        v = 1.0f;
+                    else if constexpr (SRC == SRC_RATIO)
+                        v = src[pix] / (fmaxf(src2[pix], 0.0f) + eps);
+                    else
+                        v = src[pix];
+                }
+            }
+            tile[k][tx] = v;
+        }
+    }
+    __syncthreads();
+    const size_t slab_hi = FWD ? ((size_t)zi * 2) * d.nch + c : (size_t)c;
+    const size_t slab_lo = FWD ? ((size_t)zi * 2 + 1) * d.nch + c : (size_t)d.nch + c;
+    for (int rr = ty; rr < 32; rr += 8) {
+        const int L = L0 + rr;
+        if (L >= d.Lp) break;
+        float h, l;
+        tc::split_tf32(tile[tx][rr], h, l);
+        d.src[(slab_hi * d.Lp + L) * kKC + tx] = h;
+        d.src[(slab_lo * d.Lp + L) * kKC + tx] = l;
+    }
 }
 
-size_t tcdir_smem_bytes(int NG, int WR, int WC) { return tc_smem_layout(NG, WR, WC).total; }
-
-cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
-                             cudaStream_t s) {
-    if (d.nzd <= 0) return cudaSuccess;
-    cudaError_t e = src_image ? tcdir_launch<true, 1, 0>(d, x, nullptr, 0.f, part, nullptr, nullptr, s)
-                              : tcdir_launch<true, 0, 0>(d, x, nullptr, 0.f, part, nullptr, nullptr, s);
-    if (e != cudaSuccess) return e;
-    return launch_plane_reduce(part, d.nzd, (size_t)d.H * d.W, y, accumulate, s);
-}
-
-cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
-                             float* out, const float* xold, const float* norm, cudaStream_t s) {
-    if (d.nzd <= 0) return cudaSuccess;
-#define LFM_TCB(SRCV, DSTV) \
-    if (src == SRCV && dst == DSTV) return tcdir_launch<false, SRCV, DSTV>(d, img, img2, eps, out, xold, norm, s);
-    LFM_TCB(SRC_RATIO, DST_UPDATE)
-    LFM_TCB(SRC_IMAGE2D, DST_ISRA)
-    LFM_TCB(SRC_ONES, DST_POLY)
-    LFM_TCB(SRC_IMAGE2D, DST_VOLIMAGE)
-    LFM_TCB(SRC_IMAGE2D, DST_POLY)
-    LFM_TCB(SRC_RATIO, DST_POLY)
-#undef LFM_TCB
-    return cudaErrorInvalidValue;
-}
-
-}  // namespace lfm
-
-namespace lfm {
-
-// Coefficient tiles for the tensor-core direct path, built on the device from the owned PSF slice:
-// tile (zi, grp, chunk, tap) = [hi | lo] of an NG x 32 K-major core-matrix tile whose element (n, k) is
-//   forward : G_d[b' = grp*NG + n][a = chunk*32 + k]      backward: G_d[b' = chunk*32 + k][a = grp*NG + n]
-// with G_d[b'][a] = h_{z,a}[b1 - a1 + ch + N d1][b2 - a2 + cw + N d2] (0 outside the kernel / phases).
-__global__ void tcdir_coef_kernel(TcDirArgs d, const int* __restrict__ zlist_host_order, const float* __restrict__ psf,
+// ------------------------------------------------------------------------------------------------
+// Coefficient tiles of one plane (plan time), built on the device from the owned PSF slice: tile (tap, chunk) =
+// [hi | lo] of an Ntile x 32 SWIZZLE_128B K-major tile with element (n, k) =
+//   forward : G_d[b' = n][a = chunk*32 + k],   d = -e        backward: G_d[b' = chunk*32 + k][a = n],   d = +e
+__global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane pl, int z, const float* __restrict__ psf,
                                   int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out) {
-    const int nchunks = d.Kpad / kTcKC + (d.Kpad % kTcKC ? 1 : 0);
-    const int NT = d.T1 * d.T2;
-    const int tile = blockIdx.x;   // ((zi * ngroups + grp) * nchunks + chunk) * NT + tap
-    const int tap = tile % NT;
-    const int chunk = (tile / NT) % nchunks;
-    const int grp = (tile / (NT * nchunks)) % d.ngroups;
-    const int zi = tile / (NT * nchunks * d.ngroups);
-    const int z = zlist_host_order[zi];
-    const int N = d.N, N2 = N * N;
-    const int d1 = d.d1min + tap / d.T2, d2 = d.d2min + tap % d.T2;
-    float* hi = out + (size_t)tile * d.NG * kTcKC * 2;
-    float* lo = hi + (size_t)d.NG * kTcKC;
-    for (int e = threadIdx.x; e < d.NG * kTcKC; e += blockDim.x) {
-        const int n = e / kTcKC, k = e - (e / kTcKC) * kTcKC;
-        const int ng = grp * d.NG + n, kg = chunk * kTcKC + k;
-        const int bp = fwd ? ng : kg, a = fwd ? kg : ng;
+    const int tileid = blockIdx.x;   // tap * nch + chunk
+    const int chunk = tileid % d.nch;
+    const int tap = tileid / d.nch;
+    const int N = d.N, N2 = d.N2;
+    const int e1 = pl.e1min + tap / pl.T2, e2 = pl.e2min + tap % pl.T2;
+    const int d1 = fwd ? -e1 : e1, d2 = fwd ? -e2 : e2;
+    float* hi = out + pl.coef_off + (size_t)tileid * d.Ntile * kKC * 2;
+    float* lo = hi + (size_t)d.Ntile * kKC;
+    for (int e = threadIdx.x; e < d.Ntile * kKC; e += blockDim.x) {
+        const int n = e / kKC, k = e - (e / kKC) * kKC;
+        const int kg = chunk * kKC + k;
+        const int bp = fwd ? n : kg, a = fwd ? kg : n;
         float v = 0.0f;
         if (bp < N2 && a < N2) {
             const int u = z * N2 + a;
@@ -377,24 +283,155 @@ __global__ void tcdir_coef_kernel(TcDirArgs d, const int* __restrict__ zlist_hos
         }
         float h, l;
         tc::split_tf32(v, h, l);
-        const uint32_t off = tc::kmajor_off(n, k, kTcKC) / 4;
+        const uint32_t off = tc::sw128_off(n, k) / 4;
         hi[off] = h;
         lo[off] = l;
     }
 }
 
-cudaError_t launch_tcdir_coef(const TcDirArgs& d, const int* zlist_dev, const float* psf_dev, int kh, int kw, int ch,
-                              int cw, int fwd, float* out, cudaStream_t s) {
-    const int nchunks = d.Kpad / kTcKC + (d.Kpad % kTcKC ? 1 : 0);
-    const long long tiles = (long long)d.nzd * d.ngroups * nchunks * d.T1 * d.T2;
+// ------------------------------------------------------------------------------------------------
+// host side
+
+bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, const int* d2min, const int* d2max,
+                    std::vector<TcPlane>* planes, int num_sms) {
+    d->N2 = d->N * d->N;
+    d->Ntile = (d->N2 + 15) / 16 * 16;
+    if (d->Ntile > 2 * kMaxNh) return false;
+    d->nch = (d->N2 + kKC - 1) / kKC;
+    d->kst_last = ((d->N2 - (d->nch - 1) * kKC) + 7) / 8;
+    planes->assign(d->nzd, TcPlane{});
+    int e2lo = 1 << 30, e2hi = -(1 << 30);
+    long long off = 0;
+    for (int zi = 0; zi < d->nzd; ++zi) {
+        TcPlane& pl = (*planes)[zi];
+        pl.T1 = d1max[zi] - d1min[zi] + 1;
+        pl.T2 = d2max[zi] - d2min[zi] + 1;
+        pl.e1min = fwd ? -d1max[zi] : d1min[zi];
+        pl.e2min = fwd ? -d2max[zi] : d2min[zi];
+        pl.coef_off = off;
+        off += (long long)pl.T1 * pl.T2 * d->nch * d->Ntile * kKC * 2;
+        e2lo = std::min(e2lo, pl.e2min);
+        e2hi = std::max(e2hi, pl.e2min + pl.T2 - 1);
+    }
+    d->e2lo = d->nzd > 0 ? e2lo : 0;
+    d->Wp = d->nw + (d->nzd > 0 ? e2hi - e2lo : 0);
+    d->Lp = d->nh * d->Wp;
+    d->tiles = (d->Lp + kM - 1) / kM;
+    d->grid = std::max(1, std::min(d->tiles * d->nzd, num_sms));
+    return true;
+}
+
+void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std::vector<int>* item_off,
+                    std::vector<int>* items) {
+    // longest-processing-time-first: items sorted by cost (taps), each to the least-loaded CTA
+    std::vector<std::pair<long long, int>> it;
+    for (int zi = 0; zi < d.nzd; ++zi)
+        for (int t = 0; t < d.tiles; ++t) it.push_back({(long long)planes[zi].T1 * planes[zi].T2, zi * d.tiles + t});
+    std::stable_sort(it.begin(), it.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    std::vector<long long> load(d.grid, 0);
+    std::vector<std::vector<int>> per(d.grid);
+    for (const auto& x : it) {
+        int best = 0;
+        for (int b = 1; b < d.grid; ++b)
+            if (load[b] < load[best]) best = b;
+        load[best] += x.first;
+        per[best].push_back(x.second);
+    }
+    item_off->assign(1, 0);
+    items->clear();
+    for (int b = 0; b < d.grid; ++b) {
+        std::sort(per[b].begin(), per[b].end());   // plane-major within a CTA (L2 locality of the staged source)
+        items->insert(items->end(), per[b].begin(), per[b].end());
+        item_off->push_back((int)items->size());
+    }
+}
+
+size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes) {
+    size_t n = 0;
+    for (const TcPlane& pl : planes) n += (size_t)pl.T1 * pl.T2 * d.nch * d.Ntile * kKC * 2;
+    return n;
+}
+size_t tcdir_src_floats(const TcDirArgs& d, int fwd) { return (size_t)(fwd ? 2 * d.nzd : 2) * d.nch * d.Lp * kKC; }
+size_t tcdir_part_floats(const TcDirArgs& d, int fwd) { return fwd ? (size_t)d.nzd * d.H * d.W : 0; }
+
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t tcdir_encode(TcDirArgs* d, int fwd) {
+    static TmapEncodeFn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !enc || q != cudaDriverEntryPointSuccess) {
+            enc = nullptr;
+            return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+        }
+    }
+    const cuuint64_t slabs = (cuuint64_t)(fwd ? 2 * d->nzd : 2) * d->nch;
+    cuuint64_t dims[3] = {(cuuint64_t)kKC, (cuuint64_t)d->Lp, slabs};
+    cuuint64_t strides[2] = {(cuuint64_t)kKC * 4, (cuuint64_t)d->Lp * kKC * 4};
+    cuuint32_t box[3] = {(cuuint32_t)kKC, (cuuint32_t)kM, 1}, es[3] = {1, 1, 1};
+    CUresult r = enc(&d->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->src, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
+                              int kw, int ch, int cw, int fwd, float* coef, cudaStream_t s) {
+    (void)zi;
+    const int tiles = pl.T1 * pl.T2 * d.nch;
     if (tiles <= 0) return cudaSuccess;
-    tcdir_coef_kernel<<<(unsigned)tiles, 256, 0, s>>>(d, zlist_dev, psf_dev, kh, kw, ch, cw, fwd, out);
+    tcdir_coef_kernel<<<tiles, 256, 0, s>>>(d, pl, z, psf_dev, kh, kw, ch, cw, fwd, coef);
     return cudaGetLastError();
 }
 
-size_t tcdir_coef_floats(const TcDirArgs& d) {
-    const int nchunks = d.Kpad / kTcKC + (d.Kpad % kTcKC ? 1 : 0);
-    return (size_t)d.nzd * d.ngroups * nchunks * d.T1 * d.T2 * d.NG * kTcKC * 2;
+template <bool FWD, int DST>
+static cudaError_t tcdir_main(const TcDirArgs& d, const float* xold, const float* norm, float eps, float* out,
+                              cudaStream_t s) {
+    const size_t smem = tcdir_smem_bytes(d.Ntile);
+    cudaError_t e = cudaFuncSetAttribute(tcdir_kernel<FWD, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tcdir_kernel<FWD, DST><<<d.grid, kThreads, smem, s>>>(d, xold, norm, eps, out);
+    return cudaGetLastError();
+}
+
+template <bool FWD, int SRC>
+static cudaError_t tc_stage(const TcDirArgs& d, const float* src, const float* src2, float eps, cudaStream_t s) {
+    dim3 grid((d.Lp + 31) / 32, d.nch, FWD ? d.nzd : 1);
+    tc_stage_kernel<FWD, SRC><<<grid, 256, 0, s>>>(d, src, src2, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* y, int accumulate,
+                             cudaStream_t s) {
+    if (d.nzd <= 0) return cudaSuccess;
+    cudaError_t e = src_image ? tc_stage<true, 1>(d, x, nullptr, 0.f, s) : tc_stage<true, 0>(d, x, nullptr, 0.f, s);
+    if (e != cudaSuccess) return e;
+    e = tcdir_main<true, 0>(d, nullptr, nullptr, 0.f, nullptr, s);
+    if (e != cudaSuccess) return e;
+    return launch_plane_reduce(d.part, d.nzd, (size_t)d.H * d.W, y, accumulate, s);
+}
+
+cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
+                             float* out, const float* xold, const float* norm, cudaStream_t s) {
+    if (d.nzd <= 0) return cudaSuccess;
+    cudaError_t e;
+    switch (src) {
+        case SRC_RATIO: e = tc_stage<false, SRC_RATIO>(d, img, img2, eps, s); break;
+        case SRC_ONES: e = tc_stage<false, SRC_ONES>(d, nullptr, nullptr, eps, s); break;
+        case SRC_IMAGE2D: e = tc_stage<false, SRC_IMAGE2D>(d, img, nullptr, eps, s); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    switch (dst) {
+        case DST_UPDATE: return tcdir_main<false, DST_UPDATE>(d, xold, norm, eps, out, s);
+        case DST_ISRA: return tcdir_main<false, DST_ISRA>(d, xold, norm, eps, out, s);
+        case DST_POLY: return tcdir_main<false, DST_POLY>(d, xold, norm, eps, out, s);
+        case DST_VOLIMAGE: return tcdir_main<false, DST_VOLIMAGE>(d, xold, norm, eps, out, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace lfm

@@ -418,8 +418,8 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
         ST(mark(p, ST_DIR_FWD, s));
         bool acc = p->nu_fft > 0;
         for (const TcDirArgs& tg : p->tcf) {
-            CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, p->dpart, yimg, acc ? 1 : 0, s));
-            p->pacc.launches += 2;
+            CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, acc ? 1 : 0, s));
+            p->pacc.launches += 3;
             acc = true;
         }
         for (const DirArgs& dg : p->dgroups) {
@@ -488,7 +488,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     ST(mark(p, ST_DIR_BWD, s));
     for (const TcDirArgs& tg : p->tcb) {
         CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s));
-        p->pacc.launches += 1;
+        p->pacc.launches += 2;
     }
     for (const DirArgs& dg : p->dgroups) {
         CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, aux, s));
@@ -643,10 +643,12 @@ AxisBox axis_box(int N, int c, int k0, int k1) {
 constexpr double kHbmBps = 7.0e12;
 constexpr double kXformPerUnit = 9.0e-8;
 const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 28.0e12};
-// tensor-core direct path: cycles per (tile, N-group, K-chunk, tap) iteration, SM clock
-constexpr double kTcCyclesPerTap = 3400.0;   // measured r01 (issue/latency bound)
+// tensor-core direct path: tf32 MACs per cycle per SM (1.13 PFLOP/s dense / 148 SMs / 1.9 GHz), achieved
+// fraction of it, and a fixed per-plane cost (staging, partial reduce)
+constexpr double kTcMacPerCycle = 2000.0;
+constexpr double kTcEff = 0.5;
+constexpr double kTcFixed = 5e-6;
 constexpr double kSmClock = 1.9e9;
-constexpr size_t kTcSmemLimit = 220 * 1024;
 
 }  // namespace
 
@@ -889,22 +891,20 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double units = ue - ub;
         const double t_fft = 2.0 * units * N2 * g.nkappa * 8.0 / kHbmBps + kXformPerUnit * units;
         const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
-        // tensor-core direct: union tap box of the plane and its shared-memory footprint
+        // tensor-core direct (kernels_tcdir.cu): one pipeline stage per (tile, tap, 32-phase chunk) and direction
         const int T1 = box1[z].dmax - box1[z].dmin + box1[z].D, T2 = box2[z].dmax - box2[z].dmin + box2[z].D;
-        const int NG = std::min(48, (int)round_up((size_t)N2, 16)), ngr = (N2 + NG - 1) / NG;
-        const int Kpad = (int)round_up((size_t)N2, 8), nch = (Kpad + 31) / 32;
-        const int npix = g.nh * g.nw, tiles = (npix + 127) / 128;
-        int span = 1;
-        for (int p0 = 0; p0 < npix; p0 += 128) span = std::max(span, std::min(p0 + 127, npix - 1) / g.nw - p0 / g.nw + 1);
-        const bool tc_ok = (flags & LFM_PLAN_TC_DIRECT) &&
-                           tcdir_smem_bytes(NG, span + T1 - 1, g.nw + T2 - 1) <= kTcSmemLimit;
-        const double t_tc = tc_ok ? 2.0 * tiles * ngr * nch * (double)T1 * T2 * kTcCyclesPerTap / (p->num_sms * kSmClock)
+        const int Ntile = (int)round_up((size_t)N2, 16), nch = (N2 + 31) / 32;
+        const int tiles = (g.nh * (g.nw + T2 - 1) + 127) / 128;
+        const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256;
+        const double stage_cycles = 3.0 * 4 * 128.0 * Ntile * 8 / kTcMacPerCycle / kTcEff;
+        const double t_tc = tc_ok ? 2.0 * tiles * nch * (double)T1 * T2 * stage_cycles / (p->num_sms * kSmClock) *
+                                        (units / N2) + kTcFixed
                                   : 1e30;
         int mode = 0;                            // 0 FFT, 1 SIMT direct, 2 tensor-core direct
         if (flags & LFM_PLAN_FFT_ONLY) {
             mode = 0;
         } else if (flags & LFM_PLAN_DIRECT) {
-            mode = tc_ok ? 2 : 1;
+            mode = (flags & LFM_PLAN_TC_DIRECT) && tc_ok ? 2 : 1;
         } else {
             const double best = std::min(t_fft, std::min(t_dir, t_tc));
             mode = best == t_fft ? 0 : (best == t_tc ? 2 : 1);
@@ -1007,19 +1007,18 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             p->n_direct_planes += nzd;
             coef_bytes += 2 * cf.size() * sizeof(float);
         }
-        // tensor-core direct groups: planes with identical tap boxes share one launch
+        // tensor-core direct planes: one merged launch per direction (LPT schedule over (plane, tile) items)
         {
-            std::vector<int> done(nz, 0);
-            for (int z0 = zb; z0 <= ze; ++z0) {
-                if (plane_direct[z0] != 2 || done[z0]) continue;
-                std::vector<int> zl;
-                for (int z = z0; z <= ze; ++z)
-                    if (plane_direct[z] == 2 && !done[z] && box1[z].dmin == box1[z0].dmin && box1[z].dmax == box1[z0].dmax &&
-                        box1[z].D == box1[z0].D && box2[z].dmin == box2[z0].dmin && box2[z].dmax == box2[z0].dmax &&
-                        box2[z].D == box2[z0].D) {
-                        zl.push_back(z);
-                        done[z] = 1;
-                    }
+            std::vector<int> zl, d1a, d1b, d2a, d2b;
+            for (int z = zb; z <= ze; ++z)
+                if (plane_direct[z] == 2) {
+                    zl.push_back(z);
+                    d1a.push_back(box1[z].dmin);
+                    d1b.push_back(box1[z].dmax + box1[z].D - 1);
+                    d2a.push_back(box2[z].dmin);
+                    d2b.push_back(box2[z].dmax + box2[z].D - 1);
+                }
+            if (!zl.empty()) {
                 TcDirArgs ta{};
                 ta.N = nnum;
                 ta.H = height;
@@ -1029,48 +1028,61 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 ta.unit0 = p->u0;
                 ta.nu = p->nu;
                 ta.nzd = (int)zl.size();
-                ta.NG = std::min(48, (int)round_up((size_t)N2, 16));
-                ta.ngroups = (N2 + ta.NG - 1) / ta.NG;
-                ta.Kpad = (int)round_up((size_t)N2, 8);
-                ta.d1min = box1[z0].dmin;
-                ta.d1max = box1[z0].dmax + box1[z0].D - 1;
-                ta.d2min = box2[z0].dmin;
-                ta.d2max = box2[z0].dmax + box2[z0].D - 1;
-                ta.T1 = ta.d1max - ta.d1min + 1;
-                ta.T2 = ta.d2max - ta.d2min + 1;
-                const int npix = g.nh * g.nw;
-                int span = 1;
-                for (int q0 = 0; q0 < npix; q0 += 128) span = std::max(span, std::min(q0 + 127, npix - 1) / g.nw - q0 / g.nw + 1);
-                ta.WR = span + ta.T1 - 1;
-                ta.WC = g.nw + ta.T2 - 1;
                 int* dz = nullptr;
                 PG(dalloc(p, &dz, zl.size() * sizeof(int), "tc plane list"));
                 p->dallocs.push_back(dz);
                 CKG(cudaMemcpyAsync(dz, zl.data(), zl.size() * sizeof(int), cudaMemcpyHostToDevice, s));
                 ta.zlist = dz;
-                const size_t nf = tcdir_coef_floats(ta);
-                float *cf = nullptr, *cb = nullptr;
-                PG(dalloc(p, &cf, nf * sizeof(float), "tc direct taps (forward)"));
-                p->dallocs.push_back(cf);
-                PG(dalloc(p, &cb, nf * sizeof(float), "tc direct taps (backward)"));
-                p->dallocs.push_back(cb);
-                CKG(launch_tcdir_coef(ta, dz, p->psf, kh, kw, g.ch, g.cw, 1, cf, s));
-                CKG(launch_tcdir_coef(ta, dz, p->psfb, kh, kw, g.ch, g.cw, 0, cb, s));
-                CKG(cudaStreamSynchronize(s));   // zl dies at the end of this scope
                 TcDirArgs tb = ta;
-                ta.coef = cf;
-                tb.coef = cb;
+                for (int w = 0; w < 2; ++w) {
+                    TcDirArgs& t = w ? tb : ta;
+                    std::vector<TcPlane> pls;
+                    if (!tcdir_geometry(&t, !w, d1a.data(), d1b.data(), d2a.data(), d2b.data(), &pls, p->num_sms))
+                        return guard(fail(LFM_EUNSUPPORTED, "tensor-core direct path needs Nnum^2 <= 256"));
+                    std::vector<int> ioff, items;
+                    tcdir_schedule(t, pls, &ioff, &items);
+                    TcPlane* dpl = nullptr;
+                    int *dio = nullptr, *dit = nullptr;
+                    float *cf = nullptr, *sr = nullptr, *pt = nullptr;
+                    const size_t nf = tcdir_coef_floats(t, pls), ns = tcdir_src_floats(t, !w), np = tcdir_part_floats(t, !w);
+                    PG(dalloc(p, &dpl, pls.size() * sizeof(TcPlane), "tc plane records"));
+                    p->dallocs.push_back(dpl);
+                    PG(dalloc(p, &dio, ioff.size() * sizeof(int), "tc schedule"));
+                    p->dallocs.push_back(dio);
+                    PG(dalloc(p, &dit, items.size() * sizeof(int), "tc schedule"));
+                    p->dallocs.push_back(dit);
+                    PG(dalloc(p, &cf, nf * sizeof(float), "tc direct taps"));
+                    p->dallocs.push_back(cf);
+                    PG(dalloc(p, &sr, ns * sizeof(float), "tc direct staged source"));
+                    p->dallocs.push_back(sr);
+                    if (np) {
+                        PG(dalloc(p, &pt, np * sizeof(float), "tc direct forward partials"));
+                        p->dallocs.push_back(pt);
+                    }
+                    CKG(cudaMemcpyAsync(dpl, pls.data(), pls.size() * sizeof(TcPlane), cudaMemcpyHostToDevice, s));
+                    CKG(cudaMemcpyAsync(dio, ioff.data(), ioff.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    CKG(cudaMemcpyAsync(dit, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    t.planes = dpl;
+                    t.item_off = dio;
+                    t.items = dit;
+                    t.coef = cf;
+                    t.src = sr;
+                    t.part = pt;
+                    CKG(tcdir_encode(&t, !w));
+                    for (int zi = 0; zi < t.nzd; ++zi)
+                        CKG(launch_tcdir_coef(t, pls[zi], zi, zl[zi], w ? p->psfb : p->psf, kh, kw, g.ch, g.cw, !w, cf, s));
+                    CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
+                    coef_bytes += nf * sizeof(float);
+                }
                 p->tcf.push_back(ta);
                 p->tcb.push_back(tb);
                 p->n_tc_planes += ta.nzd;
                 p->n_direct_planes += ta.nzd;
-                coef_bytes += 2 * nf * sizeof(float);
             }
         }
         p->transfer_bytes = coef_bytes;
         int maxg = 0;
         for (const DirArgs& dg : p->dgroups) maxg = std::max(maxg, dg.nzd);
-        for (const TcDirArgs& tg : p->tcf) maxg = std::max(maxg, tg.nzd);
         if (maxg > 0) PG(dalloc(p, &p->dpart, (size_t)maxg * HW * sizeof(float), "direct forward partials"));
         if (p->nu_fft > 0) {
             if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
@@ -1421,7 +1433,7 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                 acc = true;
             }
             for (const TcDirArgs& tg : p->tcf) {
-                CK(launch_tcdir_fwd(tg, xbuf(f, cur[f]), 0, p->dpart, yimg, acc ? 1 : 0, s));
+                CK(launch_tcdir_fwd(tg, xbuf(f, cur[f]), 0, yimg, acc ? 1 : 0, s));
                 acc = true;
             }
             for (const DirArgs& dg : p->dgroups) {

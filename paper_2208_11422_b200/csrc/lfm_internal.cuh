@@ -4,10 +4,12 @@
 // (plane z, input phase a), output phase b' = b1*N + b2, coarse transform Lh x Lw, kappa = k1*nk2 + k2
 // with nk2 = Lw/2 + 1 (Hermitian half plane).
 #pragma once
+#include <cuda.h>   // CUtensorMap (types only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 #include "../../include/lfm.h"
 
 namespace lfm {
@@ -93,24 +95,46 @@ struct DirArgs {
     const float* coef_b;      // [nzd][b'][D*D][a] (backward: input phase fastest)
     const int* dlo;           // [nzd][2][N][N]: dlo1[a1][b1], dlo2[a2][b2]
 };
-// tensor-core direct part (kernels_tcdir.cu)
+// tensor-core direct part (kernels_tcdir.cu).  One direction over ALL tensor-core planes of the
+// plan (one launch).  Source offsets e = -d (forward: X_a[m' - d]) or e = +d (backward: r_b'[m + d]); the source
+// is staged per iteration on a padded coarse grid shared by all planes (row pitch Wp >= nw + T2 - 1 for every
+// plane, column c holds m2 = c + e2lo) so that a tap is a plain row offset of a TMA box.
+struct TcPlane {
+    int T1, T2, e1min, e2min;   // union tap box of the plane (source offsets)
+    long long coef_off;         // floats: first coefficient tile of the plane
+};
 struct TcDirArgs {
     int N, H, W, nh, nw;
     int unit0, nu;            // owned units
-    int nzd;                  // planes in this group
+    int nzd;                  // tensor-core planes
     const int* zlist;         // [nzd] global plane index (device)
-    int NG, ngroups;          // N-phases per CTA (TMEM columns) and number of groups
-    int Kpad;                 // reduction phases padded to a multiple of 8
-    int T1, T2;               // union tap box
-    int d1min, d1max, d2min, d2max;   // tap offsets (inclusive)
-    int WR, WC;               // source window rows / cols
-    const float* coef;        // [zi][grp][chunk][tap][hi|lo][NG x 32] (direction-specific)
+    const TcPlane* planes;    // [nzd] (device)
+    int N2, Ntile;            // phases and TMEM columns per accumulator (N2 rounded up to 16, <= 256)
+    int nch, kst_last;        // reduction chunks of 32 phases; K-steps of 8 in the last chunk
+    int e2lo;                 // column origin of the staged grid (min e2min over planes)
+    int Wp, Lp, tiles;        // padded grid: Lp = nh * Wp rows of 32 phases, tiles of 128 rows
+    int grid;                 // persistent CTAs
+    const int* item_off;      // [grid + 1] CTA b runs items[item_off[b] .. item_off[b+1])   (LPT schedule)
+    const int* items;         // item = zi * tiles + tile
+    const float* coef;        // per plane [tap][chunk][hi | lo][Ntile x 32, SWIZZLE_128B]
+    float* src;               // staged source, slabs of [Lp][32] (hi / lo): fwd ((zi*2+part)*nch+c), bwd (part*nch+c)
+    float* part;              // forward per-plane partial images [nzd][H][W]
+    alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, 128, 1}, SWIZZLE_128B
 };
-size_t tcdir_smem_bytes(int NG, int WR, int WC);
-size_t tcdir_coef_floats(const TcDirArgs& d);
-cudaError_t launch_tcdir_coef(const TcDirArgs& d, const int* zlist_dev, const float* psf_dev, int kh, int kw, int ch,
-                              int cw, int fwd, float* out, cudaStream_t s);
-cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
+// geometry of one direction from the per-plane tap boxes d in [d1min, d1max] x [d2min, d2max] (host arrays)
+bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, const int* d2min, const int* d2max,
+                    std::vector<TcPlane>* planes, int num_sms);
+// LPT schedule of the (plane, tile) items over d->grid CTAs (host arrays)
+void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std::vector<int>* item_off,
+                    std::vector<int>* items);
+size_t tcdir_smem_bytes(int Ntile);
+size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes);
+size_t tcdir_src_floats(const TcDirArgs& d, int fwd);
+size_t tcdir_part_floats(const TcDirArgs& d, int fwd);
+cudaError_t tcdir_encode(TcDirArgs* d, int fwd);
+cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
+                              int kw, int ch, int cw, int fwd, float* coef, cudaStream_t s);
+cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* y, int accumulate,
                              cudaStream_t s);
 cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
                              float* out, const float* xold, const float* norm, cudaStream_t s);

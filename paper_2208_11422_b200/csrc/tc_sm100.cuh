@@ -29,6 +29,47 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;
 }
 
+// UMMA descriptor of a K-major SWIZZLE_128B tile: rows of 128 B (32 fp32 along K), 8-row atoms of 1024 B
+// (SBO = 1024), the 16-byte chunk j of row r stored at chunk j ^ (r & 7) -- the layout a TMA box with a
+// 128-byte inner dimension and CU_TENSOR_MAP_SWIZZLE_128B writes.  The tile must be 1024-byte aligned;
+// K-step s (8 tf32) starts 32*s bytes further (the swizzle is applied to the computed addresses).
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;                     // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024u >> 4) << 32;           // SBO
+    d |= (uint64_t)1u << 46;                     // descriptor version (sm_100)
+    d |= (uint64_t)2u << 61;                     // layout: SWIZZLE_128B
+    return d;
+}
+
+// byte offset of element (r, k) (k < 32) inside a K-major SWIZZLE_128B tile
+__host__ __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
+    return (uint32_t)(r * 128 + ((((k >> 2) ^ (r & 7)) & 7) << 4) + (k & 3) * 4);
+}
+
+// 3-D tiled TMA load global -> shared (box as encoded in the tensor map), completion on an mbarrier.
+// Out-of-bounds box elements (negative or past-the-end coordinates) are zero-filled.
+__device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst_smem)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// 32 lanes x 8 consecutive fp32 columns of TMEM -> registers (no wait; pair with tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // instruction descriptor: D fp32, A/B tf32, both K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

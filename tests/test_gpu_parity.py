@@ -59,7 +59,7 @@ OP_CASES = [  # (nz, N, H, W, kh, kw): tiny, ragged units, non-square, radix 2/3
 ]
 
 
-@pytest.mark.parametrize("flags", [0, 2, 4, 18, 16], ids=["hybrid", "direct", "fft", "direct-tc", "hybrid-tc"])
+@pytest.mark.parametrize("flags", [0, 2, 4, 18, 64], ids=["hybrid", "direct", "fft", "direct-tc", "hybrid-notc"])
 @pytest.mark.parametrize("case", OP_CASES, ids=[str(c) for c in OP_CASES])
 def test_projections_match_oracle(case, flags):
     nz, N, H, W, kh, kw = case
