@@ -18,6 +18,8 @@
 // (plane, pixel tile) items; forward items write per-plane partial images (summed over planes in a fixed order
 // afterwards -> deterministic), backward items write the plane's update epilogue directly.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "lfm_internal.cuh"
 #include "tc_sm100.cuh"
@@ -25,133 +27,233 @@
 namespace lfm {
 
 namespace {
-constexpr int kM = 128;            // pixels per tile (TMEM lanes)
+constexpr int kM = 128;            // pixels per CTA tile (TMEM lanes); a CTA pair covers 2 * kM pixels
 constexpr int kKC = 32;            // phases per chunk (one 128-byte swizzle row)
-constexpr int kStages = 2;         // smem pipeline depth (A hi/lo + B hi/lo per stage)
+constexpr int kASlots = 2;         // A windows in flight (one per 32-phase chunk x tap row e1)
+constexpr int kBSlots = 4;         // coefficient tiles in flight (one per tap)
 constexpr int kDrainWarps = 8;     // warps 2..9: two per TMEM lane quarter, half of the columns each
 constexpr int kThreads = 32 * (2 + kDrainWarps);
 constexpr int kMaxNh = 128;        // columns per drainer thread
 constexpr uint32_t kTmemCols = 512;   // 2 accumulators x 256 columns
-constexpr uint32_t kATile = kM * kKC * 4;   // 16 KB
+constexpr int kChainK = 16;        // default K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
 
-__host__ __device__ inline uint32_t stage_bytes(int Ntile) { return 2 * kATile + 2u * (uint32_t)Ntile * kKC * 4; }
+// per-CTA smem: A windows (hi | lo, Arows = 128 + T2max - 1 rows of 128 B each part) and B tiles (hi | lo,
+// Ntile/2 rows each: the pair splits B along N); every part 1024-byte aligned (SWIZZLE_128B atoms)
+__host__ __device__ inline uint32_t round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
+__host__ __device__ inline uint32_t apart_bytes(int Arows) { return round1k((uint32_t)Arows * kKC * 4); }
+__host__ __device__ inline uint32_t bhalf_bytes(int Ntile) { return round1k((uint32_t)(Ntile / 2) * kKC * 4); }
 }  // namespace
 
-size_t tcdir_smem_bytes(int Ntile) { return (size_t)kStages * stage_bytes(Ntile) + 1024; }
+size_t tcdir_smem_bytes(int Ntile, int Arows) {
+    return (size_t)kASlots * 2 * apart_bytes(Arows) + (size_t)kBSlots * 2 * bhalf_bytes(Ntile) + 1024;
+}
 
 // ------------------------------------------------------------------------------------------------
+// CTA pair (cluster of 2, cta_group::2): CTA rank r owns pixel rows [pair_tile*256 + 128 r, +128) of the padded
+// grid and B rows [r*Ntile/2, (r+1)*Ntile/2); the leader (rank 0) issues M=256 x N=Ntile MMAs for both; each CTA
+// drains its own TMEM lanes.  A is loaded once per (chunk, tap row e1) as a window of 128 + T2 - 1 rows: the taps
+// e2 of that row read it at a row offset (the 128-byte swizzle is address based, so any row start works).
+// Barriers: fullA/fullB and tfree live in the leader (both CTAs' TMA bytes / drainer warps count there);
+// emptyA/emptyB and acc in both CTAs (the leader's commits multicast to the pair).
 template <bool FWD, int DST>
-__global__ void __launch_bounds__(kThreads, 1) tcdir_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ xold,
-                                                            const float* __restrict__ norm, float eps, float* __restrict__ out) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tcdir_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ xold, const float* __restrict__ norm,
+                 float eps, float* __restrict__ out) {
     extern __shared__ unsigned char smem_raw[];
-    __shared__ uint64_t bar_full[kStages], bar_empty[kStages], bar_acc[2], bar_tfree[2];
+    __shared__ uint64_t bar_fullA[kASlots], bar_emptyA[kASlots], bar_fullB[kBSlots], bar_emptyB[kBSlots];
+    __shared__ uint64_t bar_acc[2], bar_tfree[2];
     __shared__ uint32_t tmem_base;
     const uint32_t raw = tc::smem_u32(smem_raw);
     unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // SWIZZLE_128B tiles: 1024-byte aligned
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ib = d.item_off[blockIdx.x], ie = d.item_off[blockIdx.x + 1];
-    const uint32_t sbytes = stage_bytes(d.Ntile);
-    const uint32_t bbytes = 2u * (uint32_t)d.Ntile * kKC * 4;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1;
+    const int ib = d.item_off[pair], ie = d.item_off[pair + 1];
+    const uint32_t apart = apart_bytes(d.Arows), bhalf = bhalf_bytes(d.Ntile);
+    unsigned char* Abase = smem;
+    unsigned char* Bbase = smem + (size_t)kASlots * 2 * apart;
+    const int Nh = d.Ntile >> 1;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            tc::mbar_init(&bar_full[i], 1);
-            tc::mbar_init(&bar_empty[i], 1);
+        for (int i = 0; i < kASlots; ++i) {
+            tc::mbar_init(&bar_fullA[i], 1);
+            tc::mbar_init(&bar_emptyA[i], 1);
+        }
+        for (int i = 0; i < kBSlots; ++i) {
+            tc::mbar_init(&bar_fullB[i], 1);
+            tc::mbar_init(&bar_emptyB[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&bar_acc[i], 1);
-            tc::mbar_init(&bar_tfree[i], kDrainWarps);
+            tc::mbar_init(&bar_tfree[i], 2 * kDrainWarps);
         }
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&d.tmap);
+        tc::tma_prefetch_desc(&d.bmap);
+        if (d.tail_w < kKC) {
+            tc::tma_prefetch_desc(&d.tmap_t);
+            tc::tma_prefetch_desc(&d.bmap_t);
+        }
     }
-    if (warp == 0) tc::tmem_alloc(&tmem_base, kTmemCols);
+    if (warp == 0) tc::tmem_alloc_pair(&tmem_base, kTmemCols);
     tc::fence_before();
-    __syncthreads();
+    tc::cluster_sync();
     tc::fence_after();
     const uint32_t tmem = tmem_base;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ============================ producer: TMA (A) + bulk copy (B) ============================
-            int it = 0;
+            // ============================ producer (both CTAs): TMA A windows + B halves ============================
+            int na = 0, nb = 0;
+            long long dbg_empty = 0, dbg_t0 = clock64();
             for (int i = ib; i < ie; ++i) {
                 const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
                 const TcPlane pl = d.planes[zi];
-                const unsigned char* coef = reinterpret_cast<const unsigned char*>(d.coef + pl.coef_off);
-                for (int c = 0; c < d.nch; ++c)
-                    for (int t = 0; t < pl.T1 * pl.T2; ++t, ++it) {
-                        const int s = it % kStages;
-                        if (it >= kStages) tc::mbar_wait(&bar_empty[s], ((it / kStages) - 1) & 1);
-                        unsigned char* st = smem + (size_t)s * sbytes;
-                        const int e1 = pl.e1min + t / pl.T2, e2 = pl.e2min + t % pl.T2;
-                        const int row = tile * kM + e1 * d.Wp + e2 - d.e2lo;
-                        const int slab_hi = FWD ? (zi * 2) * d.nch + c : c;
-                        const int slab_lo = FWD ? (zi * 2 + 1) * d.nch + c : d.nch + c;
-                        tc::mbar_arrive_expect_tx(&bar_full[s], sbytes);
-                        tc::tma_load_3d(st, &d.tmap, 0, row, slab_hi, &bar_full[s]);
-                        tc::tma_load_3d(st + kATile, &d.tmap, 0, row, slab_lo, &bar_full[s]);
-                        tc::bulk_g2s(st + 2 * kATile, coef + ((size_t)t * d.nch + c) * bbytes, bbytes, &bar_full[s]);
+                const int row0 = tile * 2 * kM + (int)rank * kM - d.e2lo + pl.e2min;
+                for (int c = 0; c < d.nch; ++c) {
+                    const bool tail = c == d.nch - 1 && d.tail_w < kKC;
+                    const void* am = tail ? (const void*)&d.tmap_t : (const void*)&d.tmap;
+                    const void* bm = tail ? (const void*)&d.bmap_t : (const void*)&d.bmap;
+                    const uint32_t w = tail ? (uint32_t)d.tail_w : (uint32_t)kKC;   // phases per row
+                    const int slab_hi = FWD ? (zi * 2) * d.nch + c : c;
+                    const int slab_lo = FWD ? (zi * 2 + 1) * d.nch + c : d.nch + c;
+                    for (int t1 = 0; t1 < pl.T1; ++t1, ++na) {
+                        const int sa = na % kASlots;
+                        const long long c0 = (d.exp & 4) ? clock64() : 0;
+                        if (na >= kASlots) tc::mbar_wait(&bar_emptyA[sa], ((na / kASlots) - 1) & 1);
+                        if (d.exp & 4) dbg_empty += clock64() - c0;
+                        unsigned char* as = Abase + (size_t)sa * 2 * apart;
+                        const int row = row0 + (pl.e1min + t1) * d.Wp;
+                        if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullA[sa], 2 * 2 * (uint32_t)d.Arows * w * 4);
+                        tc::tma_load_3d_pair(as, am, 0, row, slab_hi, &bar_fullA[sa]);
+                        tc::tma_load_3d_pair(as + apart, am, 0, row, slab_lo, &bar_fullA[sa]);
+                        for (int t2 = 0; t2 < pl.T2; ++t2, ++nb) {
+                            const int sb = nb % kBSlots;
+                            const long long c1 = (d.exp & 4) ? clock64() : 0;
+                            if (nb >= kBSlots) tc::mbar_wait(&bar_emptyB[sb], ((nb / kBSlots) - 1) & 1);
+                            if (d.exp & 4) dbg_empty += clock64() - c1;
+                            unsigned char* bs = Bbase + (size_t)sb * 2 * bhalf;
+                            const int bslab = (int)(pl.coef_off + (long long)((t1 * pl.T2 + t2) * d.nch + c) * 2);
+                            if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * w * 4);
+                            tc::tma_load_3d_pair(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb]);
+                            tc::tma_load_3d_pair(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb]);
+                        }
                     }
+                }
+            }
+            if (d.exp & 4) {
+                long long* o = d.dbg + (size_t)blockIdx.x * 8;
+                o[3] = dbg_empty;
+                o[7] = clock64() - dbg_t0;
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ============================ MMA issuer (one thread) ============================
-            const uint32_t idesc = tc::idesc_tf32(kM, d.Ntile);
-            int it = 0;
+        if (lane == 0 && rank == 0) {
+            // ============================ MMA issuer (leader CTA, one thread) ============================
+            const uint32_t idesc = tc::idesc_tf32(2 * kM, d.Ntile);
+            long long dbg_full = 0, dbg_tfree = 0, dbg_t0 = clock64();
+            int na = 0, nb = 0, g = 0, gk = 0;   // A windows, B tiles, drain group, K-steps in the open group
             for (int i = ib; i < ie; ++i) {
                 const int zi = d.items[i] / d.tiles;
-                const int NT = d.planes[zi].T1 * d.planes[zi].T2;
+                const int T1 = d.planes[zi].T1, T2 = d.planes[zi].T2, NT = T1 * T2, nst = d.nch * NT;
+                int st = 0;
                 for (int c = 0; c < d.nch; ++c) {
-                        const int ks = c == d.nch - 1 ? d.kst_last : kKC / 8;
-                    for (int t = 0; t < NT; ++t, ++it) {
-                            const int s = it % kStages, j = it & 1;
-                            tc::mbar_wait(&bar_full[s], (it / kStages) & 1);
-                            if (it >= 2) tc::mbar_wait(&bar_tfree[j], ((it >> 1) - 1) & 1);
+                    const int ks = c == d.nch - 1 ? d.kst_last : kKC / 8;
+                    const uint32_t rb = (c == d.nch - 1 && d.tail_w < kKC) ? (uint32_t)d.tail_w * 4 : 128u;   // row bytes
+                    for (int t1 = 0; t1 < T1; ++t1, ++na) {
+                        const int sa = na % kASlots;
+                        {
+                            const long long c0 = (d.exp & 4) ? clock64() : 0;
+                            tc::mbar_wait(&bar_fullA[sa], (na / kASlots) & 1);
+                            if (d.exp & 4) dbg_full += clock64() - c0;
+                        }
+                        const uint32_t a_hi0 = tc::smem_u32(Abase + (size_t)sa * 2 * apart), a_lo0 = a_hi0 + apart;
+                        for (int t2 = 0; t2 < T2; ++t2, ++nb, ++st) {
+                            const int sb = nb % kBSlots, j = g & 1;
+                            const long long c0 = (d.exp & 4) ? clock64() : 0;
+                            tc::mbar_wait(&bar_fullB[sb], (nb / kBSlots) & 1);
+                            const long long c1 = (d.exp & 4) ? clock64() : 0;
+                            if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
+                            if (d.exp & 4) {
+                                dbg_full += c1 - c0;
+                                dbg_tfree += clock64() - c1;
+                            }
                             tc::fence_after();
-                            const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * sbytes), a_lo = a_hi + kATile;
-                            const uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + (uint32_t)d.Ntile * kKC * 4;
+                            const uint32_t a_hi = a_hi0 + (uint32_t)t2 * rb, a_lo = a_lo0 + (uint32_t)t2 * rb;
+                            const uint32_t b_hi = tc::smem_u32(Bbase + (size_t)sb * 2 * bhalf), b_lo = b_hi + bhalf;
                             const uint32_t acc = tmem + (uint32_t)(j * 256);
                             for (int k = 0; k < ks; ++k) {
-                                const uint64_t ah = tc::sdesc_sw128(a_hi + 32 * k), al = tc::sdesc_sw128(a_lo + 32 * k);
-                                const uint64_t bh = tc::sdesc_sw128(b_hi + 32 * k), bl = tc::sdesc_sw128(b_lo + 32 * k);
-                                tc::mma_tf32(acc, ah, bh, idesc, k > 0 ? 1u : 0u);
-                                tc::mma_tf32(acc, ah, bl, idesc, 1u);
-                                tc::mma_tf32(acc, al, bh, idesc, 1u);
+                                const uint64_t ah = tc::sdesc_swz(a_hi + 32 * k, rb), al = tc::sdesc_swz(a_lo + 32 * k, rb);
+                                const uint64_t bh = tc::sdesc_swz(b_hi + 32 * k, rb), bl = tc::sdesc_swz(b_lo + 32 * k, rb);
+                                tc::mma_tf32_pair(acc, ah, bh, idesc, (gk == 0 && k == 0) ? 0u : 1u);
+                                tc::mma_tf32_pair(acc, ah, bl, idesc, 1u);
+                                tc::mma_tf32_pair(acc, al, bh, idesc, 1u);
                             }
-                            tc::mma_commit(&bar_empty[s]);
-                            tc::mma_commit(&bar_acc[j]);
+                            gk += ks;
+                            tc::mma_commit_pair(&bar_emptyB[sb], 3);
+                            if (t2 == T2 - 1) tc::mma_commit_pair(&bar_emptyA[sa], 3);
+                            // close the drain group at the item's end or when the next stage would exceed chain_k
+                            const int cn = (st + 1) / NT;
+                            const int ksn = cn == d.nch - 1 ? d.kst_last : kKC / 8;
+                            if (st == nst - 1 || gk + ksn > d.chain_k) {
+                                tc::mma_commit_pair(&bar_acc[j], 3);
+                                ++g;
+                                gk = 0;
+                            }
                         }
                     }
+                }
+            }
+            if (d.exp & 4) {
+                long long* o = d.dbg + (size_t)blockIdx.x * 8;
+                o[0] = dbg_full;
+                o[1] = dbg_tfree;
+                o[2] = clock64() - dbg_t0;
+                o[6] = nb;
             }
         }
     } else {
         // ============================ drainers: TMEM -> fp32 running sums, epilogue ============================
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
         const int half = (warp - 2) >> 2;             // column half
-        const int Nh = d.Ntile >> 1;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(half * Nh);
         const int r = 32 * q + lane;                  // tile row (pixel) of this thread
         float acc[kMaxNh];
 #pragma unroll
         for (int i = 0; i < kMaxNh; ++i) acc[i] = 0.0f;
-        int it = 0;
+        int g = 0;
+        long long dbg_acc = 0, dbg_epi = 0;
         for (int i = ib; i < ie; ++i) {
             const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
-            const int nst = d.nch * d.planes[zi].T1 * d.planes[zi].T2;
-            for (int st = 0; st < nst; ++st, ++it) {
-                const int j = it & 1;
-                tc::mbar_wait(&bar_acc[j], (it >> 1) & 1);
+            const int NT = d.planes[zi].T1 * d.planes[zi].T2, nst = d.nch * NT;
+            int gk = 0;
+            for (int st = 0; st < nst; ++st) {
+                const int c = st / NT;
+                gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
+                const int cn = (st + 1) / NT;
+                const int ksn = cn == d.nch - 1 ? d.kst_last : kKC / 8;
+                if (!(st == nst - 1 || gk + ksn > d.chain_k)) continue;   // group still open
+                gk = 0;
+                const int j = g & 1;
+                {
+                    const long long c0 = (d.exp & 4) ? clock64() : 0;
+                    tc::mbar_wait(&bar_acc[j], (g >> 1) & 1);
+                    if (d.exp & 4) dbg_acc += clock64() - c0;
+                }
+                ++g;
                 tc::fence_after();
                 const uint32_t base = lane_base + (uint32_t)(j * 256);
 #pragma unroll
                 for (int c0 = 0; c0 < kMaxNh; c0 += 32) {
-                    if (c0 < Nh) {
+                    if (c0 < Nh && !(d.exp & 1)) {
                         uint32_t v[32];
+                        if (c0 + 32 <= Nh) {
+                            tc::tmem_ld32_nowait(base + (uint32_t)c0, v);
+                        } else {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (c0 + 8 * u < Nh) tc::tmem_ld8_nowait(base + (uint32_t)(c0 + 8 * u), v + 8 * u);
+                            for (int u = 0; u < 4; ++u)
+                                if (c0 + 8 * u < Nh) tc::tmem_ld8_nowait(base + (uint32_t)(c0 + 8 * u), v + 8 * u);
+                        }
                         tc::tmem_wait_ld();
 #pragma unroll
                         for (int u = 0; u < 32; ++u)
@@ -160,31 +262,37 @@ __global__ void __launch_bounds__(kThreads, 1) tcdir_kernel(const __grid_constan
                 }
                 tc::fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&bar_tfree[j]);
+                if (lane == 0) tc::mbar_arrive_cluster(&bar_tfree[j], 0);
             }
             // ---- epilogue of the item ----
-            const int L = tile * kM + r;
+            const long long ce0 = (d.exp & 4) ? clock64() : 0;
+            const int L = tile * 2 * kM + (int)rank * kM + r;
             const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp;
             if (m1 < d.nh && m2 < d.nw) {
                 const size_t HW = (size_t)d.H * d.W;
+                const int z = d.zlist[zi];
 #pragma unroll
-                for (int i = 0; i < kMaxNh; ++i) {
-                    const int n = half * Nh + i;
-                    if (i < Nh && n < d.N2) {
-                        const int n1 = n / d.N, n2 = n - (n / d.N) * d.N;
-                        if constexpr (FWD) {   // n = output phase b'
-                            d.part[(size_t)zi * HW + (size_t)(n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i];
-                        } else {               // n = input phase a of plane z
-                            const int z = d.zlist[zi];
-                            const int u = z * d.N2 + n;
-                            if (u >= d.unit0 && u < d.unit0 + d.nu) {
-                                const size_t pidx = ((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2;
-                                if constexpr (DST == DST_POLY)
-                                    out[pidx] = acc[i];
-                                else if constexpr (DST == DST_VOLIMAGE)
-                                    out[((size_t)z * d.H + n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i];
-                                else
-                                    out[pidx] = update_value<DST>(xold[pidx], norm[pidx], acc[i], eps);
+                for (int i0 = 0; i0 < kMaxNh; i0 += 8) {
+                    if (i0 < Nh) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int n = half * Nh + i0 + u;
+                            if (i0 + u < Nh && n < d.N2) {
+                                const int n1 = n / d.N, n2 = n - (n / d.N) * d.N;
+                                if constexpr (FWD) {   // n = output phase b'
+                                    d.part[(size_t)zi * HW + (size_t)(n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i0 + u];
+                                } else {               // n = input phase a of plane z
+                                    const int uu = z * d.N2 + n;
+                                    if (uu >= d.unit0 && uu < d.unit0 + d.nu) {
+                                        const size_t pidx = ((size_t)(uu - d.unit0) * d.nh + m1) * d.nw + m2;
+                                        if constexpr (DST == DST_POLY)
+                                            out[pidx] = acc[i0 + u];
+                                        else if constexpr (DST == DST_VOLIMAGE)
+                                            out[((size_t)z * d.H + n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i0 + u];
+                                        else   // RL / ISRA: H^T r into the scratch, tc_update_kernel applies it
+                                            d.part[(((size_t)zi * d.N2 + n) * d.nh + m1) * d.nw + m2] = acc[i0 + u];
+                                    }
+                                }
                             }
                         }
                     }
@@ -192,11 +300,17 @@ __global__ void __launch_bounds__(kThreads, 1) tcdir_kernel(const __grid_constan
             }
 #pragma unroll
             for (int i = 0; i < kMaxNh; ++i) acc[i] = 0.0f;
+            if (d.exp & 4) dbg_epi += clock64() - ce0;
+        }
+        if ((d.exp & 4) && warp == 2 && lane == 0) {
+            long long* o = d.dbg + (size_t)blockIdx.x * 8;
+            o[4] = dbg_acc;
+            o[5] = dbg_epi;
         }
     }
     tc::fence_before();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
+    tc::cluster_sync();
+    if (warp == 0) tc::tmem_dealloc_pair(tmem, kTmemCols);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -255,8 +369,23 @@ __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ T
 }
 
 // ------------------------------------------------------------------------------------------------
+// multiplicative update of the tensor-core planes' units from the H^T r scratch (coalesced, float4)
+template <int DST>
+__global__ void __launch_bounds__(256) tc_update_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ xold,
+                                                        const float* __restrict__ norm, float eps, float* __restrict__ out) {
+    const size_t npix = (size_t)d.nh * d.nw;
+    const int zi = blockIdx.y / d.N2, a = blockIdx.y - (blockIdx.y / d.N2) * d.N2;
+    const int u = d.zlist[zi] * d.N2 + a;
+    if (u < d.unit0 || u >= d.unit0 + d.nu) return;
+    const float* bp = d.part + ((size_t)zi * d.N2 + a) * npix;
+    const size_t base = (size_t)(u - d.unit0) * npix;
+    for (size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x; m < npix; m += (size_t)gridDim.x * blockDim.x)
+        out[base + m] = update_value<DST>(xold[base + m], norm[base + m], bp[m], eps);
+}
+
+// ------------------------------------------------------------------------------------------------
 // Coefficient tiles of one plane (plan time), built on the device from the owned PSF slice: tile (tap, chunk) =
-// [hi | lo] of an Ntile x 32 SWIZZLE_128B K-major tile with element (n, k) =
+// slabs [hi], [lo] of Ntile x 32 row-major floats (the TMA load swizzles them) with element (n, k) =
 //   forward : G_d[b' = n][a = chunk*32 + k],   d = -e        backward: G_d[b' = chunk*32 + k][a = n],   d = +e
 __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane pl, int z, const float* __restrict__ psf,
                                   int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out) {
@@ -266,7 +395,7 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
     const int N = d.N, N2 = d.N2;
     const int e1 = pl.e1min + tap / pl.T2, e2 = pl.e2min + tap % pl.T2;
     const int d1 = fwd ? -e1 : e1, d2 = fwd ? -e2 : e2;
-    float* hi = out + pl.coef_off + (size_t)tileid * d.Ntile * kKC * 2;
+    float* hi = out + ((size_t)pl.coef_off + (size_t)tileid * 2) * d.Ntile * kKC;
     float* lo = hi + (size_t)d.Ntile * kKC;
     for (int e = threadIdx.x; e < d.Ntile * kKC; e += blockDim.x) {
         const int n = e / kKC, k = e - (e / kKC) * kKC;
@@ -283,9 +412,8 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
         }
         float h, l;
         tc::split_tf32(v, h, l);
-        const uint32_t off = tc::sw128_off(n, k) / 4;
-        hi[off] = h;
-        lo[off] = l;
+        hi[e] = h;
+        lo[e] = l;
     }
 }
 
@@ -299,6 +427,7 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
     if (d->Ntile > 2 * kMaxNh) return false;
     d->nch = (d->N2 + kKC - 1) / kKC;
     d->kst_last = ((d->N2 - (d->nch - 1) * kKC) + 7) / 8;
+    d->tail_w = d->kst_last == 1 ? 8 : (d->kst_last == 2 ? 16 : kKC);
     planes->assign(d->nzd, TcPlane{});
     int e2lo = 1 << 30, e2hi = -(1 << 30);
     long long off = 0;
@@ -308,16 +437,30 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
         pl.T2 = d2max[zi] - d2min[zi] + 1;
         pl.e1min = fwd ? -d1max[zi] : d1min[zi];
         pl.e2min = fwd ? -d2max[zi] : d2min[zi];
-        pl.coef_off = off;
-        off += (long long)pl.T1 * pl.T2 * d->nch * d->Ntile * kKC * 2;
+        pl.coef_off = off;   // in slabs of Ntile x 32 floats
+        off += (long long)pl.T1 * pl.T2 * d->nch * 2;
         e2lo = std::min(e2lo, pl.e2min);
         e2hi = std::max(e2hi, pl.e2min + pl.T2 - 1);
     }
+    d->nslabs = off;
+    {
+        const char* ev = getenv("LFM_TC_EXP");
+        d->exp = ev ? atoi(ev) : 0;
+        const char* ck = getenv("LFM_TC_CHAIN");   // dev: drain-group length override
+        d->chain_k = ck ? std::max(1, atoi(ck)) : kChainK;
+        d->dbg = nullptr;
+        if (d->exp & 4) cudaMalloc(&d->dbg, (size_t)2 * num_sms * 8 * sizeof(long long));   // leaked: dev only
+    }
     d->e2lo = d->nzd > 0 ? e2lo : 0;
+    int t2max = 1;
+    for (const TcPlane& pl : *planes) t2max = std::max(t2max, pl.T2);
+    if (t2max > 65) return false;   // A window box rows <= 192 (TMA box <= 256, smem budget)
+    d->Arows = kM + t2max - 1;
+    if (tcdir_smem_bytes(d->Ntile, d->Arows) > 227 * 1024) return false;
     d->Wp = d->nw + (d->nzd > 0 ? e2hi - e2lo : 0);
     d->Lp = d->nh * d->Wp;
-    d->tiles = (d->Lp + kM - 1) / kM;
-    d->grid = std::max(1, std::min(d->tiles * d->nzd, num_sms));
+    d->tiles = (d->Lp + 2 * kM - 1) / (2 * kM);   // pair tiles
+    d->grid = std::max(1, std::min(d->tiles * d->nzd, num_sms / 2));   // CTA pairs
     return true;
 }
 
@@ -348,11 +491,13 @@ void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std:
 
 size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes) {
     size_t n = 0;
-    for (const TcPlane& pl : planes) n += (size_t)pl.T1 * pl.T2 * d.nch * d.Ntile * kKC * 2;
-    return n;
+    for (const TcPlane& pl : planes) n += (size_t)pl.T1 * pl.T2 * d.nch * 2;
+    return n * d.Ntile * kKC;
 }
 size_t tcdir_src_floats(const TcDirArgs& d, int fwd) { return (size_t)(fwd ? 2 * d.nzd : 2) * d.nch * d.Lp * kKC; }
-size_t tcdir_part_floats(const TcDirArgs& d, int fwd) { return fwd ? (size_t)d.nzd * d.H * d.W : 0; }
+size_t tcdir_part_floats(const TcDirArgs& d, int fwd) {
+    return fwd ? (size_t)d.nzd * d.H * d.W : (size_t)d.nzd * d.N2 * d.nh * d.nw;
+}
 
 typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -371,10 +516,29 @@ cudaError_t tcdir_encode(TcDirArgs* d, int fwd) {
     const cuuint64_t slabs = (cuuint64_t)(fwd ? 2 * d->nzd : 2) * d->nch;
     cuuint64_t dims[3] = {(cuuint64_t)kKC, (cuuint64_t)d->Lp, slabs};
     cuuint64_t strides[2] = {(cuuint64_t)kKC * 4, (cuuint64_t)d->Lp * kKC * 4};
-    cuuint32_t box[3] = {(cuuint32_t)kKC, (cuuint32_t)kM, 1}, es[3] = {1, 1, 1};
+    cuuint32_t box[3] = {(cuuint32_t)kKC, (cuuint32_t)d->Arows, 1}, es[3] = {1, 1, 1};
     CUresult r = enc(&d->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->src, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    // coefficient slabs [nslabs][Ntile][32], each CTA of a pair loads Ntile/2 rows
+    cuuint64_t bdims[3] = {(cuuint64_t)kKC, (cuuint64_t)d->Ntile, (cuuint64_t)d->nslabs};
+    cuuint64_t bstrides[2] = {(cuuint64_t)kKC * 4, (cuuint64_t)d->Ntile * kKC * 4};
+    cuuint32_t bbox[3] = {(cuuint32_t)kKC, (cuuint32_t)(d->Ntile / 2), 1};
+    r = enc(&d->bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d->coef), bdims, bstrides, bbox, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (d->tail_w < kKC) {   // the last chunk holds <= 16 valid phases: narrow boxes, SWIZZLE_32B / 64B
+        const CUtensorMapSwizzle sw = d->tail_w == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+        cuuint32_t tbox[3] = {(cuuint32_t)d->tail_w, (cuuint32_t)d->Arows, 1};
+        cuuint32_t tbbox[3] = {(cuuint32_t)d->tail_w, (cuuint32_t)(d->Ntile / 2), 1};
+        r = enc(&d->tmap_t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->src, dims, strides, tbox, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+        r = enc(&d->bmap_t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d->coef), bdims, bstrides, tbbox, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
@@ -390,10 +554,25 @@ cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int
 template <bool FWD, int DST>
 static cudaError_t tcdir_main(const TcDirArgs& d, const float* xold, const float* norm, float eps, float* out,
                               cudaStream_t s) {
-    const size_t smem = tcdir_smem_bytes(d.Ntile);
+    const size_t smem = tcdir_smem_bytes(d.Ntile, d.Arows);
     cudaError_t e = cudaFuncSetAttribute(tcdir_kernel<FWD, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tcdir_kernel<FWD, DST><<<d.grid, kThreads, smem, s>>>(d, xold, norm, eps, out);
+    tcdir_kernel<FWD, DST><<<2 * d.grid, kThreads, smem, s>>>(d, xold, norm, eps, out);
+    if (d.exp & 4) {   // dev only: print the averaged wait counters of the leader CTAs
+        cudaStreamSynchronize(s);
+        std::vector<long long> h((size_t)2 * d.grid * 8);
+        cudaMemcpy(h.data(), d.dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        double a[8] = {0};
+        for (int b = 0; b < 2 * d.grid; b += 2)
+            for (int k = 0; k < 8; ++k) a[k] += (double)h[(size_t)b * 8 + k] / d.grid;
+        double p[8] = {0};
+        for (int b = 1; b < 2 * d.grid; b += 2)
+            for (int k = 0; k < 8; ++k) p[k] += (double)h[(size_t)b * 8 + k] / d.grid;
+        fprintf(stderr,
+                "[tc %s] leader: mma_total %.0f wait_full %.0f wait_tfree %.0f stages %.0f | prod_total %.0f "
+                "wait_empty %.0f | drain wait_acc %.0f epi %.0f || peer: prod wait_empty %.0f drain wait_acc %.0f epi %.0f\n",
+                FWD ? "fwd" : "bwd", a[2], a[0], a[1], a[6], a[7], a[3], a[4], a[5], p[3], p[4], p[5]);
+    }
     return cudaGetLastError();
 }
 
@@ -425,9 +604,18 @@ cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, cons
         default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
+    const dim3 ug((unsigned)std::min<size_t>(((size_t)d.nh * d.nw + 255) / 256, 8), (unsigned)(d.nzd * d.N2));
     switch (dst) {
-        case DST_UPDATE: return tcdir_main<false, DST_UPDATE>(d, xold, norm, eps, out, s);
-        case DST_ISRA: return tcdir_main<false, DST_ISRA>(d, xold, norm, eps, out, s);
+        case DST_UPDATE:
+            e = tcdir_main<false, DST_UPDATE>(d, xold, norm, eps, out, s);
+            if (e != cudaSuccess) return e;
+            tc_update_kernel<DST_UPDATE><<<ug, 256, 0, s>>>(d, xold, norm, eps, out);
+            return cudaGetLastError();
+        case DST_ISRA:
+            e = tcdir_main<false, DST_ISRA>(d, xold, norm, eps, out, s);
+            if (e != cudaSuccess) return e;
+            tc_update_kernel<DST_ISRA><<<ug, 256, 0, s>>>(d, xold, norm, eps, out);
+            return cudaGetLastError();
         case DST_POLY: return tcdir_main<false, DST_POLY>(d, xold, norm, eps, out, s);
         case DST_VOLIMAGE: return tcdir_main<false, DST_VOLIMAGE>(d, xold, norm, eps, out, s);
         default: return cudaErrorInvalidValue;

@@ -488,7 +488,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     ST(mark(p, ST_DIR_BWD, s));
     for (const TcDirArgs& tg : p->tcb) {
         CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s));
-        p->pacc.launches += 2;
+        p->pacc.launches += (dst == DST_UPDATE || dst == DST_ISRA) ? 3 : 2;
     }
     for (const DirArgs& dg : p->dgroups) {
         CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, aux, s));
@@ -895,7 +895,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const int T1 = box1[z].dmax - box1[z].dmin + box1[z].D, T2 = box2[z].dmax - box2[z].dmin + box2[z].D;
         const int Ntile = (int)round_up((size_t)N2, 16), nch = (N2 + 31) / 32;
         const int tiles = (g.nh * (g.nw + T2 - 1) + 127) / 128;
-        const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256;
+        const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256 && T2 <= 65;
         const double stage_cycles = 3.0 * 4 * 128.0 * Ntile * 8 / kTcMacPerCycle / kTcEff;
         const double t_tc = tc_ok ? 2.0 * tiles * nch * (double)T1 * T2 * stage_cycles / (p->num_sms * kSmClock) *
                                         (units / N2) + kTcFixed
@@ -1434,6 +1434,7 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
             }
             for (const TcDirArgs& tg : p->tcf) {
                 CK(launch_tcdir_fwd(tg, xbuf(f, cur[f]), 0, yimg, acc ? 1 : 0, s));
+                p->pacc.launches += 3;
                 acc = true;
             }
             for (const DirArgs& dg : p->dgroups) {
@@ -1466,8 +1467,10 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                 c.eps = pol->eps;
                 CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
             }
-            for (const TcDirArgs& tg : p->tcb)
+            for (const TcDirArgs& tg : p->tcb) {
                 CK(launch_tcdir_bwd(tg, SRC_RATIO, y + f * HW, p->byhat + f * HW, pol->eps, DST_UPDATE, xn, xo, p->norm, s));
+                p->pacc.launches += 3;
+            }
             for (const DirArgs& dg : p->dgroups)
                 CK(launch_dir_bwd(dg, SRC_RATIO, y + f * HW, p->byhat + f * HW, pol->eps, DST_UPDATE, xn, xo, p->norm, s));
             unsigned* mp = p->bmproj + f * HW;

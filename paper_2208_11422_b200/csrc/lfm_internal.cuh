@@ -101,7 +101,7 @@ struct DirArgs {
 // plane, column c holds m2 = c + e2lo) so that a tap is a plain row offset of a TMA box.
 struct TcPlane {
     int T1, T2, e1min, e2min;   // union tap box of the plane (source offsets)
-    long long coef_off;         // floats: first coefficient tile of the plane
+    long long coef_off;         // first coefficient slab (Ntile x 32 floats) of the plane
 };
 struct TcDirArgs {
     int N, H, W, nh, nw;
@@ -112,14 +112,24 @@ struct TcDirArgs {
     int N2, Ntile;            // phases and TMEM columns per accumulator (N2 rounded up to 16, <= 256)
     int nch, kst_last;        // reduction chunks of 32 phases; K-steps of 8 in the last chunk
     int e2lo;                 // column origin of the staged grid (min e2min over planes)
-    int Wp, Lp, tiles;        // padded grid: Lp = nh * Wp rows of 32 phases, tiles of 128 rows
-    int grid;                 // persistent CTAs
-    const int* item_off;      // [grid + 1] CTA b runs items[item_off[b] .. item_off[b+1])   (LPT schedule)
+    int Wp, Lp, tiles;        // padded grid: Lp = nh * Wp rows of 32 phases, pair tiles of 256 rows
+    int grid;                 // persistent CTA pairs (launch 2 * grid CTAs, clusters of 2)
+    const int* item_off;      // [grid + 1] pair b runs items[item_off[b] .. item_off[b+1])   (LPT schedule)
     const int* items;         // item = zi * tiles + tile
-    const float* coef;        // per plane [tap][chunk][hi | lo][Ntile x 32, SWIZZLE_128B]
+    const float* coef;        // slabs [plane][tap][chunk][hi | lo] of Ntile x 32 floats (row-major)
+    long long nslabs;         // coefficient slabs
+    int exp;                  // timing experiments only (env LFM_TC_EXP): 1 skip drains, 2 skip reloads, 4 counters
+    long long* dbg;           // exp & 4: per-CTA wait-cycle counters [grid*2][8]
     float* src;               // staged source, slabs of [Lp][32] (hi / lo): fwd ((zi*2+part)*nch+c), bwd (part*nch+c)
-    float* part;              // forward per-plane partial images [nzd][H][W]
-    alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, 128, 1}, SWIZZLE_128B
+    float* part;              // forward: per-plane partial images [nzd][H][W]; backward: H^T r of the tensor-core
+                              // planes' units, polyphase [nzd][N2][nh][nw] (update epilogues apply it afterwards)
+    int chain_k;              // K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
+    alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, Arows, 1}, SWIZZLE_128B
+    alignas(64) CUtensorMap bmap;   // 3-D {32, Ntile, nslabs} over coef, box {32, Ntile/2, 1}, SWIZZLE_128B
+    int Arows;                      // A window rows: 128 + max T2 - 1
+    int tail_w;                     // phases loaded for the last chunk: 8 (SWIZZLE_32B), 16 (64B) or 32 (main maps)
+    alignas(64) CUtensorMap tmap_t; // narrow boxes {tail_w, Arows | Ntile/2, 1} for the last chunk
+    alignas(64) CUtensorMap bmap_t;
 };
 // geometry of one direction from the per-plane tap boxes d in [d1min, d1max] x [d2min, d2max] (host arrays)
 bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, const int* d2min, const int* d2max,
@@ -127,7 +137,7 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
 // LPT schedule of the (plane, tile) items over d->grid CTAs (host arrays)
 void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std::vector<int>* item_off,
                     std::vector<int>* items);
-size_t tcdir_smem_bytes(int Ntile);
+size_t tcdir_smem_bytes(int Ntile, int Arows);
 size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes);
 size_t tcdir_src_floats(const TcDirArgs& d, int fwd);
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd);
