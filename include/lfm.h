@@ -125,6 +125,9 @@ typedef struct {
     int direct_planes;              /* planes (touching owned units) on the direct path            */
     int fft_units;                  /* owned units on the frequency path                            */
     int tc_planes;                  /* direct planes on the tcgen05 (3xTF32 tensor-core) kernels    */
+    double tc_flops_executed;       /* per projection: tensor flops the tcgen05 kernel issues (3 TF32
+                                       products, union tap boxes, padded pixel rows)                 */
+    double tc_flops_algorithmic;    /* per projection: 2 * exact taps (D x D per phase pair) * pixels */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */
@@ -168,6 +171,10 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                            const lfm_optics* optics, const lfm_dist* dist, int flags, void* stream);
 
 lfm_status lfm_plan_info(lfm_plan plan, lfm_info* info /* host */);
+
+/* The units u = z*N*N + a1*N + a2 this plan's rank owns, [*unit_begin, *unit_end) (host ints).
+ * Volumes at the boundary are the full [nz][H][W]; a rank reads / writes only its owned units' voxels. */
+lfm_status lfm_plan_owned(lfm_plan plan, int* unit_begin, int* unit_end);
 
 /* Destroys the plan and frees its device memory / communicator.  NULL is a no-op. */
 void lfm_plan_destroy(lfm_plan plan);

@@ -220,6 +220,7 @@ struct lfm_plan_s {
     std::vector<DirArgs> dgroups;   // SIMT direct planes grouped by tap-box size D (one launch per group)
     std::vector<TcDirArgs> tcf, tcb;   // tensor-core direct groups (forward / backward coefficient layouts)
     int n_tc_planes = 0;
+    double tc_flops_exec = 0.0, tc_flops_alg = 0.0;   // per projection (lfm_info)
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -643,12 +644,11 @@ AxisBox axis_box(int N, int c, int k0, int k1) {
 constexpr double kHbmBps = 7.0e12;
 constexpr double kXformPerUnit = 9.0e-8;
 const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 28.0e12};
-// tensor-core direct path: tf32 MACs per cycle per SM (1.13 PFLOP/s dense / 148 SMs / 1.9 GHz), achieved
-// fraction of it, and a fixed per-plane cost (staging, partial reduce)
-constexpr double kTcMacPerCycle = 2000.0;
-constexpr double kTcEff = 0.5;
+// tensor-core direct path: achieved fraction of the tcgen05 floor (measured r01 at c3, staging and partial
+// reduction included) and a fixed per-plane cost
+constexpr double kTcEff = 0.56;
 constexpr double kTcFixed = 5e-6;
-constexpr double kSmClock = 1.9e9;
+constexpr double kSmClock = 1.965e9;
 
 }  // namespace
 
@@ -891,14 +891,14 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double units = ue - ub;
         const double t_fft = 2.0 * units * N2 * g.nkappa * 8.0 / kHbmBps + kXformPerUnit * units;
         const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
-        // tensor-core direct (kernels_tcdir.cu): one pipeline stage per (tile, tap, 32-phase chunk) and direction
+        // tensor-core direct (kernels_tcdir.cu): per direction, CTA pairs over 256-pixel tiles of the padded grid,
+        // every tap x K-step = 3 pair MMAs of Ntile/2 cycles (tcgen05 floor), at the measured efficiency
         const int T1 = box1[z].dmax - box1[z].dmin + box1[z].D, T2 = box2[z].dmax - box2[z].dmin + box2[z].D;
-        const int Ntile = (int)round_up((size_t)N2, 16), nch = (N2 + 31) / 32;
-        const int tiles = (g.nh * (g.nw + T2 - 1) + 127) / 128;
+        const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 7) / 8;
+        const int ptiles = (g.nh * (g.nw + T2 - 1) + 255) / 256;
         const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256 && T2 <= 65;
-        const double stage_cycles = 3.0 * 4 * 128.0 * Ntile * 8 / kTcMacPerCycle / kTcEff;
-        const double t_tc = tc_ok ? 2.0 * tiles * nch * (double)T1 * T2 * stage_cycles / (p->num_sms * kSmClock) *
-                                        (units / N2) + kTcFixed
+        const double pair_cycles = (double)ptiles * T1 * T2 * ksteps * 3.0 * (Ntile / 2);
+        const double t_tc = tc_ok ? 2.0 * pair_cycles / ((p->num_sms / 2) * kSmClock * kTcEff) * (units / N2) + kTcFixed
                                   : 1e30;
         int mode = 0;                            // 0 FFT, 1 SIMT direct, 2 tensor-core direct
         if (flags & LFM_PLAN_FFT_ONLY) {
@@ -1074,6 +1074,15 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
                     coef_bytes += nf * sizeof(float);
                 }
+                {
+                    const double ksteps = (N2 + 7) / 8, ptiles = ta.tiles;
+                    for (size_t zi = 0; zi < zl.size(); ++zi) {
+                        const int z = zl[zi];
+                        const double T = (double)(d1b[zi] - d1a[zi] + 1) * (d2b[zi] - d2a[zi] + 1);
+                        p->tc_flops_exec += ptiles * T * ksteps * 3.0 * 2.0 * 256.0 * ta.Ntile * 8.0;
+                        p->tc_flops_alg += 2.0 * (double)N2 * N2 * box1[z].D * box2[z].D * g.nh * g.nw;
+                    }
+                }
                 p->tcf.push_back(ta);
                 p->tcb.push_back(tb);
                 p->n_tc_planes += ta.nzd;
@@ -1140,6 +1149,14 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
 #undef CKG
 }
 
+lfm_status lfm_plan_owned(lfm_plan p, int* unit_begin, int* unit_end) {
+    g_err[0] = 0;
+    if (!p || !unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");
+    *unit_begin = p->u0;
+    *unit_end = p->u1;
+    return LFM_OK;
+}
+
 lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     if (!p || !info) return fail(LFM_EINVAL, "NULL argument");
     info->nnum = p->geo.N;
@@ -1162,6 +1179,8 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->direct_planes = p->direct ? p->geo.nz : p->n_direct_planes;
     info->fft_units = p->direct ? 0 : p->nu_fft;
     info->tc_planes = p->direct ? 0 : p->n_tc_planes;
+    info->tc_flops_executed = p->direct ? 0.0 : p->tc_flops_exec;
+    info->tc_flops_algorithmic = p->direct ? 0.0 : p->tc_flops_alg;
     info->transfer_bytes = p->transfer_bytes;
     info->device_bytes = p->bytes;
     info->plan_ms = p->plan_ms;

@@ -60,7 +60,7 @@ class lfm_info(ctypes.Structure):
                 ("units_padded", ctypes.c_int), ("x_s", ctypes.c_int), ("y_s", ctypes.c_int),
                 ("direct", ctypes.c_int), ("transfer_bytes", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
-                ("tc_planes", ctypes.c_int)]
+                ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -90,6 +90,7 @@ _lib_estimate = _sig("lfm_plan_estimate", _i, [_i, _i, _i, _i, _i, _i, _i, _i, c
 _lib_create = _sig("lfm_plan_create", _i, [ctypes.POINTER(_P), _P, _P, _i, _i, _i, _i, _i, _i,
                                            ctypes.POINTER(lfm_optics), ctypes.POINTER(lfm_dist), _i, _P])
 _lib_info = _sig("lfm_plan_info", _i, [_P, ctypes.POINTER(lfm_info)])
+_lib_owned = _sig("lfm_plan_owned", _i, [_P, ctypes.POINTER(_i), ctypes.POINTER(_i)])
 _lib_destroy = _sig("lfm_plan_destroy", None, [_P])
 _lib_forward = _sig("lfm_forward", _i, [_P, _P, _P, _P])
 _lib_backward = _sig("lfm_backward", _i, [_P, _P, _P, _P])
@@ -116,7 +117,7 @@ _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
 EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
-            "lfm_plan_create", "lfm_plan_info", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
+            "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
 
@@ -254,6 +255,12 @@ class Plan:
         inf = lfm_info()
         _check(_lib_info(self._h, ctypes.byref(inf)))
         return inf.as_dict()
+
+    def owned(self):
+        """(unit_begin, unit_end) this rank owns (lfm_plan_owned)."""
+        b, e = _i(), _i()
+        _check(_lib_owned(self._h, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
 
     def forward(self, x, y, stream=None):
         _check_dev(x, (self.nz, self.height, self.width), "x")
