@@ -273,7 +273,9 @@ def run_ours(args):
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             tj = json.load(open(tpath))
-            traffic = tj.get(cfg.name, {}).get(dom)
+            for ent in tj.values():   # the capture of the same plan (same frequency-path unit count)
+                if ent.get("fft_units") == nu and (cfg.name == "c3" or ent is tj.get(cfg.name)):
+                    traffic = ent.get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": stage_ms[dom],
