@@ -273,8 +273,8 @@ def run_ours(args):
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             tj = json.load(open(tpath))
-            for ent in tj.values():   # the capture of the same plan (same frequency-path unit count)
-                if ent.get("fft_units") == nu and (cfg.name == "c3" or ent is tj.get(cfg.name)):
+            for key, ent in tj.items():   # a capture of the same config and plan (frequency-path unit count)
+                if key.split("_")[0] == cfg.name and ent.get("fft_units") == nu:
                     traffic = ent.get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
