@@ -351,7 +351,7 @@ def run_ours(args):
                 "transform": f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})"
                 if not info["direct"] else "direct spatial",
                 "transfer_matrix_gb_per_gpu": info["transfer_bytes"] / 1e9,
-                "hybrid": {"direct_planes": info["direct_planes"], "tc_planes": info["tc_planes"], "fft_units": info["fft_units"]},
+                "hybrid": {"direct_planes": info["direct_planes"], "tc_planes": info["tc_planes"], "fft_units": info["fft_units"], "planes_moved_for_memory": info["planes_moved_for_memory"]},
                 "l2": "inputs larger than L2: each projection streams the transfer matrices (L2 126 MB)",
                 "plan_ms": info["plan_ms"], "setup_s": setup_s,
                 "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"],

@@ -128,6 +128,8 @@ typedef struct {
     double tc_flops_executed;       /* per projection: tensor flops the tcgen05 kernel issues (3 TF32
                                        products, union tap boxes, padded pixel rows)                 */
     double tc_flops_algorithmic;    /* per projection: 2 * exact taps (D x D per phase pair) * pixels */
+    int planes_moved_for_memory;    /* planes the hybrid planner moved off the frequency path so that the
+                                       transfer matrices fit the device (memory-aware planning, §5.1)  */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */
@@ -171,6 +173,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                            const lfm_optics* optics, const lfm_dist* dist, int flags, void* stream);
 
 lfm_status lfm_plan_info(lfm_plan plan, lfm_info* info /* host */);
+
+/* Process-wide cap on the device memory later lfm_plan_create calls may plan for (bytes; 0 = the device's free
+ * memory, the default).  The hybrid planner keeps the frequency-path transfer matrices under it by moving planes
+ * to the direct (tensor-core or CUDA-core) path; LFM_ENOMEM names the limiting term if that is not enough. */
+lfm_status lfm_set_memory_limit(size_t bytes);
 
 /* The units u = z*N*N + a1*N + a2 this plan's rank owns, [*unit_begin, *unit_end) (host ints).
  * Volumes at the boundary are the full [nz][H][W]; a rank reads / writes only its owned units' voxels. */

@@ -220,6 +220,7 @@ struct lfm_plan_s {
     std::vector<DirArgs> dgroups;   // SIMT direct planes grouped by tap-box size D (one launch per group)
     std::vector<TcDirArgs> tcf, tcb;   // tensor-core direct groups (forward / backward coefficient layouts)
     int n_tc_planes = 0;
+    int mem_moved = 0;   // planes moved off the frequency path to fit the memory budget
     double tc_flops_exec = 0.0, tc_flops_alg = 0.0;   // per projection (lfm_info)
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
@@ -274,6 +275,7 @@ struct lfm_plan_s {
 namespace {
 
 constexpr int kParts = 296;
+size_t g_mem_limit = 0;   // lfm_set_memory_limit (0: the device's free memory)
 
 const char* kStageNames[LFM_N_STAGES] = {"r2c_x",      "fwd_mac",    "c2r_yhat", "dir_fwd",
                                          "allreduce_sum", "r2c_ratio", "bwd_mac", "c2r_update",
@@ -788,20 +790,23 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         p->has_optics = true;
         p->optics = *optics;
     }
-    // memory budget ("estimate the required memory size")
+    // memory budget ("estimate the required memory size"): everything but the transfer matrices must fit now;
+    // the hybrid planner below fits the transfer matrices into what remains (moving planes to the direct path)
+    size_t mem_budget = 0, nonM_bytes = 0;
     {
         SizeTerms t = size_terms(g, p->nu, p->nu_total, world, (flags & LFM_PLAN_DIRECT) != 0);
-        if (psf_t_host) t.transfer *= 2;   // a second set of transfer matrices for Ht
         size_t free_b = 0, total_b = 0;
         CKG(cudaMemGetInfo(&free_b, &total_b));
-        if (t.total() > free_b) {
-            const char* names[6] = {"transfer matrices", "spectra workspaces", "volumes", "images", "PSF staging", "metric"};
-            const size_t vals[6] = {t.transfer, t.spectra, t.volumes, t.images, t.staging, t.metric};
+        mem_budget = g_mem_limit > 0 ? std::min(g_mem_limit, free_b) : free_b;
+        nonM_bytes = t.total() - t.transfer;
+        if (nonM_bytes > mem_budget) {
+            const char* names[5] = {"spectra workspaces", "volumes", "images", "PSF staging", "metric"};
+            const size_t vals[5] = {t.spectra, t.volumes, t.images, t.staging, t.metric};
             int best = 0;
-            for (int i = 1; i < 6; ++i)
+            for (int i = 1; i < 5; ++i)
                 if (vals[i] > vals[best]) best = i;
-            return guard(fail(LFM_ENOMEM, "plan needs %zu bytes on this GPU, %zu free; limiting term: %s (%zu bytes)",
-                              t.total(), free_b, names[best], vals[best]));
+            return guard(fail(LFM_ENOMEM, "plan needs %zu bytes on this GPU besides transfer matrices, %zu available; "
+                              "limiting term: %s (%zu bytes)", nonM_bytes, mem_budget, names[best], vals[best]));
         }
     }
     if (world > 1 && !(flags & LFM_PLAN_NO_COMM)) {
@@ -862,6 +867,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     // ---- hybrid plan: per plane, the tap box of its coarse kernels and a cost model pick the
     //      direct path (D x D taps per phase pair) or the frequency path (streamed transfer matrices)
     std::vector<int> plane_direct(nz, 0), plane_D(nz, 0);
+    std::vector<double> pt_fft(nz, 0.0), pt_alt(nz, 1e30), pm_fft(nz, 0.0), pm_alt(nz, 0.0);
+    std::vector<int> p_alt(nz, 0);   // best direct alternative per plane (1 CUDA-core, 2 tensor-core, 0 none)
     std::vector<AxisBox> box1(nz), box2(nz);
     const int zb = p->nu > 0 ? p->u0 / N2 : 0, ze = p->nu > 0 ? (p->u1 - 1) / N2 : -1;
     bool too_big = false;
@@ -900,6 +907,20 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double pair_cycles = (double)ptiles * T1 * T2 * ksteps * 3.0 * (Ntile / 2);
         const double t_tc = tc_ok ? 2.0 * pair_cycles / ((p->num_sms / 2) * kSmClock * kTcEff) * (units / N2) + kTcFixed
                                   : 1e30;
+        // device bytes per plane on each path (memory-aware planning below)
+        pt_fft[z] = t_fft;
+        pm_fft[z] = units * (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
+        if (tc_ok && t_tc <= t_dir) {
+            p_alt[z] = 2;
+            pt_alt[z] = t_tc;
+            const double lp = (double)g.nh * (g.nw + T2 - 1);
+            pm_alt[z] = (double)T1 * T2 * ((N2 + 31) / 32) * 2 * Ntile * 32 * 4 * 2 + 2.0 * ((N2 + 31) / 32) * lp * 128 +
+                        2.0 * height * width * 4;
+        } else if (D <= kDirMaxD) {
+            p_alt[z] = 1;
+            pt_alt[z] = t_dir;
+            pm_alt[z] = 2.0 * units * D * D * N2 * 4 + (double)height * width * 4;
+        }
         int mode = 0;                            // 0 FFT, 1 SIMT direct, 2 tensor-core direct
         if (flags & LFM_PLAN_FFT_ONLY) {
             mode = 0;
@@ -911,6 +932,36 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         }
         plane_direct[z] = mode;
         if (mode == 1 && D > kDirMaxD) too_big = true;
+    }
+    // memory-aware planning: while the frequency-path planes' transfer matrices do not fit, move the plane whose
+    // direct alternative costs the least extra time per byte saved
+    p->mem_moved = 0;
+    if (!(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT))) {
+        auto need = [&]() {
+            double b = 0;
+            for (int z = zb; z <= ze; ++z) b += plane_direct[z] == 0 ? pm_fft[z] : pm_alt[z];
+            return b;
+        };
+        const double avail = 0.94 * (double)(mem_budget - nonM_bytes);
+        while (need() > avail) {
+            int best = -1;
+            double best_r = 1e300;
+            for (int z = zb; z <= ze; ++z) {
+                if (plane_direct[z] != 0 || p_alt[z] == 0 || pm_fft[z] <= pm_alt[z]) continue;
+                const double r = (pt_alt[z] - pt_fft[z]) / (pm_fft[z] - pm_alt[z]);
+                if (r < best_r) {
+                    best_r = r;
+                    best = z;
+                }
+            }
+            if (best < 0) break;
+            plane_direct[best] = p_alt[best];
+            ++p->mem_moved;
+        }
+        if (need() > avail)
+            return guard(fail(LFM_ENOMEM, "transfer matrices of the frequency-path planes need %.0f bytes, %.0f available "
+                              "after moving %d planes to the direct path; limiting term: transfer matrices",
+                              need(), avail, p->mem_moved));
     }
     p->direct = too_big;   // all-direct request with boxes beyond kDirMaxD: the generic spatial kernels
     if (!p->direct) {
@@ -1149,6 +1200,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
 #undef CKG
 }
 
+lfm_status lfm_set_memory_limit(size_t bytes) {
+    g_mem_limit = bytes;
+    return LFM_OK;
+}
+
 lfm_status lfm_plan_owned(lfm_plan p, int* unit_begin, int* unit_end) {
     g_err[0] = 0;
     if (!p || !unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");
@@ -1180,6 +1236,7 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->fft_units = p->direct ? 0 : p->nu_fft;
     info->tc_planes = p->direct ? 0 : p->n_tc_planes;
     info->tc_flops_executed = p->direct ? 0.0 : p->tc_flops_exec;
+    info->planes_moved_for_memory = p->mem_moved;
     info->tc_flops_algorithmic = p->direct ? 0.0 : p->tc_flops_alg;
     info->transfer_bytes = p->transfer_bytes;
     info->device_bytes = p->bytes;

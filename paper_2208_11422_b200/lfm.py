@@ -60,7 +60,8 @@ class lfm_info(ctypes.Structure):
                 ("units_padded", ctypes.c_int), ("x_s", ctypes.c_int), ("y_s", ctypes.c_int),
                 ("direct", ctypes.c_int), ("transfer_bytes", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
-                ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double)]
+                ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double),
+                ("planes_moved_for_memory", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -91,6 +92,7 @@ _lib_create = _sig("lfm_plan_create", _i, [ctypes.POINTER(_P), _P, _P, _i, _i, _
                                            ctypes.POINTER(lfm_optics), ctypes.POINTER(lfm_dist), _i, _P])
 _lib_info = _sig("lfm_plan_info", _i, [_P, ctypes.POINTER(lfm_info)])
 _lib_owned = _sig("lfm_plan_owned", _i, [_P, ctypes.POINTER(_i), ctypes.POINTER(_i)])
+_lib_memlimit = _sig("lfm_set_memory_limit", _i, [ctypes.c_size_t])
 _lib_destroy = _sig("lfm_plan_destroy", None, [_P])
 _lib_forward = _sig("lfm_forward", _i, [_P, _P, _P, _P])
 _lib_backward = _sig("lfm_backward", _i, [_P, _P, _P, _P])
@@ -117,7 +119,7 @@ _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
 EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
-            "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
+            "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_set_memory_limit", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
 
@@ -191,6 +193,11 @@ def lfm_comm_unique_id():
     buf = (ctypes.c_ubyte * 128)()
     _check(_lib_unique_id(buf))
     return bytes(buf)
+
+
+def lfm_set_memory_limit(nbytes):
+    """Cap the device memory later plans may use (0 = free memory); see include/lfm.h."""
+    _check(_lib_memlimit(int(nbytes)))
 
 
 def lfm_shard_units(nz, nnum, world, rank):

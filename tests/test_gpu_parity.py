@@ -124,6 +124,43 @@ def test_c2_operators_match_oracle(flags):
     assert rel(xb_d.cpu().numpy(), xb_ref) <= tol
 
 
+@pytest.mark.gpu
+def test_memory_aware_planning():
+    """A capped device (lfm_set_memory_limit) makes the hybrid planner move planes off the frequency path until the
+    transfer matrices fit; the operators still match the oracle.  An impossible cap fails with LFM_ENOMEM naming the
+    limiting term."""
+    L_ = L()
+    cfg = CONFIGS["c2"]   # BASELINE configs[1]: the cost model keeps about half of its planes on the frequency path
+    h = gen_psf(cfg, np.float32)
+    x = gen_volume(cfg, 1, np.float32)
+    try:
+        with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=L_.LFM_PLAN_FFT_ONLY) as full:
+            m_all = full.info()["transfer_bytes"]
+        L_.lfm_set_memory_limit(int(0.45 * m_all) + (64 << 20))
+        with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+            info = plan.info()
+            assert info["planes_moved_for_memory"] > 0
+            assert info["fft_units"] * cfg.nnum ** 2 < cfg.nz * cfg.nnum ** 4
+            tol = op_tol(info)[0]
+            y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+            plan.forward(dev(x), y_d)
+            torch.cuda.synchronize()
+            y_ref = O.forward_project(x.astype(np.float64), h.astype(np.float64))
+            assert rel(y_d.cpu().numpy(), y_ref) <= tol
+            r = (y_ref + 1.0) / (y_ref.mean() + 1.0)
+            xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            plan.backward(dev(r), xb_d)
+            torch.cuda.synchronize()
+        xb_ref = O.backward_project(r.astype(np.float32).astype(np.float64), h.astype(np.float64))
+        assert rel(xb_d.cpu().numpy(), xb_ref) <= tol
+        L_.lfm_set_memory_limit(1 << 20)
+        with pytest.raises(L_.LfmError) as e:
+            L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum))
+        assert "LFM_ENOMEM" in str(e.value) and "limiting term" in str(e.value)
+    finally:
+        L_.lfm_set_memory_limit(0)
+
+
 def tiny_problem(name="tiny", seed=1):
     cfg = CONFIGS[name]
     h = gen_psf(cfg, np.float32)
