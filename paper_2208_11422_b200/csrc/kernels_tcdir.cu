@@ -109,6 +109,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int i = ib; i < ie; ++i) {
                 const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
                 const TcPlane pl = d.planes[zi];
+                const int* rm = d.rowmask + pl.mask_off;
                 const int row0 = tile * 2 * kM + (int)rank * kM - d.e2lo + pl.e2min;
                 for (int c = 0; c < d.nch; ++c) {
                     const bool tail = c == d.nch - 1 && d.tail_w < kKC;
@@ -117,7 +118,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint32_t w = tail ? (uint32_t)d.tail_w : (uint32_t)kKC;   // phases per row
                     const int slab_hi = FWD ? (zi * 2) * d.nch + c : c;
                     const int slab_lo = FWD ? (zi * 2 + 1) * d.nch + c : d.nch + c;
-                    for (int t1 = 0; t1 < pl.T1; ++t1, ++na) {
+                    for (int t1 = 0; t1 < pl.T1; ++t1) {
+                        if (!((rm[t1] >> c) & 1)) continue;   // all taps of this window are zero
                         const int sa = na % kASlots;
                         const long long c0 = (d.exp & 4) ? clock64() : 0;
                         if (na >= kASlots) tc::mbar_wait(&bar_emptyA[sa], ((na / kASlots) - 1) & 1);
@@ -138,6 +140,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             tc::tma_load_3d_pair(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb]);
                             tc::tma_load_3d_pair(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb]);
                         }
+                        ++na;
                     }
                 }
             }
@@ -155,20 +158,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int na = 0, nb = 0, g = 0, gk = 0;   // A windows, B tiles, drain group, K-steps in the open group
             for (int i = ib; i < ie; ++i) {
                 const int zi = d.items[i] / d.tiles;
-                const int T1 = d.planes[zi].T1, T2 = d.planes[zi].T2, NT = T1 * T2, nst = d.nch * NT;
-                int st = 0;
+                const TcPlane pl = d.planes[zi];
+                const int* rm = d.rowmask + pl.mask_off;
+                const int T1 = pl.T1, T2 = pl.T2;
                 for (int c = 0; c < d.nch; ++c) {
                     const int ks = c == d.nch - 1 ? d.kst_last : kKC / 8;
                     const uint32_t rb = (c == d.nch - 1 && d.tail_w < kKC) ? (uint32_t)d.tail_w * 4 : 128u;   // row bytes
-                    for (int t1 = 0; t1 < T1; ++t1, ++na) {
+                    for (int t1 = 0; t1 < T1; ++t1) {
+                        if (!((rm[t1] >> c) & 1)) continue;
                         const int sa = na % kASlots;
+                        const bool last_win = c * T1 + t1 == pl.last_win;
                         {
                             const long long c0 = (d.exp & 4) ? clock64() : 0;
                             tc::mbar_wait(&bar_fullA[sa], (na / kASlots) & 1);
                             if (d.exp & 4) dbg_full += clock64() - c0;
                         }
                         const uint32_t a_hi0 = tc::smem_u32(Abase + (size_t)sa * 2 * apart), a_lo0 = a_hi0 + apart;
-                        for (int t2 = 0; t2 < T2; ++t2, ++nb, ++st) {
+                        for (int t2 = 0; t2 < T2; ++t2, ++nb) {
                             const int sb = nb % kBSlots, j = g & 1;
                             const long long c0 = (d.exp & 4) ? clock64() : 0;
                             tc::mbar_wait(&bar_fullB[sb], (nb / kBSlots) & 1);
@@ -192,15 +198,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             gk += ks;
                             tc::mma_commit_pair(&bar_emptyB[sb], 3);
                             if (t2 == T2 - 1) tc::mma_commit_pair(&bar_emptyA[sa], 3);
-                            // close the drain group at the item's end or when the next stage would exceed chain_k
-                            const int cn = (st + 1) / NT;
-                            const int ksn = cn == d.nch - 1 ? d.kst_last : kKC / 8;
-                            if (st == nst - 1 || gk + ksn > d.chain_k) {
+                            // close the drain group at the item's last stage or before it could exceed chain_k
+                            if ((last_win && t2 == T2 - 1) || gk + kKC / 8 > d.chain_k) {
                                 tc::mma_commit_pair(&bar_acc[j], 3);
                                 ++g;
                                 gk = 0;
                             }
                         }
+                        ++na;
                     }
                 }
             }
@@ -225,14 +230,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         long long dbg_acc = 0, dbg_epi = 0;
         for (int i = ib; i < ie; ++i) {
             const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
-            const int NT = d.planes[zi].T1 * d.planes[zi].T2, nst = d.nch * NT;
+            const TcPlane pl = d.planes[zi];
+            const int* rm = d.rowmask + pl.mask_off;
             int gk = 0;
-            for (int st = 0; st < nst; ++st) {
-                const int c = st / NT;
+            for (int st = 0, nst = pl.T1 * pl.T2 * d.nch; st < nst; ++st) {   // stages in (c, t1, t2) order
+                const int c = st / (pl.T1 * pl.T2), t1 = (st / pl.T2) % pl.T1, t2 = st % pl.T2;
+                if (!((rm[t1] >> c) & 1)) continue;
                 gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
-                const int cn = (st + 1) / NT;
-                const int ksn = cn == d.nch - 1 ? d.kst_last : kKC / 8;
-                if (!(st == nst - 1 || gk + ksn > d.chain_k)) continue;   // group still open
+                if (!((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k)) continue;
                 gk = 0;
                 const int j = g & 1;
                 {
@@ -388,7 +393,10 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const __grid_constant__ 
 // slabs [hi], [lo] of Ntile x 32 row-major floats (the TMA load swizzles them) with element (n, k) =
 //   forward : G_d[b' = n][a = chunk*32 + k],   d = -e        backward: G_d[b' = chunk*32 + k][a = n],   d = +e
 __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane pl, int z, const float* __restrict__ psf,
-                                  int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out) {
+                                  int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out, int* __restrict__ nzflag) {
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
     const int tileid = blockIdx.x;   // tap * nch + chunk
     const int chunk = tileid % d.nch;
     const int tap = tileid / d.nch;
@@ -414,7 +422,10 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
         tc::split_tf32(v, h, l);
         hi[e] = h;
         lo[e] = l;
+        if (v != 0.0f) any = 1;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) nzflag[tileid] = any;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -469,7 +480,8 @@ void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std:
     // longest-processing-time-first: items sorted by cost (taps), each to the least-loaded CTA
     std::vector<std::pair<long long, int>> it;
     for (int zi = 0; zi < d.nzd; ++zi)
-        for (int t = 0; t < d.tiles; ++t) it.push_back({(long long)planes[zi].T1 * planes[zi].T2, zi * d.tiles + t});
+        for (int t = 0; t < d.tiles; ++t)
+            it.push_back({(long long)std::max(1, planes[zi].active_windows) * planes[zi].T2, zi * d.tiles + t});
     std::stable_sort(it.begin(), it.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
     std::vector<long long> load(d.grid, 0);
     std::vector<std::vector<int>> per(d.grid);
@@ -543,12 +555,42 @@ cudaError_t tcdir_encode(TcDirArgs* d, int fwd) {
 }
 
 cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
-                              int kw, int ch, int cw, int fwd, float* coef, cudaStream_t s) {
+                              int kw, int ch, int cw, int fwd, float* coef, int* nzflags, cudaStream_t s) {
     (void)zi;
     const int tiles = pl.T1 * pl.T2 * d.nch;
     if (tiles <= 0) return cudaSuccess;
-    tcdir_coef_kernel<<<tiles, 256, 0, s>>>(d, pl, z, psf_dev, kh, kw, ch, cw, fwd, coef);
+    tcdir_coef_kernel<<<tiles, 256, 0, s>>>(d, pl, z, psf_dev, kh, kw, ch, cw, fwd, coef, nzflags);
     return cudaGetLastError();
+}
+
+void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const std::vector<int>& nzflags,
+                        std::vector<int>* rowmask) {
+    rowmask->clear();
+    long long tile0 = 0;   // first (tap, chunk) flag of the plane
+    for (TcPlane& pl : *planes) {
+        pl.mask_off = (int)rowmask->size();
+        pl.last_win = -1;
+        pl.active_windows = 0;
+        for (int t1 = 0; t1 < pl.T1; ++t1) {
+            int m = 0;
+            for (int c = 0; c < d.nch; ++c)
+                for (int t2 = 0; t2 < pl.T2; ++t2)
+                    if (nzflags[(size_t)(tile0 + (long long)(t1 * pl.T2 + t2) * d.nch + c)]) m |= 1 << c;
+            rowmask->push_back(m);
+        }
+        for (int c = 0; c < d.nch; ++c)
+            for (int t1 = 0; t1 < pl.T1; ++t1)
+                if (((*rowmask)[pl.mask_off + t1] >> c) & 1) {
+                    pl.last_win = c * pl.T1 + t1;
+                    ++pl.active_windows;
+                }
+        if (pl.last_win < 0) {   // an all-zero plane still runs one (zero) window so that its outputs are written
+            (*rowmask)[pl.mask_off] |= 1;
+            pl.last_win = 0;
+            pl.active_windows = 1;
+        }
+        tile0 += (long long)pl.T1 * pl.T2 * d.nch;
+    }
 }
 
 template <bool FWD, int DST>

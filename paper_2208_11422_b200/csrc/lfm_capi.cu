@@ -222,6 +222,7 @@ struct lfm_plan_s {
     int n_tc_planes = 0;
     int mem_moved = 0;   // planes moved off the frequency path to fit the memory budget
     double tc_flops_exec = 0.0, tc_flops_alg = 0.0;   // per projection (lfm_info)
+    double tc_active_frac = 0.0;                       // mean fraction of nonzero (chunk, tap row) windows
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -1090,18 +1091,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     std::vector<TcPlane> pls;
                     if (!tcdir_geometry(&t, !w, d1a.data(), d1b.data(), d2a.data(), d2b.data(), &pls, p->num_sms))
                         return guard(fail(LFM_EUNSUPPORTED, "tensor-core direct path needs Nnum^2 <= 256"));
-                    std::vector<int> ioff, items;
-                    tcdir_schedule(t, pls, &ioff, &items);
-                    TcPlane* dpl = nullptr;
-                    int *dio = nullptr, *dit = nullptr;
                     float *cf = nullptr, *sr = nullptr, *pt = nullptr;
+                    int* nzf = nullptr;
                     const size_t nf = tcdir_coef_floats(t, pls), ns = tcdir_src_floats(t, !w), np = tcdir_part_floats(t, !w);
-                    PG(dalloc(p, &dpl, pls.size() * sizeof(TcPlane), "tc plane records"));
-                    p->dallocs.push_back(dpl);
-                    PG(dalloc(p, &dio, ioff.size() * sizeof(int), "tc schedule"));
-                    p->dallocs.push_back(dio);
-                    PG(dalloc(p, &dit, items.size() * sizeof(int), "tc schedule"));
-                    p->dallocs.push_back(dit);
+                    size_t ntile = 0;
+                    for (const TcPlane& pl : pls) ntile += (size_t)pl.T1 * pl.T2 * t.nch;
                     PG(dalloc(p, &cf, nf * sizeof(float), "tc direct taps"));
                     p->dallocs.push_back(cf);
                     PG(dalloc(p, &sr, ns * sizeof(float), "tc direct staged source"));
@@ -1110,29 +1104,55 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                         PG(dalloc(p, &pt, np * sizeof(float), "tc direct forward partials"));
                         p->dallocs.push_back(pt);
                     }
-                    CKG(cudaMemcpyAsync(dpl, pls.data(), pls.size() * sizeof(TcPlane), cudaMemcpyHostToDevice, s));
-                    CKG(cudaMemcpyAsync(dio, ioff.data(), ioff.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-                    CKG(cudaMemcpyAsync(dit, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-                    t.planes = dpl;
-                    t.item_off = dio;
-                    t.items = dit;
+                    PG(dalloc(p, &nzf, ntile * sizeof(int), "tc tile flags"));
                     t.coef = cf;
                     t.src = sr;
                     t.part = pt;
-                    CKG(tcdir_encode(&t, !w));
+                    // coefficient tiles + nonzero flags -> windows that can be skipped (edge tap rows x chunks)
                     for (int zi = 0; zi < t.nzd; ++zi)
-                        CKG(launch_tcdir_coef(t, pls[zi], zi, zl[zi], w ? p->psfb : p->psf, kh, kw, g.ch, g.cw, !w, cf, s));
+                        CKG(launch_tcdir_coef(t, pls[zi], zi, zl[zi], w ? p->psfb : p->psf, kh, kw, g.ch, g.cw, !w, cf,
+                                              nzf + pls[zi].coef_off / 2, s));
+                    std::vector<int> flags_h(ntile), rowmask;
+                    CKG(cudaMemcpyAsync(flags_h.data(), nzf, ntile * sizeof(int), cudaMemcpyDeviceToHost, s));
+                    CKG(cudaStreamSynchronize(s));
+                    cudaFree(nzf);
+                    tcdir_window_masks(t, &pls, flags_h, &rowmask);
+                    std::vector<int> ioff, items;
+                    tcdir_schedule(t, pls, &ioff, &items);
+                    TcPlane* dpl = nullptr;
+                    int *dio = nullptr, *dit = nullptr, *drm = nullptr;
+                    PG(dalloc(p, &dpl, pls.size() * sizeof(TcPlane), "tc plane records"));
+                    p->dallocs.push_back(dpl);
+                    PG(dalloc(p, &drm, rowmask.size() * sizeof(int), "tc window masks"));
+                    p->dallocs.push_back(drm);
+                    PG(dalloc(p, &dio, ioff.size() * sizeof(int), "tc schedule"));
+                    p->dallocs.push_back(dio);
+                    PG(dalloc(p, &dit, items.size() * sizeof(int), "tc schedule"));
+                    p->dallocs.push_back(dit);
+                    CKG(cudaMemcpyAsync(dpl, pls.data(), pls.size() * sizeof(TcPlane), cudaMemcpyHostToDevice, s));
+                    CKG(cudaMemcpyAsync(drm, rowmask.data(), rowmask.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    CKG(cudaMemcpyAsync(dio, ioff.data(), ioff.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    CKG(cudaMemcpyAsync(dit, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    t.planes = dpl;
+                    t.rowmask = drm;
+                    t.item_off = dio;
+                    t.items = dit;
+                    CKG(tcdir_encode(&t, !w));
                     CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
                     coef_bytes += nf * sizeof(float);
-                }
-                {
-                    const double ksteps = (N2 + 7) / 8, ptiles = ta.tiles;
-                    for (size_t zi = 0; zi < zl.size(); ++zi) {
-                        const int z = zl[zi];
-                        const double T = (double)(d1b[zi] - d1a[zi] + 1) * (d2b[zi] - d2a[zi] + 1);
-                        p->tc_flops_exec += ptiles * T * ksteps * 3.0 * 2.0 * 256.0 * ta.Ntile * 8.0;
-                        p->tc_flops_alg += 2.0 * (double)N2 * N2 * box1[z].D * box2[z].D * g.nh * g.nw;
-                    }
+                    if (!w)   // executed tensor flops of one projection: 3 pair MMAs per K-step of every nonzero window tap
+                        for (size_t zi = 0; zi < pls.size(); ++zi) {
+                            const TcPlane& pl = pls[zi];
+                            double ks_all = 0;
+                            for (int c = 0; c < t.nch; ++c)
+                                for (int t1 = 0; t1 < pl.T1; ++t1)
+                                    if ((rowmask[pl.mask_off + t1] >> c) & 1)
+                                        ks_all += (double)pl.T2 * (c == t.nch - 1 ? t.kst_last : 4);
+                            p->tc_flops_exec += (double)t.tiles * ks_all * 3.0 * 2.0 * 256.0 * t.Ntile * 8.0;
+                            p->tc_active_frac += (double)pl.active_windows / (pl.T1 * t.nch) / pls.size();
+                            const int z = zl[zi];
+                            p->tc_flops_alg += 2.0 * (double)N2 * N2 * box1[z].D * box2[z].D * g.nh * g.nw;
+                        }
                 }
                 p->tcf.push_back(ta);
                 p->tcb.push_back(tb);

@@ -102,6 +102,9 @@ struct DirArgs {
 struct TcPlane {
     int T1, T2, e1min, e2min;   // union tap box of the plane (source offsets)
     long long coef_off;         // first coefficient slab (Ntile x 32 floats) of the plane
+    int mask_off;               // rowmask[mask_off + t1]: bit c set if window (chunk c, tap row t1) has a nonzero tap
+    int last_win;               // c * T1 + t1 of the last nonzero window
+    int active_windows;         // number of nonzero windows
 };
 struct TcDirArgs {
     int N, H, W, nh, nw;
@@ -109,6 +112,7 @@ struct TcDirArgs {
     int nzd;                  // tensor-core planes
     const int* zlist;         // [nzd] global plane index (device)
     const TcPlane* planes;    // [nzd] (device)
+    const int* rowmask;       // nonzero (chunk, tap row) windows, see TcPlane (device)
     int N2, Ntile;            // phases and TMEM columns per accumulator (N2 rounded up to 16, <= 256)
     int nch, kst_last;        // reduction chunks of 32 phases; K-steps of 8 in the last chunk
     int e2lo;                 // column origin of the staged grid (min e2min over planes)
@@ -143,7 +147,10 @@ size_t tcdir_src_floats(const TcDirArgs& d, int fwd);
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd);
 cudaError_t tcdir_encode(TcDirArgs* d, int fwd);
 cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
-                              int kw, int ch, int cw, int fwd, float* coef, cudaStream_t s);
+                              int kw, int ch, int cw, int fwd, float* coef, int* nzflags, cudaStream_t s);
+// from the per-(tap, chunk) nonzero flags of every plane: row masks, last windows, active counts (host)
+void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const std::vector<int>& nzflags,
+                        std::vector<int>* rowmask);
 cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* y, int accumulate,
                              cudaStream_t s);
 cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
