@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) metric_rows_kernel(const unsigned* __rest
         if (lane == 0) {
             for (int r = 0; r < nr; ++r) {
                 if (task < xs)
-                    T1[(size_t)(i0 + r) * xs + task] = acc[r];
+                    T1[(size_t)task * H + i0 + r] = acc[r];   // column-major: member sums read it coalesced
                 else
                     rowsq[i0 + r] = acc[r];
             }
@@ -219,62 +219,63 @@ __global__ void __launch_bounds__(256) metric_rows_kernel(const unsigned* __rest
     }
 }
 
-// F on the region members, Parseval norm, entropy.  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) metric_final_kernel(int H, int xs, int ys, const double* __restrict__ Cr,
-                                                            const double* __restrict__ T1,
-                                                            const double* __restrict__ rowsq, const int2* __restrict__ mem,
-                                                            int nmem, double* __restrict__ out) {
-    __shared__ double red[32];
-    __shared__ double s_norm;
+// Parseval norm ||m|| from the row sums (every CTA, the same fixed order -> identical value everywhere)
+__device__ double metric_norm(const double* __restrict__ rowsq, int H, double* red) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    // ||m||^2: thread-strided partial sums, warp tree, then warp 0 over warps (fixed order)
     double t = 0.0;
     for (int i = threadIdx.x; i < H; i += blockDim.x) t += rowsq[i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp] = t;
+    __syncthreads();
+    double v = lane < nw ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    return sqrt(v);
+}
+
+// F(u, v) = sum_i Cr[u][i] T1[v][i] for region member k (one warp each), entropy term -w log2 w, w = |F| / ||m||
+__global__ void __launch_bounds__(256) metric_member_kernel(int H, const double* __restrict__ Cr,
+                                                            const double* __restrict__ T1,
+                                                            const double* __restrict__ rowsq,
+                                                            const int2* __restrict__ mem, int nmem,
+                                                            double* __restrict__ term, double* __restrict__ out) {
+    __shared__ double red[32];
+    const double L = metric_norm(rowsq, H, red);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[1] = L;
+    if (k >= nmem) return;
+    const int u = mem[k].x, v = mem[k].y;
+    const double* cr = Cr + (size_t)u * H;
+    const double* t1 = T1 + (size_t)v * H;
+    double f = 0.0;
+    for (int i = lane; i < H; i += 32) f = fma(cr[i], t1[i], f);
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    if (lane == 0) {
+        double e = 0.0;
+        if (L > 0.0) {
+            const double w = fabs(f) / L;
+            if (w > 0.0) e = -w * log2(w);
+        }
+        term[k] = e;
+    }
+}
+
+// E = 2 / (xs ys) * sum_k term[k] in a fixed order (one CTA)
+__global__ void __launch_bounds__(1024) metric_sum_kernel(int xs, int ys, const double* __restrict__ term, int nmem,
+                                                          double* __restrict__ out) {
+    __shared__ double red[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double t = 0.0;
+    for (int k = threadIdx.x; k < nmem; k += blockDim.x) t += term[k];
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     if (lane == 0) red[warp] = t;
     __syncthreads();
     if (warp == 0) {
         double v = lane < nw ? red[lane] : 0.0;
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) s_norm = sqrt(v);
+        if (lane == 0) out[0] = out[1] > 0.0 ? 2.0 / ((double)xs * (double)ys) * v : 0.0;
     }
-    __syncthreads();
-    const double L = s_norm;
-    // each warp evaluates F for members warp, warp+nw, ... and accumulates its entropy terms
-    double wsum = 0.0;
-    for (int k = warp; k < nmem; k += nw) {
-        const int u = mem[k].x, v = mem[k].y;
-        const double* cr = Cr + (size_t)u * H;
-        double f = 0.0;
-        for (int i = lane; i < H; i += 32) f = fma(cr[i], T1[(size_t)i * xs + v], f);
-        for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-        if (L > 0.0) {
-            const double w = fabs(f) / L;
-            if (w > 0.0) wsum += -w * log2(w);
-        }
-    }
-    __syncthreads();
-    if (lane == 0) red[warp] = wsum;
-    __syncthreads();
-    if (warp == 0) {
-        double v = lane < nw ? red[lane] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
-            out[0] = (L > 0.0) ? 2.0 / ((double)xs * (double)ys) * v : 0.0;
-            out[1] = L;
-        }
-    }
-}
-
-cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
-                          const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
-                          double* out, cudaStream_t s) {
-    const size_t smem = (size_t)kMetricRows * W * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(metric_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    metric_rows_kernel<<<(H + kMetricRows - 1) / kMetricRows, 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq);
-    metric_final_kernel<<<1, 1024, 0, s>>>(H, xs, ys, Cr, T1, rowsq, members, nmem, out);
-    return cudaGetLastError();
 }
 
 // ---- ratio image (direct path): r = y / (max(yhat,0) + eps) ----

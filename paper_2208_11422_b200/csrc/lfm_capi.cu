@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <vector>
@@ -119,7 +120,8 @@ lfm_status metric_alloc(MetricDev* m, const Region& r, int H, int W, cudaStream_
     dct_rows(W, r.xs, &cw);
     CK(cudaMalloc(&m->Cr, cr.size() * sizeof(double)));
     CK(cudaMalloc(&m->Cw, cw.size() * sizeof(double)));
-    CK(cudaMalloc(&m->T1, (size_t)H * r.xs * sizeof(double)));
+    // T1 = (m C_W^T) column-major [xs][H], followed by the per-member entropy terms of launch_metric
+    CK(cudaMalloc(&m->T1, ((size_t)H * r.xs + std::max(r.tri.size(), r.rect.size())) * sizeof(double)));
     CK(cudaMalloc(&m->rowsq, (size_t)H * sizeof(double)));
     CK(cudaMalloc(&m->out, 8 * sizeof(double)));
     CK(cudaMalloc(&m->mem[0], r.tri.size() * sizeof(int2)));
@@ -649,7 +651,7 @@ constexpr double kXformPerUnit = 9.0e-8;
 const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 28.0e12};
 // tensor-core direct path: achieved fraction of the tcgen05 floor (measured r01 at c3, staging and partial
 // reduction included) and a fixed per-plane cost
-constexpr double kTcEff = 0.56;
+constexpr double kTcEff = 0.68;
 constexpr double kTcFixed = 5e-6;
 constexpr double kSmClock = 1.965e9;
 
@@ -905,8 +907,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 7) / 8;
         const int ptiles = (g.nh * (g.nw + T2 - 1) + 255) / 256;
         const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256 && T2 <= 65;
-        const double pair_cycles = (double)ptiles * T1 * T2 * ksteps * 3.0 * (Ntile / 2);
-        const double t_tc = tc_ok ? 2.0 * pair_cycles / ((p->num_sms / 2) * kSmClock * kTcEff) * (units / N2) + kTcFixed
+        // the two edge tap rows are active for about half of the 32-phase chunks (window skipping, §5.3)
+        const double act = T1 >= 3 ? 1.0 - 1.0 / T1 : 1.0;
+        const double pair_cycles = (double)ptiles * T1 * T2 * act * ksteps * 3.0 * (Ntile / 2);
+        static const double tc_eff = getenv("LFM_TC_EFF") ? atof(getenv("LFM_TC_EFF")) : kTcEff;   // dev override
+        const double t_tc = tc_ok ? 2.0 * pair_cycles / ((p->num_sms / 2) * kSmClock * tc_eff) * (units / N2) + kTcFixed
                                   : 1e30;
         // device bytes per plane on each path (memory-aware planning below)
         pt_fft[z] = t_fft;
