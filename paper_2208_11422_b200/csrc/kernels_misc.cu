@@ -175,7 +175,7 @@ cudaError_t launch_sum_stats(const float* p, size_t n, double* partials, int npa
 // ---- metric ----
 constexpr int kMetricRows = 4;
 
-// T1[i][v] = sum_j m[i][j] Cw[v][j] (v < xs) and rowsq[i] = sum_j m[i][j]^2, fp64, kMetricRows rows per CTA
+// T1[v][i] = sum_j m[i][j] Cw[v][j] (v < xs) and rowsq[i] = sum_j m[i][j]^2, fp64, kMetricRows rows per CTA
 __global__ void __launch_bounds__(256) metric_rows_kernel(const unsigned* __restrict__ mbits, int H, int W, int xs,
                                                           const double* __restrict__ Cw, double* __restrict__ T1,
                                                           double* __restrict__ rowsq) {
@@ -276,6 +276,20 @@ __global__ void __launch_bounds__(1024) metric_sum_kernel(int xs, int ys, const 
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) out[0] = out[1] > 0.0 ? 2.0 / ((double)xs * (double)ys) * v : 0.0;
     }
+}
+
+cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
+                          const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
+                          double* out, cudaStream_t s) {
+    const size_t smem = (size_t)kMetricRows * W * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(metric_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    metric_rows_kernel<<<(H + kMetricRows - 1) / kMetricRows, 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq);
+    // the per-member terms follow T1 ([xs][H] doubles) in the same allocation (MetricDev)
+    double* term = T1 + (size_t)xs * H;
+    metric_member_kernel<<<(nmem + 7) / 8, 256, 0, s>>>(H, Cr, T1, rowsq, members, nmem, term, out);
+    metric_sum_kernel<<<1, 1024, 0, s>>>(xs, ys, term, nmem, out);
+    return cudaGetLastError();
 }
 
 // ---- ratio image (direct path): r = y / (max(yhat,0) + eps) ----

@@ -511,7 +511,7 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
     ST(mark(p, ST_METRIC, s));
     CK(launch_metric(p->mproj, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
                      p->met.nmem[ri], p->met.T1, p->met.rowsq, p->met.out, s));
-    p->pacc.launches += 2;
+    p->pacc.launches += 3;
     ST(mark(p, LFM_N_STAGES, s));
     return LFM_OK;
 }
