@@ -408,6 +408,7 @@ def run_c5(args):
     yb = torch.from_numpy(np.stack(ys)).cuda()
     xb = torch.zeros((F, nz, H, W), device="cuda")
     plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.warmup))
+    plan.profile(True)
     plan.profile_read(reset=True)
     clocks = ClockSampler(0)
     clocks.start()
@@ -421,6 +422,10 @@ def run_c5(args):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     prof = plan.profile_read(reset=True)
+    plan.profile(False)
+    groups = {"transforms_x": "r2c_x", "fwd_mac_batch": "fwd_mac", "per_frame_forward_rest": "c2r_yhat",
+              "bwd_mac_batch": "bwd_mac", "per_frame_update_rest": "c2r_update"}
+    stage_ms = {g: prof["ms"][k] / max(1, prof["count"][k]) for g, k in groups.items()}
     auto = plan.rl_iterate_batch(yb, xb, L.make_policy(mode="auto", max_iters=50))
     line = {"metric": "frame-iterations/s (c5 time-lapse, frame-batched lockstep RL)", "value": F * args.steps / (ms / 1e3),
             "unit": "frame-iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -428,7 +433,8 @@ def run_c5(args):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"c5: batch of {F} time-lapse frames of the c3 geometry (Nnum=15, 1005x1005, 51 planes)",
                        "frames_per_batch": F, "plan_flags": args.flags or 4, "fft_units": info["fft_units"],
-                       "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"]}},
+                       "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"]},
+                       "batch_stage_avg_ms": stage_ms},
             "gpu_launches": prof["launches"], "clocks": clk}
     print(json.dumps(line), flush=True)
     plan.close()

@@ -7,6 +7,7 @@
 // bound by HBM bandwidth.  M is read with streaming (evict-first) 32-byte loads; every other operand
 // is small and L2/shared-memory resident.
 #include "lfm_internal.cuh"
+#include "tc_sm100.cuh"   // mbarrier / bulk-copy helpers
 
 namespace lfm {
 
@@ -272,6 +273,100 @@ __global__ void __launch_bounds__(128) bwd_mac_batch_kernel(const float2* __rest
     }
 }
 
+// Forward batched MAC for F >= 8: 128 threads per kappa, each owns output phases b' = tid and tid + 128, so every
+// shared-memory broadcast of G feeds twice the FMAs (the F = 16 kernel above was bound by smem load issue).
+template <int F>
+__global__ void __launch_bounds__(128) fwd_mac_batch2_kernel(const float2* __restrict__ M, const float2* __restrict__ G,
+                                                             long long g_fstride, float2* __restrict__ Y,
+                                                             long long y_fstride, int N2, int nu_pad) {
+    extern __shared__ float4 smb[];
+    auto ms = reinterpret_cast<float2 (*)[kBatchKT][257]>(smb);                                  // [2][KT][257]
+    auto gs = reinterpret_cast<float4 (*)[kBatchKT][F / 2]>(smb + (2 * kBatchKT * 257 + 1) / 2);   // [2][KT][F/2]
+    const long long kap = blockIdx.x;
+    const int tid = threadIdx.x;
+    const float2* Mk = M + kap * N2 * (long long)nu_pad;
+    const int ntiles = nu_pad / kBatchKT;
+    const int seg_row0 = tid >> 3, seg_q = tid & 7;    // rows seg_row0 + 16*i, float4 column seg_q
+    float4 mreg[16];
+    float4 greg[(kBatchKT * F / 2 + 127) / 128];
+    auto load_tile = [&](int t) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int row = seg_row0 + 16 * i;
+            mreg[i] = row < N2 ? __ldcs(reinterpret_cast<const float4*>(Mk + (long long)row * nu_pad + t * kBatchKT) + seg_q)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < (kBatchKT * F / 2 + 127) / 128; ++j) {
+            const int e = tid + 128 * j;
+            if (e < kBatchKT * F / 2) {
+                const int k = e / (F / 2), fp = e - (e / (F / 2)) * (F / 2);
+                const float2 g0 = G[2 * fp * g_fstride + kap * nu_pad + t * kBatchKT + k];
+                const float2 g1 = G[(2 * fp + 1) * g_fstride + kap * nu_pad + t * kBatchKT + k];
+                greg[j] = make_float4(g0.x, g0.y, g1.x, g1.y);
+            }
+        }
+    };
+    auto store_tile = [&](int b) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int row = seg_row0 + 16 * i;
+            ms[b][2 * seg_q][row] = make_float2(mreg[i].x, mreg[i].y);
+            ms[b][2 * seg_q + 1][row] = make_float2(mreg[i].z, mreg[i].w);
+        }
+#pragma unroll
+        for (int j = 0; j < (kBatchKT * F / 2 + 127) / 128; ++j) {
+            const int e = tid + 128 * j;
+            if (e < kBatchKT * F / 2) {
+                const int k = e / (F / 2), fp = e - (e / (F / 2)) * (F / 2);
+                gs[b][k][fp] = greg[j];
+            }
+        }
+    };
+    float ar0[F], ai0[F], ar1[F], ai1[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) ar0[f] = ai0[f] = ar1[f] = ai1[f] = 0.f;
+    load_tile(0);
+    store_tile(0);
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+        const int b = t & 1;
+        if (t + 1 < ntiles) load_tile(t + 1);
+#pragma unroll 4
+        for (int k = 0; k < kBatchKT; ++k) {
+            const float2 m0 = ms[b][k][tid];
+            const float2 m1 = ms[b][k][tid + 128];
+#pragma unroll
+            for (int fp = 0; fp < F / 2; ++fp) {
+                const float4 g = gs[b][k][fp];
+                ar0[2 * fp] = fmaf(m0.x, g.x, ar0[2 * fp]);
+                ar0[2 * fp] = fmaf(-m0.y, g.y, ar0[2 * fp]);
+                ai0[2 * fp] = fmaf(m0.x, g.y, ai0[2 * fp]);
+                ai0[2 * fp] = fmaf(m0.y, g.x, ai0[2 * fp]);
+                ar0[2 * fp + 1] = fmaf(m0.x, g.z, ar0[2 * fp + 1]);
+                ar0[2 * fp + 1] = fmaf(-m0.y, g.w, ar0[2 * fp + 1]);
+                ai0[2 * fp + 1] = fmaf(m0.x, g.w, ai0[2 * fp + 1]);
+                ai0[2 * fp + 1] = fmaf(m0.y, g.z, ai0[2 * fp + 1]);
+                ar1[2 * fp] = fmaf(m1.x, g.x, ar1[2 * fp]);
+                ar1[2 * fp] = fmaf(-m1.y, g.y, ar1[2 * fp]);
+                ai1[2 * fp] = fmaf(m1.x, g.y, ai1[2 * fp]);
+                ai1[2 * fp] = fmaf(m1.y, g.x, ai1[2 * fp]);
+                ar1[2 * fp + 1] = fmaf(m1.x, g.z, ar1[2 * fp + 1]);
+                ar1[2 * fp + 1] = fmaf(-m1.y, g.w, ar1[2 * fp + 1]);
+                ai1[2 * fp + 1] = fmaf(m1.x, g.w, ai1[2 * fp + 1]);
+                ai1[2 * fp + 1] = fmaf(m1.y, g.z, ai1[2 * fp + 1]);
+            }
+        }
+        if (t + 1 < ntiles) store_tile(b ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        if (tid < N2) Y[f * y_fstride + kap * N2 + tid] = make_float2(ar0[f], ai0[f]);
+        if (tid + 128 < N2) Y[f * y_fstride + kap * N2 + tid + 128] = make_float2(ar1[f], ai1[f]);
+    }
+}
+
 cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_fstride, float2* Y, long long y_fstride,
                                  int F, int nkappa, int N2, int nu_pad, cudaStream_t s) {
     if (N2 > 256 || nu_pad % kBatchKT) return cudaErrorInvalidValue;
@@ -283,15 +378,112 @@ cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_f
         if (e != cudaSuccess) return e;                                                                         \
         fwd_mac_batch_kernel<FV><<<nkappa, 256, smem, s>>>(M, G, g_fstride, Y, y_fstride, N2, nu_pad);          \
         break;
-    switch (F) {
-        LFM_FB(2)
-        LFM_FB(4)
-        LFM_FB(8)
-        LFM_FB(16)
-        default: return cudaErrorInvalidValue;
+#define LFM_FB2(FV)                                                                                              \
+    case FV:                                                                                                     \
+        e = cudaFuncSetAttribute(fwd_mac_batch2_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                          \
+        fwd_mac_batch2_kernel<FV><<<nkappa, 128, smem, s>>>(M, G, g_fstride, Y, y_fstride, N2, nu_pad);          \
+        break;
+    if (N2 <= 256 && F >= 8) {
+        switch (F) {
+            LFM_FB2(8)
+            LFM_FB2(16)
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (F) {
+            LFM_FB(2)
+            LFM_FB(4)
+            LFM_FB(8)
+            LFM_FB(16)
+            default: return cudaErrorInvalidValue;
+        }
     }
+#undef LFM_FB2
 #undef LFM_FB
     return cudaGetLastError();
+}
+
+// Backward batched MAC, staged version (F >= 8): a CTA of 256 threads owns 1024 units (4 per thread) of one kappa and
+// all F frames; the rows M[kappa][b'][u0 .. u0+1024) stream into shared memory by 1-D bulk copies through a 4-deep
+// mbarrier ring (4 rows per stage), so the 128 fp32 accumulators per thread never wait on HBM latency.
+constexpr int kBBU = 1024, kBBRows = 4, kBBStages = 4;
+
+template <int F>
+__global__ void __launch_bounds__(288, 1) bwd_mac_batch_staged_kernel(const float2* __restrict__ M, const float2* __restrict__ R,
+                                                                      long long r_fstride, float2* __restrict__ Xh,
+                                                                      long long x_fstride, int N2, int nu_pad) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ uint64_t full[kBBStages], empty[kBBStages];
+    float2* rs = reinterpret_cast<float2*>(sm);                                  // [N2][F]
+    unsigned char* stage = sm + (((size_t)N2 * F * sizeof(float2) + 127) & ~(size_t)127);
+    const long long kap = blockIdx.y;
+    const int u0 = blockIdx.x * kBBU;
+    const int nu_here = min(kBBU, nu_pad - u0);                                  // multiple of 16
+    const uint32_t row_bytes = (uint32_t)nu_here * sizeof(float2);
+    const uint32_t stage_bytes = kBBRows * kBBU * sizeof(float2);
+    const int ngroups = (N2 + kBBRows - 1) / kBBRows;
+    const float2* Mk = M + kap * N2 * (long long)nu_pad + u0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kBBStages; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 8);   // the 8 compute warps
+        }
+        tc::mbar_fence_init();
+    }
+    for (int e = threadIdx.x; e < N2 * F; e += blockDim.x) {
+        const int bq = e / F, f = e - (e / F) * F;
+        rs[e] = R[f * r_fstride + kap * N2 + bq];
+    }
+    __syncthreads();
+    if (warp == 8) {
+        // ---- producer warp: rows of M into the ring ----
+        if (lane == 0)
+            for (int gi = 0; gi < ngroups; ++gi) {
+                const int s = gi % kBBStages;
+                if (gi >= kBBStages) tc::mbar_wait(&empty[s], ((gi / kBBStages) - 1) & 1);
+                const int nr = min(kBBRows, N2 - gi * kBBRows);
+                tc::mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                for (int q = 0; q < nr; ++q)
+                    tc::bulk_g2s(stage + (size_t)s * stage_bytes + (size_t)q * kBBU * sizeof(float2),
+                                 Mk + (long long)(gi * kBBRows + q) * nu_pad, row_bytes, &full[s]);
+            }
+        return;
+    }
+    float acc[F][8];
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[f][i] = 0.f;
+    const int v = threadIdx.x;   // units 4v .. 4v+3 of the tile
+    for (int gi = 0; gi < ngroups; ++gi) {
+        const int s = gi % kBBStages;
+        tc::mbar_wait(&full[s], (gi / kBBStages) & 1);
+        const f8* rows = reinterpret_cast<const f8*>(stage + (size_t)s * stage_bytes);
+        const int nr = min(kBBRows, N2 - gi * kBBRows);
+        if (4 * v < nu_here) {
+#pragma unroll
+            for (int q = 0; q < kBBRows; ++q) {
+                if (q < nr) {
+                    const f8 m = rows[q * (kBBU / 4) + v];
+                    const float2* rr = rs + (gi * kBBRows + q) * F;
+#pragma unroll
+                    for (int f = 0; f < F; ++f) cjmac4(m, rr[f], acc[f]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);   // this warp is done with slot s
+    }
+    if (4 * v < nu_here) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+            float4* o = reinterpret_cast<float4*>(Xh + f * x_fstride + kap * nu_pad + u0) + 2 * v;
+            o[0] = make_float4(acc[f][0], acc[f][1], acc[f][2], acc[f][3]);
+            o[1] = make_float4(acc[f][4], acc[f][5], acc[f][6], acc[f][7]);
+        }
+    }
 }
 
 cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_fstride, float2* Xh, long long x_fstride,
@@ -303,9 +495,22 @@ cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_f
     switch (F) {
         case 2: bwd_mac_batch_kernel<2><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
         case 4: bwd_mac_batch_kernel<4><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
-        case 8: bwd_mac_batch_kernel<8><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
-        case 16: bwd_mac_batch_kernel<16><<<grid, threads, smem, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad); break;
-        default: return cudaErrorInvalidValue;
+        default: break;
+    }
+    if (F == 2 || F == 4) return cudaGetLastError();
+    if (F != 8 && F != 16) return cudaErrorInvalidValue;
+    // F >= 8: staged kernel (fp32-ALU bound, rows streamed through shared memory)
+    const size_t ssm = (((size_t)N2 * F * sizeof(float2) + 127) & ~(size_t)127) + (size_t)kBBStages * kBBRows * kBBU * sizeof(float2);
+    const dim3 sgrid((nu_pad + kBBU - 1) / kBBU, nkappa);
+    cudaError_t e;
+    if (F == 8) {
+        e = cudaFuncSetAttribute(bwd_mac_batch_staged_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        if (e != cudaSuccess) return e;
+        bwd_mac_batch_staged_kernel<8><<<sgrid, 288, ssm, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad);
+    } else {
+        e = cudaFuncSetAttribute(bwd_mac_batch_staged_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        if (e != cudaSuccess) return e;
+        bwd_mac_batch_staged_kernel<16><<<sgrid, 288, ssm, s>>>(M, R, r_fstride, Xh, x_fstride, N2, nu_pad);
     }
     return cudaGetLastError();
 }

@@ -1510,14 +1510,19 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
             while (nxt[f] == cur[f] || nxt[f] == best[f]) ++nxt[f];
         if (ms_host) CK(cudaEventRecord(p->ev0, s));
         // ---- forward: coarse transforms per frame, one batched pass over M, inverse per frame ----
+        // (profile stages here are batch groups: r2c_x = all frames' transforms, fwd_mac = the batched pass,
+        //  c2r_yhat = per-frame inverse + direct planes + ratio transform, bwd_mac, c2r_update = per-frame rest)
+        ST(mark(p, ST_R2C_X, s));
         if (p->nu_fft > 0) {
             for (int f = 0; f < F; ++f)
                 if (!stopped[f])
                     CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                                   r2c_args(SRC_POLY, xbuf(f, cur[f]), nullptr, 0.f, p->nu_fft, p->bG + f * sG, p->nu_fft_pad), s));
+            ST(mark(p, ST_FWD_MAC, s));
             CK(launch_fwd_mac_batch(p->M, p->bG, sG, p->bY, sY, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
             p->pacc.launches += 1;
         }
+        ST(mark(p, ST_C2R_YHAT, s));
         for (int f = 0; f < F; ++f) {
             if (stopped[f]) continue;
             float* yimg = p->byhat + f * HW;
@@ -1548,10 +1553,15 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                               r2c_args(SRC_RATIO, y + f * HW, yimg, pol->eps, N2, p->bR + f * sY, N2), s));
         }
         // ---- backward: one batched pass over M^H, inverse + update per frame ----
+        ST(mark(p, ST_DIR_FWD, s));   // (empty stages: the batch groups above hold their work)
+        ST(mark(p, ST_ALLRED_SUM, s));
+        ST(mark(p, ST_R2C_RATIO, s));
+        ST(mark(p, ST_BWD_MAC, s));
         if (p->nu_fft > 0) {
             CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
             p->pacc.launches += 1;
         }
+        ST(mark(p, ST_C2R_UPD, s));
         for (int f = 0; f < F; ++f) {
             if (stopped[f]) continue;
             float* xo = xbuf(f, cur[f]);
@@ -1582,9 +1592,20 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                              p->met.nmem[ri], p->met.T1, p->met.rowsq, p->bent + 2 * f, s));
             p->pacc.launches += 4;
         }
+        ST(mark(p, ST_DIR_BWD, s));
+        ST(mark(p, ST_MAXPROJ, s));
+        ST(mark(p, ST_METRIC, s));
+        ST(mark(p, LFM_N_STAGES, s));
         if (ms_host) CK(cudaEventRecord(p->ev1, s));
         CK(cudaMemcpyAsync(p->bhost, p->bent, 2 * F * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (p->prof)
+            for (int st = 0; st < LFM_N_STAGES; ++st) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, p->pev[st], p->pev[st + 1]));
+                p->pacc.ms[st] += ms;
+                p->pacc.count[st] += 1;
+            }
         if (ms_host) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));

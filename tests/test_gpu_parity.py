@@ -471,7 +471,7 @@ def test_supplied_ht(flags):
         assert rel(a_d.cpu().numpy(), b_d.cpu().numpy().astype(np.float64)) <= 1e-6
 
 
-@pytest.mark.parametrize("name,F,flags", [("tiny", 4, 0), ("tiny", 2, 4), ("c2", 4, 4), ("s15", 8, 0)])
+@pytest.mark.parametrize("name,F,flags", [("tiny", 4, 0), ("tiny", 2, 4), ("c2", 4, 4), ("s15", 8, 0), ("c2", 16, 4), ("s15", 16, 4)])
 def test_batched_frames_match_single(name, F, flags):
     """f1: lockstep frame batching -- each frame's iterate, series, best and stop equal the single-frame plan's
     (and so the oracle's) within fp32 re-association (1e-5), in fixed and auto modes."""
