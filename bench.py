@@ -293,9 +293,15 @@ def run_ours(args):
         ex = info["tc_flops_executed"] / (t[kk] / 1e3) / 1e12
         al = info["tc_flops_algorithmic"] / (t[kk] / 1e3) / 1e12
         peak3 = tf32_sus / 3.0   # an fp32-accurate contraction on tf32 tensor cores costs 3 products (3xTF32)
+        tc_traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            for key, ent in json.load(open(tpath)).items():
+                if key.split("_")[0] == cfg.name and ent.get("fft_units") == info["fft_units"]:
+                    tc_traffic = ent.get("tcdir_" + kk.split("_")[1])
         roof_tc = {"bound": "tensor", "kernel": "tcdir_kernel (" + kk + " stage: staging + kernel + reduction)",
                    "achieved": al, "peak": peak3, "unit": "TFLOP/s", "frac": al / peak3,
-                   "traffic": None, "avg_launch_ms": t[kk],
+                   "traffic": tc_traffic, "avg_launch_ms": t[kk],
                    "algorithmic_flops_per_launch": info["tc_flops_algorithmic"],
                    "achieved_is": "algorithmic fp32 flops (SURVEY 8(d): 2*H*W*K(z)^2 non-zero taps per plane) / stage time",
                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32",

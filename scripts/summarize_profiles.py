@@ -1,0 +1,80 @@
+"""Dev: turn gpurun_out/{launches.csv, prof_final.ncu-rep, bench_final.json} into the committed profiles/ summaries.
+usage: python scripts/summarize_profiles.py <tag>     (writes profiles/<tag>_*.json|csv, updates profiles/ncu_traffic.json)"""
+import collections
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01_final"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = os.path.join(ROOT, "gpurun_out")
+P = os.path.join(ROOT, "profiles")
+
+# ---- launch list (ncu --metrics gpu__time_duration.sum, serialised) ----
+lines = [ln for ln in open(os.path.join(G, "launches.csv")) if not ln.startswith("==")]
+r = list(csv.reader(lines))
+h = r[0]
+ik, iv = h.index("Kernel Name"), h.index("Metric Value")
+tot, cnt = collections.OrderedDict(), collections.Counter()
+for row in r[1:]:
+    if len(row) <= iv:
+        continue
+    name = row[ik].split("(")[0].replace("void ", "").strip()
+    tot[name] = tot.get(name, 0.0) + float(row[iv].replace(",", ""))
+    cnt[name] += 1
+iters = cnt["lfm::metric_sum_kernel"] or cnt["lfm::metric_final_kernel"]
+per = {n: {"launches": cnt[n], "avg_ms": tot[n] / cnt[n] / 1e6} for n in tot}
+it_k = {n: v for n, v in per.items() if v["launches"] in (iters, iters + 1)}
+step = sum(v["avg_ms"] for v in it_k.values())
+order = sorted(it_k.items(), key=lambda kv: -kv[1]["avg_ms"])
+summ = {"command": "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-calls 1 (c3, default hybrid plan)",
+        "ncu": "--metrics gpu__time_duration.sum --clock-control none (serialised, cold-cache per launch)",
+        "rl_iterations_in_capture": iters,
+        "per_iteration_kernels_ms": {n: round(v["avg_ms"], 4) for n, v in order},
+        "per_iteration_kernel_sum_ms": round(step, 3),
+        "share_of_iteration": {n: round(v["avg_ms"] / step, 4) for n, v in order},
+        "all_kernels": per}
+json.dump(summ, open(os.path.join(P, f"{tag}_launch_summary.json"), "w"), indent=1)
+shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, f"{tag}_launches_bench_c3.csv"))
+
+# ---- ncu --set full of the dominant kernels ----
+raw = subprocess.run(["ncu", "-i", os.path.join(G, "prof_final.ncu-rep"), "--page", "raw", "--csv"],
+                     capture_output=True, text=True).stdout
+rr = list(csv.reader(raw.splitlines()))
+h, u = rr[0], dict(zip(rr[0], rr[1]))
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+out = []
+for row in rr[2:]:
+    d = dict(zip(h, row))
+    f = lambda k: float(d[k]) if d.get(k, "") not in ("", "n/a") else None
+    rb = f("dram__bytes_read.sum") * scale[u["dram__bytes_read.sum"]]
+    wb = f("dram__bytes_write.sum") * scale[u["dram__bytes_write.sum"]]
+    ms = f("gpu__time_duration.sum")
+    out.append({"kernel": d["Kernel Name"].split("(")[0], "ms": ms, "dram_read_bytes": rb, "dram_write_bytes": wb,
+                "dram_gbs": (rb + wb) / ms / 1e6, "gpu_dram_pct": f("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                "tensor_active_pct": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "lts_pct": f("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "grid": int(f("launch__grid_size")), "regs": int(f("launch__registers_per_thread"))})
+json.dump(out, open(os.path.join(P, f"{tag}_ncu_full.json"), "w"), indent=1)
+for e in out:
+    print(e)
+
+# ---- traffic per launch for the bench's roofline objects (same config and plan) ----
+bench = json.loads(open(os.path.join(G, "bench_final.json")).read().strip().splitlines()[-1])
+shutil.copy(os.path.join(G, "bench_final.json"), os.path.join(P, f"{tag}_bench.json"))
+fft_units = bench["config"]["hybrid"]["fft_units"]
+t = json.load(open(os.path.join(P, "ncu_traffic.json")))
+ent = {"fft_units": fft_units, "source": f"profiles/{tag}_ncu_full.json (ncu --set full, dram read + write bytes per launch)"}
+for e in out:
+    k = e["kernel"]
+    key = "fwd_mac" if k == "fwd_mac_kernel" else "bwd_mac" if k == "bwd_mac_kernel" else \
+        "tcdir_fwd" if "tcdir_kernel<1" in k else "tcdir_bwd" if "tcdir_kernel<0" in k else None
+    if key:
+        ent[key] = e["dram_read_bytes"] + e["dram_write_bytes"]
+t[f"c3_hybrid_{fft_units}"] = ent
+json.dump(t, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
+print(json.dumps(summ["share_of_iteration"], indent=0), step)
+print("bench:", bench["value"], bench["ms_per_step"], bench["roofline"]["frac"], bench["e2e"]["value"])

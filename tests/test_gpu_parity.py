@@ -128,34 +128,42 @@ def test_c2_operators_match_oracle(flags):
 def test_memory_aware_planning():
     """A capped device (lfm_set_memory_limit) makes the hybrid planner move planes off the frequency path until the
     transfer matrices fit; the operators still match the oracle.  An impossible cap fails with LFM_ENOMEM naming the
-    limiting term."""
+    limiting term.  PSF bank: two wide planes (per-pair tap box D = 13: the frequency path is faster, the tensor-core
+    taps need less memory than their transfer matrices) and two narrow ones (D = 1)."""
     L_ = L()
-    cfg = CONFIGS["c2"]   # BASELINE configs[1]: the cost model keeps about half of its planes on the frequency path
-    h = gen_psf(cfg, np.float32)
-    x = gen_volume(cfg, 1, np.float32)
+    N, H, W, K = 11, 319, 319, 143
+    rng = np.random.default_rng(11)
+    h = np.zeros((4, N, N, K, K), np.float32)
+    h[:2] = rng.uniform(0, 1, (2, N, N, K, K))
+    c = K // 2
+    h[2:, :, :, c - 5:c + 6, c - 5:c + 6] = rng.uniform(0, 1, (2, N, N, 11, 11))
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    x = rng.uniform(0, 1, (4, H, W)).astype(np.float32)
     try:
-        with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=L_.LFM_PLAN_FFT_ONLY) as full:
+        with L_.Plan(h, N, H, W, optics=optics(N)) as free:
+            assert free.info()["fft_units"] > 0
+        with L_.Plan(h, N, H, W, optics=optics(N), flags=L_.LFM_PLAN_FFT_ONLY) as full:
             m_all = full.info()["transfer_bytes"]
-        L_.lfm_set_memory_limit(int(0.45 * m_all) + (64 << 20))
-        with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        est, _ = L_.lfm_plan_estimate(N, 4, K, K, H, W)   # all-frequency-path estimate: transfer + the rest
+        L_.lfm_set_memory_limit(int(est - m_all + 0.45 * m_all))   # fits only after moving the wide planes
+        with L_.Plan(h, N, H, W, optics=optics(N)) as plan:
             info = plan.info()
             assert info["planes_moved_for_memory"] > 0
-            assert info["fft_units"] * cfg.nnum ** 2 < cfg.nz * cfg.nnum ** 4
             tol = op_tol(info)[0]
-            y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+            y_d = torch.zeros((H, W), device="cuda")
             plan.forward(dev(x), y_d)
             torch.cuda.synchronize()
             y_ref = O.forward_project(x.astype(np.float64), h.astype(np.float64))
             assert rel(y_d.cpu().numpy(), y_ref) <= tol
             r = (y_ref + 1.0) / (y_ref.mean() + 1.0)
-            xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            xb_d = torch.zeros((4, H, W), device="cuda")
             plan.backward(dev(r), xb_d)
             torch.cuda.synchronize()
         xb_ref = O.backward_project(r.astype(np.float32).astype(np.float64), h.astype(np.float64))
         assert rel(xb_d.cpu().numpy(), xb_ref) <= tol
         L_.lfm_set_memory_limit(1 << 20)
         with pytest.raises(L_.LfmError) as e:
-            L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum))
+            L_.Plan(h, N, H, W, optics=optics(N))
         assert "LFM_ENOMEM" in str(e.value) and "limiting term" in str(e.value)
     finally:
         L_.lfm_set_memory_limit(0)
