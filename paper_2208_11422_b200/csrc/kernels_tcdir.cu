@@ -274,31 +274,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int L = tile * 2 * kM + (int)rank * kM + r;
             const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp;
             if (m1 < d.nh && m2 < d.nw) {
-                const size_t HW = (size_t)d.H * d.W;
+                const size_t npix = (size_t)d.nh * d.nw;
                 const int z = d.zlist[zi];
+                const int n0 = half * Nh;
+                // polyphase destinations: column n is npix floats after column n-1 (coalesced across lanes)
+                const bool fast = FWD || DST == DST_UPDATE || DST == DST_ISRA || DST == DST_POLY;
+                const bool owned_all = z * d.N2 >= d.unit0 && (z + 1) * d.N2 <= d.unit0 + d.nu;
+                if (fast && (FWD || DST != DST_POLY || owned_all)) {
+                    float* p;
+                    if constexpr (FWD || DST == DST_UPDATE || DST == DST_ISRA)   // per-plane partial / H^T r scratch
+                        p = d.part + ((size_t)zi * d.N2 + n0) * npix + (size_t)m1 * d.nw + m2;
+                    else
+                        p = out + ((size_t)(z * d.N2 + n0 - d.unit0)) * npix + (size_t)m1 * d.nw + m2;
+                    if (owned_all || FWD) {
 #pragma unroll
-                for (int i0 = 0; i0 < kMaxNh; i0 += 8) {
-                    if (i0 < Nh) {
+                        for (int i = 0; i < kMaxNh; ++i)
+                            if (i < Nh && n0 + i < d.N2) p[(size_t)i * npix] = acc[i];
+                    } else {
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int n = half * Nh + i0 + u;
-                            if (i0 + u < Nh && n < d.N2) {
-                                const int n1 = n / d.N, n2 = n - (n / d.N) * d.N;
-                                if constexpr (FWD) {   // n = output phase b'
-                                    d.part[(size_t)zi * HW + (size_t)(n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i0 + u];
-                                } else {               // n = input phase a of plane z
-                                    const int uu = z * d.N2 + n;
-                                    if (uu >= d.unit0 && uu < d.unit0 + d.nu) {
-                                        const size_t pidx = ((size_t)(uu - d.unit0) * d.nh + m1) * d.nw + m2;
-                                        if constexpr (DST == DST_POLY)
-                                            out[pidx] = acc[i0 + u];
-                                        else if constexpr (DST == DST_VOLIMAGE)
-                                            out[((size_t)z * d.H + n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i0 + u];
-                                        else   // RL / ISRA: H^T r into the scratch, tc_update_kernel applies it
-                                            d.part[(((size_t)zi * d.N2 + n) * d.nh + m1) * d.nw + m2] = acc[i0 + u];
-                                    }
-                                }
-                            }
+                        for (int i = 0; i < kMaxNh; ++i) {
+                            const int uu = z * d.N2 + n0 + i;
+                            if (i < Nh && n0 + i < d.N2 && uu >= d.unit0 && uu < d.unit0 + d.nu) p[(size_t)i * npix] = acc[i];
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kMaxNh; ++i) {
+                        const int n = n0 + i;
+                        const int uu = z * d.N2 + n;
+                        if (i < Nh && n < d.N2 && uu >= d.unit0 && uu < d.unit0 + d.nu) {
+                            const int n1 = n / d.N, n2 = n - (n / d.N) * d.N;
+                            if constexpr (DST == DST_VOLIMAGE)
+                                out[((size_t)z * d.H + n1 + d.N * m1) * d.W + n2 + d.N * m2] = acc[i];
+                            else
+                                out[((size_t)(uu - d.unit0) * d.nh + m1) * d.nw + m2] = acc[i];
                         }
                     }
                 }
@@ -370,6 +379,31 @@ __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ T
         tc::split_tf32(tile[tx][rr], h, l);
         d.src[(slab_hi * d.Lp + L) * kKC + tx] = h;
         d.src[(slab_lo * d.Lp + L) * kKC + tx] = l;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// forward reduction: y (+)= sum_zi part[zi][b'][m] (plane order fixed -> deterministic), interleaved into the image
+// y[b1 + N m1][b2 + N m2].  One CTA per lenslet row m1: reads are contiguous along m2, the N image rows of the CTA
+// are written from shared memory.
+__global__ void __launch_bounds__(256) tc_fwd_reduce_kernel(const __grid_constant__ TcDirArgs d, float* __restrict__ y,
+                                                            int accumulate) {
+    extern __shared__ float accs[];   // [N][nw]: output phases (b1, 0..N-1) of lenslet row m1
+    const int m1 = blockIdx.x, b1 = blockIdx.y;
+    const size_t npix = (size_t)d.nh * d.nw;
+    const int per = d.N * d.nw;
+    for (int e = threadIdx.x; e < per; e += blockDim.x) {
+        const int b2 = e / d.nw, m2 = e - (e / d.nw) * d.nw;
+        const float* src = d.part + (size_t)(b1 * d.N + b2) * npix + (size_t)m1 * d.nw + m2;
+        float v = 0.0f;
+        for (int zi = 0; zi < d.nzd; ++zi) v += __ldcs(src + (size_t)zi * d.N2 * npix);
+        accs[e] = v;
+    }
+    __syncthreads();
+    float* o = y + (size_t)(b1 + d.N * m1) * d.W;
+    for (int t = threadIdx.x; t < d.W; t += blockDim.x) {
+        const float v = accs[(t % d.N) * d.nw + t / d.N];
+        o[t] = accumulate ? o[t] + v : v;
     }
 }
 
@@ -508,7 +542,8 @@ size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes)
 }
 size_t tcdir_src_floats(const TcDirArgs& d, int fwd) { return (size_t)(fwd ? 2 * d.nzd : 2) * d.nch * d.Lp * kKC; }
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd) {
-    return fwd ? (size_t)d.nzd * d.H * d.W : (size_t)d.nzd * d.N2 * d.nh * d.nw;
+    (void)fwd;   // forward: per-plane partials; backward: H^T r scratch -- both polyphase [nzd][N2][nh][nw]
+    return (size_t)d.nzd * d.N2 * d.nh * d.nw;
 }
 
 typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -632,7 +667,9 @@ cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, 
     if (e != cudaSuccess) return e;
     e = tcdir_main<true, 0>(d, nullptr, nullptr, 0.f, nullptr, s);
     if (e != cudaSuccess) return e;
-    return launch_plane_reduce(d.part, d.nzd, (size_t)d.H * d.W, y, accumulate, s);
+    const size_t rsm = (size_t)d.N * d.nw * sizeof(float);
+    tc_fwd_reduce_kernel<<<dim3(d.nh, d.N), 256, rsm, s>>>(d, y, accumulate);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,

@@ -125,8 +125,8 @@ struct TcDirArgs {
     int exp;                  // timing experiments only (env LFM_TC_EXP): 1 skip drains, 2 skip reloads, 4 counters
     long long* dbg;           // exp & 4: per-CTA wait-cycle counters [grid*2][8]
     float* src;               // staged source, slabs of [Lp][32] (hi / lo): fwd ((zi*2+part)*nch+c), bwd (part*nch+c)
-    float* part;              // forward: per-plane partial images [nzd][H][W]; backward: H^T r of the tensor-core
-                              // planes' units, polyphase [nzd][N2][nh][nw] (update epilogues apply it afterwards)
+    float* part;              // polyphase [nzd][N2][nh][nw]: forward per-plane partials (tc_fwd_reduce_kernel sums
+                              // and interleaves them), backward H^T r (update epilogues apply it afterwards)
     int chain_k;              // K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
     alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, Arows, 1}, SWIZZLE_128B
     alignas(64) CUtensorMap bmap;   // 3-D {32, Ntile, nslabs} over coef, box {32, Ntile/2, 1}, SWIZZLE_128B
