@@ -221,9 +221,7 @@ def run_ours(args):
     plan.rl_iterate(y_d, x_d, L.make_policy(mode="fixed", n_iters=args.warmup))
     torch.cuda.synchronize()
 
-    # timed region: exactly K iterations
-    plan.profile(True)
-    plan.profile_read(reset=True)
+    # timed region: exactly K iterations (no per-stage events: graph modes stay on)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -238,6 +236,11 @@ def run_ours(args):
     if dist:
         dist.barrier()
     clk = clocks.stop()
+    # per-stage breakdown (roofline launch times, stage shares): a separate profiled run of the same K iterations
+    plan.profile(True)
+    plan.profile_read(reset=True)
+    plan.rl_iterate(y_d, x_d, L.make_policy(mode="fixed", n_iters=args.steps, init_from_x=True))
+    torch.cuda.synchronize()
     prof = plan.profile_read(reset=True)
     plan.profile(False)
     ms = ev0.elapsed_time(ev1)

@@ -106,7 +106,11 @@ enum {
     LFM_PLAN_TC_DIRECT = 16,/* with LFM_PLAN_DIRECT: every plane on the tcgen05 3xTF32 kernel         */
     LFM_PLAN_GRAPHS = 32,   /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
                                non-default stream; not combined with lfm_profile timing)             */
-    LFM_PLAN_NO_TC = 64     /* hybrid without the tensor-core direct kernel                          */
+    LFM_PLAN_NO_TC = 64,    /* hybrid without the tensor-core direct kernel                          */
+    LFM_PLAN_DEVICE_LOOP = 128 /* lfm_rl_iterate runs the whole loop as one CUDA graph: a conditional WHILE
+                               node over two unrolled iterations, the stop rule and the argmax snapshot
+                               evaluated on the device -- no host round trip per iteration (
+                               needs a non-default stream; ms_host receives the per-iteration average) */
 };
 
 /* Information about a plan. */

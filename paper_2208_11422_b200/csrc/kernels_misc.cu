@@ -304,4 +304,70 @@ cudaError_t launch_ratio(const float* y, const float* yhat, float* r, size_t n, 
     return cudaGetLastError();
 }
 
+// ---- device-resident auto-stop loop (LFM_PLAN_DEVICE_LOOP) ----
+// The stop rule of lfm_rl_iterate (reading C15) evaluated on the device after each iteration: appends E_k to the
+// series, counts strict decreases, tracks the argmax (ties -> smallest k) and sets the WHILE / IF conditions of the
+// captured loop graph.  Same double comparisons as the host loop, so the decisions are identical.
+__global__ void loop_reset_kernel(LoopState* st) {
+    st->k = 0;
+    st->dec = 0;
+    st->best_k = 0;
+    st->stop = 0;
+    st->improved = 0;
+    st->prev = 0.0;
+    st->best_e = -INFINITY;
+}
+
+__global__ void stop_rule_kernel(LoopState* st, const double* __restrict__ e_dev, double* __restrict__ series, int mode,
+                                 int n_iters, int min_iters, int patience, int cap, cudaGraphConditionalHandle h_loop,
+                                 cudaGraphConditionalHandle h_second, int has_second) {
+    const int k = ++st->k;
+    const double e = e_dev[0];
+    series[k - 1] = e;
+    if (k > 1 && e < st->prev)
+        ++st->dec;
+    else
+        st->dec = 0;
+    st->prev = e;
+    st->improved = e > st->best_e;
+    if (st->improved) {
+        st->best_e = e;
+        st->best_k = k;
+    }
+    const bool stop = mode == LFM_MODE_FIXED ? k >= n_iters : ((k >= min_iters && st->dec >= patience) || k >= cap);
+    st->stop = stop;
+    cudaGraphSetConditional(h_loop, stop ? 0u : 1u);
+    if (has_second) cudaGraphSetConditional(h_second, stop ? 0u : 1u);
+}
+
+// x_best <- x when the last iteration improved E (grid-stride, float4 when aligned)
+__global__ void cond_copy_kernel(const LoopState* __restrict__ st, const float* __restrict__ src, float* __restrict__ dst,
+                                 size_t n) {
+    if (!st->improved) return;
+    const size_t n4 = n / 4;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) d4[i] = s4[i];
+    for (size_t i = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_loop_reset(LoopState* st, cudaStream_t s) {
+    loop_reset_kernel<<<1, 1, 0, s>>>(st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stop_rule(LoopState* st, const double* e_dev, double* series, const lfm_policy* pol, int cap,
+                             cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_second, int has_second,
+                             cudaStream_t s) {
+    stop_rule_kernel<<<1, 1, 0, s>>>(st, e_dev, series, pol->mode, pol->n_iters, pol->min_iters, pol->patience, cap,
+                                     h_loop, h_second, has_second);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cond_copy(const LoopState* st, const float* src, float* dst, size_t n, cudaStream_t s) {
+    cond_copy_kernel<<<592, 256, 0, s>>>(st, src, dst, n);
+    return cudaGetLastError();
+}
+
 }  // namespace lfm

@@ -257,6 +257,19 @@ struct lfm_plan_s {
     };
     std::vector<GraphKey> gkeys;
     std::vector<cudaGraphExec_t> gexec;
+    // device-resident auto-stop loop (LFM_PLAN_DEVICE_LOOP): one graph = WHILE node over two unrolled
+    // iterations (xb[0] -> xb[1] -> xb[0]), stop rule and argmax snapshot (into xb[2]) on the device
+    bool dloop = false;
+    struct LoopKey {
+        const float* y;
+        float eps;
+        int region, update, mode, n_iters, min_iters, patience, max_iters;
+    };
+    std::vector<LoopKey> lkeys;
+    std::vector<cudaGraphExec_t> lexec;
+    LoopState* lstate = nullptr;
+    double* lseries = nullptr;
+    int lseries_cap = 0;
     // frame-batched lockstep buffers (lfm_rl_iterate_batch), capacity bcap frames
     int bcap = 0;
     float2 *bG = nullptr, *bXh = nullptr, *bY = nullptr, *bR = nullptr;
@@ -296,6 +309,9 @@ inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
 void plan_free(lfm_plan p) {
     if (!p) return;
     for (cudaGraphExec_t g : p->gexec) cudaGraphExecDestroy(g);
+    for (cudaGraphExec_t g : p->lexec) cudaGraphExecDestroy(g);
+    cudaFree(p->lstate);
+    cudaFree(p->lseries);
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -569,6 +585,91 @@ lfm_status step_graph(lfm_plan p, const float* y, int cur, int nxt, const lfm_po
     return LFM_OK;
 }
 
+
+// one RL iteration xb[src] -> xb[dst] + device stop rule + argmax snapshot, captured into graph g
+lfm_status capture_half(lfm_plan p, cudaGraph_t g, const float* y, const lfm_policy* pol, int cap, int src, int dst,
+                        cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_second, int has_second,
+                        cudaStream_t s) {
+    const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
+    CK(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    lfm_status st = op_step(p, y, p->xb[src], p->xb[dst], pol->eps, pol->region, true, s, pol->update, p->hty);
+    cudaError_t ce = cudaSuccess;
+    if (st == LFM_OK) ce = launch_stop_rule(p->lstate, p->met.out, p->lseries, pol, cap, h_loop, h_second, has_second, s);
+    if (st == LFM_OK && ce == cudaSuccess) ce = launch_cond_copy(p->lstate, p->xb[dst], p->xb[2], vol, s);
+    cudaGraph_t out = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(s, &out);
+    if (st != LFM_OK) return st;
+    if (ce != cudaSuccess || ee != cudaSuccess)
+        return fail(LFM_ECUDA, "loop capture failed: %s", cudaGetErrorString(ce != cudaSuccess ? ce : ee));
+    return LFM_OK;
+}
+
+// the device-resident loop graph for (y, policy): WHILE(h) { it(0->1); IF(h2) { it(1->0) } }
+lfm_status loop_graph(lfm_plan p, const float* y, const lfm_policy* pol, int cap, cudaGraphExec_t* exec_out,
+                      cudaStream_t s) {
+    for (size_t i = 0; i < p->lkeys.size(); ++i) {
+        const auto& k = p->lkeys[i];
+        if (k.y == y && k.eps == pol->eps && k.region == pol->region && k.update == pol->update && k.mode == pol->mode &&
+            k.n_iters == pol->n_iters && k.min_iters == pol->min_iters && k.patience == pol->patience &&
+            k.max_iters == pol->max_iters) {
+            *exec_out = p->lexec[i];
+            return LFM_OK;
+        }
+    }
+    if (s == nullptr) return fail(LFM_EINVAL, "LFM_PLAN_DEVICE_LOOP needs a non-default stream (legacy stream cannot be captured)");
+    cudaGraph_t G = nullptr;
+    CK(cudaGraphCreate(&G, 0));
+    auto bail = [&](lfm_status st) {
+        cudaGraphDestroy(G);
+        return st;
+    };
+#define LG(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) return bail(fail(LFM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
+    } while (0)
+    cudaGraphConditionalHandle h_loop, h_second;
+    LG(cudaGraphConditionalHandleCreate(&h_loop, G, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    LG(cudaGraphAddNode(&wnode, G, nullptr, 0, &wp));
+    cudaGraph_t W = wp.conditional.phGraph_out[0];
+    LG(cudaGraphConditionalHandleCreate(&h_second, W, 0, cudaGraphCondAssignDefault));
+    cudaGraph_t A = nullptr;
+    LG(cudaGraphCreate(&A, 0));
+    lfm_status st = capture_half(p, A, y, pol, cap, 0, 1, h_loop, h_second, 1, s);
+    if (st != LFM_OK) {
+        cudaGraphDestroy(A);
+        return bail(st);
+    }
+    cudaGraphNode_t anode;
+    cudaError_t ae = cudaGraphAddChildGraphNode(&anode, W, nullptr, 0, A);
+    cudaGraphDestroy(A);
+    LG(ae);
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_second;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    LG(cudaGraphAddNode(&inode, W, &anode, 1, &ip));
+    st = capture_half(p, ip.conditional.phGraph_out[0], y, pol, cap, 1, 0, h_loop, h_second, 0, s);
+    if (st != LFM_OK) return bail(st);
+    cudaGraphExec_t exec = nullptr;
+    LG(cudaGraphInstantiate(&exec, G, 0));
+#undef LG
+    cudaGraphDestroy(G);
+    p->lkeys.push_back({y, pol->eps, pol->region, pol->update, pol->mode, pol->n_iters, pol->min_iters, pol->patience,
+                        pol->max_iters});
+    p->lexec.push_back(exec);
+    *exec_out = exec;
+    return LFM_OK;
+}
+
 lfm_status check_policy(const lfm_policy* pol) {
     if (!pol) return fail(LFM_EINVAL, "policy is NULL");
     if (pol->mode != LFM_MODE_FIXED && pol->mode != LFM_MODE_AUTO) return fail(LFM_EINVAL, "policy.mode=%d", pol->mode);
@@ -756,6 +857,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     } while (0)
     p->geo = g;
     p->graphs = (flags & LFM_PLAN_GRAPHS) != 0;
+    p->dloop = (flags & LFM_PLAN_DEVICE_LOOP) != 0;
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
@@ -1331,6 +1433,40 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         CK(launch_fill_dev(p->xb[cur], vol, p->stats, p->norm_sum, s));   // c0 = sum y / sum H^T 1
     }
     const int cap = pol->mode == LFM_MODE_FIXED ? pol->n_iters : pol->max_iters;
+    if (p->dloop && !p->prof) {
+        // device-resident loop: one graph launch, no host round trip per iteration
+        if (!p->lstate) ST(dalloc(p, &p->lstate, sizeof(LoopState), "loop state"));
+        if (p->lseries_cap < cap) {
+            cudaFree(p->lseries);
+            p->lseries = nullptr;
+            ST(dalloc(p, &p->lseries, (size_t)cap * sizeof(double), "loop series"));
+            p->lseries_cap = cap;
+            for (cudaGraphExec_t g : p->lexec) cudaGraphExecDestroy(g);   // captured the old series pointer
+            p->lexec.clear();
+            p->lkeys.clear();
+        }
+        cudaGraphExec_t exec = nullptr;
+        ST(loop_graph(p, y, pol, cap, &exec, s));
+        CK(launch_loop_reset(p->lstate, s));
+        if (ms_host) CK(cudaEventRecord(p->ev0, s));
+        CK(cudaGraphLaunch(exec, s));
+        if (ms_host) CK(cudaEventRecord(p->ev1, s));
+        LoopState hs;
+        CK(cudaMemcpyAsync(&hs, p->lstate, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(series_host, p->lseries, (size_t)hs.k * sizeof(double), cudaMemcpyDeviceToHost));
+        if (ms_host) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            for (int i = 0; i < hs.k; ++i) ms_host[i] = ms / hs.k;   // per-iteration average (one graph launch)
+        }
+        p->pacc.iterations += hs.k;
+        ST(gather_to_image(p, p->xb[2], x, s));
+        CK(cudaStreamSynchronize(s));
+        *best_iter = hs.best_k;
+        *stop_iter = hs.k;
+        return LFM_OK;
+    }
     double best_e = -INFINITY, prev = 0.0;
     int decreases = 0, k = 0, best_k = 0;
     for (;;) {

@@ -161,6 +161,17 @@ cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, floa
 cudaError_t launch_dir_bwd(const DirArgs& d, int src, const float* img, const float* img2, float eps, int dst, float* out,
                            const float* xold, const float* norm, cudaStream_t s);
 
+// device-resident auto-stop loop state (kernels_misc.cu, LFM_PLAN_DEVICE_LOOP)
+struct LoopState {
+    int k, dec, best_k, stop, improved;
+    double prev, best_e;
+};
+cudaError_t launch_loop_reset(LoopState* st, cudaStream_t s);
+cudaError_t launch_stop_rule(LoopState* st, const double* e_dev, double* series, const lfm_policy* pol, int cap,
+                             cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_second, int has_second,
+                             cudaStream_t s);
+cudaError_t launch_cond_copy(const LoopState* st, const float* src, float* dst, size_t n, cudaStream_t s);
+
 // launchers (kernels_fft.cu)
 cudaError_t launch_r2c(const XformGeom& g, const FftDesc& fh, const FftDesc& fw, const float2* tw_h,
                        const float2* tw_w, const R2CArgs& a, cudaStream_t s);

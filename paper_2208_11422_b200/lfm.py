@@ -28,6 +28,7 @@ LFM_MODE_FIXED, LFM_MODE_AUTO = 0, 1
 LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
+LFM_PLAN_DEVICE_LOOP = 128
 
 
 class LfmError(RuntimeError):

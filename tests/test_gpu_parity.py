@@ -521,3 +521,29 @@ def test_graph_replay_identical(name):
     (r0, x0), (r1, x1) = out[0], out[L().LFM_PLAN_GRAPHS]
     assert (r0["stop_iter"], r0["best_iter"]) == (r1["stop_iter"], r1["best_iter"])
     assert r0["series"] == r1["series"] and np.array_equal(x0, x1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,mode,update", [("tiny", "auto", "rl"), ("s15", "auto", "rl"), ("c2", "fixed", "rl"),
+                                              ("tiny", "auto", "isra")])
+def test_device_loop_identical(name, mode, update):
+    """f4: with LFM_PLAN_DEVICE_LOOP the whole auto-stop loop is one graph launch (conditional WHILE node, stop rule
+    and argmax snapshot on the device).  Same kernels in the same order as the host loop, so the series, the stop /
+    best iterations and the returned argmax volume are bit-identical."""
+    cfg, h, hd, y = tiny_problem(name, 2)
+    s = torch.cuda.Stream()
+    pol = L().make_policy(mode=mode, max_iters=30, n_iters=8, update=update)
+    out = {}
+    with torch.cuda.stream(s):
+        for flags in (0, L().LFM_PLAN_DEVICE_LOOP):
+            with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+                x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                for _ in range(2):   # second call replays the cached graph
+                    r = plan.rl_iterate(dev(y), x_d, pol, want_ms=True, stream=s)
+                    s.synchronize()
+                out[flags] = (r, x_d.cpu().numpy())
+    (r0, x0), (r1, x1) = out[0], out[L().LFM_PLAN_DEVICE_LOOP]
+    assert (r0["stop_iter"], r0["best_iter"]) == (r1["stop_iter"], r1["best_iter"])
+    assert r0["series"] == r1["series"] and np.array_equal(x0, x1)
+    if mode == "fixed":
+        assert r1["stop_iter"] == 8
