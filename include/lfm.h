@@ -107,6 +107,8 @@ enum {
     LFM_PLAN_GRAPHS = 32,   /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
                                non-default stream; not combined with lfm_profile timing)             */
     LFM_PLAN_NO_TC = 64,    /* hybrid without the tensor-core direct kernel                          */
+    LFM_PLAN_EVEN_SHARDS = 256, /* world > 1: split the units evenly (lfm_shard_units) instead of by the
+                               cost model (lfm_shard_units_balanced, the default)                     */
     LFM_PLAN_DEVICE_LOOP = 128 /* lfm_rl_iterate runs the whole loop as one CUDA graph: a conditional WHILE
                                node over two unrolled iterations, the stop rule and the argmax snapshot
                                evaluated on the device -- no host round trip per iteration (
@@ -152,6 +154,16 @@ lfm_status lfm_comm_unique_id(unsigned char* id_out);
  * nz*N*N units (z-major u = z*N*N + a*N + b); the first (nu mod world) ranks own one extra unit
  * (S:334's even split, refined from planes to (z,a) units). */
 lfm_status lfm_shard_units(int nz, int nnum, int world, int rank, int* unit_begin, int* unit_end);
+
+/* Host-only: the cost-balanced contiguous unit range of `rank` -- the ownership lfm_plan_create uses
+ * for world > 1 unless LFM_PLAN_EVEN_SHARDS.  From the FULL PSF (host, [nz][N][N][kh][kw]) every plane's path and
+ * per-iteration time are estimated with the hybrid cost model; frequency-path and CUDA-core
+ * planes may be cut between any two units, tensor-core planes only at plane borders (their cost does not shrink
+ * with the owned fraction).  Cuts are placed at the cost quantiles k/world.  `flags` as for lfm_plan_create
+ * (LFM_PLAN_EVEN_SHARDS returns the even split).  *est_seconds (nullable) receives the estimated per-iteration
+ * time of the returned range.  Deterministic: every rank computes the same partition. */
+lfm_status lfm_shard_units_balanced(const float* psf_host, int nnum, int nz, int kh, int kw, int height, int width,
+                                    int world, int rank, int flags, int* unit_begin, int* unit_end, double* est_seconds);
 
 /* Memory estimate before allocation (Fig. 1 "estimate the required memory size").
  * Writes the bytes one rank needs into *bytes_per_gpu (host).  If budget_bytes > 0 and the estimate

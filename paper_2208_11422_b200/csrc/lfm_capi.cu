@@ -213,6 +213,7 @@ struct lfm_plan_s {
     XformGeom xall{};   // every owned unit (layout conversion, max-projection, generic direct path)
     FftDesc fh{}, fw{};
     int rank = 0, world = 1;
+    std::vector<int> rcut;   // rank r owns units [rcut[r], rcut[r+1])
     bool comm = false, direct = false;
     ncclComm_t nccl = nullptr;
     int u0 = 0, u1 = 0, nu = 0, nu_pad = 0, nu_total = 0;
@@ -703,8 +704,7 @@ lfm_status gather_to_image(lfm_plan p, const float* xp_local, float* x, cudaStre
     const size_t per = (size_t)p->geo.nh * p->geo.nw;
     NK(ncclGroupStart());
     for (int r = 0; r < p->world; ++r) {
-        int b, e;
-        unit_range(p->nu_total, p->world, r, &b, &e);
+        const int b = p->rcut[r], e = p->rcut[r + 1];
         if (e <= b) continue;
         ncclResult_t rr = ncclBroadcast(r == p->rank ? (const void*)xp_local : nullptr, p->xfull + (size_t)b * per,
                                         (size_t)(e - b) * per, ncclFloat, r, p->nccl, s);
@@ -755,6 +755,105 @@ const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 
 constexpr double kTcEff = 0.68;
 constexpr double kTcFixed = 5e-6;
 constexpr double kSmClock = 1.965e9;
+
+// ---- cost-balanced sharding ----
+// Per plane, as if one rank owned all of it: the path the hybrid cost model picks and its time per iteration.
+// Frequency-path and CUDA-core planes cost in proportion to the units a rank owns; a tensor-core plane costs its
+// whole-plane time whatever fraction a rank owns (the kernel runs every phase), so it is never split.
+struct PlaneCost {
+    double t;
+    int atomic;
+};
+
+double tc_plane_time(const AxisBox& b1, const AxisBox& b2, const Geo& g, int N2, int num_sms) {
+    const int T1 = b1.dmax - b1.dmin + b1.D, T2 = b2.dmax - b2.dmin + b2.D;
+    const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 7) / 8;
+    const int ptiles = (g.nh * (g.nw + T2 - 1) + 255) / 256;
+    const double act = T1 >= 3 ? 1.0 - 1.0 / T1 : 1.0;   // edge tap rows: about half the chunks skipped
+    const double pair_cycles = (double)ptiles * T1 * T2 * act * ksteps * 3.0 * (Ntile / 2);
+    static const double tc_eff = getenv("LFM_TC_EFF") ? atof(getenv("LFM_TC_EFF")) : kTcEff;   // dev override
+    return 2.0 * pair_cycles / ((num_sms / 2) * kSmClock * tc_eff) + kTcFixed;
+}
+
+std::vector<PlaneCost> plane_costs(const float* psf, int nnum, const Geo& g, int flags, int num_sms) {
+    const int N2 = nnum * nnum, kh = g.kh, kw = g.kw;
+    const size_t kk = (size_t)kh * kw;
+    std::vector<PlaneCost> pc(g.nz);
+    for (int z = 0; z < g.nz; ++z) {
+        int k0 = kh, k1 = -1, j0 = kw, j1 = -1;
+        for (int a = 0; a < N2; ++a) {
+            const float* ker = psf + ((size_t)z * N2 + a) * kk;
+            for (int i = 0; i < kh; ++i)
+                for (int j = 0; j < kw; ++j)
+                    if (ker[(size_t)i * kw + j] != 0.0f) {
+                        k0 = std::min(k0, i);
+                        k1 = std::max(k1, i);
+                        j0 = std::min(j0, j);
+                        j1 = std::max(j1, j);
+                    }
+        }
+        if (k1 < 0) {
+            k0 = k1 = g.ch;
+            j0 = j1 = g.cw;
+        }
+        const AxisBox b1 = axis_box(nnum, g.ch, k0, k1), b2 = axis_box(nnum, g.cw, j0, j1);
+        const int D = std::max(b1.D, b2.D);
+        const int T2 = b2.dmax - b2.dmin + b2.D;
+        const double t_fft = 2.0 * N2 * N2 * (double)g.nkappa * 8.0 / kHbmBps + kXformPerUnit * N2;
+        const double t_dir = D <= kDirMaxD ? 2.0 * N2 * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
+        const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && round_up((size_t)N2, 16) <= 256 && T2 <= 65;
+        const double t_tc = tc_ok ? tc_plane_time(b1, b2, g, N2, num_sms) : 1e30;
+        int mode;
+        if (flags & LFM_PLAN_FFT_ONLY)
+            mode = 0;
+        else if (flags & LFM_PLAN_DIRECT)
+            mode = (flags & LFM_PLAN_TC_DIRECT) && tc_ok ? 2 : 1;
+        else {
+            const double best = std::min(t_fft, std::min(t_dir, t_tc));
+            mode = best == t_fft ? 0 : (best == t_tc ? 2 : 1);
+        }
+        pc[z].t = mode == 0 ? t_fft : (mode == 2 ? t_tc : (D <= kDirMaxD ? t_dir : t_fft));
+        pc[z].atomic = mode == 2;
+    }
+    return pc;
+}
+
+// contiguous unit ranges [cut[r], cut[r+1]) whose estimated costs are as equal as the cut granularity allows:
+// frequency-path / CUDA-core planes may be cut between any two units, tensor-core planes only at their borders
+std::vector<int> balanced_cuts(const std::vector<PlaneCost>& pc, int N2, int world) {
+    const int nz = (int)pc.size();
+    double total = 0;
+    for (const PlaneCost& c : pc) total += c.t;
+    std::vector<int> cut(world + 1, 0);
+    cut[world] = nz * N2;
+    for (int r = 1; r < world; ++r) {
+        const double target = total * r / world;
+        double pre = 0;
+        int u = nz * N2;
+        for (int z = 0; z < nz; ++z) {
+            if (pre + pc[z].t >= target) {
+                if (pc[z].atomic)
+                    u = (target - pre <= pre + pc[z].t - target) ? z * N2 : (z + 1) * N2;
+                else
+                    u = z * N2 + (int)std::lround((target - pre) / std::max(pc[z].t, 1e-30) * N2);
+                break;
+            }
+            pre += pc[z].t;
+        }
+        cut[r] = std::max(cut[r - 1], std::min(u, nz * N2));
+    }
+    return cut;
+}
+
+double range_cost(const std::vector<PlaneCost>& pc, int N2, int b, int e) {
+    double t = 0;
+    for (int z = 0; z < (int)pc.size(); ++z) {
+        const int lo = std::max(b, z * N2), hi = std::min(e, (z + 1) * N2);
+        if (hi <= lo) continue;
+        t += pc[z].atomic ? pc[z].t : pc[z].t * (hi - lo) / N2;
+    }
+    return t;
+}
 
 }  // namespace
 
@@ -861,14 +960,25 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
-    unit_range(p->nu_total, world, rank, &p->u0, &p->u1);
-    p->nu = p->u1 - p->u0;
-    p->nu_pad = (int)round_up((size_t)(p->nu > 0 ? p->nu : 1), 16);
     {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    // ownership: cost-balanced contiguous unit ranges (every rank computes all of them from the full PSF), or the
+    // even split with LFM_PLAN_EVEN_SHARDS
+    p->rcut.assign(world + 1, 0);
+    if (world > 1 && !(flags & LFM_PLAN_EVEN_SHARDS)) {
+        for (size_t i = 0, n = (size_t)p->nu_total * kh * kw; i < n; ++i)
+            if (!(psf_host[i] >= 0.0f)) return guard(fail(LFM_ENEG, "psf has a negative (or NaN) entry at unit %zu (S:192)", i / ((size_t)kh * kw)));
+        p->rcut = balanced_cuts(plane_costs(psf_host, nnum, g, flags, p->num_sms), nnum * nnum, world);
+    } else {
+        for (int r = 0; r < world; ++r) unit_range(p->nu_total, world, r, &p->rcut[r], &p->rcut[r + 1]);
+    }
+    p->u0 = p->rcut[rank];
+    p->u1 = p->rcut[rank + 1];
+    p->nu = p->u1 - p->u0;
+    p->nu_pad = (int)round_up((size_t)(p->nu > 0 ? p->nu : 1), 16);
     // PSF validation over the owned slice
     const size_t kk = (size_t)kh * kw;
     const float* psf_own = psf_host + (size_t)p->u0 * kk;
@@ -1013,8 +1123,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double act = T1 >= 3 ? 1.0 - 1.0 / T1 : 1.0;
         const double pair_cycles = (double)ptiles * T1 * T2 * act * ksteps * 3.0 * (Ntile / 2);
         static const double tc_eff = getenv("LFM_TC_EFF") ? atof(getenv("LFM_TC_EFF")) : kTcEff;   // dev override
-        const double t_tc = tc_ok ? 2.0 * pair_cycles / ((p->num_sms / 2) * kSmClock * tc_eff) * (units / N2) + kTcFixed
-                                  : 1e30;
+        (void)pair_cycles;
+        const double t_tc = tc_ok ? tc_plane_time(box1[z], box2[z], g, N2, p->num_sms) : 1e30;   // whole plane
         // device bytes per plane on each path (memory-aware planning below)
         pt_fft[z] = t_fft;
         pm_fft[z] = units * (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
@@ -1325,6 +1435,31 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     return LFM_OK;
 #undef PG
 #undef CKG
+}
+
+lfm_status lfm_shard_units_balanced(const float* psf_host, int nnum, int nz, int kh, int kw, int height, int width,
+                                    int world, int rank, int flags, int* unit_begin, int* unit_end, double* est_seconds) {
+    g_err[0] = 0;
+    if (!psf_host || !unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(LFM_EINVAL, "rank=%d world=%d", rank, world);
+    Geo g;
+    ST(make_geo(nnum, nz, kh, kw, height, width, /*direct=*/false, &g));
+    int num_sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();   // host-only use (no device): B200 defaults
+        num_sms = 148;
+    }
+    const std::vector<PlaneCost> pc = plane_costs(psf_host, nnum, g, flags, num_sms);
+    const int N2 = nnum * nnum;
+    std::vector<int> cut(world + 1, 0);
+    if (flags & LFM_PLAN_EVEN_SHARDS)
+        for (int r = 0; r < world; ++r) unit_range(nz * N2, world, r, &cut[r], &cut[r + 1]);
+    else
+        cut = balanced_cuts(pc, N2, world);
+    *unit_begin = cut[rank];
+    *unit_end = cut[rank + 1];
+    if (est_seconds) *est_seconds = range_cost(pc, N2, cut[rank], cut[rank + 1]);
+    return LFM_OK;
 }
 
 lfm_status lfm_set_memory_limit(size_t bytes) {

@@ -28,7 +28,7 @@ LFM_MODE_FIXED, LFM_MODE_AUTO = 0, 1
 LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
-LFM_PLAN_DEVICE_LOOP = 128
+LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS = 128, 256
 
 
 class LfmError(RuntimeError):
@@ -94,6 +94,8 @@ _lib_create = _sig("lfm_plan_create", _i, [ctypes.POINTER(_P), _P, _P, _i, _i, _
 _lib_info = _sig("lfm_plan_info", _i, [_P, ctypes.POINTER(lfm_info)])
 _lib_owned = _sig("lfm_plan_owned", _i, [_P, ctypes.POINTER(_i), ctypes.POINTER(_i)])
 _lib_memlimit = _sig("lfm_set_memory_limit", _i, [ctypes.c_size_t])
+_lib_shard_bal = _sig("lfm_shard_units_balanced", _i, [_P, _i, _i, _i, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_i),
+                                                      ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double)])
 _lib_destroy = _sig("lfm_plan_destroy", None, [_P])
 _lib_forward = _sig("lfm_forward", _i, [_P, _P, _P, _P])
 _lib_backward = _sig("lfm_backward", _i, [_P, _P, _P, _P])
@@ -120,7 +122,7 @@ _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
 EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
-            "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_set_memory_limit", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
+            "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_set_memory_limit", "lfm_shard_units_balanced", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
 
@@ -194,6 +196,16 @@ def lfm_comm_unique_id():
     buf = (ctypes.c_ubyte * 128)()
     _check(_lib_unique_id(buf))
     return bytes(buf)
+
+
+def lfm_shard_units_balanced(psf, nnum, height, width, world, rank, flags=0):
+    """(unit_begin, unit_end, est_seconds) of `rank` under the cost-balanced sharding (include/lfm.h)."""
+    psf = np.ascontiguousarray(psf, dtype=np.float32)
+    nz, kh, kw = psf.shape[0], psf.shape[3], psf.shape[4]
+    b, e, t = _i(), _i(), ctypes.c_double()
+    _check(_lib_shard_bal(psf.ctypes.data, nnum, nz, kh, kw, height, width, world, rank, flags, ctypes.byref(b),
+                          ctypes.byref(e), ctypes.byref(t)))
+    return b.value, e.value, t.value
 
 
 def lfm_set_memory_limit(nbytes):

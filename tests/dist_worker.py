@@ -1,5 +1,6 @@
 """World-size-N CPU (gloo) rehearsal of the sharded RL iteration the GPU path runs over NCCL
-(DESIGN.md §7): each rank owns the units lfm_shard_units() gives it, computes its partial forward
+(DESIGN.md §7): each rank owns the units the product's partition gives it (cost-balanced, as lfm_plan_create
+uses by default, or the even split with LFM_TEST_EVEN_SHARDS=1), computes its partial forward
 projection, C1 = allreduce(sum) of yhat, a local backward projection + update of its own units,
 C2 = allreduce(max) of its partial z max-projection, the metric on the reduced projection, and a
 final gather.  The arithmetic is the oracle's (this is test infrastructure); the partition and the
@@ -39,7 +40,10 @@ def main():
     h = gen_psf(cfg, np.float64)
     y = poisson(O.forward_project(gen_volume(cfg, 1), h), 101)
     nz, N, H, W = cfg.nz, cfg.nnum, cfg.height, cfg.width
-    u0, u1 = L.lfm_shard_units(nz, N, world, rank)
+    if os.environ.get("LFM_TEST_EVEN_SHARDS") == "1":
+        u0, u1 = L.lfm_shard_units(nz, N, world, rank)
+    else:
+        u0, u1, _ = L.lfm_shard_units_balanced(h.astype(np.float32), N, H, W, world, rank)
     zz, pp, qq = np.meshgrid(np.arange(nz), np.arange(H), np.arange(W), indexing="ij")
     unit = (zz * N + pp % N) * N + qq % N
     own = (unit >= u0) & (unit < u1)

@@ -18,11 +18,11 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_rl_gloo(world):
+@pytest.mark.parametrize("world,part", [(2, "balanced"), (3, "balanced"), (2, "even"), (3, "even")])
+def test_sharded_rl_gloo(world, part):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "dist_worker.py")]
-    env = dict(os.environ, OMP_NUM_THREADS="2")
+    env = dict(os.environ, OMP_NUM_THREADS="2", LFM_TEST_EVEN_SHARDS="1" if part == "even" else "0")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(" ok") == world

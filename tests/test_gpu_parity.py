@@ -292,7 +292,8 @@ def test_virtual_shards_partition():
         for rank in range(world):
             with L_.Plan(h, 3, 27, 27, optics=optics(3), rank=rank, world=world, flags=L_.LFM_PLAN_NO_COMM) as plan:
                 info = plan.info()
-                assert plan.owned() == L_.lfm_shard_units(4, 3, world, rank) == (info["unit_begin"], info["unit_end"])
+                assert plan.owned() == L_.lfm_shard_units_balanced(h, 3, 27, 27, world, rank)[:2] == (
+                    info["unit_begin"], info["unit_end"])
                 y_d = torch.zeros((27, 27), device="cuda")
                 plan.forward(dev(x), y_d)
                 xb_d = torch.full((4, 27, 27), -1.0, device="cuda")
