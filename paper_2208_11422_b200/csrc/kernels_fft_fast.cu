@@ -92,6 +92,7 @@ struct FastGeom {
     static constexpr int UBR = (int)((PER <= 50 * 1024 ? 100 * 1024 : 200 * 1024) / PER);
     static constexpr int UB = UBR > 8 ? 8 : (UBR < 1 ? 1 : UBR);
     static constexpr size_t SMEM = (size_t)(L + 1) * 8 + (size_t)UB * PER;
+    static constexpr size_t smem_for(int ub) { return (size_t)(L + 1) * 8 + (size_t)ub * PER; }
 };
 
 template <int SRC>
@@ -135,10 +136,11 @@ __device__ __forceinline__ float src_value(const XformGeom& g, const R2CArgs& a,
 
 }
 
-template <int L, int SRC>
+// UBV images per CTA (FastGeom<L>::UB by default; 1 when a launch has fewer transforms than would fill the chip)
+template <int L, int SRC, int UBV>
 __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g, const float2* __restrict__ twg, R2CArgs a) {
     using FG = FastGeom<L>;
-    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = FG::UB;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = UBV;
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);   // keep 16-byte alignment
@@ -232,10 +234,10 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g
     }
 }
 
-template <int L, int DST>
+template <int L, int DST, int UBV>
 __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g, const float2* __restrict__ twg, C2RArgs a) {
     using FG = FastGeom<L>;
-    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = FG::UB;
+    constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = UBV;
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);
@@ -326,53 +328,55 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
     }
 }
 
+template <int L, int SRC, int UBV>
+static cudaError_t r2c_fast_go(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s) {
+    const size_t smem = FastGeom<L>::smem_for(UBV);
+    cudaError_t e = cudaFuncSetAttribute(r2c_fast_kernel<L, SRC, UBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    r2c_fast_kernel<L, SRC, UBV><<<(unsigned)((a.ntrans + UBV - 1) / UBV), 512, smem, s>>>(g, tw, a);
+    return cudaGetLastError();
+}
+
+template <int L, int DST, int UBV>
+static cudaError_t c2r_fast_go(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s) {
+    const size_t smem = FastGeom<L>::smem_for(UBV);
+    cudaError_t e = cudaFuncSetAttribute(c2r_fast_kernel<L, DST, UBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    c2r_fast_kernel<L, DST, UBV><<<(unsigned)((a.ntrans + UBV - 1) / UBV), 512, smem, s>>>(g, tw, a);
+    return cudaGetLastError();
+}
+
+// one image per CTA when the default packing would leave most SMs idle (the N^2 output-phase transforms)
+constexpr int kFewTransforms = 2 * 148;
+
 template <int L>
 static cudaError_t r2c_fast_L(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s) {
-    const size_t smem = FastGeom<L>::SMEM;
     constexpr int UB = FastGeom<L>::UB;
-    const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
-    cudaError_t e = cudaSuccess;
-#define LFM_FAST_R2C(SRCV)                                                                               \
-    case SRCV:                                                                                           \
-        e = cudaFuncSetAttribute(r2c_fast_kernel<L, SRCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e != cudaSuccess) return e;                                                                  \
-        r2c_fast_kernel<L, SRCV><<<grid, 512, smem, s>>>(g, tw, a);                                  \
-        break;
+    const bool few = UB > 1 && (a.ntrans + UB - 1) / UB < kFewTransforms;
     switch (a.src) {
-        LFM_FAST_R2C(SRC_POLY)
-        LFM_FAST_R2C(SRC_IMAGE)
-        LFM_FAST_R2C(SRC_RATIO)
-        LFM_FAST_R2C(SRC_ONES)
-        LFM_FAST_R2C(SRC_KERNEL)
-        LFM_FAST_R2C(SRC_IMAGE2D)
+        case SRC_POLY: return r2c_fast_go<L, SRC_POLY, UB>(g, tw, a, s);
+        case SRC_IMAGE: return r2c_fast_go<L, SRC_IMAGE, UB>(g, tw, a, s);
+        case SRC_KERNEL: return r2c_fast_go<L, SRC_KERNEL, UB>(g, tw, a, s);
+        case SRC_RATIO: return few ? r2c_fast_go<L, SRC_RATIO, 1>(g, tw, a, s) : r2c_fast_go<L, SRC_RATIO, UB>(g, tw, a, s);
+        case SRC_ONES: return few ? r2c_fast_go<L, SRC_ONES, 1>(g, tw, a, s) : r2c_fast_go<L, SRC_ONES, UB>(g, tw, a, s);
+        case SRC_IMAGE2D:
+            return few ? r2c_fast_go<L, SRC_IMAGE2D, 1>(g, tw, a, s) : r2c_fast_go<L, SRC_IMAGE2D, UB>(g, tw, a, s);
         default: return cudaErrorInvalidValue;
     }
-#undef LFM_FAST_R2C
-    return cudaGetLastError();
 }
 
 template <int L>
 static cudaError_t c2r_fast_L(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s) {
-    const size_t smem = FastGeom<L>::SMEM;
     constexpr int UB = FastGeom<L>::UB;
-    const unsigned grid = (unsigned)((a.ntrans + UB - 1) / UB);
-    cudaError_t e = cudaSuccess;
-#define LFM_FAST_C2R(DSTV)                                                                               \
-    case DSTV:                                                                                           \
-        e = cudaFuncSetAttribute(c2r_fast_kernel<L, DSTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e != cudaSuccess) return e;                                                                  \
-        c2r_fast_kernel<L, DSTV><<<grid, 512, smem, s>>>(g, tw, a);                                  \
-        break;
+    const bool few = UB > 1 && (a.ntrans + UB - 1) / UB < kFewTransforms;
     switch (a.dst) {
-        LFM_FAST_C2R(DST_IMAGE)
-        LFM_FAST_C2R(DST_POLY)
-        LFM_FAST_C2R(DST_VOLIMAGE)
-        LFM_FAST_C2R(DST_UPDATE)
-        LFM_FAST_C2R(DST_ISRA)
+        case DST_IMAGE: return few ? c2r_fast_go<L, DST_IMAGE, 1>(g, tw, a, s) : c2r_fast_go<L, DST_IMAGE, UB>(g, tw, a, s);
+        case DST_POLY: return c2r_fast_go<L, DST_POLY, UB>(g, tw, a, s);
+        case DST_VOLIMAGE: return c2r_fast_go<L, DST_VOLIMAGE, UB>(g, tw, a, s);
+        case DST_UPDATE: return c2r_fast_go<L, DST_UPDATE, UB>(g, tw, a, s);
+        case DST_ISRA: return c2r_fast_go<L, DST_ISRA, UB>(g, tw, a, s);
         default: return cudaErrorInvalidValue;
     }
-#undef LFM_FAST_C2R
-    return cudaGetLastError();
 }
 
 bool fast_fft_size(int Lh, int Lw) {
