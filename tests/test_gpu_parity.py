@@ -435,6 +435,42 @@ def test_c3_one_rl_step_sampled(c3_plan):
     assert e > 0
 
 
+@pytest.mark.parametrize("flags", [0, 18], ids=["hybrid", "all-tc"])
+def test_c4_geometry_sampled(flags):
+    """Maximum sizes: the c4 geometry (Nnum 15, 2025^2 image, K = 225) with 6 planes whose per-pair tap boxes span
+    D = 3 / 9 / 15 -- on the tensor-core path a 17 x 17 union box (289 taps) over 135 x 151 coarse pixels.  Forward at
+    64 sampled pixels and backward at 64 sampled voxels against the oracle's one-output evaluators."""
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS["c4"], name="c4_6", nz=6)
+    h = gen_psf(cfg, np.float32)
+    hd = h.astype(np.float64)
+    H, W = cfg.height, cfg.width
+    rng = np.random.default_rng(4)
+    x = rng.uniform(0, 1, (cfg.nz, H, W)).astype(np.float32)
+    with L().Plan(h, cfg.nnum, H, W, optics=optics(cfg.nnum), flags=flags) as plan:
+        info = plan.info()
+        if flags == 18:
+            assert info["tc_planes"] == cfg.nz
+        y_d = torch.zeros((H, W), device="cuda")
+        plan.forward(dev(x), y_d)
+        torch.cuda.synchronize()
+        yg = y_d.cpu().numpy()
+        s = np.concatenate([[0, 0, H - 1, H - 1, 7, H // 2], rng.integers(0, H, 58)])
+        t = np.concatenate([[0, W - 1, 0, W - 1, W // 2, 3], rng.integers(0, W, 58)])
+        ref = O.forward_points(x.astype(np.float64), hd, s, t)
+        assert np.abs(yg[s, t] - ref).max() <= 1e-5 * np.abs(yg).max()
+        r = rng.uniform(0.5, 1.5, (H, W)).astype(np.float32)
+        xb_d = torch.zeros((cfg.nz, H, W), device="cuda")
+        plan.backward(dev(r), xb_d)
+        torch.cuda.synchronize()
+    z = np.concatenate([[0, cfg.nz - 1, 2, 3], rng.integers(0, cfg.nz, 60)])
+    p = np.concatenate([[0, H - 1, 1000, 14], rng.integers(0, H, 60)])
+    q = np.concatenate([[0, W - 1, 1001, 2024], rng.integers(0, W, 60)])
+    refb = O.backward_points(r.astype(np.float64), hd, z, p, q)
+    got = xb_d[torch.from_numpy(z).cuda(), torch.from_numpy(p).cuda(), torch.from_numpy(q).cuda()].cpu().numpy()
+    assert np.abs(got - refb).max() <= 1e-5 * np.abs(refb).max()
+
+
 @pytest.mark.parametrize("flags", [0, 2, 4, 18], ids=["hybrid", "direct", "fft", "direct-tc"])
 def test_isra_matches_oracle(flags):
     """MATLAB-lineage ISRA update x * H^T y / H^T H x from x0 = H^T y; 1 and 10 iterations."""
