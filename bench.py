@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-calls", type=int, default=2, help="timed lfm_deconvolve_host calls (after one untimed "
                     "warm-up call that allocates the staging buffers)")
-    ap.add_argument("--cpu-rows", type=int, default=96, help="rows of the oracle's bounded CPU sample")
+    ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the oracle's bounded CPU sample (~10-30 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="lfm_plan_create flags (2 = direct path)")
     ap.add_argument("--frames", type=int, default=8, help="c5: frames per lockstep batch (2/4/8/16)")
@@ -310,6 +310,9 @@ def run_ours(args):
                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32",
                    "executed_tensor_tflops": ex, "executed_frac_of_tf32_peak": ex / tf32_sus,
                    "executed_frac_of_tf32_burst_peak": ex / tf32_burst,
+                   "peak_note": "the sustained bf16 GEMM of MEASURED_PEAKS ran power-capped (median "
+                                f"{pk.get('clocks_under_load', {}).get('sm_mhz_median', 'n/a')} MHz); this step's "
+                                "clocks are in 'clocks' -- compare executed_frac_of_tf32_burst_peak too",
                    "executed_is": "issued tcgen05 flops (3 TF32 products over the union tap boxes, skipped windows excluded)",
                    "tc_planes": info["tc_planes"], "stage_ms": t}
     # the dominant kernel (longest average launch) carries the primary roofline
