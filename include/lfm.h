@@ -107,6 +107,8 @@ enum {
     LFM_PLAN_GRAPHS = 32,   /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
                                non-default stream; not combined with lfm_profile timing)             */
     LFM_PLAN_NO_TC = 64,    /* hybrid without the tensor-core direct kernel                          */
+    LFM_PLAN_FORCE_COMM = 512, /* create the NCCL communicator even for world = 1 (dist->nccl_id required):
+                               every collective of the sharded path runs, over one rank (testing)    */
     LFM_PLAN_EVEN_SHARDS = 256, /* world > 1: split the units evenly (lfm_shard_units) instead of by the
                                cost model (lfm_shard_units_balanced, the default)                     */
     LFM_PLAN_DEVICE_LOOP = 128 /* lfm_rl_iterate runs the whole loop as one CUDA graph: a conditional WHILE

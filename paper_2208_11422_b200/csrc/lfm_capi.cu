@@ -1024,7 +1024,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                               "limiting term: %s (%zu bytes)", nonM_bytes, mem_budget, names[best], vals[best]));
         }
     }
-    if (world > 1 && !(flags & LFM_PLAN_NO_COMM)) {
+    if ((world > 1 && !(flags & LFM_PLAN_NO_COMM)) || (flags & LFM_PLAN_FORCE_COMM)) {
+        if (!dist) return guard(fail(LFM_EINVAL, "LFM_PLAN_FORCE_COMM needs an lfm_dist with an NCCL unique id"));
         ncclUniqueId id;
         memcpy(&id, dist->nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&p->nccl, world, id, rank);

@@ -28,7 +28,7 @@ LFM_MODE_FIXED, LFM_MODE_AUTO = 0, 1
 LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
-LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS = 128, 256
+LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS, LFM_PLAN_FORCE_COMM = 128, 256, 512
 
 
 class LfmError(RuntimeError):
@@ -240,7 +240,7 @@ class Plan:
         nz, _, _, kh, kw = psf.shape
         self.nz, self.nnum, self.kh, self.kw, self.height, self.width = nz, nnum, kh, kw, height, width
         dist = None
-        if world > 1 or rank:
+        if world > 1 or rank or nccl_id is not None:
             dist = lfm_dist()
             dist.rank, dist.world = rank, world
             if nccl_id is not None:

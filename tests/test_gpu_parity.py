@@ -584,3 +584,34 @@ def test_device_loop_identical(name, mode, update):
     assert r0["series"] == r1["series"] and np.array_equal(x0, x1)
     if mode == "fixed":
         assert r1["stop_iter"] == 8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [0, 32, 128], ids=["eager", "graphs", "device-loop"])
+def test_nccl_one_rank_identical(extra):
+    """The sharded path's collectives executed for real over a one-rank NCCL communicator (LFM_PLAN_FORCE_COMM):
+    communicator init from lfm_comm_unique_id, allreduce(sum) of yhat, allreduce(max) of the max-projection, the
+    broadcast-gather of x_best -- eagerly, inside captured graphs and inside the conditional device loop.  Over one
+    rank every collective is an identity, so results are bit-identical to the plan without a communicator."""
+    L_ = L()
+    cfg, h, hd, y = tiny_problem("c2", 3)
+    s = torch.cuda.Stream()
+    pol = L_.make_policy(mode="auto", max_iters=20)
+    out = {}
+    with torch.cuda.stream(s):
+        for force in (False, True):
+            kw = dict(nccl_id=L_.lfm_comm_unique_id(), flags=extra | L_.LFM_PLAN_FORCE_COMM) if force else dict(flags=extra)
+            with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), stream=s, **kw) as plan:
+                x = gen_volume(cfg, 2, np.float32)
+                yh = torch.zeros((cfg.height, cfg.width), device="cuda")
+                plan.forward(dev(x), yh, stream=s)
+                xb = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                plan.backward(dev(y.astype(np.float32)), xb, stream=s)
+                x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                r = plan.rl_iterate(dev(y), x_d, pol, stream=s)
+                s.synchronize()
+                out[force] = (yh.cpu().numpy(), xb.cpu().numpy(), r, x_d.cpu().numpy())
+    a, b = out[False], out[True]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert (a[2]["stop_iter"], a[2]["best_iter"], a[2]["series"]) == (b[2]["stop_iter"], b[2]["best_iter"], b[2]["series"])
+    assert np.array_equal(a[3], b[3])
