@@ -1,0 +1,280 @@
+// kernels_mac_tc.cu -- frame-batched forward MAC on the 5th-generation tensor cores ("FP32 SIMT first,
+// then tcgen05 3xTF32").
+//
+// Per coarse frequency kappa the batched forward projection is a complex GEMM over the frequency-path units u:
+//   Y_f[kappa][b'] = sum_u M[kappa][b'][u] G_f[kappa][u]          (F frames)
+// written as a real GEMM over K = (u, re/im) interleaved, which is exactly M's memory layout [b'][u] complex:
+//   D[b'][n] = sum_k A[b'][k] B[n][k],   A = M[kappa] viewed as real (K-major, streamed by TMA),
+//   B rows n = 2f   : ( Gr(u0), -Gi(u0), Gr(u1), -Gi(u1), ...)  -> D[b'][2f]   = Re Y_f[b']
+//   B rows n = 2f+1 : ( Gi(u0),  Gr(u0), Gi(u1),  Gr(u1), ...)  -> D[b'][2f+1] = Im Y_f[b']
+// 3xTF32: A_hi is the raw fp32 tile (the tensor core truncates it to TF32 = hi), A_lo = rna_tf32(a - hi) is written
+// next to it by SIMT warps; B_hi and B_lo (rna splits) are stacked in one tile of 4F rows, so one MMA with N = 4F
+// gives A_hi·B_hi | A_hi·B_lo and a second with N = 2F (the B_hi half) gives A_lo·B_hi.  The three column blocks are
+// summed by the drainers in fp32 with round-to-nearest after every 16 K-steps (tcgen05 accumulation truncates).
+//
+// CTA = (kappa, half of the output phases): M = 128 rows b' in [128 h, 128 h + 128) (rows >= N^2 are TMA zero fill).
+// Warp roles: 0 TMA producer, 1-8 prep (A_lo + B build), 9 MMA issuer (one thread), 10-13 drainers / epilogue.
+#include <algorithm>
+
+#include "lfm_internal.cuh"
+#include "tc_sm100.cuh"
+
+namespace lfm {
+
+namespace {
+constexpr int kMtM = 128;                 // rows (output phases) per CTA
+constexpr int kMtKC = 32;                 // K floats per chunk (16 complex units, one 128-byte swizzle row)
+constexpr int kMtChain = 4;               // chunks (x 4 K-steps) per drain group
+constexpr int kMtThreads = 448;           // 1 producer + 8 prep + 1 MMA + 4 drainer warps
+constexpr int kMtPrep = 8;
+constexpr uint32_t kMtATile = kMtM * kMtKC * 4;   // 16 KB
+
+__host__ __device__ inline uint32_t mt_round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
+__host__ __device__ inline uint32_t mt_btile(int F) { return mt_round1k((uint32_t)(4 * F) * kMtKC * 4); }
+__host__ __device__ inline uint32_t mt_gtile(int F) { return (uint32_t)F * kMtKC * 4; }   // F rows of 128 B
+__host__ __device__ inline uint32_t mt_stage(int F) { return 2 * kMtATile + mt_btile(F) + mt_round1k(mt_gtile(F)); }
+__host__ __device__ inline int mt_stages(int F) { return F >= 32 ? 4 : 5; }
+}  // namespace
+
+size_t mac_tc_smem_bytes(int F) { return (size_t)mt_stages(F) * mt_stage(F) + 1024; }
+
+template <int F>
+__global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_constant__ MacTcArgs d) {
+    constexpr int S = F >= 32 ? 4 : 5;
+    constexpr int NB = 4 * F;       // rows of the stacked B tile (B_hi: 0..2F-1, B_lo: 2F..4F-1)
+    constexpr int NSET = 6 * F;     // TMEM columns per accumulator set: hi*hi | hi*lo | lo*hi
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar_fullA[S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
+    __shared__ uint32_t tmem_base;
+    const uint32_t raw = tc::smem_u32(smem_raw);
+    unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sbytes = mt_stage(F);
+    const int nitems = 2 * d.nkappa;
+    const int nchunks = 2 * d.nu_pad / kMtKC;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            tc::mbar_init(&bar_fullA[i], 1);
+            tc::mbar_init(&bar_ready[i], kMtPrep);
+            tc::mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bar_acc[i], 1);
+            tc::mbar_init(&bar_tfree[i], 4);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&d.tmapM);
+        tc::tma_prefetch_desc(&d.tmapG);
+    }
+    if (warp == 0) tc::tmem_alloc(&tmem_base, 2 * NSET <= 256 ? 256 : 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- producer: A tiles (rows b' of M[kappa], 32 K floats) ----
+            int it = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                const int kap = item >> 1, h = item & 1;
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = it % S;
+                    if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
+                    unsigned char* st = smem + (size_t)s * sbytes;
+                    tc::mbar_arrive_expect_tx(&bar_fullA[s], kMtATile + mt_gtile(F));
+                    tc::tma_load_3d(st, &d.tmapM, c * kMtKC, h * kMtM, kap, &bar_fullA[s]);
+                    // the frames' G for this chunk: F rows of 16 complex units (plain row-major)
+                    tc::tma_load_3d(st + 2 * kMtATile + mt_btile(F), &d.tmapG,
+                                    (int)((long long)kap * 2 * d.nu_pad % d.gsplit) + c * kMtKC,
+                                    (int)((long long)kap * 2 * d.nu_pad / d.gsplit), 0, &bar_fullA[s]);
+                }
+            }
+        }
+    } else if (warp <= kMtPrep) {
+        // ---- prep warps: A_lo = rna_tf32(a - trunc_tf32(a)); stacked B_hi | B_lo from the frames' G ----
+        constexpr int NP = 32 * kMtPrep;                 // prep threads
+        constexpr int NA = (int)(kMtATile / 16) / NP;    // float4 of the A tile per thread
+        constexpr int NE = (2 * F * kMtKC) / NP;         // B elements per thread (per stacked half)
+        const int pt = threadIdx.x - 32;
+        int it = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            for (int c = 0; c < nchunks; ++c, ++it) {
+                const int s = it % S;
+                tc::mbar_wait(&bar_fullA[s], (it / S) & 1);
+                unsigned char* st = smem + (size_t)s * sbytes;
+                const float4* ahi = reinterpret_cast<const float4*>(st);
+                float4* alo = reinterpret_cast<float4*>(st + kMtATile);
+                unsigned char* bt = st + 2 * kMtATile;
+                const float2* gt = reinterpret_cast<const float2*>(bt + mt_btile(F));   // [F][16] complex
+                float4 a[NA];
+                float2 gv[NE];
+#pragma unroll
+                for (int i = 0; i < NA; ++i) a[i] = ahi[pt + NP * i];   // loads first (ILP)
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                    const int e = pt + NP * i, n = e / kMtKC, k = e - (e / kMtKC) * kMtKC;
+                    gv[i] = gt[(n >> 1) * (kMtKC / 2) + (k >> 1)];
+                }
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {   // elementwise: the swizzle is irrelevant
+                    float4 l;
+                    l.x = tc::tf32_lo_of_trunc(a[i].x);
+                    l.y = tc::tf32_lo_of_trunc(a[i].y);
+                    l.z = tc::tf32_lo_of_trunc(a[i].z);
+                    l.w = tc::tf32_lo_of_trunc(a[i].w);
+                    alo[pt + NP * i] = l;
+                }
+                // B element (n, k), n < 2F: frame f = n / 2, unit j = k / 2 of the chunk, component k & 1
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                    const int e = pt + NP * i, n = e / kMtKC, k = e - (e / kMtKC) * kMtKC;
+                    const float2 g = gv[i];
+                    const float v = (n & 1) == 0 ? ((k & 1) ? -g.y : g.x) : ((k & 1) ? g.x : g.y);
+                    float hi, lo;
+                    tc::split_tf32(v, hi, lo);
+                    *reinterpret_cast<float*>(bt + tc::sw128_off(n, k)) = hi;
+                    *reinterpret_cast<float*>(bt + tc::sw128_off(2 * F + n, k)) = lo;
+                }
+                tc::fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_ready[s]);
+            }
+        }
+    } else if (warp == kMtPrep + 1) {
+        if (lane == 0) {   // ---- MMA issuer ----
+            const uint32_t id1 = tc::idesc_tf32(kMtM, NB), id2 = tc::idesc_tf32(kMtM, 2 * F);
+            int it = 0, g = 0, gk = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = it % S, j = g & 1;
+                    tc::mbar_wait(&bar_ready[s], (it / S) & 1);
+                    if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
+                    tc::fence_after();
+                    const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * sbytes), a_lo = a_hi + kMtATile;
+                    const uint32_t b = a_hi + 2 * kMtATile;
+                    const uint32_t acc = tmem + (uint32_t)(j * NSET);
+                    for (int k = 0; k < kMtKC / 8; ++k) {
+                        const uint64_t ah = tc::sdesc_sw128(a_hi + 32 * k), al = tc::sdesc_sw128(a_lo + 32 * k);
+                        const uint64_t bd = tc::sdesc_sw128(b + 32 * k);
+                        tc::mma_tf32(acc, ah, bd, id1, (gk == 0 && k == 0) ? 0u : 1u);                 // hi*hi | hi*lo
+                        tc::mma_tf32(acc + 4 * F, al, bd, id2, (gk == 0 && k == 0) ? 0u : 1u);         // lo*hi
+                    }
+                    tc::mma_commit(&bar_empty[s]);
+                    if (++gk == kMtChain || c == nchunks - 1) {
+                        tc::mma_commit(&bar_acc[j]);
+                        ++g;
+                        gk = 0;
+                    }
+                }
+            }
+        }
+    } else {
+        // ---- drainers: TMEM -> fp32 running sums (2F per thread), epilogue ----
+        const int q = warp & 3;   // warps 10-13: lane quarters 2, 3, 0, 1
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+        float acc[2 * F];
+#pragma unroll
+        for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        int g = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            const int kap = item >> 1, h = item & 1;
+            for (int c0 = 0; c0 < nchunks; c0 += kMtChain) {
+                const int j = g & 1;
+                tc::mbar_wait(&bar_acc[j], (g >> 1) & 1);
+                ++g;
+                tc::fence_after();
+                const uint32_t base = lane_base + (uint32_t)(j * NSET);
+#pragma unroll
+                for (int b0 = 0; b0 < 3; ++b0) {   // column blocks hi*hi, hi*lo, lo*hi (2F columns each)
+#pragma unroll
+                    for (int c8 = 0; c8 < 2 * F; c8 += 8) {
+                        uint32_t v[8];
+                        tc::tmem_ld8_nowait(base + (uint32_t)(b0 * 2 * F + c8), v);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[c8 + u] += __uint_as_float(v[u]);
+                    }
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_tfree[j]);
+            }
+            const int row = h * kMtM + 32 * q + lane;
+            if (row < d.N2) {
+#pragma unroll
+                for (int f = 0; f < F; ++f)
+                    d.Y[(long long)f * d.y_fstride + (long long)kap * d.N2 + row] = make_float2(acc[2 * f], acc[2 * f + 1]);
+            }
+#pragma unroll
+            for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * NSET <= 256 ? 256 : 512);
+}
+
+typedef CUresult (*MtEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t mac_tc_encode(MacTcArgs* d, const float2* M) {
+    static MtEncodeFn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !enc || q != cudaDriverEntryPointSuccess) {
+            enc = nullptr;
+            return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+        }
+    }
+    // M as real floats [kappa][N2][2 * nu_pad]; box {32 floats, 128 rows, 1}; rows >= N2 are zero fill
+    cuuint64_t dims[3] = {(cuuint64_t)2 * d->nu_pad, (cuuint64_t)d->N2, (cuuint64_t)d->nkappa};
+    cuuint64_t strides[2] = {(cuuint64_t)d->nu_pad * 8, (cuuint64_t)d->N2 * d->nu_pad * 8};
+    cuuint32_t box[3] = {(cuuint32_t)kMtKC, (cuuint32_t)kMtM, 1}, es[3] = {1, 1, 1};
+    CUresult r = enc(&d->tmapM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(M), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// G tiles: the frames' spectra [F][kappa][nu_pad] complex viewed as real floats with rows of gsplit floats
+// (a divisor of 2 * nu_pad * nkappa so that a chunk never straddles two rows): dims {gsplit, rows, F}
+cudaError_t mac_tc_encode_g(MacTcArgs* d, const float2* G, long long g_fstride, int F) {
+    MtEncodeFn enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !enc || q != cudaDriverEntryPointSuccess) return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+    const long long per_frame = 2LL * d->nu_pad * d->nkappa;   // floats
+    d->gsplit = 2 * d->nu_pad;                                   // one kappa per row: chunks stay inside a row
+    cuuint64_t dims[3] = {(cuuint64_t)d->gsplit, (cuuint64_t)(per_frame / d->gsplit), (cuuint64_t)F};
+    cuuint64_t strides[2] = {(cuuint64_t)d->gsplit * 4, (cuuint64_t)g_fstride * 8};
+    cuuint32_t box[3] = {(cuuint32_t)kMtKC, 1, (cuuint32_t)F}, es[3] = {1, 1, 1};
+    CUresult r = enc(&d->tmapG, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(G), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cudaStream_t s) {
+    const size_t smem = mac_tc_smem_bytes(F);
+    const int grid = std::max(1, std::min(2 * d.nkappa, num_sms));
+    cudaError_t e;
+#define LFM_MT(FV)                                                                                           \
+    case FV:                                                                                                 \
+        e = cudaFuncSetAttribute(fmb_tc_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                      \
+        fmb_tc_kernel<FV><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        break;
+    switch (F) {
+        LFM_MT(8)
+        LFM_MT(16)
+        LFM_MT(32)
+        default: return cudaErrorInvalidValue;
+    }
+#undef LFM_MT
+    return cudaGetLastError();
+}
+
+}  // namespace lfm

@@ -271,6 +271,10 @@ struct lfm_plan_s {
     LoopState* lstate = nullptr;
     double* lseries = nullptr;
     int lseries_cap = 0;
+    // frame-batched forward MAC on tcgen05 (F >= 8), tensor map over M encoded on first use
+    bool mac_tc_ready = false, mac_tc_off = false;
+    int mac_tc_F = 0;
+    MacTcArgs mac_tc{};
     // frame-batched lockstep buffers (lfm_rl_iterate_batch), capacity bcap frames
     int bcap = 0;
     float2 *bG = nullptr, *bXh = nullptr, *bY = nullptr, *bR = nullptr;
@@ -957,6 +961,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->geo = g;
     p->graphs = (flags & LFM_PLAN_GRAPHS) != 0;
     p->dloop = (flags & LFM_PLAN_DEVICE_LOOP) != 0;
+    p->mac_tc_off = (flags & LFM_PLAN_NO_TC) != 0;
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
@@ -1791,7 +1796,26 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                     CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                                   r2c_args(SRC_POLY, xbuf(f, cur[f]), nullptr, 0.f, p->nu_fft, p->bG + f * sG, p->nu_fft_pad), s));
             ST(mark(p, ST_FWD_MAC, s));
-            CK(launch_fwd_mac_batch(p->M, p->bG, sG, p->bY, sY, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            if (!p->mac_tc_off && F >= 8 && N2 <= 256) {   // tcgen05 3xTF32 batched MAC
+                if (!p->mac_tc_ready) {
+                    p->mac_tc.nkappa = p->geo.nkappa;
+                    p->mac_tc.N2 = N2;
+                    p->mac_tc.nu_pad = p->nu_fft_pad;
+                    CK(mac_tc_encode(&p->mac_tc, p->M));
+                    p->mac_tc_ready = true;
+                }
+                if (p->mac_tc.G != p->bG || p->mac_tc.g_fstride != sG || p->mac_tc_F != F) {
+                    CK(mac_tc_encode_g(&p->mac_tc, p->bG, sG, F));
+                    p->mac_tc_F = F;
+                }
+                p->mac_tc.G = p->bG;
+                p->mac_tc.g_fstride = sG;
+                p->mac_tc.Y = p->bY;
+                p->mac_tc.y_fstride = sY;
+                CK(launch_fwd_mac_batch_tc(p->mac_tc, F, p->num_sms, s));
+            } else {
+                CK(launch_fwd_mac_batch(p->M, p->bG, sG, p->bY, sY, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            }
             p->pacc.launches += 1;
         }
         ST(mark(p, ST_C2R_YHAT, s));

@@ -191,6 +191,21 @@ cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_f
                                  int F, int nkappa, int N2, int nu_pad, cudaStream_t s);   // F in {2,4,8,16}
 cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_fstride, float2* Xh, long long x_fstride,
                                  int F, int nkappa, int N2, int nu_pad, cudaStream_t s);
+// (kernels_mac_tc.cu) frame-batched forward MAC on tcgen05 (3xTF32), F in {8, 16, 32}
+struct MacTcArgs {
+    int nkappa, N2, nu_pad;
+    const float2* G;          // [F][kappa][nu_pad] complex, frame stride g_fstride
+    long long g_fstride;
+    float2* Y;                // [F][kappa][N2] complex, frame stride y_fstride
+    long long y_fstride;
+    alignas(64) CUtensorMap tmapM;   // M as real floats [kappa][N2][2 nu_pad], box {32, 128, 1}, SWIZZLE_128B
+    long long gsplit;                // floats per row of the G map (2 nu_pad: one kappa per row)
+    alignas(64) CUtensorMap tmapG;   // G as real floats {gsplit, kappa, F}, box {32, 1, F}, no swizzle
+};
+cudaError_t mac_tc_encode_g(MacTcArgs* d, const float2* G, long long g_fstride, int F);
+size_t mac_tc_smem_bytes(int F);
+cudaError_t mac_tc_encode(MacTcArgs* d, const float2* M);
+cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cudaStream_t s);
 // (kernels_misc.cu)
 cudaError_t launch_fill(float* p, size_t n, float v, cudaStream_t s);
 cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double* den, cudaStream_t s);

@@ -242,5 +242,14 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     lo = __uint_as_float(l);
 }
 
+// residual of the tensor core's own TF32 view of an fp32 operand: the MMA truncates x to TF32 (low 13 mantissa bits
+// dropped), so for a raw fp32 A tile the matching low part is rna_tf32(x - trunc_tf32(x))
+__device__ __forceinline__ float tf32_lo_of_trunc(float x) {
+    const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    uint32_t l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+    return __uint_as_float(l);
+}
+
 }  // namespace tc
 }  // namespace lfm
