@@ -81,6 +81,70 @@ __device__ __forceinline__ void warp_fft(float2* base, int stride, const float2*
     }
 }
 
+// Two independent transforms per warp (lanes 0-15 -> base0, 16-31 -> base1) for every stage whose butterfly count
+// L/R fits in 16 lanes (both radix-5 stages of L = 75, all stages of L = 15, 16, 36): the radix-5 stages of a lone
+// transform keep only 15 of 32 lanes busy, and the kernels are issue-bound.  Stages with more butterflies run the
+// two transforms one after the other.  base1 == base0 (an odd task left over) is allowed: in a paired stage both
+// halves then compute and store identical values; sequential stages skip the second pass.
+template <int L, int R, int NS, bool INV>
+__device__ __forceinline__ void warp_stage_pair(float2* base0, float2* base1, int stride, const float2* __restrict__ tw,
+                                                int lane) {
+    constexpr int LR = L / R;
+    static_assert(LR <= 16, "paired stage needs L/R <= 16");
+    constexpr int TWS = L / (NS * R);
+    const int j = lane & 15;
+    float2* base = (lane & 16) ? base1 : base0;
+    float2 v[R];
+    if (j < LR) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = base[(j + q * LR) * stride];
+        if constexpr (NS > 1) {
+            const int k = j % NS;
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                float2 w = tw[q * k * TWS];
+                if (INV) w.y = -w.y;
+                v[q] = c_mul(v[q], w);
+            }
+        }
+        small_dft<R, INV>(v);
+    }
+    __syncwarp();
+    if (j < LR) {
+        const int k = j % NS;
+        const int o = (j - k) * R + k;
+#pragma unroll
+        for (int q = 0; q < R; ++q) base[(o + q * NS) * stride] = v[q];
+    }
+    __syncwarp();
+}
+
+template <int L>
+constexpr bool has_pair_stage() {
+    constexpr Radices F = factorize(L);
+    for (int i = 0; i < F.n; ++i)
+        if (L / F.r[i] <= 16) return true;
+    return false;
+}
+
+template <int L, int S, int NS, bool INV>
+__device__ __forceinline__ void warp_fft2(float2* base0, float2* base1, int stride, const float2* __restrict__ tw,
+                                          int lane) {
+    constexpr Radices F = factorize(L);
+    if constexpr (S == 0 && !has_pair_stage<L>()) {
+        warp_fft<L, 0, 1, INV>(base0, stride, tw, lane);   // one transform per warp (PW = 1): base1 == base0
+    } else if constexpr (S < F.n) {
+        constexpr int R = F.r[S];
+        if constexpr (L / R <= 16) {
+            warp_stage_pair<L, R, NS, INV>(base0, base1, stride, tw, lane);
+        } else {
+            warp_stage<L, R, NS, INV>(base0, stride, tw, lane);
+            if (base1 != base0) warp_stage<L, R, NS, INV>(base1, stride, tw, lane);
+        }
+        warp_fft2<L, S + 1, NS * R, INV>(base0, base1, stride, tw, lane);
+    }
+}
+
 template <int L>
 struct FastGeom {
     static constexpr int NK2 = L / 2 + 1;
@@ -94,6 +158,35 @@ struct FastGeom {
     static constexpr size_t SMEM = (size_t)(L + 1) * 8 + (size_t)UB * PER;
     static constexpr size_t smem_for(int ub) { return (size_t)(L + 1) * 8 + (size_t)ub * PER; }
 };
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// sources read straight from one array at base(t) + i * row_pitch + j * col_stride (plus the yhat array for RATIO)
+template <int SRC>
+constexpr bool strided_src() {
+    return SRC == SRC_POLY || SRC == SRC_IMAGE || SRC == SRC_IMAGE2D || SRC == SRC_RATIO;
+}
+template <int SRC>
+__device__ __forceinline__ long long src_base(const XformGeom& g, int t) {
+    if constexpr (SRC == SRC_POLY) {
+        return (long long)(g.umap ? g.umap[t] : t) * g.nh * g.nw;
+    } else if constexpr (SRC == SRC_IMAGE) {
+        const int u = g.unit0 + (g.umap ? g.umap[t] : t);
+        const int N2 = g.N * g.N;
+        const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+        return ((long long)z * g.H + a1) * g.W + a2;
+    } else {   // IMAGE2D, RATIO: t = output phase (b1, b2)
+        return (long long)(t / g.N) * g.W + t % g.N;
+    }
+}
 
 template <int SRC>
 __device__ __forceinline__ float src_value(const XformGeom& g, const R2CArgs& a, int t, int i, int j) {
@@ -141,6 +234,7 @@ template <int L, int SRC, int UBV>
 __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g, const float2* __restrict__ twg, R2CArgs a) {
     using FG = FastGeom<L>;
     constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = UBV;
+    constexpr int PW = has_pair_stage<L>() ? 2 : 1;   // transforms per warp in the row / column phases
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);   // keep 16-byte alignment
@@ -154,7 +248,67 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
 
     // 1. packed rows (row 2pr in re, 2pr+1 in im) at buf[ui*S + pr*2*RHO + col]; unpacked rows >= 2P are zero.
-    //    One warp per packed row: one division per row, coalesced loads along the row.
+    //    One warp per packed row.  Strided sources: per-unit base offsets are resolved once (umap) and the row
+    //    elements go global -> shared by cp.async, so every lane keeps all its rows' loads in flight at once.
+    __shared__ long long s_base[UB];
+    if constexpr (strided_src<SRC>()) {
+        if (threadIdx.x < nt) s_base[threadIdx.x] = src_base<SRC>(g, t0 + threadIdx.x);
+        __syncthreads();
+        const long long rp = (SRC == SRC_POLY) ? (long long)g.nw : (long long)g.N * g.W;
+        const int cs = (SRC == SRC_POLY) ? 1 : g.N;
+        for (int row = warp; row < nt * P; row += nwarps) {
+            const int ui = row / P;
+            const int pr = row - ui * P;
+            float2* dst = buf + ui * S + pr * 2 * RHO;
+            const bool two = (2 * pr + 1 < nrows);
+            const long long o0 = s_base[ui] + 2 * pr * rp;
+            if constexpr (SRC == SRC_RATIO) {
+                float y0[NBL], y1[NBL], h0[NBL], h1[NBL];
+#pragma unroll
+                for (int t = 0; t < NBL; ++t) {
+                    const int col = lane + 32 * t;
+                    y0[t] = y1[t] = h0[t] = h1[t] = 0.0f;
+                    if (col < ncols) {
+                        y0[t] = a.in[o0 + (long long)col * cs];
+                        h0[t] = a.in2[o0 + (long long)col * cs];
+                        if (two) {
+                            y1[t] = a.in[o0 + rp + (long long)col * cs];
+                            h1[t] = a.in2[o0 + rp + (long long)col * cs];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NBL; ++t) {
+                    const int col = lane + 32 * t;
+                    if (col < L) {
+                        float re = 0.0f, im = 0.0f;
+                        if (col < ncols) {
+                            re = y0[t] / (fmaxf(h0[t], 0.0f) + a.eps);
+                            if (two) im = y1[t] / (fmaxf(h1[t], 0.0f) + a.eps);
+                        }
+                        dst[col] = make_float2(re, im);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < NBL; ++t) {
+                    const int col = lane + 32 * t;
+                    if (col < L) {
+                        if (col < ncols) {
+                            cp_async4(&dst[col].x, a.in + o0 + (long long)col * cs);
+                            if (two)
+                                cp_async4(&dst[col].y, a.in + o0 + rp + (long long)col * cs);
+                            else
+                                dst[col].y = 0.0f;
+                        } else {
+                            dst[col] = make_float2(0.0f, 0.0f);
+                        }
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();
+    } else
     for (int row = warp; row < nt * P; row += nwarps) {
         const int ui = row / P;
         const int pr = row - ui * P;
@@ -183,36 +337,51 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) r2c_fast_kernel(XformGeom g
     }
     __syncthreads();
     // 2. per warp: row FFT of a packed pair, then the Hermitian split in place into rows 2pr, 2pr+1
-    for (int tr = warp; tr < nt * P; tr += nwarps) {
-        const int ui = tr / P, pr = tr - ui * P;
-        float2* row = buf + ui * S + pr * 2 * RHO;
-        warp_fft<L, 0, 1, false>(row, 1, tw, lane);
-        float2 Z[NBL], Q[NBL];
+    for (int tp = PW * warp; tp < nt * P; tp += PW * nwarps) {
+        const int ntr = min(PW, nt * P - tp);
+        int prs[2];
+        float2* rows[2];
 #pragma unroll
-        for (int t = 0; t < NBL; ++t) {
-            const int k = lane + 32 * t;
-            if (k < NK2) {
-                Z[t] = row[k];
-                Q[t] = row[k == 0 ? 0 : L - k];
-            }
+        for (int h = 0; h < 2; ++h) {
+            const int tr = tp + (h < ntr ? h : 0);
+            const int ui = tr / P;
+            prs[h] = tr - ui * P;
+            rows[h] = buf + ui * S + prs[h] * 2 * RHO;
         }
-        __syncwarp();
+        warp_fft2<L, 0, 1, false>(rows[0], rows[PW - 1], 1, tw, lane);
 #pragma unroll
-        for (int t = 0; t < NBL; ++t) {
-            const int k = lane + 32 * t;
-            if (k < NK2) {
-                const float2 q = make_float2(Q[t].x, -Q[t].y);   // conj(Z[-k])
-                row[k] = make_float2(0.5f * (Z[t].x + q.x), 0.5f * (Z[t].y + q.y));
-                if (2 * pr + 1 < L) row[RHO + k] = make_float2(0.5f * (Z[t].y - q.y), -0.5f * (Z[t].x - q.x));
+        for (int h = 0; h < 2; ++h) {
+            if (h >= ntr) break;
+            float2* row = rows[h];
+            const int pr = prs[h];
+            float2 Z[NBL], Q[NBL];
+#pragma unroll
+            for (int t = 0; t < NBL; ++t) {
+                const int k = lane + 32 * t;
+                if (k < NK2) {
+                    Z[t] = row[k];
+                    Q[t] = row[k == 0 ? 0 : L - k];
+                }
             }
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < NBL; ++t) {
+                const int k = lane + 32 * t;
+                if (k < NK2) {
+                    const float2 q = make_float2(Q[t].x, -Q[t].y);   // conj(Z[-k])
+                    row[k] = make_float2(0.5f * (Z[t].x + q.x), 0.5f * (Z[t].y + q.y));
+                    if (2 * pr + 1 < L) row[RHO + k] = make_float2(0.5f * (Z[t].y - q.y), -0.5f * (Z[t].x - q.x));
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
     __syncthreads();
     // 3. column FFTs (stride RHO)
-    for (int tr = warp; tr < nt * NK2; tr += nwarps) {
-        const int ui = tr / NK2, k2 = tr - ui * NK2;
-        warp_fft<L, 0, 1, false>(buf + ui * S + k2, RHO, tw, lane);
+    for (int tp = PW * warp; tp < nt * NK2; tp += PW * nwarps) {
+        const int tq = min(tp + PW - 1, nt * NK2 - 1);
+        const int ui0 = tp / NK2, ui1 = tq / NK2;
+        warp_fft2<L, 0, 1, false>(buf + ui0 * S + (tp - ui0 * NK2), buf + ui1 * S + (tq - ui1 * NK2), RHO, tw, lane);
     }
     __syncthreads();
     // 4. kappa-major store, UB units contiguous per kappa (UB compile-time: no run-time division)
@@ -238,6 +407,7 @@ template <int L, int DST, int UBV>
 __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g, const float2* __restrict__ twg, C2RArgs a) {
     using FG = FastGeom<L>;
     constexpr int NK2 = FG::NK2, RHO = FG::RHO, S = FG::S, NBL = FG::NBL, UB = UBV;
+    constexpr int PW = has_pair_stage<L>() ? 2 : 1;   // transforms per warp in the row / column phases
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* buf = sm + L + (L & 1);
@@ -253,74 +423,120 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_fast_kernel(XformGeom g
         if (ui >= nt) continue;
         const int k1 = kap / NK2;
         const int k2 = kap - k1 * NK2;
-        buf[ui * S + k1 * RHO + k2] = a.in[(long long)kap * a.in_ld + t0 + ui];
+        cp_async8(&buf[ui * S + k1 * RHO + k2], &a.in[(long long)kap * a.in_ld + t0 + ui]);
     }
+    __shared__ int s_lu[UB];   // local unit of each transform (DST_POLY / VOLIMAGE / UPDATE / ISRA)
+    if (threadIdx.x < nt) s_lu[threadIdx.x] = g.umap ? g.umap[t0 + threadIdx.x] : t0 + threadIdx.x;
+    cp_async_wait_all();
     __syncthreads();
     // 2. inverse column FFTs
-    for (int tr = warp; tr < nt * NK2; tr += nwarps) {
-        const int ui = tr / NK2, k2 = tr - ui * NK2;
-        warp_fft<L, 0, 1, true>(buf + ui * S + k2, RHO, tw, lane);
+    for (int tp = PW * warp; tp < nt * NK2; tp += PW * nwarps) {
+        const int tq = min(tp + PW - 1, nt * NK2 - 1);
+        const int ui0 = tp / NK2, ui1 = tq / NK2;
+        warp_fft2<L, 0, 1, true>(buf + ui0 * S + (tp - ui0 * NK2), buf + ui1 * S + (tq - ui1 * NK2), RHO, tw, lane);
     }
     __syncthreads();
     // 3. per warp and packed row pair: Hermitian row rebuild, inverse row FFT, crop / scale / epilogue
     const int nh = g.nh, nw = g.nw;
     const int P = (nh + 1) / 2;
     const float scale = 1.0f / (float)(L * L);
-    for (int tr = warp; tr < nt * P; tr += nwarps) {
-        const int ui = tr / P, pr = tr - ui * P;
-        float2* row = buf + ui * S + pr * 2 * RHO;
-        const bool has1 = (2 * pr + 1 < nh);
-        float2 Z[NBL];
+    for (int tp = PW * warp; tp < nt * P; tp += PW * nwarps) {
+        const int ntr = min(PW, nt * P - tp);
+        int uis[2], prs[2];
+        float2* rows[2];
 #pragma unroll
-        for (int t = 0; t < NBL; ++t) {
-            const int k = lane + 32 * t;
-            if (k < L) {
-                const bool mirror = (k >= NK2);
-                const int kk = mirror ? L - k : k;
-                float2 A0 = row[kk];
-                float2 A1 = has1 ? row[RHO + kk] : make_float2(0.0f, 0.0f);
-                if (mirror) {
-                    A0.y = -A0.y;
-                    A1.y = -A1.y;
+        for (int h = 0; h < 2; ++h) {
+            const int tr = tp + (h < ntr ? h : 0);
+            uis[h] = tr / P;
+            prs[h] = tr - uis[h] * P;
+            rows[h] = buf + uis[h] * S + prs[h] * 2 * RHO;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h >= ntr) break;
+            float2* row = rows[h];
+            const bool has1 = (2 * prs[h] + 1 < nh);
+            float2 Z[NBL];
+#pragma unroll
+            for (int t = 0; t < NBL; ++t) {
+                const int k = lane + 32 * t;
+                if (k < L) {
+                    const bool mirror = (k >= NK2);
+                    const int kk = mirror ? L - k : k;
+                    float2 A0 = row[kk];
+                    float2 A1 = has1 ? row[RHO + kk] : make_float2(0.0f, 0.0f);
+                    if (mirror) {
+                        A0.y = -A0.y;
+                        A1.y = -A1.y;
+                    }
+                    if (k == 0 || 2 * k == L) {
+                        A0.y = 0.0f;
+                        A1.y = 0.0f;
+                    }
+                    Z[t] = make_float2(A0.x - A1.y, A0.y + A1.x);
                 }
-                if (k == 0 || 2 * k == L) {
-                    A0.y = 0.0f;
-                    A1.y = 0.0f;
-                }
-                Z[t] = make_float2(A0.x - A1.y, A0.y + A1.x);
             }
-        }
-        __syncwarp();
+            __syncwarp();
 #pragma unroll
-        for (int t = 0; t < NBL; ++t) {
-            const int k = lane + 32 * t;
-            if (k < L) row[k] = Z[t];
+            for (int t = 0; t < NBL; ++t) {
+                const int k = lane + 32 * t;
+                if (k < L) row[k] = Z[t];
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        warp_fft<L, 0, 1, true>(row, 1, tw, lane);
-        const int t = t0 + ui;
-        for (int j = lane; j < nw; j += 32) {
-            const float2 zz = row[j];
+        warp_fft2<L, 0, 1, true>(rows[0], rows[PW - 1], 1, tw, lane);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (h == 1 && !has1) break;
-                const int i = 2 * pr + h;
-                const float v = (h ? zz.y : zz.x) * scale;
-                if constexpr (DST == DST_IMAGE) {
-                    const int b1 = t / g.N, b2 = t % g.N;
-                    a.out[(size_t)(b1 + g.N * i) * g.W + b2 + g.N * j] = v;
-                } else if constexpr (DST == DST_POLY) {
-                    a.out[((size_t)(g.umap ? g.umap[t] : t) * nh + i) * nw + j] = v;
-                } else {
-                    const int lu = g.umap ? g.umap[t] : t;
-                    const int u = g.unit0 + lu;
-                    const int N2 = g.N * g.N;
-                    const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
-                    if constexpr (DST == DST_VOLIMAGE) {
-                        a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
-                    } else {
-                        const size_t pidx = ((size_t)lu * nh + i) * nw + j;
-                        a.out[pidx] = update_value<DST>(a.xold[pidx], a.norm[pidx], v, a.eps);
+        for (int hh = 0; hh < 2; ++hh) {
+            if (hh >= ntr) break;
+            const float2* row = rows[hh];
+            const int pr = prs[hh];
+            const bool has1 = (2 * pr + 1 < nh);
+            const int t = t0 + uis[hh];
+            if constexpr (DST == DST_UPDATE || DST == DST_ISRA) {
+                // all of the row pair's x_old / aux loads first, then the update and the stores
+                const size_t base = ((size_t)s_lu[uis[hh]] * nh + 2 * pr) * nw;
+                float xo[NBL][2], ax[NBL][2];
+#pragma unroll
+                for (int c = 0; c < NBL; ++c) {
+                    const int j = lane + 32 * c;
+                    xo[c][0] = xo[c][1] = ax[c][0] = ax[c][1] = 0.0f;
+                    if (j < nw) {
+                        xo[c][0] = a.xold[base + j];
+                        ax[c][0] = a.norm[base + j];
+                        if (has1) {
+                            xo[c][1] = a.xold[base + nw + j];
+                            ax[c][1] = a.norm[base + nw + j];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NBL; ++c) {
+                    const int j = lane + 32 * c;
+                    if (j < nw) {
+                        const float2 zz = row[j];
+                        a.out[base + j] = update_value<DST>(xo[c][0], ax[c][0], zz.x * scale, a.eps);
+                        if (has1) a.out[base + nw + j] = update_value<DST>(xo[c][1], ax[c][1], zz.y * scale, a.eps);
+                    }
+                }
+            } else {
+                for (int j = lane; j < nw; j += 32) {
+                    const float2 zz = row[j];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && !has1) break;
+                        const int i = 2 * pr + h;
+                        const float v = (h ? zz.y : zz.x) * scale;
+                        if constexpr (DST == DST_IMAGE) {
+                            const int b1 = t / g.N, b2 = t % g.N;
+                            a.out[(size_t)(b1 + g.N * i) * g.W + b2 + g.N * j] = v;
+                        } else if constexpr (DST == DST_POLY) {
+                            a.out[((size_t)s_lu[uis[hh]] * nh + i) * nw + j] = v;
+                        } else {
+                            const int u = g.unit0 + s_lu[uis[hh]];
+                            const int N2 = g.N * g.N;
+                            const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+                            a.out[((size_t)z * g.H + a1 + g.N * i) * g.W + a2 + g.N * j] = v;
+                        }
                     }
                 }
             }
