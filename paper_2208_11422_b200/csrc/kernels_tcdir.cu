@@ -29,6 +29,7 @@ namespace lfm {
 namespace {
 constexpr int kM = 128;            // pixels per CTA tile (TMEM lanes); a CTA pair covers 2 * kM pixels
 constexpr int kKC = 32;            // phases per chunk (one 128-byte swizzle row)
+constexpr int kStagePB = 4;        // 32-pixel blocks per tc_stage_kernel CTA
 constexpr int kASlots = 2;         // A windows in flight (one per 32-phase chunk x tap row e1)
 constexpr int kBSlots = 4;         // coefficient tiles in flight (one per tap)
 constexpr int kDrainWarps = 8;     // warps 2..9: two per TMEM lane quarter, half of the columns each
@@ -335,51 +336,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 template <bool FWD, int SRC>
 __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ src,
                                                        const float* __restrict__ src2, float eps) {
-    __shared__ float tile[kKC][33];
-    const int L0 = blockIdx.x * 32, c = blockIdx.y, zi = blockIdx.z;
+    // kStagePB blocks of 32 padded pixels per CTA; every thread issues all its kStagePB * 4 loads before the first use
+    __shared__ float tile[kStagePB][kKC][33];
+    const int L0 = blockIdx.x * 32 * kStagePB, c = blockIdx.y, zi = blockIdx.z;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     {
-        const int L = L0 + tx;
-        const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp + d.e2lo;
-        const bool pv = L < d.Lp && m1 < d.nh && m2 >= 0 && m2 < d.nw;
-        for (int k = ty; k < kKC; k += 8) {
-            const int ph = c * kKC + k;
-            float v = 0.0f;
-            if (pv && ph < d.N2) {
-                const int p1 = ph / d.N, p2 = ph - (ph / d.N) * d.N;
-                if constexpr (FWD) {
-                    const int z = d.zlist[zi];
-                    const int u = z * d.N2 + ph;
-                    if (u >= d.unit0 && u < d.unit0 + d.nu) {
-                        if constexpr (SRC == 0)
-                            v = src[((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2];
-                        else
-                            v = src[((size_t)z * d.H + p1 + d.N * m1) * d.W + p2 + d.N * m2];
+        float v[kStagePB][kKC / 8];
+        float w[kStagePB][kKC / 8];   // yhat for SRC_RATIO
+#pragma unroll
+        for (int j = 0; j < kStagePB; ++j) {
+            const int L = L0 + 32 * j + tx;
+            const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp + d.e2lo;
+            const bool pv = L < d.Lp && m1 < d.nh && m2 >= 0 && m2 < d.nw;
+#pragma unroll
+            for (int i = 0; i < kKC / 8; ++i) {
+                const int ph = c * kKC + ty + 8 * i;
+                v[j][i] = 0.0f;
+                w[j][i] = 0.0f;
+                if (pv && ph < d.N2) {
+                    const int p1 = ph / d.N, p2 = ph - (ph / d.N) * d.N;
+                    if constexpr (FWD) {
+                        const int z = d.zlist[zi];
+                        const int u = z * d.N2 + ph;
+                        if (u >= d.unit0 && u < d.unit0 + d.nu) {
+                            if constexpr (SRC == 0)
+                                v[j][i] = src[((size_t)(u - d.unit0) * d.nh + m1) * d.nw + m2];
+                            else
+                                v[j][i] = src[((size_t)z * d.H + p1 + d.N * m1) * d.W + p2 + d.N * m2];
+                        }
+                    } else {
+                        const size_t pix = (size_t)(p1 + d.N * m1) * d.W + p2 + d.N * m2;
+                        if constexpr (SRC == SRC_ONES) {
+                            v[j][i] = 1.0f;
+                        } else if constexpr (SRC == SRC_RATIO) {
+                            v[j][i] = src[pix];
+                            w[j][i] = src2[pix];
+                        } else {
+                            v[j][i] = src[pix];
+                        }
                     }
-                } else {
-                    const size_t pix = (size_t)(p1 + d.N * m1) * d.W + p2 + d.N * m2;
-                    if constexpr (SRC == SRC_ONES)
-                        v = 1.0f;
-                    else if constexpr (SRC == SRC_RATIO)
-                        v = src[pix] / (fmaxf(src2[pix], 0.0f) + eps);
-                    else
-                        v = src[pix];
                 }
             }
-            tile[k][tx] = v;
         }
+#pragma unroll
+        for (int j = 0; j < kStagePB; ++j)
+#pragma unroll
+            for (int i = 0; i < kKC / 8; ++i) {
+                float x = v[j][i];
+                if constexpr (!FWD && SRC == SRC_RATIO) {
+                    const int L = L0 + 32 * j + tx;
+                    const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp + d.e2lo;
+                    const bool pv = L < d.Lp && m1 < d.nh && m2 >= 0 && m2 < d.nw;
+                    const int ph = c * kKC + ty + 8 * i;
+                    x = (pv && ph < d.N2) ? x / (fmaxf(w[j][i], 0.0f) + eps) : 0.0f;
+                }
+                tile[j][ty + 8 * i][tx] = x;
+            }
     }
     __syncthreads();
     const size_t slab_hi = FWD ? ((size_t)zi * 2) * d.nch + c : (size_t)c;
     const size_t slab_lo = FWD ? ((size_t)zi * 2 + 1) * d.nch + c : (size_t)d.nch + c;
-    for (int rr = ty; rr < 32; rr += 8) {
-        const int L = L0 + rr;
-        if (L >= d.Lp) break;
-        float h, l;
-        tc::split_tf32(tile[tx][rr], h, l);
-        d.src[(slab_hi * d.Lp + L) * kKC + tx] = h;
-        d.src[(slab_lo * d.Lp + L) * kKC + tx] = l;
-    }
+#pragma unroll
+    for (int j = 0; j < kStagePB; ++j)
+        for (int rr = ty; rr < 32; rr += 8) {
+            const int L = L0 + 32 * j + rr;
+            if (L >= d.Lp) break;
+            float h, l;
+            tc::split_tf32(tile[j][tx][rr], h, l);
+            d.src[(slab_hi * d.Lp + L) * kKC + tx] = h;
+            d.src[(slab_lo * d.Lp + L) * kKC + tx] = l;
+        }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -396,7 +422,8 @@ __global__ void __launch_bounds__(256) tc_fwd_reduce_kernel(const __grid_constan
         const int b2 = e / d.nw, m2 = e - (e / d.nw) * d.nw;
         const float* src = d.part + (size_t)(b1 * d.N + b2) * npix + (size_t)m1 * d.nw + m2;
         float v = 0.0f;
-        for (int zi = 0; zi < d.nzd; ++zi) v += __ldcs(src + (size_t)zi * d.N2 * npix);
+#pragma unroll 8
+        for (int zi = 0; zi < d.nzd; ++zi) v += __ldcs(src + (size_t)zi * d.N2 * npix);   // plane order fixed
         accs[e] = v;
     }
     __syncthreads();
@@ -655,7 +682,7 @@ static cudaError_t tcdir_main(const TcDirArgs& d, const float* xold, const float
 
 template <bool FWD, int SRC>
 static cudaError_t tc_stage(const TcDirArgs& d, const float* src, const float* src2, float eps, cudaStream_t s) {
-    dim3 grid((d.Lp + 31) / 32, d.nch, FWD ? d.nzd : 1);
+    dim3 grid((d.Lp + 32 * kStagePB - 1) / (32 * kStagePB), d.nch, FWD ? d.nzd : 1);
     tc_stage_kernel<FWD, SRC><<<grid, 256, 0, s>>>(d, src, src2, eps);
     return cudaGetLastError();
 }
