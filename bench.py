@@ -261,6 +261,13 @@ def run_ours(args):
     else:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     stage_ms = {k: prof["ms"][k] / max(1, prof["count"][k]) for k in prof["ms"]}
+    # per-kernel launch times, CUDA events on the stream (SM partition) each kernel runs on
+    kern_ms = {{"mac_fwd": "fwd_mac", "mac_bwd": "bwd_mac", "tc_fwd": "dir_fwd", "tc_bwd": "dir_bwd"}[k]:
+               prof["kern_ms"][k] / max(1, prof["kern_count"][k]) for k in prof["kern_ms"]}
+    parts = info["partition_sms"]     # [fwd, bwd] x [tensor-core SMs, MAC SMs]; 0 = whole GPU, one after the other
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    mac_sms = {"fwd_mac": parts[0][1] or nsm, "bwd_mac": parts[1][1] or nsm}
+    tc_sms = {"dir_fwd": parts[0][0] or nsm, "dir_bwd": parts[1][0] or nsm}
     alg = {
         "fwd_mac": kap_min * N2 * nu * 8 + kap_min * nu * 8 + kap_min * N2 * 8,   # M + G + Y
         "bwd_mac": kap_min * N2 * nu * 8 + kap_min * N2 * 8 + kap_min * nu * 8,   # M + R + Xh
@@ -270,8 +277,8 @@ def run_ours(args):
         roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
                 "traffic": None}
     else:
-        dom = max(("fwd_mac", "bwd_mac"), key=lambda k: stage_ms[k])
-        achieved = alg[dom] / (stage_ms[dom] / 1e3) / 1e9
+        dom = max(("fwd_mac", "bwd_mac"), key=lambda k: kern_ms[k])
+        achieved = alg[dom] / (kern_ms[dom] / 1e3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -281,9 +288,12 @@ def run_ours(args):
                     traffic = ent.get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": stage_ms[dom],
-                "both": {k: {"avg_ms": stage_ms[k], "achieved_gbs": alg[k] / (stage_ms[k] / 1e3) / 1e9,
-                             "frac": alg[k] / (stage_ms[k] / 1e3) / 1e9 / peak} for k in alg}}
+                "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": kern_ms[dom],
+                "sms": mac_sms[dom],
+                "partition_note": "on an SM partition (DESIGN.md §5.5) the MAC shares the GPU with the tensor-core "
+                                  "kernel; its stream rate is bounded per SM, not by HBM" if parts[0][0] else None,
+                "both": {k: {"avg_ms": kern_ms[k], "achieved_gbs": alg[k] / (kern_ms[k] / 1e3) / 1e9, "sms": mac_sms[k],
+                             "frac": alg[k] / (kern_ms[k] / 1e3) / 1e9 / peak} for k in alg}}
     # secondary roofline: the tcgen05 direct kernel (tensor-bound), per projection stage
     roof_tc = None
     if info.get("tc_planes", 0) > 0:
@@ -291,7 +301,7 @@ def run_ours(args):
         ratio = 1.1 / 2.25   # tf32 / bf16 dense nominal (B200_PROFILING.md)
         tf32_sus = pk.get("bf16_tflops_sustained", 2250.0 * 0.62) * ratio
         tf32_burst = pk.get("bf16_tflops", 2250.0 * 0.76) * ratio
-        t = {k: stage_ms[k] for k in ("dir_fwd", "dir_bwd")}
+        t = {k: kern_ms[k] for k in ("dir_fwd", "dir_bwd")}
         kk = max(t, key=lambda k: t[k])
         ex = info["tc_flops_executed"] / (t[kk] / 1e3) / 1e12
         al = info["tc_flops_algorithmic"] / (t[kk] / 1e3) / 1e12
@@ -302,11 +312,12 @@ def run_ours(args):
             for key, ent in json.load(open(tpath)).items():
                 if key.split("_")[0] == cfg.name and ent.get("fft_units") == info["fft_units"]:
                     tc_traffic = ent.get("tcdir_" + kk.split("_")[1])
-        roof_tc = {"bound": "tensor", "kernel": "tcdir_kernel (" + kk + " stage: staging + kernel + reduction)",
+        roof_tc = {"bound": "tensor", "kernel": "tcdir_kernel (" + kk.split("_")[1] + ")",
                    "achieved": al, "peak": peak3, "unit": "TFLOP/s", "frac": al / peak3,
+                   "sms": tc_sms[kk], "frac_of_partition_peak": al / (peak3 * tc_sms[kk] / nsm),
                    "traffic": tc_traffic, "avg_launch_ms": t[kk],
                    "algorithmic_flops_per_launch": info["tc_flops_algorithmic"],
-                   "achieved_is": "algorithmic fp32 flops (SURVEY 8(d): 2*H*W*K(z)^2 non-zero taps per plane) / stage time",
+                   "achieved_is": "algorithmic fp32 flops (SURVEY 8(d): 2*H*W*K(z)^2 non-zero taps per plane) / kernel time",
                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32",
                    "executed_tensor_tflops": ex, "executed_frac_of_tf32_peak": ex / tf32_sus,
                    "executed_frac_of_tf32_burst_peak": ex / tf32_burst,
@@ -314,10 +325,10 @@ def run_ours(args):
                                 f"{pk.get('clocks_under_load', {}).get('sm_mhz_median', 'n/a')} MHz); this step's "
                                 "clocks are in 'clocks' -- compare executed_frac_of_tf32_burst_peak too",
                    "executed_is": "issued tcgen05 flops (3 TF32 products over the union tap boxes, skipped windows excluded)",
-                   "tc_planes": info["tc_planes"], "stage_ms": t}
+                   "tc_planes": info["tc_planes"], "kernel_ms": t}
     # the dominant kernel (longest average launch) carries the primary roofline
     roof_primary = roof
-    if roof_tc is not None and (info["fft_units"] == 0 or max(roof_tc["stage_ms"].values()) > stage_ms[dom]):
+    if roof_tc is not None and (info["fft_units"] == 0 or max(roof_tc["kernel_ms"].values()) > kern_ms[dom]):
         roof_primary = roof_tc
     share = {k: prof["ms"][k] / max(1e-9, sum(prof["ms"].values())) for k in prof["ms"]}
 
@@ -376,7 +387,11 @@ def run_ours(args):
                 "plan_ms": info["plan_ms"], "setup_s": setup_s,
                 "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"],
                               "decision_margin": margin, "series": s},
-                "stage_share": share, "stage_avg_ms": stage_ms,
+                "stage_share": share, "stage_avg_ms": stage_ms, "kernel_avg_ms": kern_ms,
+                "sm_partitions": {"forward": {"tc_sms": parts[0][0], "mac_sms": parts[0][1]},
+                                  "backward": {"tc_sms": parts[1][0], "mac_sms": parts[1][1]},
+                                  "note": "0 = the projection's tensor-core and frequency-path halves run one after "
+                                          "the other on the whole GPU"},
             },
             "roofline": roof_primary,
             "roofline_mac": roof,

@@ -138,6 +138,8 @@ typedef struct {
     double tc_flops_algorithmic;    /* per projection: 2 * exact taps (D x D per phase pair) * pixels */
     int planes_moved_for_memory;    /* planes the hybrid planner moved off the frequency path so that the
                                        transfer matrices fit the device (memory-aware planning, §5.1)  */
+    int partition_sms[2][2];        /* SM partitions of the [forward, backward] projection:
+                                       [tensor-core SMs, frequency-path SMs]; 0 = run one after the other */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */
@@ -268,6 +270,10 @@ typedef struct {
     long long count[LFM_N_STAGES];    /* number of timed executions per stage   */
     long long launches;               /* kernels launched by the library so far */
     long long iterations;             /* RL iterations executed so far          */
+    double kern_ms[4];                /* summed device ms of the dominant kernels, timed on the stream (or SM
+                                         partition) that runs them: tcgen05 forward, forward MAC, tcgen05
+                                         backward (+ its update), backward MAC                           */
+    long long kern_count[4];
 } lfm_profile_t;
 
 /* enable != 0 turns per-stage event timing on.  Counters keep accumulating until read with reset. */

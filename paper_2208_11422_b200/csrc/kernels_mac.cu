@@ -6,6 +6,8 @@
 // Both stream M exactly once per call at 1 complex MAC (8 flop) per 8-byte element, so they are
 // bound by HBM bandwidth.  M is read with streaming (evict-first) 32-byte loads; every other operand
 // is small and L2/shared-memory resident.
+#include <cstdlib>
+
 #include "lfm_internal.cuh"
 #include "tc_sm100.cuh"   // mbarrier / bulk-copy helpers
 
@@ -46,42 +48,45 @@ __device__ __forceinline__ void cmac4(const f8& m, const float4& g0, const float
 }
 
 // Persistent: each CTA owns a contiguous range of (kappa, b') rows; G[kappa] is staged in shared
-// memory whenever kappa changes; one warp computes one row's dot product (lane-strided 32-byte
-// loads, 8 in flight per lane = 8 KB per warp), then a warp-shuffle reduction.
-__global__ void __launch_bounds__(512, 1) fwd_mac_kernel(const float2* __restrict__ M, const float2* __restrict__ G,
-                                                      float2* __restrict__ Y, int N2, int nu_pad, long long rows) {
+// memory whenever kappa changes; one warp computes one row's dot product (lane-strided 32-byte loads,
+// NL in flight per lane = NL KB per warp), then a warp-shuffle reduction.  MINB CTAs per SM.
+template <int NT, int NL, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fwd_mac_kernel(const float2* __restrict__ M, const float2* __restrict__ G,
+                                                         float2* __restrict__ Y, int N2, int nu_pad, long long rows) {
     extern __shared__ float4 gs[];
     const int nv = nu_pad >> 2;                       // 32-byte vectors per row
     const long long r_begin = rows * blockIdx.x / gridDim.x;
     const long long r_end = rows * (blockIdx.x + 1) / gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
+    constexpr int nwarps = NT / 32;
     long long r = r_begin;
     while (r < r_end) {
         const long long kap = r / N2;
         long long r_k_end = (kap + 1) * N2;
         if (r_k_end > r_end) r_k_end = r_end;
-        __syncthreads();
         const float4* gsrc = reinterpret_cast<const float4*>(G + kap * nu_pad);
-        for (int v = threadIdx.x; v < 2 * nv; v += blockDim.x) gs[v] = gsrc[v];
+        __syncthreads();
+        // split planes: gs[v] = the first two complex values of vector v, gs[nv + v] = the last two, so that a
+        // warp's lane-strided 16-byte reads are contiguous (conflict-free)
+        for (int v = threadIdx.x; v < 2 * nv; v += NT) gs[(v & 1) * nv + (v >> 1)] = gsrc[v];
         __syncthreads();
         for (long long row = r + warp; row < r_k_end; row += nwarps) {
             const f8* mrow = reinterpret_cast<const f8*>(M + row * nu_pad);
             float ar0 = 0.f, ai0 = 0.f, ar1 = 0.f, ai1 = 0.f;
             int v = lane;
-            for (; v + 7 * 32 < nv; v += 8 * 32) {
-                f8 m[8];
+            for (; v + (NL - 1) * 32 < nv; v += NL * 32) {
+                f8 m[NL];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) m[q] = ld_stream8(mrow + v + q * 32);
+                for (int q = 0; q < NL; ++q) m[q] = ld_stream8(mrow + v + q * 32);
 #pragma unroll
-                for (int q = 0; q < 8; q += 2) {
-                    cmac4(m[q], gs[2 * (v + q * 32)], gs[2 * (v + q * 32) + 1], ar0, ai0);
-                    cmac4(m[q + 1], gs[2 * (v + (q + 1) * 32)], gs[2 * (v + (q + 1) * 32) + 1], ar1, ai1);
+                for (int q = 0; q < NL; q += 2) {
+                    cmac4(m[q], gs[v + q * 32], gs[nv + v + q * 32], ar0, ai0);
+                    cmac4(m[q + 1], gs[v + (q + 1) * 32], gs[nv + v + (q + 1) * 32], ar1, ai1);
                 }
             }
             for (; v < nv; v += 32) {
                 const f8 m = ld_stream8(mrow + v);
-                cmac4(m, gs[2 * v], gs[2 * v + 1], ar0, ai0);
+                cmac4(m, gs[v], gs[nv + v], ar0, ai0);
             }
             float ar = ar0 + ar1, ai = ai0 + ai1;
 #pragma unroll
@@ -515,17 +520,27 @@ cudaError_t launch_bwd_mac_batch(const float2* M, const float2* R, long long r_f
     return cudaGetLastError();
 }
 
-cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
-                           cudaStream_t s) {
+template <int NT, int NL, int MINB>
+static cudaError_t fwd_mac_v(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
+                             cudaStream_t s) {
     const size_t smem = (size_t)nu_pad * sizeof(float2);
-    cudaError_t e = cudaFuncSetAttribute(fwd_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(fwd_mac_kernel<NT, NL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
-    const int per_sm = 1;   // 512 threads x ~121 registers: one persistent CTA per SM
     long long rows = (long long)nkappa * N2;
-    long long grid = (long long)num_sms * per_sm;
+    long long grid = (long long)num_sms * MINB;   // persistent: MINB CTAs per SM
     if (grid > rows) grid = rows;
-    fwd_mac_kernel<<<(unsigned)grid, 512, smem, s>>>(M, G, Y, N2, nu_pad, rows);
+    fwd_mac_kernel<NT, NL, MINB><<<(unsigned)grid, NT, smem, s>>>(M, G, Y, N2, nu_pad, rows);
     return cudaGetLastError();
+}
+
+// whole GPU: one 16-warp CTA per SM, 8 loads in flight per lane (HBM-bound at ~90 % of peak);
+// SM partition (§5.5, below the HBM limit, bound per SM): four 8-warp CTAs per SM, 4 loads per lane (measured
+// 4.53 vs 4.91 ms on 52 SMs at c3)
+cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
+                           int partition, cudaStream_t s) {
+    if (partition) return fwd_mac_v<256, 4, 4>(M, G, Y, nkappa, N2, nu_pad, num_sms, s);
+    return fwd_mac_v<512, 8, 1>(M, G, Y, nkappa, N2, nu_pad, num_sms, s);
 }
 
 cudaError_t launch_bwd_mac(const float2* M, const float2* R, float2* Xh, int nkappa, int N2, int nu_pad,

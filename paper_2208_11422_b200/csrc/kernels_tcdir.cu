@@ -661,6 +661,9 @@ static cudaError_t tcdir_main(const TcDirArgs& d, const float* xold, const float
     const size_t smem = tcdir_smem_bytes(d.Ntile, d.Arows);
     cudaError_t e = cudaFuncSetAttribute(tcdir_kernel<FWD, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // SMs configured for the largest shared-memory carveout, so that a co-resident MAC CTA fits beside it (§5.5)
+    e = cudaFuncSetAttribute(tcdir_kernel<FWD, DST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
     tcdir_kernel<FWD, DST><<<2 * d.grid, kThreads, smem, s>>>(d, xold, norm, eps, out);
     if (d.exp & 4) {   // dev only: print the averaged wait counters of the leader CTAs
         cudaStreamSynchronize(s);
@@ -688,28 +691,42 @@ static cudaError_t tc_stage(const TcDirArgs& d, const float* src, const float* s
 }
 
 cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* y, int accumulate,
-                             cudaStream_t s) {
+                             cudaStream_t s, int parts) {
     if (d.nzd <= 0) return cudaSuccess;
-    cudaError_t e = src_image ? tc_stage<true, 1>(d, x, nullptr, 0.f, s) : tc_stage<true, 0>(d, x, nullptr, 0.f, s);
-    if (e != cudaSuccess) return e;
-    e = tcdir_main<true, 0>(d, nullptr, nullptr, 0.f, nullptr, s);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (parts & TC_PART_STAGE) {
+        e = src_image ? tc_stage<true, 1>(d, x, nullptr, 0.f, s) : tc_stage<true, 0>(d, x, nullptr, 0.f, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (parts & TC_PART_MAIN) {
+        e = tcdir_main<true, 0>(d, nullptr, nullptr, 0.f, nullptr, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (!(parts & TC_PART_FINISH)) return cudaSuccess;
     const size_t rsm = (size_t)d.N * d.nw * sizeof(float);
     tc_fwd_reduce_kernel<<<dim3(d.nh, d.N), 256, rsm, s>>>(d, y, accumulate);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
-                             float* out, const float* xold, const float* norm, cudaStream_t s) {
-    if (d.nzd <= 0) return cudaSuccess;
-    cudaError_t e;
+static cudaError_t tc_stage_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps,
+                                cudaStream_t s) {
     switch (src) {
-        case SRC_RATIO: e = tc_stage<false, SRC_RATIO>(d, img, img2, eps, s); break;
-        case SRC_ONES: e = tc_stage<false, SRC_ONES>(d, nullptr, nullptr, eps, s); break;
-        case SRC_IMAGE2D: e = tc_stage<false, SRC_IMAGE2D>(d, img, nullptr, eps, s); break;
+        case SRC_RATIO: return tc_stage<false, SRC_RATIO>(d, img, img2, eps, s);
+        case SRC_ONES: return tc_stage<false, SRC_ONES>(d, nullptr, nullptr, eps, s);
+        case SRC_IMAGE2D: return tc_stage<false, SRC_IMAGE2D>(d, img, nullptr, eps, s);
         default: return cudaErrorInvalidValue;
     }
-    if (e != cudaSuccess) return e;
+}
+
+cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
+                             float* out, const float* xold, const float* norm, cudaStream_t s, int parts) {
+    if (d.nzd <= 0) return cudaSuccess;
+    cudaError_t e;
+    if (parts & TC_PART_STAGE) {
+        e = tc_stage_bwd(d, src, img, img2, eps, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (!(parts & TC_PART_MAIN)) return cudaSuccess;
     const dim3 ug((unsigned)std::min<size_t>(((size_t)d.nh * d.nw + 255) / 256, 8), (unsigned)(d.nzd * d.N2));
     switch (dst) {
         case DST_UPDATE:

@@ -282,6 +282,16 @@ struct lfm_plan_s {
     unsigned* bmproj = nullptr;
     double *bent = nullptr, *bhost = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // co-resident projections: the tensor-core direct kernel on a high-priority side stream, the
+    // frequency-path MAC beside it on the caller's stream, one fork / join per projection
+    struct Part {
+        int sms_tc = 0, sms_mac = 0;                // SMs of the two sides
+        CUgreenCtx gtc = nullptr, gmac = nullptr;   // green contexts over disjoint SM sets
+        cudaStream_t stc = nullptr, smac = nullptr;
+    };
+    Part part[2];   // [forward, backward] projection; part[d].stc == nullptr: the two run one after the other
+    cudaEvent_t evf = nullptr, evj = nullptr, evj2 = nullptr;
+    cudaEvent_t kev[4][2] = {};   // kernel timers (lfm_profile_t.kern_ms)
     bool prof = false;
     cudaEvent_t pev[LFM_N_STAGES + 1] = {};
     lfm_profile_t pacc{};
@@ -308,6 +318,100 @@ enum { ST_R2C_X = 0, ST_FWD_MAC, ST_C2R_YHAT, ST_DIR_FWD, ST_ALLRED_SUM, ST_R2C_
 inline lfm_status mark(lfm_plan p, int stage, cudaStream_t s) {
     if (!p->prof) return LFM_OK;
     CK(cudaEventRecord(p->pev[stage], s));
+    return LFM_OK;
+}
+
+// ---- §5.5 SM partitions (green contexts; driver entry points fetched through the runtime, no -lcuda) ----
+struct GreenApi {
+    CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+    CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned) = nullptr;
+    CUresult (*gen_desc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+    CUresult (*create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+    CUresult (*destroy)(CUgreenCtx) = nullptr;
+    CUresult (*stream)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+    bool ok = false;
+};
+
+const GreenApi& green_api() {
+    static GreenApi a = [] {
+        GreenApi g;
+        cudaDriverEntryPointQueryResult q;
+        auto get = [&](const char* n, void** f) {
+            return cudaGetDriverEntryPoint(n, f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+        };
+        g.ok = get("cuDeviceGetDevResource", (void**)&g.get_res) && get("cuDevSmResourceSplitByCount", (void**)&g.split) &&
+               get("cuDevResourceGenerateDesc", (void**)&g.gen_desc) && get("cuGreenCtxCreate", (void**)&g.create) &&
+               get("cuGreenCtxDestroy", (void**)&g.destroy) && get("cuGreenCtxStreamCreate", (void**)&g.stream);
+        return g;
+    }();
+    return a;
+}
+
+void green_free(lfm_plan p) {
+    const GreenApi& g = green_api();
+    for (auto& pt : p->part) {
+        if (pt.stc) cudaStreamDestroy(pt.stc);
+        if (pt.smac) cudaStreamDestroy(pt.smac);
+        if (pt.gtc && g.ok) g.destroy(pt.gtc);
+        if (pt.gmac && g.ok) g.destroy(pt.gmac);
+        pt = lfm_plan_s::Part{};
+    }
+    for (cudaEvent_t* e : {&p->evf, &p->evj, &p->evj2}) {
+        if (*e) cudaEventDestroy(*e);
+        *e = nullptr;
+    }
+}
+
+// split the device's SMs into a tensor-core side of >= want_tc SMs (rounded by the driver) and the rest for the
+// frequency path; false (the projection then runs its two halves one after the other) if the driver cannot
+bool green_split(lfm_plan p, int dev, int want_tc, lfm_plan_s::Part* out) {
+    const GreenApi& g = green_api();
+    if (!g.ok) return false;
+    CUdevResource all{}, grp{}, rest{};
+    if (g.get_res((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+    unsigned n = 1;
+    if (g.split(&grp, &n, &all, &rest, 0, (unsigned)want_tc) != CUDA_SUCCESS || n != 1) return false;
+    if (rest.sm.smCount < 8) return false;
+    CUdevResourceDesc dt = nullptr, dm = nullptr;
+    lfm_plan_s::Part pt;
+    bool ok = g.gen_desc(&dt, &grp, 1) == CUDA_SUCCESS && g.gen_desc(&dm, &rest, 1) == CUDA_SUCCESS &&
+              g.create(&pt.gtc, dt, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+              g.create(&pt.gmac, dm, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+              g.stream((CUstream*)&pt.stc, pt.gtc, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS &&
+              g.stream((CUstream*)&pt.smac, pt.gmac, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS;
+    for (cudaEvent_t* e : {&p->evf, &p->evj, &p->evj2})
+        if (ok && !*e) ok = cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        if (pt.stc) cudaStreamDestroy(pt.stc);
+        if (pt.smac) cudaStreamDestroy(pt.smac);
+        if (pt.gtc) g.destroy(pt.gtc);
+        if (pt.gmac) g.destroy(pt.gmac);
+        return false;
+    }
+    pt.sms_tc = (int)grp.sm.smCount;
+    pt.sms_mac = (int)rest.sm.smCount;
+    *out = pt;
+    return true;
+}
+
+// kernel timer k (0 tc fwd, 1 mac fwd, 2 tc bwd, 3 mac bwd): start (e = 0) / end (e = 1) on stream s; a kernel
+// that did not run this iteration (its plan has no such planes / units) leaves both events unrecorded
+inline lfm_status kmark(lfm_plan p, int k, int e, cudaStream_t s) {
+    if (!p->prof) return LFM_OK;
+    CK(cudaEventRecord(p->kev[k][e], s));
+    return LFM_OK;
+}
+
+lfm_status read_kernel_timers(lfm_plan p, int mask = 0xF) {
+    for (int k = 0; k < 4; ++k) {
+        if (!((mask >> k) & 1)) continue;
+        const bool ran = (k & 1) ? p->nu_fft > 0 : !(k < 2 ? p->tcf.empty() : p->tcb.empty());
+        if (!ran) continue;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p->kev[k][0], p->kev[k][1]));
+        p->pacc.kern_ms[k] += ms;
+        p->pacc.kern_count[k] += 1;
+    }
     return LFM_OK;
 }
 
@@ -353,10 +457,14 @@ void plan_free(lfm_plan p) {
     cudaFree(p->bent);
     if (p->bhost) cudaFreeHost(p->bhost);
     if (p->host) cudaFreeHost(p->host);
+    green_free(p);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     for (auto& e : p->pev)
         if (e) cudaEventDestroy(e);
+    for (auto& kv : p->kev)
+        for (auto& e : kv)
+            if (e) cudaEventDestroy(e);
     metric_free(&p->met);
     delete p;
 }
@@ -424,28 +532,54 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
         CK(launch_direct_fwd(xp, p->psf, yimg, p->xall, s));
         p->pacc.launches += 1;
     } else {
-        if (p->nu_fft > 0) {
+        // tensor-core planes: stage the source; FFT units: coarse transforms.  Then the two halves of the projection
+        // -- tcgen05 kernel and frequency-path MAC + C2R -- run side by side on the plan's SM partitions (§5.5) or one
+        // after the other on `s`; afterwards the direct planes' partial images are added onto the C2R output.
+        const lfm_plan_s::Part& pt = p->part[0];
+        const bool split = pt.stc != nullptr;
+        for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, s, TC_PART_STAGE));
+        if (p->nu_fft > 0)
             CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                           r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), s));
-            ST(mark(p, ST_FWD_MAC, s));
-            CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, p->num_sms, s));
-            ST(mark(p, ST_C2R_YHAT, s));
+        ST(mark(p, ST_FWD_MAC, s));
+        cudaStream_t st = s, sm = s;
+        if (split) {
+            CK(cudaEventRecord(p->evf, s));
+            CK(cudaStreamWaitEvent(pt.stc, p->evf, 0));
+            CK(cudaStreamWaitEvent(pt.smac, p->evf, 0));
+            st = pt.stc;
+            sm = pt.smac;
+        }
+        if (!p->tcf.empty()) {
+            ST(kmark(p, 0, 0, st));
+            for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_MAIN));
+            ST(kmark(p, 0, 1, st));
+        }
+        if (p->nu_fft > 0) {
+            ST(kmark(p, 1, 0, sm));
+            CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
+                              split, sm));
+            ST(kmark(p, 1, 1, sm));
             C2RArgs c{};
             c.dst = DST_IMAGE;
             c.in = p->Y;
             c.in_ld = N2;
             c.ntrans = N2;
             c.out = yimg;
-            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, sm));
             p->pacc.launches += 3;
-        } else {
-            ST(mark(p, ST_FWD_MAC, s));
-            ST(mark(p, ST_C2R_YHAT, s));
         }
+        if (split) {
+            CK(cudaEventRecord(p->evj, pt.stc));
+            CK(cudaEventRecord(p->evj2, pt.smac));
+            CK(cudaStreamWaitEvent(s, p->evj, 0));
+            CK(cudaStreamWaitEvent(s, p->evj2, 0));
+        }
+        ST(mark(p, ST_C2R_YHAT, s));
         ST(mark(p, ST_DIR_FWD, s));
         bool acc = p->nu_fft > 0;
         for (const TcDirArgs& tg : p->tcf) {
-            CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, acc ? 1 : 0, s));
+            CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, acc ? 1 : 0, s, TC_PART_FINISH));
             p->pacc.launches += 3;
             acc = true;
         }
@@ -492,11 +626,33 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         ST(mark(p, ST_MAXPROJ, s));
         return LFM_OK;
     }
-    if (p->nu_fft > 0) {
+    // as in the forward (§5.5); the two halves write disjoint units of `out`
+    const lfm_plan_s::Part& pt = p->part[1];
+    const bool split = pt.stc != nullptr;
+    for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s, TC_PART_STAGE));
+    if (p->nu_fft > 0)
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
-        ST(mark(p, ST_BWD_MAC, s));
-        CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, s));
-        ST(mark(p, ST_C2R_UPD, s));
+    ST(mark(p, ST_BWD_MAC, s));
+    cudaStream_t st = s, sm = s;
+    if (split) {
+        CK(cudaEventRecord(p->evf, s));
+        CK(cudaStreamWaitEvent(pt.stc, p->evf, 0));
+        CK(cudaStreamWaitEvent(pt.smac, p->evf, 0));
+        st = pt.stc;
+        sm = pt.smac;
+    }
+    if (!p->tcb.empty()) {
+        ST(kmark(p, 2, 0, st));
+        for (const TcDirArgs& tg : p->tcb) {
+            CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_MAIN));
+            p->pacc.launches += (dst == DST_UPDATE || dst == DST_ISRA) ? 3 : 2;
+        }
+        ST(kmark(p, 2, 1, st));
+    }
+    if (p->nu_fft > 0) {
+        ST(kmark(p, 3, 0, sm));
+        CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
+        ST(kmark(p, 3, 1, sm));
         C2RArgs c{};
         c.dst = dst;
         c.in = p->Xh;
@@ -506,17 +662,17 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         c.xold = xold;
         c.norm = aux;
         c.eps = eps;
-        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, sm));
         p->pacc.launches += 3;
-    } else {
-        ST(mark(p, ST_BWD_MAC, s));
-        ST(mark(p, ST_C2R_UPD, s));
     }
+    if (split) {
+        CK(cudaEventRecord(p->evj, pt.stc));
+        CK(cudaEventRecord(p->evj2, pt.smac));
+        CK(cudaStreamWaitEvent(s, p->evj, 0));
+        CK(cudaStreamWaitEvent(s, p->evj2, 0));
+    }
+    ST(mark(p, ST_C2R_UPD, s));
     ST(mark(p, ST_DIR_BWD, s));
-    for (const TcDirArgs& tg : p->tcb) {
-        CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s));
-        p->pacc.launches += (dst == DST_UPDATE || dst == DST_ISRA) ? 3 : 2;
-    }
     for (const DirArgs& dg : p->dgroups) {
         CK(launch_dir_bwd(dg, src, img, img2, eps, dst, out, xold, aux, s));
         p->pacc.launches += 1;
@@ -759,6 +915,32 @@ const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 
 constexpr double kTcEff = 0.68;
 constexpr double kTcFixed = 5e-6;
 constexpr double kSmClock = 1.965e9;
+// SM partitions (§5.5): below the HBM limit a frequency-path MAC streams at a per-SM rate (measured r01 on 36-68 SMs
+// at c3: forward ~90 GB/s, backward ~112 GB/s per SM incl. its C2R), the tcgen05 kernel scales with its SM count;
+// running side by side costs ~0.45 ms of mutual interference (L2 / HBM) per projection at c3
+constexpr double kMacSmBps[2] = {90e9, 112e9};
+constexpr double kHbmPartBps = 6.4e12;
+constexpr double kSplitPenalty = 0.45e-3;
+
+// tensor-core SMs for direction d (0 forward, 1 backward), or 0 when one-after-the-other is predicted faster.
+// t_tc: the direction's tcgen05 time on the whole GPU; bytes: its transfer-matrix stream.
+int choose_partition(double t_tc, double bytes, int d, int num_sms) {
+    const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F");   // dev override (0 = one after the other)
+    if (ev) return atoi(ev);
+    const double serial = t_tc + bytes / kHbmBps;
+    double best = serial;
+    int best_s = 0;
+    for (int sm_tc = 16; sm_tc <= num_sms - 16; sm_tc += 8) {
+        const int sm_mac = num_sms - sm_tc;
+        const double t_mac = bytes / std::min(kHbmPartBps, kMacSmBps[d] * sm_mac);
+        const double t = std::max(t_tc * num_sms / sm_tc, t_mac) + kSplitPenalty;
+        if (t < best) {
+            best = t;
+            best_s = sm_tc;
+        }
+    }
+    return best < 0.97 * serial ? best_s : 0;
+}
 
 // ---- cost-balanced sharding ----
 // Per plane, as if one rank owned all of it: the path the hybrid cost model picks and its time per iteration.
@@ -965,11 +1147,9 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->rank = rank;
     p->world = world;
     p->nu_total = nz * nnum * nnum;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
     // ownership: cost-balanced contiguous unit ranges (every rank computes all of them from the full PSF), or the
     // even split with LFM_PLAN_EVEN_SHARDS
     p->rcut.assign(world + 1, 0);
@@ -1282,6 +1462,25 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             p->n_direct_planes += nzd;
             coef_bytes += 2 * cf.size() * sizeof(float);
         }
+        // §5.5: with planes on both the tensor cores and the frequency path, each projection runs its two halves side
+        // by side on disjoint SM partitions (green contexts) when the cost model says that beats running them one after
+        // the other; the tensor-core schedule of each direction is laid out for its partition
+        int tc_sms[2] = {p->num_sms, p->num_sms};
+        if (!(flags & LFM_PLAN_DEVICE_LOOP) && !getenv("LFM_SERIAL")) {
+            double t_tc = 0.0, units_fft = 0.0;
+            int nsimt = 0;
+            for (int z = zb; z <= ze; ++z) {
+                const double units = std::min<long long>(p->u1, (long long)(z + 1) * N2) - std::max<long long>(p->u0, (long long)z * N2);
+                if (plane_direct[z] == 2) t_tc += 0.5 * pt_alt[z];   // per direction
+                if (plane_direct[z] == 0) units_fft += units;
+                nsimt += plane_direct[z] == 1;
+            }
+            const double bytes = units_fft * N2 * g.nkappa * 8.0;   // M streamed once per direction
+            for (int d = 0; d < 2 && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
+                const int want = choose_partition(t_tc, bytes, d, p->num_sms);
+                if (want > 0 && green_split(p, dev, want, &p->part[d])) tc_sms[d] = p->part[d].sms_tc;
+            }
+        }
         // tensor-core direct planes: one merged launch per direction (LPT schedule over (plane, tile) items)
         {
             std::vector<int> zl, d1a, d1b, d2a, d2b;
@@ -1312,7 +1511,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 for (int w = 0; w < 2; ++w) {
                     TcDirArgs& t = w ? tb : ta;
                     std::vector<TcPlane> pls;
-                    if (!tcdir_geometry(&t, !w, d1a.data(), d1b.data(), d2a.data(), d2b.data(), &pls, p->num_sms))
+                    if (!tcdir_geometry(&t, !w, d1a.data(), d1b.data(), d2a.data(), d2b.data(), &pls, tc_sms[w]))
                         return guard(fail(LFM_EUNSUPPORTED, "tensor-core direct path needs Nnum^2 <= 256"));
                     float *cf = nullptr, *sr = nullptr, *pt = nullptr;
                     int* nzf = nullptr;
@@ -1505,6 +1704,10 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->tc_planes = p->direct ? 0 : p->n_tc_planes;
     info->tc_flops_executed = p->direct ? 0.0 : p->tc_flops_exec;
     info->planes_moved_for_memory = p->mem_moved;
+    for (int d = 0; d < 2; ++d) {
+        info->partition_sms[d][0] = p->part[d].sms_tc;
+        info->partition_sms[d][1] = p->part[d].sms_mac;
+    }
     info->tc_flops_algorithmic = p->direct ? 0.0 : p->tc_flops_alg;
     info->transfer_bytes = p->transfer_bytes;
     info->device_bytes = p->bytes;
@@ -1633,6 +1836,7 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
                 p->pacc.ms[st] += ms;
                 p->pacc.count[st] += 1;
             }
+            ST(read_kernel_timers(p));
         }
         if (ms_host) {
             float ms = 0.f;
@@ -1812,10 +2016,13 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                 p->mac_tc.g_fstride = sG;
                 p->mac_tc.Y = p->bY;
                 p->mac_tc.y_fstride = sY;
+                ST(kmark(p, 1, 0, s));
                 CK(launch_fwd_mac_batch_tc(p->mac_tc, F, p->num_sms, s));
             } else {
+                ST(kmark(p, 1, 0, s));
                 CK(launch_fwd_mac_batch(p->M, p->bG, sG, p->bY, sY, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
             }
+            ST(kmark(p, 1, 1, s));
             p->pacc.launches += 1;
         }
         ST(mark(p, ST_C2R_YHAT, s));
@@ -1854,7 +2061,9 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         ST(mark(p, ST_R2C_RATIO, s));
         ST(mark(p, ST_BWD_MAC, s));
         if (p->nu_fft > 0) {
+            ST(kmark(p, 3, 0, s));
             CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            ST(kmark(p, 3, 1, s));
             p->pacc.launches += 1;
         }
         ST(mark(p, ST_C2R_UPD, s));
@@ -1895,13 +2104,15 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         if (ms_host) CK(cudaEventRecord(p->ev1, s));
         CK(cudaMemcpyAsync(p->bhost, p->bent, 2 * F * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (p->prof)
+        if (p->prof) {
             for (int st = 0; st < LFM_N_STAGES; ++st) {
                 float ms = 0.f;
                 CK(cudaEventElapsedTime(&ms, p->pev[st], p->pev[st + 1]));
                 p->pacc.ms[st] += ms;
                 p->pacc.count[st] += 1;
             }
+            ST(read_kernel_timers(p, 0xA));   // the batched MACs (tensor-core planes run per frame)
+        }
         if (ms_host) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
@@ -1942,8 +2153,11 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
 
 lfm_status lfm_profile(lfm_plan p, int enable) {
     if (!p) return fail(LFM_EINVAL, "plan is NULL");
-    if (enable && !p->pev[0])
+    if (enable && !p->pev[0]) {
         for (auto& e : p->pev) CK(cudaEventCreate(&e));
+        for (auto& kv : p->kev)
+            for (auto& e : kv) CK(cudaEventCreate(&e));
+    }
     if (enable && !p->has_optics) return fail(LFM_EINVAL, "profiling times lfm_rl_iterate, which needs optics");
     p->prof = enable != 0;
     return LFM_OK;

@@ -151,10 +151,12 @@ cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int
 // from the per-(tap, chunk) nonzero flags of every plane: row masks, last windows, active counts (host)
 void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const std::vector<int>& nzflags,
                         std::vector<int>* rowmask);
+// launch pieces: stage the source (hi/lo split), the tcgen05 kernel (+ the backward update), the forward plane reduction
+enum { TC_PART_STAGE = 1, TC_PART_MAIN = 2, TC_PART_FINISH = 4, TC_PART_ALL = 7 };
 cudaError_t launch_tcdir_fwd(const TcDirArgs& d, const float* x, int src_image, float* y, int accumulate,
-                             cudaStream_t s);
+                             cudaStream_t s, int parts = TC_PART_ALL);
 cudaError_t launch_tcdir_bwd(const TcDirArgs& d, int src, const float* img, const float* img2, float eps, int dst,
-                             float* out, const float* xold, const float* norm, cudaStream_t s);
+                             float* out, const float* xold, const float* norm, cudaStream_t s, int parts = TC_PART_ALL);
 cudaError_t launch_plane_reduce(const float* part, int nzd, size_t hw, float* y, int accumulate, cudaStream_t s);
 cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, float* part, float* y, int accumulate,
                            cudaStream_t s);  // part: [nzd][H][W] scratch
@@ -183,8 +185,8 @@ cudaError_t launch_r2c_fast(const XformGeom& g, const float2* tw, const R2CArgs&
 cudaError_t launch_c2r_fast(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s);
 void set_fast_fft_enabled(bool on);
 // (kernels_mac.cu)
-cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad,
-                           int num_sms, cudaStream_t s);
+cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
+                           int partition, cudaStream_t s);   // partition: launch shape for an SM partition (§5.5)
 cudaError_t launch_bwd_mac(const float2* M, const float2* R, float2* Xh, int nkappa, int N2, int nu_pad,
                            cudaStream_t s);
 cudaError_t launch_fwd_mac_batch(const float2* M, const float2* G, long long g_fstride, float2* Y, long long y_fstride,

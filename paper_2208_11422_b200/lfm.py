@@ -62,10 +62,12 @@ class lfm_info(ctypes.Structure):
                 ("direct", ctypes.c_int), ("transfer_bytes", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
                 ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double),
-                ("planes_moved_for_memory", ctypes.c_int)]
+                ("planes_moved_for_memory", ctypes.c_int), ("partition_sms", (ctypes.c_int * 2) * 2)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["partition_sms"] = [[self.partition_sms[i][j] for j in range(2)] for i in range(2)]
+        return d
 
 
 _P = ctypes.c_void_p
@@ -113,7 +115,10 @@ LFM_N_STAGES = 11
 
 class lfm_profile_t(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * LFM_N_STAGES), ("count", ctypes.c_longlong * LFM_N_STAGES),
-                ("launches", ctypes.c_longlong), ("iterations", ctypes.c_longlong)]
+                ("launches", ctypes.c_longlong), ("iterations", ctypes.c_longlong),
+                ("kern_ms", ctypes.c_double * 4), ("kern_count", ctypes.c_longlong * 4)]
+
+KERNEL_NAMES = ["tc_fwd", "mac_fwd", "tc_bwd", "mac_bwd"]
 
 
 _lib_profile = _sig("lfm_profile", _i, [_P, _i])
@@ -359,7 +364,9 @@ class Plan:
         _check(_lib_profile_read(self._h, ctypes.byref(pr), 1 if reset else 0))
         return dict(ms={STAGE_NAMES[i]: pr.ms[i] for i in range(LFM_N_STAGES)},
                     count={STAGE_NAMES[i]: pr.count[i] for i in range(LFM_N_STAGES)},
-                    launches=pr.launches, iterations=pr.iterations)
+                    launches=pr.launches, iterations=pr.iterations,
+                    kern_ms={KERNEL_NAMES[i]: pr.kern_ms[i] for i in range(4)},
+                    kern_count={KERNEL_NAMES[i]: pr.kern_count[i] for i in range(4)})
 
     def quality(self, x, region=LFM_REGION_TRIANGLE, stream=None):
         _check_dev(x, (self.nz, self.height, self.width), "x")
