@@ -263,7 +263,7 @@ def run_ours(args):
     stage_ms = {k: prof["ms"][k] / max(1, prof["count"][k]) for k in prof["ms"]}
     # per-kernel launch times, CUDA events on the stream (SM partition) each kernel runs on
     kern_ms = {{"mac_fwd": "fwd_mac", "mac_bwd": "bwd_mac", "tc_fwd": "dir_fwd", "tc_bwd": "dir_bwd"}[k]:
-               prof["kern_ms"][k] / max(1, prof["kern_count"][k]) for k in prof["kern_ms"]}
+               max(1e-6, prof["kern_ms"][k] / max(1, prof["kern_count"][k])) for k in prof["kern_ms"]}
     parts = info["partition_sms"]     # [fwd, bwd] x [tensor-core SMs, MAC SMs]; 0 = whole GPU, one after the other
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     mac_sms = {"fwd_mac": parts[0][1] or nsm, "bwd_mac": parts[1][1] or nsm}

@@ -49,7 +49,9 @@ __device__ __forceinline__ void cmac4(const f8& m, const float4& g0, const float
 
 // Persistent: each CTA owns a contiguous range of (kappa, b') rows; G[kappa] is staged in shared
 // memory whenever kappa changes; one warp computes one row's dot product (lane-strided 32-byte loads,
-// NL in flight per lane = NL KB per warp), then a warp-shuffle reduction.  MINB CTAs per SM.
+// NL in flight per lane = NL KB per warp), then a warp-shuffle reduction.  MINB CTAs per SM.  A lane's vectors
+// j = 0, 1, 2, ... alternate between two accumulators in j order, so the result is bit-identical for every NL
+// and launch shape (the SM-partition and whole-GPU variants agree exactly).
 template <int NT, int NL, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fwd_mac_kernel(const float2* __restrict__ M, const float2* __restrict__ G,
                                                          float2* __restrict__ Y, int N2, int nu_pad, long long rows) {
@@ -84,9 +86,11 @@ __global__ void __launch_bounds__(NT, MINB) fwd_mac_kernel(const float2* __restr
                     cmac4(m[q + 1], gs[v + (q + 1) * 32], gs[nv + v + (q + 1) * 32], ar1, ai1);
                 }
             }
-            for (; v < nv; v += 32) {
+            // tail: vector j of the lane still goes to accumulator j & 1, so every NL sums in the same order
+            for (int jv = (v - lane) >> 5; v < nv; v += 32, ++jv) {
                 const f8 m = ld_stream8(mrow + v);
-                cmac4(m, gs[v], gs[nv + v], ar0, ai0);
+                if (jv & 1) cmac4(m, gs[v], gs[nv + v], ar1, ai1);
+                else cmac4(m, gs[v], gs[nv + v], ar0, ai0);
             }
             float ar = ar0 + ar1, ai = ai0 + ai1;
 #pragma unroll

@@ -107,6 +107,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // ============================ producer (both CTAs): TMA A windows + B halves ============================
             int na = 0, nb = 0;
             long long dbg_empty = 0, dbg_t0 = clock64();
+            // A windows and coefficient tiles are re-read from L2 by other CTAs (taps, pixel tiles): keep them there
+            // ahead of a concurrent MAC's evict-first stream (§5.5; LFM_TC_EXP bit 8 turns the hint off)
+            const uint64_t pol = tc::policy_evict_last();
+            const bool hint = !(d.exp & 8);
             for (int i = ib; i < ie; ++i) {
                 const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
                 const TcPlane pl = d.planes[zi];
@@ -128,8 +132,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         unsigned char* as = Abase + (size_t)sa * 2 * apart;
                         const int row = row0 + (pl.e1min + t1) * d.Wp;
                         if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullA[sa], 2 * 2 * (uint32_t)d.Arows * w * 4);
-                        tc::tma_load_3d_pair(as, am, 0, row, slab_hi, &bar_fullA[sa]);
-                        tc::tma_load_3d_pair(as + apart, am, 0, row, slab_lo, &bar_fullA[sa]);
+                        if (hint) {
+                            tc::tma_load_3d_pair_hint(as, am, 0, row, slab_hi, &bar_fullA[sa], pol);
+                            tc::tma_load_3d_pair_hint(as + apart, am, 0, row, slab_lo, &bar_fullA[sa], pol);
+                        } else {
+                            tc::tma_load_3d_pair(as, am, 0, row, slab_hi, &bar_fullA[sa]);
+                            tc::tma_load_3d_pair(as + apart, am, 0, row, slab_lo, &bar_fullA[sa]);
+                        }
                         for (int t2 = 0; t2 < pl.T2; ++t2, ++nb) {
                             const int sb = nb % kBSlots;
                             const long long c1 = (d.exp & 4) ? clock64() : 0;
@@ -138,8 +147,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             unsigned char* bs = Bbase + (size_t)sb * 2 * bhalf;
                             const int bslab = (int)(pl.coef_off + (long long)((t1 * pl.T2 + t2) * d.nch + c) * 2);
                             if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * w * 4);
-                            tc::tma_load_3d_pair(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb]);
-                            tc::tma_load_3d_pair(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb]);
+                            if (hint) {
+                                tc::tma_load_3d_pair_hint(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb], pol);
+                                tc::tma_load_3d_pair_hint(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb], pol);
+                            } else {
+                                tc::tma_load_3d_pair(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb]);
+                                tc::tma_load_3d_pair(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb]);
+                            }
                         }
                         ++na;
                     }

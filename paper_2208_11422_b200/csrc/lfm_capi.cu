@@ -402,7 +402,16 @@ inline lfm_status kmark(lfm_plan p, int k, int e, cudaStream_t s) {
     return LFM_OK;
 }
 
+// dev timing knob LFM_PART_SKIP (results are wrong with it set): 1 skips the tensor-core kernels, 2 the MACs, so that
+// either half of a partitioned projection can be timed alone on its partition
+int part_skip() {
+    static const int v = getenv("LFM_PART_SKIP") ? atoi(getenv("LFM_PART_SKIP")) : 0;
+    return v;
+}
+
 lfm_status read_kernel_timers(lfm_plan p, int mask = 0xF) {
+    mask &= part_skip() & 1 ? 0xA : 0xF;
+    mask &= part_skip() & 2 ? 0x5 : 0xF;
     for (int k = 0; k < 4; ++k) {
         if (!((mask >> k) & 1)) continue;
         const bool ran = (k & 1) ? p->nu_fft > 0 : !(k < 2 ? p->tcf.empty() : p->tcb.empty());
@@ -550,12 +559,12 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
             st = pt.stc;
             sm = pt.smac;
         }
-        if (!p->tcf.empty()) {
+        if (!p->tcf.empty() && !(part_skip() & 1)) {
             ST(kmark(p, 0, 0, st));
             for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_MAIN));
             ST(kmark(p, 0, 1, st));
         }
-        if (p->nu_fft > 0) {
+        if (p->nu_fft > 0 && !(part_skip() & 2)) {
             ST(kmark(p, 1, 0, sm));
             CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
                               split, sm));
@@ -641,7 +650,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         st = pt.stc;
         sm = pt.smac;
     }
-    if (!p->tcb.empty()) {
+    if (!p->tcb.empty() && !(part_skip() & 1)) {
         ST(kmark(p, 2, 0, st));
         for (const TcDirArgs& tg : p->tcb) {
             CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_MAIN));
@@ -649,7 +658,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         }
         ST(kmark(p, 2, 1, st));
     }
-    if (p->nu_fft > 0) {
+    if (p->nu_fft > 0 && !(part_skip() & 2)) {
         ST(kmark(p, 3, 0, sm));
         CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
         ST(kmark(p, 3, 1, sm));
@@ -915,30 +924,40 @@ const double kDirFlops[kDirMaxD + 1] = {1.0, 6.0e12, 14.0e12, 22.0e12, 26.0e12, 
 constexpr double kTcEff = 0.68;
 constexpr double kTcFixed = 5e-6;
 constexpr double kSmClock = 1.965e9;
-// SM partitions (§5.5): below the HBM limit a frequency-path MAC streams at a per-SM rate (measured r01 on 36-68 SMs
-// at c3: forward ~90 GB/s, backward ~112 GB/s per SM incl. its C2R), the tcgen05 kernel scales with its SM count;
-// running side by side costs ~0.45 ms of mutual interference (L2 / HBM) per projection at c3
-constexpr double kMacSmBps[2] = {90e9, 112e9};
+// SM partitions (§5.5), fitted to r01 measurements at c3 (scripts/gpu_part_sweep.sh, 88-120 tensor-core SMs) in
+// terms of this cost model's own estimates (t_tc = 2.96 ms, 18.5 GB of transfer matrices per direction at c3):
+//   tcgen05 side by side with a MAC on S SMs = kTcPartEff * kTcConc[d] * t_tc * N / S;
+//   the MAC streams kMacSmBps[d] per SM alone (the whole GPU tops out at HBM), kMacConc[d] slower side by side,
+//   followed by its C2R (kC2rFull[d] on the whole GPU, scaled by N / SMs).
+constexpr double kTcPartEff = 1.0;
+constexpr double kTcConc[2] = {1.10, 1.16};
+constexpr double kMacSmBps[2] = {110e9, 136e9};
+constexpr double kMacConc[2] = {1.17, 1.12};
+constexpr double kC2rFull[2] = {0.02e-3, 0.15e-3};
 constexpr double kHbmPartBps = 6.4e12;
-constexpr double kSplitPenalty = 0.45e-3;
 
 // tensor-core SMs for direction d (0 forward, 1 backward), or 0 when one-after-the-other is predicted faster.
 // t_tc: the direction's tcgen05 time on the whole GPU; bytes: its transfer-matrix stream.
 int choose_partition(double t_tc, double bytes, int d, int num_sms) {
     const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F");   // dev override (0 = one after the other)
     if (ev) return atoi(ev);
-    const double serial = t_tc + bytes / kHbmBps;
+    const double serial = t_tc + bytes / kHbmBps + kC2rFull[d];
     double best = serial;
     int best_s = 0;
     for (int sm_tc = 16; sm_tc <= num_sms - 16; sm_tc += 8) {
         const int sm_mac = num_sms - sm_tc;
-        const double t_mac = bytes / std::min(kHbmPartBps, kMacSmBps[d] * sm_mac);
-        const double t = std::max(t_tc * num_sms / sm_tc, t_mac) + kSplitPenalty;
+        const double t_tcp = kTcConc[d] * kTcPartEff * t_tc * num_sms / sm_tc;
+        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps, kMacSmBps[d] * sm_mac) +
+                             kC2rFull[d] * num_sms / sm_mac;
+        const double t = std::max(t_tcp, t_mac);
         if (t < best) {
             best = t;
             best_s = sm_tc;
         }
     }
+    if (getenv("LFM_PLAN_VERBOSE"))
+        fprintf(stderr, "[lfm plan] direction %d: t_tc %.3f ms, MAC %.2f GB, serial %.3f ms, best %.3f ms at %d tc SMs\n",
+                d, t_tc * 1e3, bytes / 1e9, serial * 1e3, best * 1e3, best_s);
     return best < 0.97 * serial ? best_s : 0;
 }
 

@@ -81,6 +81,23 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst_smem, const void* tma
         : "memory");
 }
 
+// as tma_load_3d_pair with an L2 cache-policy hint (createpolicy), e.g. evict_last for tiles that other CTAs re-read
+// while a concurrent kernel streams through L2 (§5.5)
+__device__ __forceinline__ void tma_load_3d_pair_hint(void* dst_smem, const void* tmap, int c0, int c1, int c2,
+                                                      uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst_smem)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & 0xFEFFFFFFu), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

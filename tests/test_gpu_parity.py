@@ -615,3 +615,49 @@ def test_nccl_one_rank_identical(extra):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert (a[2]["stop_iter"], a[2]["best_iter"], a[2]["series"]) == (b[2]["stop_iter"], b[2]["best_iter"], b[2]["series"])
     assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [0, 32], ids=["eager", "graphs"])
+def test_sm_partitions_identical(flags, monkeypatch):
+    """§5.5: with the tensor-core planes and the frequency-path MAC side by side on disjoint SM partitions (green
+    contexts, forced here with LFM_TC_SMS_F / _B) every kernel computes the same sums in the same order as the
+    one-after-the-other plan (LFM_SERIAL): projections, the RL series and the volumes are bit-identical, eagerly
+    and inside captured graphs."""
+    cfg, h, hd, y = tiny_problem("c2", 2)
+    x = gen_volume(cfg, 3, np.float32)
+    r_img = np.asarray(y, np.float32) / np.float32(max(float(np.max(y)), 1.0)) + np.float32(0.5)
+    s = torch.cuda.Stream()
+    out = {}
+    with torch.cuda.stream(s):
+        for mode in ("serial", "split"):
+            if mode == "serial":
+                monkeypatch.setenv("LFM_SERIAL", "1")
+            else:
+                monkeypatch.delenv("LFM_SERIAL", raising=False)
+                monkeypatch.setenv("LFM_TC_SMS_F", "96")
+                monkeypatch.setenv("LFM_TC_SMS_B", "104")
+            with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+                info = plan.info()
+                if info["tc_planes"] == 0 or info["fft_units"] == 0:
+                    pytest.skip("c2 hybrid plan has no mixed tensor-core / frequency-path planes")
+                y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+                plan.forward(dev(x), y_d, stream=s)
+                xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                plan.backward(dev(r_img), xb_d, stream=s)
+                x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+                plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=2), stream=s)
+                res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=6), stream=s)
+                s.synchronize()
+                out[mode] = (info["partition_sms"], y_d.cpu().numpy(), xb_d.cpu().numpy(), res["series"],
+                             x_d.cpu().numpy())
+            monkeypatch.delenv("LFM_TC_SMS_F", raising=False)
+            monkeypatch.delenv("LFM_TC_SMS_B", raising=False)
+    ps, pp = out["serial"][0], out["split"][0]
+    assert ps == [[0, 0], [0, 0]]
+    assert pp[0][0] >= 96 and pp[1][0] >= 104 and pp[0][1] > 0 and pp[1][1] > 0
+    for a, b in zip(out["serial"][1:], out["split"][1:]):
+        if isinstance(a, list):
+            assert a == b
+        else:
+            assert np.array_equal(a, b)
