@@ -934,31 +934,53 @@ constexpr double kTcConc[2] = {1.10, 1.16};
 constexpr double kMacSmBps[2] = {110e9, 136e9};
 constexpr double kMacConc[2] = {1.17, 1.12};
 constexpr double kC2rFull[2] = {0.02e-3, 0.15e-3};
-constexpr double kHbmPartBps = 6.4e12;
+// HBM ceiling of a MAC partition (measured alone on 60-68 SMs: forward 6.3, backward 6.6 TB/s; side by side the
+// backward still reaches 6.7 TB/s, hence the higher backward figure before kMacConc)
+constexpr double kHbmPartBps[2] = {6.6e12, 7.5e12};
 
-// tensor-core SMs for direction d (0 forward, 1 backward), or 0 when one-after-the-other is predicted faster.
-// t_tc: the direction's tcgen05 time on the whole GPU; bytes: its transfer-matrix stream.
-int choose_partition(double t_tc, double bytes, int d, int num_sms) {
-    const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F");   // dev override (0 = one after the other)
-    if (ev) return atoi(ev);
+// predicted time of one direction (0 forward, 1 backward) of a projection whose tensor-core planes take t_tc on the
+// whole GPU and whose frequency-path planes stream `bytes`: run one after the other, or side by side on the best SM
+// partition (*best_s tensor-core SMs, 0 = one after the other)
+double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s) {
     const double serial = t_tc + bytes / kHbmBps + kC2rFull[d];
     double best = serial;
-    int best_s = 0;
+    *best_s = 0;
+    if (t_tc <= 0 || bytes <= 0) return serial;
     for (int sm_tc = 16; sm_tc <= num_sms - 16; sm_tc += 8) {
         const int sm_mac = num_sms - sm_tc;
-        const double t_tcp = kTcConc[d] * kTcPartEff * t_tc * num_sms / sm_tc;
-        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps, kMacSmBps[d] * sm_mac) +
+        const double t_tcp = kTcPartEff * kTcConc[d] * t_tc * num_sms / sm_tc;
+        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps[d], kMacSmBps[d] * sm_mac) +
                              kC2rFull[d] * num_sms / sm_mac;
         const double t = std::max(t_tcp, t_mac);
         if (t < best) {
             best = t;
-            best_s = sm_tc;
+            *best_s = sm_tc;
         }
     }
+    if (best >= 0.97 * serial) {   // not worth two green contexts
+        *best_s = 0;
+        return serial;
+    }
+    return best;
+}
+
+// SM partitions are used unless the plan runs the device-resident loop (its conditional graph body cannot hold
+// kernels of other contexts), the driver lacks green contexts, or LFM_SERIAL is set (dev)
+bool partitions_allowed(int flags) {
+    return !(flags & (LFM_PLAN_DEVICE_LOOP | LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT)) && !getenv("LFM_SERIAL") &&
+           green_api().ok;
+}
+
+// tensor-core SMs for direction d, or 0 when one-after-the-other is predicted faster
+int choose_partition(double t_tc, double bytes, int d, int num_sms) {
+    const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F");   // dev override (0 = one after the other)
+    if (ev) return atoi(ev);
+    int best_s = 0;
+    const double best = partition_time(t_tc, bytes, d, num_sms, &best_s);
     if (getenv("LFM_PLAN_VERBOSE"))
-        fprintf(stderr, "[lfm plan] direction %d: t_tc %.3f ms, MAC %.2f GB, serial %.3f ms, best %.3f ms at %d tc SMs\n",
-                d, t_tc * 1e3, bytes / 1e9, serial * 1e3, best * 1e3, best_s);
-    return best < 0.97 * serial ? best_s : 0;
+        fprintf(stderr, "[lfm plan] direction %d: t_tc %.3f ms, MAC %.2f GB, predicted %.3f ms at %d tc SMs\n", d,
+                t_tc * 1e3, bytes / 1e9, best * 1e3, best_s);
+    return best_s;
 }
 
 // ---- cost-balanced sharding ----
@@ -1485,7 +1507,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         // by side on disjoint SM partitions (green contexts) when the cost model says that beats running them one after
         // the other; the tensor-core schedule of each direction is laid out for its partition
         int tc_sms[2] = {p->num_sms, p->num_sms};
-        if (!(flags & LFM_PLAN_DEVICE_LOOP) && !getenv("LFM_SERIAL")) {
+        if (partitions_allowed(flags)) {
             double t_tc = 0.0, units_fft = 0.0;
             int nsimt = 0;
             for (int z = zb; z <= ze; ++z) {
