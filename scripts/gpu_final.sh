@@ -11,6 +11,6 @@ $CMD > gpurun_out/ncu_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launch-list rc=$?"
 python scripts/prof_step.py --iters 2 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"mac_kernel|tcdir_kernel" -s 4 -c 4 -o gpurun_out/prof_final python scripts/prof_step.py --iters 2 > gpurun_out/ncu_full.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"mac_kernel|tcdir_kernel" -s 6 -c 4 -o gpurun_out/prof_final python scripts/prof_step.py --iters 2 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 tail -3 gpurun_out/ncu_full.log
