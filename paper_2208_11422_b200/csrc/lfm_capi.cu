@@ -409,6 +409,24 @@ int part_skip() {
     return v;
 }
 
+// fork the caller's stream s onto the projection's two partition streams (*st tensor cores, *sm MAC)
+lfm_status fork(lfm_plan p, const lfm_plan_s::Part& pt, cudaStream_t s, cudaStream_t* st, cudaStream_t* sm) {
+    CK(cudaEventRecord(p->evf, s));
+    CK(cudaStreamWaitEvent(pt.stc, p->evf, 0));
+    CK(cudaStreamWaitEvent(pt.smac, p->evf, 0));
+    *st = pt.stc;
+    *sm = pt.smac;
+    return LFM_OK;
+}
+
+// s waits for everything issued so far on the partition stream ps
+lfm_status join(lfm_plan p, cudaStream_t ps, cudaEvent_t ev, cudaStream_t s) {
+    (void)p;
+    CK(cudaEventRecord(ev, ps));
+    CK(cudaStreamWaitEvent(s, ev, 0));
+    return LFM_OK;
+}
+
 lfm_status read_kernel_timers(lfm_plan p, int mask = 0xF) {
     mask &= part_skip() & 1 ? 0xA : 0xF;
     mask &= part_skip() & 2 ? 0x5 : 0xF;
@@ -552,13 +570,7 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
                           r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), s));
         ST(mark(p, ST_FWD_MAC, s));
         cudaStream_t st = s, sm = s;
-        if (split) {
-            CK(cudaEventRecord(p->evf, s));
-            CK(cudaStreamWaitEvent(pt.stc, p->evf, 0));
-            CK(cudaStreamWaitEvent(pt.smac, p->evf, 0));
-            st = pt.stc;
-            sm = pt.smac;
-        }
+        if (split) ST(fork(p, pt, s, &st, &sm));
         if (!p->tcf.empty() && !(part_skip() & 1)) {
             ST(kmark(p, 0, 0, st));
             for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_MAIN));
@@ -569,21 +581,21 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
             CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
                               split, sm));
             ST(kmark(p, 1, 1, sm));
+        }
+        // join the MAC partition, then the C2R on the whole GPU (on the small MAC partition it would lengthen the
+        // critical path), then the tensor-core partition
+        if (split) ST(join(p, pt.smac, p->evj2, s));
+        if (p->nu_fft > 0) {
             C2RArgs c{};
             c.dst = DST_IMAGE;
             c.in = p->Y;
             c.in_ld = N2;
             c.ntrans = N2;
             c.out = yimg;
-            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, sm));
+            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
             p->pacc.launches += 3;
         }
-        if (split) {
-            CK(cudaEventRecord(p->evj, pt.stc));
-            CK(cudaEventRecord(p->evj2, pt.smac));
-            CK(cudaStreamWaitEvent(s, p->evj, 0));
-            CK(cudaStreamWaitEvent(s, p->evj2, 0));
-        }
+        if (split) ST(join(p, pt.stc, p->evj, s));
         ST(mark(p, ST_C2R_YHAT, s));
         ST(mark(p, ST_DIR_FWD, s));
         bool acc = p->nu_fft > 0;
@@ -643,13 +655,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
     ST(mark(p, ST_BWD_MAC, s));
     cudaStream_t st = s, sm = s;
-    if (split) {
-        CK(cudaEventRecord(p->evf, s));
-        CK(cudaStreamWaitEvent(pt.stc, p->evf, 0));
-        CK(cudaStreamWaitEvent(pt.smac, p->evf, 0));
-        st = pt.stc;
-        sm = pt.smac;
-    }
+    if (split) ST(fork(p, pt, s, &st, &sm));
     if (!p->tcb.empty() && !(part_skip() & 1)) {
         ST(kmark(p, 2, 0, st));
         for (const TcDirArgs& tg : p->tcb) {
@@ -662,6 +668,9 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         ST(kmark(p, 3, 0, sm));
         CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
         ST(kmark(p, 3, 1, sm));
+    }
+    if (split) ST(join(p, pt.smac, p->evj2, s));   // C2R + update on the whole GPU, as in the forward
+    if (p->nu_fft > 0) {
         C2RArgs c{};
         c.dst = dst;
         c.in = p->Xh;
@@ -671,15 +680,10 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         c.xold = xold;
         c.norm = aux;
         c.eps = eps;
-        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, sm));
+        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
         p->pacc.launches += 3;
     }
-    if (split) {
-        CK(cudaEventRecord(p->evj, pt.stc));
-        CK(cudaEventRecord(p->evj2, pt.smac));
-        CK(cudaStreamWaitEvent(s, p->evj, 0));
-        CK(cudaStreamWaitEvent(s, p->evj2, 0));
-    }
+    if (split) ST(join(p, pt.stc, p->evj, s));
     ST(mark(p, ST_C2R_UPD, s));
     ST(mark(p, ST_DIR_BWD, s));
     for (const DirArgs& dg : p->dgroups) {
@@ -928,7 +932,7 @@ constexpr double kSmClock = 1.965e9;
 // terms of this cost model's own estimates (t_tc = 2.96 ms, 18.5 GB of transfer matrices per direction at c3):
 //   tcgen05 side by side with a MAC on S SMs = kTcPartEff * kTcConc[d] * t_tc * N / S;
 //   the MAC streams kMacSmBps[d] per SM alone (the whole GPU tops out at HBM), kMacConc[d] slower side by side,
-//   followed by its C2R (kC2rFull[d] on the whole GPU, scaled by N / SMs).
+//   its C2R (kC2rFull[d]) runs on the whole GPU after the join.
 constexpr double kTcPartEff = 1.0;
 constexpr double kTcConc[2] = {1.10, 1.16};
 constexpr double kMacSmBps[2] = {110e9, 136e9};
@@ -949,9 +953,8 @@ double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s
     for (int sm_tc = 16; sm_tc <= num_sms - 16; sm_tc += 8) {
         const int sm_mac = num_sms - sm_tc;
         const double t_tcp = kTcPartEff * kTcConc[d] * t_tc * num_sms / sm_tc;
-        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps[d], kMacSmBps[d] * sm_mac) +
-                             kC2rFull[d] * num_sms / sm_mac;
-        const double t = std::max(t_tcp, t_mac);
+        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps[d], kMacSmBps[d] * sm_mac);
+        const double t = std::max(t_tcp, t_mac) + kC2rFull[d];   // the C2R runs on the whole GPU after the join
         if (t < best) {
             best = t;
             *best_s = sm_tc;
