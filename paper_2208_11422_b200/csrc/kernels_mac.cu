@@ -6,6 +6,7 @@
 // Both stream M exactly once per call at 1 complex MAC (8 flop) per 8-byte element, so they are
 // bound by HBM bandwidth.  M is read with streaming (evict-first) 32-byte loads; every other operand
 // is small and L2/shared-memory resident.
+#include <algorithm>
 #include <cstdlib>
 
 #include "lfm_internal.cuh"
@@ -531,8 +532,14 @@ static cudaError_t fwd_mac_v(const float2* M, const float2* G, float2* Y, int nk
     cudaError_t e = cudaFuncSetAttribute(fwd_mac_kernel<NT, NL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+    // persistent: as many CTAs per SM as are resident at once (<= MINB; a large G[kappa] row in shared memory can
+    // allow fewer -- a non-resident CTA would run its static row range after the others)
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_mac_kernel<NT, NL, MINB>, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
     long long rows = (long long)nkappa * N2;
-    long long grid = (long long)num_sms * MINB;   // persistent: MINB CTAs per SM
+    long long grid = (long long)num_sms * std::min(per_sm, MINB);
     if (grid > rows) grid = rows;
     fwd_mac_kernel<NT, NL, MINB><<<(unsigned)grid, NT, smem, s>>>(M, G, Y, N2, nu_pad, rows);
     return cudaGetLastError();

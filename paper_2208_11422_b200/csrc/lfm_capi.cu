@@ -945,7 +945,7 @@ constexpr double kHbmPartBps[2] = {6.6e12, 7.5e12};
 // predicted time of one direction (0 forward, 1 backward) of a projection whose tensor-core planes take t_tc on the
 // whole GPU and whose frequency-path planes stream `bytes`: run one after the other, or side by side on the best SM
 // partition (*best_s tensor-core SMs, 0 = one after the other)
-double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s) {
+double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s, double mac_rate_scale = 1.0) {
     const double serial = t_tc + bytes / kHbmBps + kC2rFull[d];
     double best = serial;
     *best_s = 0;
@@ -953,7 +953,7 @@ double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s
     for (int sm_tc = 16; sm_tc <= num_sms - 16; sm_tc += 8) {
         const int sm_mac = num_sms - sm_tc;
         const double t_tcp = kTcPartEff * kTcConc[d] * t_tc * num_sms / sm_tc;
-        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps[d], kMacSmBps[d] * sm_mac);
+        const double t_mac = kMacConc[d] * bytes / std::min(kHbmPartBps[d], kMacSmBps[d] * mac_rate_scale * sm_mac);
         const double t = std::max(t_tcp, t_mac) + kC2rFull[d];   // the C2R runs on the whole GPU after the join
         if (t < best) {
             best = t;
@@ -975,11 +975,11 @@ bool partitions_allowed(int flags) {
 }
 
 // tensor-core SMs for direction d, or 0 when one-after-the-other is predicted faster
-int choose_partition(double t_tc, double bytes, int d, int num_sms) {
+int choose_partition(double t_tc, double bytes, int d, int num_sms, double mac_rate_scale) {
     const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F");   // dev override (0 = one after the other)
     if (ev) return atoi(ev);
     int best_s = 0;
-    const double best = partition_time(t_tc, bytes, d, num_sms, &best_s);
+    const double best = partition_time(t_tc, bytes, d, num_sms, &best_s, mac_rate_scale);
     if (getenv("LFM_PLAN_VERBOSE"))
         fprintf(stderr, "[lfm plan] direction %d: t_tc %.3f ms, MAC %.2f GB, predicted %.3f ms at %d tc SMs\n", d,
                 t_tc * 1e3, bytes / 1e9, best * 1e3, best_s);
@@ -1521,7 +1521,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             }
             const double bytes = units_fft * N2 * g.nkappa * 8.0;   // M streamed once per direction
             for (int d = 0; d < 2 && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
-                const int want = choose_partition(t_tc, bytes, d, p->num_sms);
+                // the partition's forward MAC keeps four 8-warp CTAs per SM in flight while G[kappa] fits four times in
+                // shared memory; fewer resident CTAs stream proportionally less (c4: 3 CTAs, ~81 GB/s per SM)
+                const double gsm = round_up((size_t)std::max(units_fft, 1.0), 16) * 8.0 + 1024.0;
+                const double scale = d == 0 ? std::min(4.0, std::floor(228.0 * 1024.0 / gsm)) / 4.0 : 1.0;
+                const int want = choose_partition(t_tc, bytes, d, p->num_sms, scale);
                 if (want > 0 && green_split(p, dev, want, &p->part[d])) tc_sms[d] = p->part[d].sms_tc;
             }
         }
