@@ -31,7 +31,7 @@ constexpr int kM = 128;            // pixels per CTA tile (TMEM lanes); a CTA pa
 constexpr int kKC = 32;            // phases per chunk (one 128-byte swizzle row)
 constexpr int kStagePB = 4;        // 32-pixel blocks per tc_stage_kernel CTA
 constexpr int kASlots = 2;         // A windows in flight (one per 32-phase chunk x tap row e1)
-constexpr int kBSlots = 4;         // coefficient tiles in flight (one per tap)
+constexpr int kBSlots = 5;         // coefficient tiles in flight (one per tap)
 constexpr int kDrainWarps = 8;     // warps 2..9: two per TMEM lane quarter, half of the columns each
 constexpr int kThreads = 32 * (2 + kDrainWarps);
 constexpr int kMaxNh = 128;        // columns per drainer thread
@@ -111,6 +111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // ahead of a concurrent MAC's evict-first stream (§5.5; LFM_TC_EXP bit 8 turns the hint off)
             const uint64_t pol = tc::policy_evict_last();
             const bool hint = !(d.exp & 8);
+            const bool ranged = !(d.exp & 16);   // LFM_TC_EXP bit 16: full-width MMAs (no column ranges)
+            int gk = 0;                          // K-steps in the open drain group (mirrors the issuer)
             for (int i = ib; i < ie; ++i) {
                 const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
                 const TcPlane pl = d.planes[zi];
@@ -139,20 +141,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             tc::tma_load_3d_pair(as, am, 0, row, slab_hi, &bar_fullA[sa]);
                             tc::tma_load_3d_pair(as + apart, am, 0, row, slab_lo, &bar_fullA[sa]);
                         }
+                        const bool last_win = c * pl.T1 + t1 == pl.last_win;
                         for (int t2 = 0; t2 < pl.T2; ++t2, ++nb) {
                             const int sb = nb % kBSlots;
+                            const bool gstart = gk == 0;
+                            gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
+                            if ((last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k) gk = 0;
                             const long long c1 = (d.exp & 4) ? clock64() : 0;
                             if (nb >= kBSlots) tc::mbar_wait(&bar_emptyB[sb], ((nb / kBSlots) - 1) & 1);
                             if (d.exp & 4) dbg_empty += clock64() - c1;
                             unsigned char* bs = Bbase + (size_t)sb * 2 * bhalf;
                             const int bslab = (int)(pl.coef_off + (long long)((t1 * pl.T2 + t2) * d.nch + c) * 2);
+                            // B rows of this CTA: its half of the tile's MMA column range [n0, n0 + nn) (a drain
+                            // group's first stage runs full width: its MMA initialises every accumulator column)
+                            int brow = (int)rank * Nh;
+                            if (ranged && !gstart) {
+                                const int rg = d.trange[bslab >> 1];
+                                brow = (rg & 0xFFFF) + (int)rank * (rg >> 17);
+                            }
                             if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * w * 4);
                             if (hint) {
-                                tc::tma_load_3d_pair_hint(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb], pol);
-                                tc::tma_load_3d_pair_hint(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb], pol);
+                                tc::tma_load_3d_pair_hint(bs, bm, 0, brow, bslab, &bar_fullB[sb], pol);
+                                tc::tma_load_3d_pair_hint(bs + bhalf, bm, 0, brow, bslab + 1, &bar_fullB[sb], pol);
                             } else {
-                                tc::tma_load_3d_pair(bs, bm, 0, (int)rank * Nh, bslab, &bar_fullB[sb]);
-                                tc::tma_load_3d_pair(bs + bhalf, bm, 0, (int)rank * Nh, bslab + 1, &bar_fullB[sb]);
+                                tc::tma_load_3d_pair(bs, bm, 0, brow, bslab, &bar_fullB[sb]);
+                                tc::tma_load_3d_pair(bs + bhalf, bm, 0, brow, bslab + 1, &bar_fullB[sb]);
                             }
                         }
                         ++na;
@@ -169,6 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0 && rank == 0) {
             // ============================ MMA issuer (leader CTA, one thread) ============================
             const uint32_t idesc = tc::idesc_tf32(2 * kM, d.Ntile);
+            const bool ranged = !(d.exp & 16);
             long long dbg_full = 0, dbg_tfree = 0, dbg_t0 = clock64();
             int na = 0, nb = 0, g = 0, gk = 0;   // A windows, B tiles, drain group, K-steps in the open group
             for (int i = ib; i < ie; ++i) {
@@ -202,13 +216,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             tc::fence_after();
                             const uint32_t a_hi = a_hi0 + (uint32_t)t2 * rb, a_lo = a_lo0 + (uint32_t)t2 * rb;
                             const uint32_t b_hi = tc::smem_u32(Bbase + (size_t)sb * 2 * bhalf), b_lo = b_hi + bhalf;
-                            const uint32_t acc = tmem + (uint32_t)(j * 256);
-                            for (int k = 0; k < ks; ++k) {
+                            // column range of the tile (the zero columns outside it would only add exact zeros, so
+                            // the accumulated sums are bit-identical to full-width MMAs); full width at a group start
+                            uint32_t n0 = 0, nn = (uint32_t)d.Ntile, idesc_s = idesc;
+                            if (ranged && gk != 0) {
+                                const int rg = d.trange[(pl.coef_off >> 1) + (t1 * T2 + t2) * d.nch + c];
+                                n0 = (uint32_t)(rg & 0xFFFF);
+                                nn = (uint32_t)(rg >> 16);
+                                idesc_s = tc::idesc_tf32(2 * kM, (int)nn);
+                            }
+                            const uint32_t acc = tmem + (uint32_t)(j * 256) + n0;
+                            for (int k = 0; k < ks && nn > 0; ++k) {
                                 const uint64_t ah = tc::sdesc_swz(a_hi + 32 * k, rb), al = tc::sdesc_swz(a_lo + 32 * k, rb);
                                 const uint64_t bh = tc::sdesc_swz(b_hi + 32 * k, rb), bl = tc::sdesc_swz(b_lo + 32 * k, rb);
-                                tc::mma_tf32_pair(acc, ah, bh, idesc, (gk == 0 && k == 0) ? 0u : 1u);
-                                tc::mma_tf32_pair(acc, ah, bl, idesc, 1u);
-                                tc::mma_tf32_pair(acc, al, bh, idesc, 1u);
+                                tc::mma_tf32_pair(acc, ah, bh, idesc_s, (gk == 0 && k == 0) ? 0u : 1u);
+                                tc::mma_tf32_pair(acc, ah, bl, idesc_s, 1u);
+                                tc::mma_tf32_pair(acc, al, bh, idesc_s, 1u);
                             }
                             gk += ks;
                             tc::mma_commit_pair(&bar_emptyB[sb], 3);
@@ -469,8 +492,12 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const __grid_constant__ 
 //   forward : G_d[b' = n][a = chunk*32 + k],   d = -e        backward: G_d[b' = chunk*32 + k][a = n],   d = +e
 __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane pl, int z, const float* __restrict__ psf,
                                   int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out, int* __restrict__ nzflag) {
-    __shared__ int any;
-    if (threadIdx.x == 0) any = 0;
+    __shared__ int any, nmin, nmax;
+    if (threadIdx.x == 0) {
+        any = 0;
+        nmin = 1 << 30;
+        nmax = -1;
+    }
     __syncthreads();
     const int tileid = blockIdx.x;   // tap * nch + chunk
     const int chunk = tileid % d.nch;
@@ -497,10 +524,33 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
         tc::split_tf32(v, h, l);
         hi[e] = h;
         lo[e] = l;
-        if (v != 0.0f) any = 1;
+        if (v != 0.0f) {
+            any = 1;
+            atomicMin(&nmin, n);
+            atomicMax(&nmax, n);
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) nzflag[tileid] = any;
+    // nonzero flag of the tile = its nonzero B-row (N) range, packed nmin | (nmax + 1) << 16 (0: all zero)
+    if (threadIdx.x == 0) nzflag[tileid] = any ? (nmin | ((nmax + 1) << 16)) : 0;
+}
+
+// per-tile MMA column ranges (§5.3 column ranges): n0 | nn << 16, the nonzero B rows [nmin, nmax] widened to n0 a
+// multiple of 8 and nn a multiple of 16 (the pair MMA's N), inside [0, Ntile); nn = 0 for an all-zero tile
+void tcdir_ranges(const TcDirArgs& d, const std::vector<int>& nzflags, std::vector<int>* ranges) {
+    ranges->resize(nzflags.size());
+    for (size_t i = 0; i < nzflags.size(); ++i) {
+        const int f = nzflags[i];
+        if (!f) {
+            (*ranges)[i] = 0;
+            continue;
+        }
+        const int nmin = f & 0xFFFF, nend = f >> 16;
+        int n0 = nmin / 8 * 8;
+        int nn = (nend - n0 + 15) / 16 * 16;
+        if (n0 + nn > d.Ntile) n0 = d.Ntile - nn;
+        (*ranges)[i] = n0 | (nn << 16);
+    }
 }
 
 // ------------------------------------------------------------------------------------------------

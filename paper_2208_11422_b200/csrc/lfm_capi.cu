@@ -1587,6 +1587,23 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     CKG(cudaStreamSynchronize(s));
                     cudaFree(nzf);
                     tcdir_window_masks(t, &pls, flags_h, &rowmask);
+                    std::vector<int> ranges;
+                    tcdir_ranges(t, flags_h, &ranges);
+                    if (getenv("LFM_PLAN_VERBOSE")) {
+                        double sn = 0, nzt = 0;
+                        for (int r : ranges)
+                            if (r) {
+                                sn += r >> 16;
+                                ++nzt;
+                            }
+                        fprintf(stderr, "[lfm plan] tc %s: %zu tiles, %.0f nonzero, mean MMA width %.1f of %d\n",
+                                w ? "bwd" : "fwd", ranges.size(), nzt, nzt > 0 ? sn / nzt : 0.0, t.Ntile);
+                    }
+                    int* drg = nullptr;
+                    PG(dalloc(p, &drg, ranges.size() * sizeof(int), "tc column ranges"));
+                    p->dallocs.push_back(drg);
+                    CKG(cudaMemcpyAsync(drg, ranges.data(), ranges.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+                    t.trange = drg;
                     std::vector<int> ioff, items;
                     tcdir_schedule(t, pls, &ioff, &items);
                     TcPlane* dpl = nullptr;
@@ -1610,15 +1627,24 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     CKG(tcdir_encode(&t, !w));
                     CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
                     coef_bytes += nf * sizeof(float);
-                    if (!w)   // executed tensor flops of one projection: 3 pair MMAs per K-step of every nonzero window tap
+                    if (!w)   // executed tensor flops of one projection: 3 pair MMAs per K-step of every nonzero window
+                              // tap, over the tile's column range (full width at a drain group's first stage)
                         for (size_t zi = 0; zi < pls.size(); ++zi) {
                             const TcPlane& pl = pls[zi];
-                            double ks_all = 0;
+                            double col_ks = 0;
+                            int gk = 0;
                             for (int c = 0; c < t.nch; ++c)
-                                for (int t1 = 0; t1 < pl.T1; ++t1)
-                                    if ((rowmask[pl.mask_off + t1] >> c) & 1)
-                                        ks_all += (double)pl.T2 * (c == t.nch - 1 ? t.kst_last : 4);
-                            p->tc_flops_exec += (double)t.tiles * ks_all * 3.0 * 2.0 * 256.0 * t.Ntile * 8.0;
+                                for (int t1 = 0; t1 < pl.T1; ++t1) {
+                                    if (!((rowmask[pl.mask_off + t1] >> c) & 1)) continue;
+                                    for (int t2 = 0; t2 < pl.T2; ++t2) {
+                                        const int ks = c == t.nch - 1 ? t.kst_last : 4;
+                                        const int rg = ranges[(size_t)pl.coef_off / 2 + (size_t)(t1 * pl.T2 + t2) * t.nch + c];
+                                        col_ks += (double)ks * (gk == 0 ? t.Ntile : (rg >> 16));
+                                        gk += ks;
+                                        if ((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + 4 > t.chain_k) gk = 0;
+                                    }
+                                }
+                            p->tc_flops_exec += (double)t.tiles * col_ks * 3.0 * 2.0 * 256.0 * 8.0;
                             p->tc_active_frac += (double)pl.active_windows / (pl.T1 * t.nch) / pls.size();
                             const int z = zl[zi];
                             p->tc_flops_alg += 2.0 * (double)N2 * N2 * box1[z].D * box2[z].D * g.nh * g.nw;

@@ -128,6 +128,7 @@ struct TcDirArgs {
     float* part;              // polyphase [nzd][N2][nh][nw]: forward per-plane partials (tc_fwd_reduce_kernel sums
                               // and interleaves them), backward H^T r (update epilogues apply it afterwards)
     int chain_k;              // K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
+    const int* trange;        // [tiles] MMA column range per coefficient tile: n0 | nn << 16 (tcdir_ranges; device)
     alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, Arows, 1}, SWIZZLE_128B
     alignas(64) CUtensorMap bmap;   // 3-D {32, Ntile, nslabs} over coef, box {32, Ntile/2, 1}, SWIZZLE_128B
     int Arows;                      // A window rows: 128 + max T2 - 1
@@ -146,6 +147,8 @@ size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes)
 size_t tcdir_src_floats(const TcDirArgs& d, int fwd);
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd);
 cudaError_t tcdir_encode(TcDirArgs* d, int fwd);
+// per-tile MMA column ranges from the packed nonzero-row flags of tcdir_coef_kernel (host)
+void tcdir_ranges(const TcDirArgs& d, const std::vector<int>& nzflags, std::vector<int>* ranges);
 cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
                               int kw, int ch, int cw, int fwd, float* coef, int* nzflags, cudaStream_t s);
 // from the per-(tap, chunk) nonzero flags of every plane: row masks, last windows, active counts (host)

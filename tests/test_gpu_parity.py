@@ -661,3 +661,40 @@ def test_sm_partitions_identical(flags, monkeypatch):
             assert a == b
         else:
             assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,flags", [("s15", 18), ("c2", 0)], ids=["s15-all-tc", "c2-hybrid"])
+def test_tc_column_ranges_bit_identical(name, flags, monkeypatch):
+    """§5.3 column ranges: every tcgen05 MMA after a drain group's first runs only over its coefficient tile's nonzero
+    columns.  The skipped columns would add exact zeros, so projections and RL iterates are bit-identical to the
+    full-width MMAs (LFM_TC_EXP=16)."""
+    cfg, h, hd, y = tiny_problem(name, 2)
+    x = gen_volume(cfg, 3, np.float32)
+    r_img = np.asarray(y, np.float32) / np.float32(max(float(np.max(y)), 1.0)) + np.float32(0.5)
+    out = {}
+    for mode in ("full", "ranged"):
+        if mode == "full":
+            monkeypatch.setenv("LFM_TC_EXP", "16")
+        else:
+            monkeypatch.delenv("LFM_TC_EXP", raising=False)
+        with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+            info = plan.info()
+            if info["tc_planes"] == 0:
+                pytest.skip("plan has no tensor-core planes")
+            y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
+            plan.forward(dev(x), y_d)
+            xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            plan.backward(dev(r_img), xb_d)
+            x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+            res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=4))
+            torch.cuda.synchronize()
+            out[mode] = (y_d.cpu().numpy(), xb_d.cpu().numpy(), res["series"], x_d.cpu().numpy(),
+                         info["tc_flops_executed"])
+    a, b = out["full"], out["ranged"]
+    for u, v in zip(a[:4], b[:4]):
+        if isinstance(u, list):
+            assert u == v
+        else:
+            assert np.array_equal(u, v)
+    assert b[4] <= a[4]   # executed tensor flops never grow
