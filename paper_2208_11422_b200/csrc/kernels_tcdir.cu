@@ -179,8 +179,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            // ============================ MMA issuer (leader CTA, one thread) ============================
+        if (rank == 0) {
+            // ==================== MMA issuer (leader CTA, whole warp, one elected lane issues) ====================
+            // The loop runs converged on warp-uniform values, descriptors are built once per stage (+2 per 32-byte
+            // K-step), so each MMA costs a few uniform instructions: a single-thread issue loop cost ~75-95 cycles
+            // per MMA (scripts/tc_rate_test.cu), above the ~100-cycle MMAs of narrowed column ranges.
             const uint32_t idesc = tc::idesc_tf32(2 * kM, d.Ntile);
             const bool ranged = !(d.exp & 16);
             long long dbg_full = 0, dbg_tfree = 0, dbg_t0 = clock64();
@@ -226,19 +229,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                 idesc_s = tc::idesc_tf32(2 * kM, (int)nn);
                             }
                             const uint32_t acc = tmem + (uint32_t)(j * 256) + n0;
-                            for (int k = 0; k < ks && nn > 0; ++k) {
-                                const uint64_t ah = tc::sdesc_swz(a_hi + 32 * k, rb), al = tc::sdesc_swz(a_lo + 32 * k, rb);
-                                const uint64_t bh = tc::sdesc_swz(b_hi + 32 * k, rb), bl = tc::sdesc_swz(b_lo + 32 * k, rb);
-                                tc::mma_tf32_pair(acc, ah, bh, idesc_s, (gk == 0 && k == 0) ? 0u : 1u);
-                                tc::mma_tf32_pair(acc, ah, bl, idesc_s, 1u);
-                                tc::mma_tf32_pair(acc, al, bh, idesc_s, 1u);
-                            }
+                            const uint64_t ah = tc::sdesc_swz(a_hi, rb), al = tc::sdesc_swz(a_lo, rb);
+                            const uint64_t bh = tc::sdesc_swz(b_hi, rb), bl = tc::sdesc_swz(b_lo, rb);
+                            if (nn > 0)
+                                for (int k = 0; k < ks; ++k) {   // K-step k: start address + 32 k bytes = field + 2 k
+                                    const uint64_t dk = 2 * (uint64_t)k;
+                                    tc::mma_tf32_pair_elect(acc, ah + dk, bh + dk, idesc_s, (gk == 0 && k == 0) ? 0u : 1u);
+                                    tc::mma_tf32_pair_elect(acc, ah + dk, bl + dk, idesc_s, 1u);
+                                    tc::mma_tf32_pair_elect(acc, al + dk, bh + dk, idesc_s, 1u);
+                                }
                             gk += ks;
-                            tc::mma_commit_pair(&bar_emptyB[sb], 3);
-                            if (t2 == T2 - 1) tc::mma_commit_pair(&bar_emptyA[sa], 3);
+                            tc::mma_commit_pair_elect(&bar_emptyB[sb], 3);
+                            if (t2 == T2 - 1) tc::mma_commit_pair_elect(&bar_emptyA[sa], 3);
                             // close the drain group at the item's last stage or before it could exceed chain_k
                             if ((last_win && t2 == T2 - 1) || gk + kKC / 8 > d.chain_k) {
-                                tc::mma_commit_pair(&bar_acc[j], 3);
+                                tc::mma_commit_pair_elect(&bar_acc[j], 3);
                                 ++g;
                                 gk = 0;
                             }
@@ -247,7 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (d.exp & 4) {
+            if ((d.exp & 4) && lane == 0) {
                 long long* o = d.dbg + (size_t)blockIdx.x * 8;
                 o[0] = dbg_full;
                 o[1] = dbg_tfree;

@@ -121,6 +121,24 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t d_tmem, uint64_t a, uint6
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// warp-wide issue (§5.3): the calling warp is converged and every operand is warp-uniform; one elected lane issues.
+// Keeping the issuing loop uniform lets the compiler hold descriptors in uniform registers (no per-MMA waterfall loop
+// of ELECT / R2UR / BRA.U.ANY around a single-thread issue).
+__device__ __forceinline__ void mma_tf32_pair_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                    uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
 // pair commit: arrive once on the mbarrier at this offset in every CTA of `mask`
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(

@@ -13,7 +13,7 @@
 using namespace lfm;
 constexpr int NT = 240;
 
-__global__ void __cluster_dims__(2, 1, 1) rate(int mode, int R, long long* cyc) {
+__global__ void __cluster_dims__(2, 1, 1) rate(int mode, int R, long long* cyc, int n_mma) {
     extern __shared__ unsigned char sm_raw[];
     __shared__ uint64_t bar_st[3], bar_acc[2];
     __shared__ uint32_t tmem_base;
@@ -32,8 +32,43 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int mode, int R, long long* cyc) 
     tc::cluster_sync();
     tc::fence_after();
     const uint32_t tm = tmem_base;
-    if (threadIdx.x == 0 && rank == 0) {
-        const uint32_t idesc = tc::idesc_tf32(256, NT);
+    if (mode == 3 && threadIdx.x < 32 && rank == 0) {   // whole warp, uniform loop, elected issue, precomputed descs
+        const uint32_t idesc = tc::idesc_tf32(256, n_mma);
+        long long t0 = clock64();
+        int g = 0, gk = 0;
+        for (int it = 0; it < R; ++it) {
+            const int s = it % 3, j = g & 1;
+            if (it >= 3) tc::mbar_wait(&bar_st[s], ((it / 3) - 1) & 1);
+            if (gk == 0 && g >= 2) tc::mbar_wait(&bar_acc[j], ((g >> 1) - 1) & 1);
+            tc::fence_after();
+            const uint32_t a_hi = tc::smem_u32(sm + (size_t)s * 62 * 1024), a_lo = a_hi + 16384;
+            const uint32_t b_hi = a_hi + 32768, b_lo = b_hi + NT / 2 * 128;
+            const uint32_t acc = tm + (uint32_t)(j * 256);
+            const uint64_t ah0 = tc::sdesc_sw128(a_hi), al0 = tc::sdesc_sw128(a_lo);
+            const uint64_t bh0 = tc::sdesc_sw128(b_hi), bl0 = tc::sdesc_sw128(b_lo);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                tc::mma_tf32_pair_elect(acc, ah0 + 2 * k, bh0 + 2 * k, idesc, (gk == 0 && k == 0) ? 0u : 1u);
+                tc::mma_tf32_pair_elect(acc, ah0 + 2 * k, bl0 + 2 * k, idesc, 1u);
+                tc::mma_tf32_pair_elect(acc, al0 + 2 * k, bh0 + 2 * k, idesc, 1u);
+            }
+            gk += 4;
+            tc::mma_commit_pair_elect(&bar_st[s], 1);
+            if (gk >= 8) {
+                tc::mma_commit_pair_elect(&bar_acc[j], 1);
+                ++g;
+                gk = 0;
+            }
+        }
+        __shared__ uint64_t bar_end3;
+        if (threadIdx.x == 0) tc::mbar_init(&bar_end3, 1);
+        __syncwarp();
+        tc::mbar_fence_init();
+        tc::mma_commit_pair_elect(&bar_end3, 1);
+        tc::mbar_wait(&bar_end3, 0);
+        if (threadIdx.x == 0) cyc[0] = clock64() - t0;
+    } else if (mode < 3 && threadIdx.x == 0 && rank == 0) {
+        const uint32_t idesc = tc::idesc_tf32(256, n_mma);
         long long t0 = clock64();
         int g = 0, gk = 0;
         for (int it = 0; it < R; ++it) {
@@ -81,19 +116,20 @@ int main() {
     cudaMalloc(&d, 8);
     const int smem = 3 * 62 * 1024 + 1024;
     cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int mode = 0; mode < 3; ++mode) {
-        const int R = 2000;
-        rate<<<2, 128, smem>>>(mode, R, d);
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) {
-            printf("mode %d error %s\n", mode, cudaGetErrorString(e));
-            return 1;
+    for (int n_mma : {240, 208, 160, 128, 64}) {   // MMA N (B rows split across the pair): does the time scale with N?
+        for (int mode = 0; mode < 4; ++mode) {
+            const int R = 2000;
+            rate<<<2, 128, smem>>>(mode, R, d, n_mma);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) {
+                printf("mode %d error %s\n", mode, cudaGetErrorString(e));
+                return 1;
+            }
+            long long c;
+            cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+            printf("N %d mode %d: %lld cycles for %d stages (%.1f cyc/MMA; N/2 = %d)\n", n_mma, mode, c, R,
+                   (double)c / (R * 12), n_mma / 2);
         }
-        long long c;
-        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-        const double ideal = (double)R * 12 * 120;
-        printf("mode %d: %lld cycles for %d stages (%.1f cyc/MMA, ideal 120) -> %.1f%% of floor\n", mode, c, R,
-               (double)c / (R * 12), 100.0 * ideal / c);
     }
     return 0;
 }
