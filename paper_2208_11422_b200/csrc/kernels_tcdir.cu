@@ -274,14 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = ib; i < ie; ++i) {
             const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
             const TcPlane pl = d.planes[zi];
-            const int* rm = d.rowmask + pl.mask_off;
-            int gk = 0;
-            for (int st = 0, nst = pl.T1 * pl.T2 * d.nch; st < nst; ++st) {   // stages in (c, t1, t2) order
-                const int c = st / (pl.T1 * pl.T2), t1 = (st / pl.T2) % pl.T1, t2 = st % pl.T2;
-                if (!((rm[t1] >> c) & 1)) continue;
-                gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
-                if (!((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k)) continue;
-                gk = 0;
+            for (int gi = 0; gi < pl.ngroups; ++gi) {   // the item's drain groups (counted at plan time)
                 const int j = g & 1;
                 {
                     const long long c0 = (d.exp & 4) ? clock64() : 0;
@@ -720,6 +713,20 @@ void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const 
             pl.last_win = 0;
             pl.active_windows = 1;
         }
+        // drain groups of one item: the issuer's stage walk (c, t1 of nonzero windows, t2), closing a group at the
+        // last window's last tap or before it would exceed chain_k K-steps -- the drainers only need the count
+        pl.ngroups = 0;
+        for (int c = 0, gk = 0; c < d.nch; ++c)
+            for (int t1 = 0; t1 < pl.T1; ++t1) {
+                if (!(((*rowmask)[pl.mask_off + t1] >> c) & 1)) continue;
+                for (int t2 = 0; t2 < pl.T2; ++t2) {
+                    gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
+                    if ((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k) {
+                        ++pl.ngroups;
+                        gk = 0;
+                    }
+                }
+            }
         tile0 += (long long)pl.T1 * pl.T2 * d.nch;
     }
 }

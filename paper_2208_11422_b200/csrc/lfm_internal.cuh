@@ -105,6 +105,7 @@ struct TcPlane {
     int mask_off;               // rowmask[mask_off + t1]: bit c set if window (chunk c, tap row t1) has a nonzero tap
     int last_win;               // c * T1 + t1 of the last nonzero window
     int active_windows;         // number of nonzero windows
+    int ngroups;                // TMEM drain groups per (plane, tile) item (the issuer's stage walk, host-counted)
 };
 struct TcDirArgs {
     int N, H, W, nh, nw;
