@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
             }
         }
     } else if (warp == kMtPrep + 1) {
-        if (lane == 0) {   // ---- MMA issuer ----
+        {   // ---- MMA issuer: the whole warp on uniform values, one elected lane issues (§5.3) ----
             const uint32_t id1 = tc::idesc_tf32(kMtM, NB), id2 = tc::idesc_tf32(kMtM, 2 * F);
             int it = 0, g = 0, gk = 0;
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -154,15 +154,16 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
                     const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * sbytes), a_lo = a_hi + kMtATile;
                     const uint32_t b = a_hi + 2 * kMtATile;
                     const uint32_t acc = tmem + (uint32_t)(j * NSET);
-                    for (int k = 0; k < kMtKC / 8; ++k) {
-                        const uint64_t ah = tc::sdesc_sw128(a_hi + 32 * k), al = tc::sdesc_sw128(a_lo + 32 * k);
-                        const uint64_t bd = tc::sdesc_sw128(b + 32 * k);
-                        tc::mma_tf32(acc, ah, bd, id1, (gk == 0 && k == 0) ? 0u : 1u);                 // hi*hi | hi*lo
-                        tc::mma_tf32(acc + 4 * F, al, bd, id2, (gk == 0 && k == 0) ? 0u : 1u);         // lo*hi
+                    const uint64_t ah0 = tc::sdesc_sw128(a_hi), al0 = tc::sdesc_sw128(a_lo), bd0 = tc::sdesc_sw128(b);
+#pragma unroll
+                    for (int k = 0; k < kMtKC / 8; ++k) {   // K-step k: start address + 32 k bytes = field + 2 k
+                        const uint64_t dk = 2 * (uint64_t)k;
+                        tc::mma_tf32_elect(acc, ah0 + dk, bd0 + dk, id1, (gk == 0 && k == 0) ? 0u : 1u);          // hi*hi | hi*lo
+                        tc::mma_tf32_elect(acc + 4 * F, al0 + dk, bd0 + dk, id2, (gk == 0 && k == 0) ? 0u : 1u);  // lo*hi
                     }
-                    tc::mma_commit(&bar_empty[s]);
+                    tc::mma_commit_elect(&bar_empty[s]);
                     if (++gk == kMtChain || c == nchunks - 1) {
-                        tc::mma_commit(&bar_acc[j]);
+                        tc::mma_commit_elect(&bar_acc[j]);
                         ++g;
                         gk = 0;
                     }
