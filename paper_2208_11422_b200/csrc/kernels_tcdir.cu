@@ -36,7 +36,8 @@ constexpr int kDrainWarps = 8;     // warps 2..9: two per TMEM lane quarter, hal
 constexpr int kThreads = 32 * (2 + kDrainWarps);
 constexpr int kMaxNh = 128;        // columns per drainer thread
 constexpr uint32_t kTmemCols = 512;   // 2 accumulators x 256 columns
-constexpr int kChainK = 16;        // default K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
+constexpr int kChainK = 24;        // default K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
+                                   // (16 -> 24: -2 % tcgen05 time at c3; parity tests pass up to 32)
 
 // per-CTA smem: A windows (hi | lo, Arows = 128 + T2max - 1 rows of 128 B each part) and B tiles (hi | lo,
 // Ntile/2 rows each: the pair splits B along N); every part 1024-byte aligned (SWIZZLE_128B atoms)

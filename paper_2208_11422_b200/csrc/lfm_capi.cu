@@ -934,7 +934,7 @@ constexpr double kSmClock = 1.965e9;
 //   the MAC streams kMacSmBps[d] per SM alone (the whole GPU tops out at HBM), kMacConc[d] slower side by side,
 //   its C2R (kC2rFull[d]) runs on the whole GPU after the join.
 constexpr double kTcPartEff = 1.0;
-constexpr double kTcConc[2] = {0.96, 1.01};   // after the warp-uniform MMA issue (r01: 1.10, 1.16 before)
+constexpr double kTcConc[2] = {0.93, 0.95};   // warp-uniform MMA issue, 24-K-step drain groups (1.10, 1.16 before)
 constexpr double kMacSmBps[2] = {110e9, 136e9};
 constexpr double kMacConc[2] = {1.17, 1.12};
 constexpr double kC2rFull[2] = {0.02e-3, 0.15e-3};
