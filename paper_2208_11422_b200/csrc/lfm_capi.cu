@@ -248,6 +248,10 @@ struct lfm_plan_s {
     double* stats = nullptr;    // 3
     double* host = nullptr;     // pinned 8 doubles
     float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
+    // lfm_deconvolve_host: every improving iterate is converted and copied to the host on a side stream while the
+    // next iteration runs, so the call returns without a final 0.2-1.7 GB device-to-host copy
+    cudaStream_t scopy = nullptr;
+    cudaEvent_t evconv[3] = {nullptr, nullptr, nullptr};
     // CUDA-graph replay of one iteration (LFM_PLAN_GRAPHS): one graph per (cur, next) buffer pair,
     // keyed also by the measurement pointer and the policy scalars baked into the captured launches
     bool graphs = false;
@@ -485,6 +489,9 @@ void plan_free(lfm_plan p) {
     if (p->bhost) cudaFreeHost(p->bhost);
     if (p->host) cudaFreeHost(p->host);
     green_free(p);
+    if (p->scopy) cudaStreamDestroy(p->scopy);
+    for (cudaEvent_t e : p->evconv)
+        if (e) cudaEventDestroy(e);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     for (auto& e : p->pev)
@@ -1828,13 +1835,25 @@ lfm_status lfm_rl_step(lfm_plan p, const float* y, const float* x_in, float* x_o
     return LFM_OK;
 }
 
+lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, int* best_iter, int* stop_iter,
+                   double* series_host, float* ms_host, cudaStream_t s, float* host_mirror, bool* mirrored);
+
 lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy* pol, int* best_iter, int* stop_iter,
                           double* series_host, float* ms_host, void* stream) {
     g_err[0] = 0;
     if (!p || !y || !x || !best_iter || !stop_iter || !series_host) return fail(LFM_EINVAL, "NULL argument");
+    bool mirrored = false;
+    return rl_loop(p, y, x, pol, best_iter, stop_iter, series_host, ms_host, as_stream(stream), nullptr, &mirrored);
+}
+
+// the RL loop; host_mirror (single rank, host loop only): each improving iterate is written to x (device, image
+// layout) and copied to host_mirror on p->scopy while the next iteration runs; *mirrored tells whether host_mirror
+// holds x_best on return (the caller then skips its own copy)
+lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, int* best_iter, int* stop_iter,
+                   double* series_host, float* ms_host, cudaStream_t s, float* host_mirror, bool* mirrored) {
+    *mirrored = false;
     ST(check_policy(pol));
     if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the stop rule needs the DCT-entropy metric");
-    cudaStream_t s = as_stream(stream);
     ST(check_y(p, y, s));
     const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
     int cur = 0, best = -1;
@@ -1885,12 +1904,23 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         *stop_iter = hs.k;
         return LFM_OK;
     }
+    const bool mirror = host_mirror && !p->comm;
+    if (mirror && !p->scopy) {
+        CK(cudaStreamCreateWithFlags(&p->scopy, cudaStreamNonBlocking));
+        for (auto& e : p->evconv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    bool conv_pending[3] = {false, false, false};
+    int mirrored_buf = -1;
     double best_e = -INFINITY, prev = 0.0;
     int decreases = 0, k = 0, best_k = 0;
     for (;;) {
         ++k;
         int nxt = 0;
         while (nxt == cur || nxt == best) ++nxt;
+        if (conv_pending[nxt]) {   // the side stream may still read this buffer (an earlier best being mirrored)
+            CK(cudaStreamWaitEvent(s, p->evconv[nxt], 0));
+            conv_pending[nxt] = false;
+        }
         if (ms_host) CK(cudaEventRecord(p->ev0, s));
         if (p->graphs && !p->prof) {
             ST(step_graph(p, y, cur, nxt, pol, s));
@@ -1927,6 +1957,15 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
             best_e = e;
             best_k = k;
             best = nxt;
+            if (mirror) {   // iteration k is complete (synchronised above): convert + copy it on the side stream
+                ST(gather_to_image(p, p->xb[nxt], x, p->scopy));
+                CK(cudaEventRecord(p->evconv[nxt], p->scopy));
+                conv_pending[nxt] = true;
+                CK(cudaMemcpyAsync(host_mirror, x, (size_t)p->geo.nz * p->geo.H * p->geo.W * sizeof(float),
+                                   cudaMemcpyDeviceToHost, p->scopy));
+                mirrored_buf = nxt;
+                p->pacc.launches += 1;
+            }
         }
         cur = nxt;
         bool stop;
@@ -1937,8 +1976,14 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
         if (stop) break;
     }
     if (best < 0) best = cur;
-    ST(gather_to_image(p, p->xb[best], x, s));
-    CK(cudaStreamSynchronize(s));
+    if (mirror && mirrored_buf == best) {   // x and host_mirror already hold x_best once the side stream drains
+        CK(cudaStreamSynchronize(p->scopy));
+        *mirrored = true;
+    } else {
+        if (mirror) CK(cudaStreamSynchronize(p->scopy));   // no in-flight mirror may overwrite x after this point
+        ST(gather_to_image(p, p->xb[best], x, s));
+        CK(cudaStreamSynchronize(s));
+    }
     *best_iter = best_k;
     *stop_iter = k;
     return LFM_OK;
@@ -1956,8 +2001,16 @@ lfm_status lfm_deconvolve_host(lfm_plan p, const float* y_host, float* x_host, c
     if (!p->x_stage) ST(dalloc(p, &p->x_stage, V * sizeof(float), "x staging"));
     CK(cudaMemcpyAsync(p->y_stage, y_host, HW * sizeof(float), cudaMemcpyHostToDevice, s));
     if (pol->init_from_x) CK(cudaMemcpyAsync(p->x_stage, x_host, V * sizeof(float), cudaMemcpyHostToDevice, s));
-    ST(lfm_rl_iterate(p, p->y_stage, p->x_stage, pol, best_iter, stop_iter, series_host, ms_host, stream));
-    CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
+    // the host loop mirrors each improving iterate into x_host while the next iteration runs (the device-resident
+    // loop has no per-iteration host step: it copies once at the end)
+    // (only into page-locked memory: a copy into pageable memory would block the host loop)
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, x_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();   // clear a possible error of the query
+    bool mirrored = false;
+    ST(rl_loop(p, p->y_stage, p->x_stage, pol, best_iter, stop_iter, series_host, ms_host, s,
+               (p->dloop || !pinned) ? nullptr : x_host, &mirrored));
+    if (!mirrored) CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return LFM_OK;
 }

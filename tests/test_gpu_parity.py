@@ -698,3 +698,22 @@ def test_tc_column_ranges_bit_identical(name, flags, monkeypatch):
         else:
             assert np.array_equal(u, v)
     assert b[4] <= a[4]   # executed tensor flops never grow
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,mode", [("tiny", "auto"), ("c2", "auto"), ("s15", "fixed")])
+def test_host_call_pinned_mirror(name, mode):
+    """lfm_deconvolve_host into page-locked memory: each improving iterate is converted and copied to the host on a
+    side stream while the next iteration runs, and the call skips its final copy.  The returned volume, series and
+    stop / best iterations equal the device call's."""
+    cfg, h, hd, y = tiny_problem(name, 5)
+    pol = L().make_policy(mode=mode, max_iters=30, n_iters=6)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
+        x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
+        r1 = plan.rl_iterate(dev(y), x_d, pol)
+        torch.cuda.synchronize()
+        xh_t = torch.full((cfg.nz, cfg.height, cfg.width), -1.0, dtype=torch.float32).pin_memory()
+        r2 = plan.deconvolve_host(np.ascontiguousarray(y, np.float32), xh_t.numpy(), pol)
+        assert (r1["stop_iter"], r1["best_iter"]) == (r2["stop_iter"], r2["best_iter"])
+        assert r1["series"] == r2["series"]
+        assert np.array_equal(xh_t.numpy(), x_d.cpu().numpy())
