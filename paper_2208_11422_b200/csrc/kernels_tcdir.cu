@@ -158,6 +158,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             int brow = (int)rank * Nh;
                             if (ranged && !gstart) {
                                 const int rg = d.trange[bslab >> 1];
+                                if (rg == 0) {   // all-zero tile: the issuer skips its MMAs, so nothing to load
+                                    if (rank == 0) tc::mbar_arrive(&bar_fullB[sb]);
+                                    continue;
+                                }
                                 brow = (rg & 0xFFFF) + (int)rank * (rg >> 17);
                             }
                             if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * w * 4);
