@@ -216,6 +216,207 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
     if (warp == 0) tc::tmem_dealloc(tmem, 2 * NSET <= 256 ? 256 : 512);
 }
 
+// ================================================================================================================
+// Frame-batched BACKWARD MAC on tcgen05: per kappa  Xh_f[u] = sum_b' conj(M[b'][u]) R_f[b'].
+// M[kappa] is [b'][u] complex (u contiguous), so with u' = (u, re/im) interleaved as the GEMM's M dimension and b' as
+// K, A[u'][b'] = M_float[b'][u'] is an MN-major operand (SWIZZLE_128B_BASE32B: the only MN-major tf32 layout),
+// loaded by TMA straight from the transfer matrices.  B rows n = 2f + p hold R_f's real (p = 0) / imaginary (p = 1)
+// parts, so D[u'][2f + p] = sum_b' A[u'][b'] R_p,f[b'] and, with (re, im) = rows (2u, 2u + 1),
+//   Re Xh = D[2u][2f] + D[2u+1][2f+1],   Im Xh = D[2u][2f+1] - D[2u+1][2f]     (conj(m) r, no extra factor).
+// 3xTF32 exactly as in the forward (A_hi raw, A_lo by the prep warps, B_hi | B_lo stacked).  Item = (kappa, 128 u').
+// ================================================================================================================
+namespace {
+constexpr int kBmKC = 32;                                   // K rows (b') per chunk
+__host__ __device__ inline uint32_t bm_stage(int F) { return 2 * kMtATile + mt_btile(F); }
+}  // namespace
+
+size_t bmac_tc_smem_bytes(int F) { return (size_t)mt_stages(F) * bm_stage(F) + 1024; }
+
+template <int F>
+__global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_constant__ BmacTcArgs d) {
+    constexpr int S = F >= 32 ? 4 : 5;
+    constexpr int NB = 4 * F;
+    constexpr int NSET = 6 * F;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar_fullA[S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
+    __shared__ uint32_t tmem_base;
+    const uint32_t raw = tc::smem_u32(smem_raw);
+    unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sbytes = bm_stage(F);
+    const int ntile = (2 * d.nu_pad + kMtM - 1) / kMtM;
+    const int nitems = d.nkappa * ntile;
+    const int nchunks = (d.N2 + kBmKC - 1) / kBmKC;
+    const int kst_last = ((d.N2 - (nchunks - 1) * kBmKC) + 7) / 8;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            tc::mbar_init(&bar_fullA[i], 1);
+            tc::mbar_init(&bar_ready[i], kMtPrep);
+            tc::mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bar_acc[i], 1);
+            tc::mbar_init(&bar_tfree[i], 4);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&d.tmapA);
+    }
+    if (warp == 0) tc::tmem_alloc(&tmem_base, 2 * NSET <= 256 ? 256 : 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- producer: A = 4 MN blocks of 32 u' x 32 b' (4 KB each) ----
+            int it = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                const int kap = item / ntile, t = item - kap * ntile;
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = it % S;
+                    if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
+                    unsigned char* st = smem + (size_t)s * sbytes;
+                    tc::mbar_arrive_expect_tx(&bar_fullA[s], kMtATile);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        tc::tma_load_3d(st + b * 4096, &d.tmapA, t * kMtM + 32 * b, c * kBmKC, kap, &bar_fullA[s]);
+                }
+            }
+        }
+    } else if (warp <= kMtPrep) {
+        // ---- prep warps: A_lo = rna_tf32(a - trunc_tf32(a)); stacked B_hi | B_lo rows (f, re/im) from R (global,
+        //      L2-resident: a kappa row of R is 225 x 8 bytes, not a TMA-legal stride) ----
+        constexpr int NP = 32 * kMtPrep;
+        constexpr int NA = (int)(kMtATile / 16) / NP;
+        constexpr int NE = (2 * F * kBmKC) / NP;
+        const int pt = threadIdx.x - 32;
+        int it = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            const int kap = item / ntile;
+            for (int c = 0; c < nchunks; ++c, ++it) {
+                const int s = it % S;
+                float2 rv[NE];
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {   // issued before the wait: overlaps the A tile's arrival
+                    const int e = pt + NP * i, n = e / kBmKC, k = e - (e / kBmKC) * kBmKC, bq = c * kBmKC + k;
+                    rv[i] = bq < d.N2 ? __ldg(d.R + (long long)(n >> 1) * d.r_fstride + (long long)kap * d.N2 + bq)
+                                      : make_float2(0.f, 0.f);
+                }
+                tc::mbar_wait(&bar_fullA[s], (it / S) & 1);
+                unsigned char* st = smem + (size_t)s * sbytes;
+                const float4* ahi = reinterpret_cast<const float4*>(st);
+                float4* alo = reinterpret_cast<float4*>(st + kMtATile);
+                unsigned char* bt = st + 2 * kMtATile;
+                float4 a[NA];
+#pragma unroll
+                for (int i = 0; i < NA; ++i) a[i] = ahi[pt + NP * i];
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {   // elementwise: the swizzle is irrelevant
+                    float4 l;
+                    l.x = tc::tf32_lo_of_trunc(a[i].x);
+                    l.y = tc::tf32_lo_of_trunc(a[i].y);
+                    l.z = tc::tf32_lo_of_trunc(a[i].z);
+                    l.w = tc::tf32_lo_of_trunc(a[i].w);
+                    alo[pt + NP * i] = l;
+                }
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {   // B element (n = 2f + p, k = b' in the chunk)
+                    const int e = pt + NP * i, n = e / kBmKC, k = e - (e / kBmKC) * kBmKC;
+                    const float v = (n & 1) ? rv[i].y : rv[i].x;
+                    float hi, lo;
+                    tc::split_tf32(v, hi, lo);
+                    *reinterpret_cast<float*>(bt + tc::sw128_off(n, k)) = hi;
+                    *reinterpret_cast<float*>(bt + tc::sw128_off(2 * F + n, k)) = lo;
+                }
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_ready[s]);
+            }
+        }
+    } else if (warp == kMtPrep + 1) {
+        {   // ---- MMA issuer: whole warp, uniform values, one elected lane issues ----
+            const uint32_t id1 = tc::idesc_tf32(kMtM, NB) | (1u << 15), id2 = tc::idesc_tf32(kMtM, 2 * F) | (1u << 15);
+            int it = 0, g = 0, gk = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = it % S, j = g & 1;
+                    tc::mbar_wait(&bar_ready[s], (it / S) & 1);
+                    if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
+                    tc::fence_after();
+                    const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * sbytes), a_lo = a_hi + kMtATile;
+                    const uint32_t b = a_hi + 2 * kMtATile;
+                    const uint32_t acc = tmem + (uint32_t)(j * NSET);
+                    // A: MN-major SWIZZLE_128B_BASE32B, LBO = 4 KB between 32-element M blocks, SBO = 512 B between
+                    // 4-row K groups; K-step k starts 8 rows = 1 KB further.  B: K-major SW128 (+32 B per K-step).
+                    const uint64_t ah0 = tc::sdesc(a_hi, 4096, 512) | ((uint64_t)1u << 61);
+                    const uint64_t al0 = tc::sdesc(a_lo, 4096, 512) | ((uint64_t)1u << 61);
+                    const uint64_t bd0 = tc::sdesc_sw128(b);
+                    const int ks = c == nchunks - 1 ? kst_last : kBmKC / 8;
+                    for (int k = 0; k < ks; ++k) {
+                        const uint64_t da = 64 * (uint64_t)k, db = 2 * (uint64_t)k;
+                        tc::mma_tf32_elect(acc, ah0 + da, bd0 + db, id1, (gk == 0 && k == 0) ? 0u : 1u);        // hi*hi | hi*lo
+                        tc::mma_tf32_elect(acc + 4 * F, al0 + da, bd0 + db, id2, (gk == 0 && k == 0) ? 0u : 1u);  // lo*hi
+                    }
+                    tc::mma_commit_elect(&bar_empty[s]);
+                    if (++gk == kMtChain || c == nchunks - 1) {
+                        tc::mma_commit_elect(&bar_acc[j]);
+                        ++g;
+                        gk = 0;
+                    }
+                }
+            }
+        }
+    } else {
+        // ---- drainers: TMEM -> fp32 running sums (2F per thread, row u'), pair (re, im) rows, epilogue ----
+        const int q = warp & 3;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+        float acc[2 * F];
+#pragma unroll
+        for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        int g = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            const int kap = item / ntile, t = item - kap * ntile;
+            for (int c0 = 0; c0 < nchunks; c0 += kMtChain) {
+                const int j = g & 1;
+                tc::mbar_wait(&bar_acc[j], (g >> 1) & 1);
+                ++g;
+                tc::fence_after();
+                const uint32_t base = lane_base + (uint32_t)(j * NSET);
+#pragma unroll
+                for (int b0 = 0; b0 < 3; ++b0) {
+#pragma unroll
+                    for (int c8 = 0; c8 < 2 * F; c8 += 8) {
+                        uint32_t v[8];
+                        tc::tmem_ld8_nowait(base + (uint32_t)(b0 * 2 * F + c8), v);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[c8 + u] += __uint_as_float(v[u]);
+                    }
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_tfree[j]);
+            }
+            const int row = t * kMtM + 32 * q + lane;   // u' = 2u + (re/im)
+            const int u = row >> 1;
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                const float oR = __shfl_down_sync(0xffffffffu, acc[2 * f], 1);       // odd (im) row's values
+                const float oI = __shfl_down_sync(0xffffffffu, acc[2 * f + 1], 1);
+                if (!(lane & 1) && u < d.nu_pad)
+                    d.Xh[(long long)f * d.x_fstride + (long long)kap * d.nu_pad + u] =
+                        make_float2(acc[2 * f] + oI, acc[2 * f + 1] - oR);
+            }
+#pragma unroll
+            for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * NSET <= 256 ? 256 : 512);
+}
+
 typedef CUresult (*MtEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -275,6 +476,42 @@ cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cuda
         default: return cudaErrorInvalidValue;
     }
 #undef LFM_MT
+    return cudaGetLastError();
+}
+
+// A: M as real floats {2 nu_pad (u'), N2 (b'), kappa}, box {32, 32, 1}, SWIZZLE_128B_ATOM_32B (the MN-major tf32
+// layout)
+cudaError_t bmac_tc_encode(BmacTcArgs* d, const float2* M) {
+    MtEncodeFn enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !enc || q != cudaDriverEntryPointSuccess) return e != cudaSuccess ? e : cudaErrorSymbolNotFound;
+    cuuint64_t dims[3] = {(cuuint64_t)2 * d->nu_pad, (cuuint64_t)d->N2, (cuuint64_t)d->nkappa};
+    cuuint64_t strides[2] = {(cuuint64_t)d->nu_pad * 8, (cuuint64_t)d->N2 * d->nu_pad * 8};
+    cuuint32_t box[3] = {32, (cuuint32_t)kBmKC, 1}, es[3] = {1, 1, 1};
+    CUresult r = enc(&d->tmapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(M), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bwd_mac_batch_tc(const BmacTcArgs& d, int F, int num_sms, cudaStream_t s) {
+    const size_t smem = bmac_tc_smem_bytes(F);
+    const int nitems = d.nkappa * ((2 * d.nu_pad + kMtM - 1) / kMtM);
+    const int grid = std::max(1, std::min(nitems, num_sms));
+    cudaError_t e;
+#define LFM_BM(FV)                                                                                           \
+    case FV:                                                                                                 \
+        e = cudaFuncSetAttribute(bmb_tc_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                      \
+        bmb_tc_kernel<FV><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        break;
+    switch (F) {
+        LFM_BM(8)
+        LFM_BM(16)
+        default: return cudaErrorInvalidValue;
+    }
+#undef LFM_BM
     return cudaGetLastError();
 }
 

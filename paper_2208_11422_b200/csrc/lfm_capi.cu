@@ -279,6 +279,9 @@ struct lfm_plan_s {
     bool mac_tc_ready = false, mac_tc_off = false;
     int mac_tc_F = 0;
     MacTcArgs mac_tc{};
+    // frame-batched backward MAC on tcgen05 (F = 8, 16), tensor maps re-encoded when the batch buffers change
+    BmacTcArgs bmac_tc{};
+    int bmac_F = 0;   // nonzero once the map is encoded
     // frame-batched lockstep buffers (lfm_rl_iterate_batch), capacity bcap frames
     int bcap = 0;
     float2 *bG = nullptr, *bXh = nullptr, *bY = nullptr, *bR = nullptr;
@@ -2189,7 +2192,22 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         ST(mark(p, ST_BWD_MAC, s));
         if (p->nu_fft > 0) {
             ST(kmark(p, 3, 0, s));
-            CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            if (!p->mac_tc_off && (F == 8 || F == 16) && !getenv("LFM_BWD_BATCH_SIMT")) {   // tcgen05 3xTF32
+                if (!p->bmac_F) {   // tensor map over the (backward) transfer matrices, once
+                    p->bmac_tc.nkappa = p->geo.nkappa;
+                    p->bmac_tc.N2 = N2;
+                    p->bmac_tc.nu_pad = p->nu_fft_pad;
+                    CK(bmac_tc_encode(&p->bmac_tc, p->Mb));
+                    p->bmac_F = F;
+                }
+                p->bmac_tc.Xh = p->bXh;
+                p->bmac_tc.x_fstride = sG;
+                p->bmac_tc.R = p->bR;
+                p->bmac_tc.r_fstride = sY;
+                CK(launch_bwd_mac_batch_tc(p->bmac_tc, F, p->num_sms, s));
+            } else {
+                CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+            }
             ST(kmark(p, 3, 1, s));
             p->pacc.launches += 1;
         }

@@ -212,6 +212,18 @@ cudaError_t mac_tc_encode_g(MacTcArgs* d, const float2* G, long long g_fstride, 
 size_t mac_tc_smem_bytes(int F);
 cudaError_t mac_tc_encode(MacTcArgs* d, const float2* M);
 cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cudaStream_t s);
+// frame-batched backward MAC on tcgen05 (MN-major transfer matrices, kernels_mac_tc.cu)
+struct BmacTcArgs {
+    int nkappa, N2, nu_pad;
+    float2* Xh;               // [F][kappa][nu_pad] complex, frame stride x_fstride
+    long long x_fstride;
+    const float2* R;          // [F][kappa][N2] complex, frame stride r_fstride
+    long long r_fstride;
+    alignas(64) CUtensorMap tmapA;   // M as floats {2 nu_pad, N2, kappa}, box {32, 32, 1}, SWIZZLE_128B_ATOM_32B
+};
+size_t bmac_tc_smem_bytes(int F);
+cudaError_t bmac_tc_encode(BmacTcArgs* d, const float2* M);
+cudaError_t launch_bwd_mac_batch_tc(const BmacTcArgs& d, int F, int num_sms, cudaStream_t s);
 // (kernels_misc.cu)
 cudaError_t launch_fill(float* p, size_t n, float v, cudaStream_t s);
 cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double* den, cudaStream_t s);

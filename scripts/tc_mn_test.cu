@@ -11,20 +11,23 @@
 using namespace lfm;
 constexpr int K = 32;
 
-__host__ __device__ inline uint32_t mn_off(int m, int k) {   // bytes, MN-major SW128 tile (M = 128, K = 32)
+// bytes, MN-major tile (M = 128, K = 32): variant 0/1 SWIZZLE_128B (16-byte chunks ^ row & 7); variant 2
+// SWIZZLE_128B_BASE32B (32-byte chunks ^ row & 3), the layout the CUTLASS builders require for MN-major tf32
+__host__ __device__ inline uint32_t mn_off(int m, int k, int variant) {
     const int b = m / 32, c = m % 32;
+    if (variant == 2) return (uint32_t)(b * 4096 + k * 128 + (((c >> 3) ^ (k & 3)) << 5) + (c & 7) * 4);
     return (uint32_t)(b * 4096 + k * 128 + ((((c * 4) >> 4) ^ (k & 7)) << 4) + ((c * 4) & 15));
 }
 __host__ __device__ inline uint32_t k_off(int n, int k) {   // bytes, K-major SW128 tile (rows n of 32 floats)
     return (uint32_t)(n * 128 + ((((k * 4) >> 4) ^ (n & 7)) << 4) + ((k * 4) & 15));
 }
-__device__ inline uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ inline uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
     d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1u << 46;
-    d |= (uint64_t)2u << 61;
+    d |= (uint64_t)layout << 61;
     return d;
 }
 
@@ -43,8 +46,8 @@ __global__ void tc_mn(const float* A, const float* B, float* C, int N, int varia
         const int m = e / K, k = e % K;
         float h, l;
         tc::split_tf32(A[e], h, l);
-        *reinterpret_cast<float*>(a_hi + mn_off(m, k)) = h;
-        *reinterpret_cast<float*>(a_lo + mn_off(m, k)) = l;
+        *reinterpret_cast<float*>(a_hi + mn_off(m, k, variant)) = h;
+        *reinterpret_cast<float*>(a_lo + mn_off(m, k, variant)) = l;
     }
     for (int e = threadIdx.x; e < N * K; e += blockDim.x) {
         const int n = e / K, k = e % K;
@@ -66,9 +69,10 @@ __global__ void tc_mn(const float* A, const float* B, float* C, int N, int varia
     if (threadIdx.x == 0) {
         const uint32_t idesc = tc::idesc_tf32(128, N) | (1u << 15);   // A MN-major
         for (int s = 0; s < K / 8; ++s) {
-            const uint32_t lbo = variant ? 1024 : 4096, sbo = variant ? 4096 : 1024;
-            const uint64_t ah = desc(tc::smem_u32(a_hi) + s * 1024, lbo, sbo);
-            const uint64_t al = desc(tc::smem_u32(a_lo) + s * 1024, lbo, sbo);
+            const uint32_t lbo = variant == 1 ? 1024 : 4096, sbo = variant == 1 ? 4096 : (variant == 2 ? 512 : 1024);
+            const uint32_t lay = variant == 2 ? 1u : 2u;
+            const uint64_t ah = desc(tc::smem_u32(a_hi) + s * 1024, lbo, sbo, lay);
+            const uint64_t al = desc(tc::smem_u32(a_lo) + s * 1024, lbo, sbo, lay);
             const uint64_t bh = tc::sdesc_sw128(tc::smem_u32(b_hi) + s * 32);
             const uint64_t bl = tc::sdesc_sw128(tc::smem_u32(b_lo) + s * 32);
             tc::mma_tf32(tm, ah, bh, idesc, s > 0);
@@ -97,7 +101,7 @@ __global__ void tc_mn(const float* A, const float* B, float* C, int N, int varia
 
 int main() {
     int fails = 0;
-    for (int variant = 0; variant < 2; ++variant)
+    for (int variant = 0; variant < 3; ++variant)
     for (int N : {32, 64}) {
         std::vector<float> A(128 * K), B(N * K), C(128 * N);
         srand(99 + N);
