@@ -1,6 +1,8 @@
-// Dev test (not product): tcgen05 kind::tf32 with an MN-major A operand (SWIZZLE_128B): A tile [M=128][K=32] stored
-// as 4 blocks of 32 M-elements, each [32 K rows][128 B] (8-row swizzle atoms), LBO = 4 KB between M blocks,
-// SBO = 1 KB between 8-row K groups; B K-major as in the product kernels.  C = A * B^T vs fp64, 1x and 3xTF32.
+// Dev test (not product): tcgen05 kind::tf32 with an MN-major A operand: A tile [M=128][K=32] stored as 4 blocks of
+// 32 M-elements, each [32 K rows][128 B]; B K-major as in the product kernels.  C = A * B^T vs fp64, 1x and 3xTF32.
+// Variants 0 / 1 (SWIZZLE_128B, 16-byte chunks ^ row & 7, LBO/SBO either way) leave the accumulator untouched;
+// variant 2 (SWIZZLE_128B_BASE32B: 32-byte chunks ^ row & 3, LBO = 4 KB, SBO = 512 B, layout type 1) is the valid
+// MN-major tf32 layout, used by the batched backward MAC (kernels_mac_tc.cu).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
