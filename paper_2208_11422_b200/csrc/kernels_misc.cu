@@ -31,40 +31,61 @@ cudaError_t launch_fill_dev(float* p, size_t n, const double* num, const double*
     return cudaGetLastError();
 }
 
-// image-order threads: pixel (z, p, q) of plane z belongs to unit z*N^2 + (p%N)*N + q%N
-__global__ void poly_image_kernel(const float* __restrict__ src, float* __restrict__ dst, XformGeom g, int ub, int uc,
-                                  int to_image) {
-    const int N = g.N, N2 = N * N;
-    const int zb = ub / N2, ze = (ub + uc - 1) / N2;
-    const size_t plane = (size_t)g.H * g.W;
-    const size_t total = (size_t)(ze - zb + 1) * plane;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        const int z = zb + (int)(e / plane);
-        const int pix = (int)(e % plane);
-        const int p = pix / g.W, q = pix % g.W;
-        const int u = z * N2 + (p % N) * N + (q % N);
-        if (u < ub || u >= ub + uc) continue;
-        const size_t pi = ((size_t)(u - ub) * g.nh + p / N) * g.nw + q / N;
-        const size_t ii = (size_t)z * plane + pix;
-        if (to_image)
-            dst[ii] = src[pi];
-        else
-            dst[pi] = src[ii];
+// Row-tiled layout conversion: one CTA per image row (z, p).  The row's pixels q = a2 + N m2 belong to the N units
+// u = z N^2 + (p mod N) N + a2, each a contiguous run of nw floats at coarse row m1 = p / N of the polyphase volume,
+// so both sides are read / written coalesced and the interleave happens in shared memory (W floats).
+template <bool TO_IMAGE>
+__global__ void __launch_bounds__(256) poly_image_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                              XformGeom g, int ub, int uc, int zb) {
+    extern __shared__ float rowbuf[];   // [N][nw]
+    const int N = g.N, N2 = N * N, nw = g.nw;
+    const int z = zb + (int)(blockIdx.x / g.H), p = (int)(blockIdx.x % g.H);
+    const int a1 = p % N, m1 = p / N;
+    const int u0 = z * N2 + a1 * N;   // unit of a2 = 0
+    const size_t ppix = (size_t)g.nh * nw;
+    float* row = dst + ((size_t)z * g.H + p) * g.W;
+    const float* irow = src + ((size_t)z * g.H + p) * g.W;
+    if (TO_IMAGE) {
+        for (int e = threadIdx.x; e < N * nw; e += blockDim.x) {
+            const int a2 = e / nw, m2 = e - a2 * nw, u = u0 + a2;
+            if (u >= ub && u < ub + uc) rowbuf[e] = src[(size_t)(u - ub) * ppix + (size_t)m1 * nw + m2];
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < g.W; q += blockDim.x) {
+            const int a2 = q % N, m2 = q / N, u = u0 + a2;
+            if (u >= ub && u < ub + uc) row[q] = rowbuf[a2 * nw + m2];
+        }
+    } else {
+        for (int q = threadIdx.x; q < g.W; q += blockDim.x) {
+            const int a2 = q % N, m2 = q / N;
+            rowbuf[a2 * nw + m2] = irow[q];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < N * nw; e += blockDim.x) {
+            const int a2 = e / nw, m2 = e - a2 * nw, u = u0 + a2;
+            if (u >= ub && u < ub + uc) dst[(size_t)(u - ub) * ppix + (size_t)m1 * nw + m2] = rowbuf[e];
+        }
     }
+}
+
+template <bool TO_IMAGE>
+static cudaError_t poly_image_rows(const float* src, float* dst, const XformGeom& g, int ub, int uc, cudaStream_t s) {
+    if (uc <= 0) return cudaSuccess;
+    const int N2 = g.N * g.N;
+    const int zb = ub / N2, ze = (ub + uc - 1) / N2;
+    const size_t smem = (size_t)g.N * g.nw * sizeof(float);
+    poly_image_rows_kernel<TO_IMAGE><<<(unsigned)((ze - zb + 1) * g.H), 256, smem, s>>>(src, dst, g, ub, uc, zb);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_poly_to_image(const float* xp, float* x, const XformGeom& g, int unit_begin, int unit_count,
                                  cudaStream_t s) {
-    if (unit_count <= 0) return cudaSuccess;
-    poly_image_kernel<<<2368, 256, 0, s>>>(xp, x, g, unit_begin, unit_count, 1);
-    return cudaGetLastError();
+    return poly_image_rows<true>(xp, x, g, unit_begin, unit_count, s);
 }
 
 cudaError_t launch_image_to_poly(const float* x, float* xp, const XformGeom& g, int unit_begin, int unit_count,
                                  cudaStream_t s) {
-    if (unit_count <= 0) return cudaSuccess;
-    poly_image_kernel<<<2368, 256, 0, s>>>(x, xp, g, unit_begin, unit_count, 0);
-    return cudaGetLastError();
+    return poly_image_rows<false>(x, xp, g, unit_begin, unit_count, s);
 }
 
 // z max-projection of the owned units of an image-layout volume (lfm_quality)
