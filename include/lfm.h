@@ -245,7 +245,10 @@ lfm_status lfm_rl_iterate_batch(lfm_plan plan, int frames, const float* y, float
                                 int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
 /* End-to-end call with HOST buffers: copies y in (H2D), runs lfm_rl_iterate, copies the argmax-E
- * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best). */
+ * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best).
+ * When x_host is page-locked (cudaHostAlloc / pinned) and the plan has a single rank, every improving iterate is
+ * copied into x_host on a side stream while the next iteration runs, so x_host holds intermediate iterates during
+ * the call and x_best when it returns (no final copy); pageable memory gets the single final copy. */
 lfm_status lfm_deconvolve_host(lfm_plan plan, const float* y_host, float* x_host, const lfm_policy* policy,
                                int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
