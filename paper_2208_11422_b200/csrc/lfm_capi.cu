@@ -2192,7 +2192,8 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         ST(mark(p, ST_BWD_MAC, s));
         if (p->nu_fft > 0) {
             ST(kmark(p, 3, 0, s));
-            if (!p->mac_tc_off && (F == 8 || F == 16) && !getenv("LFM_BWD_BATCH_SIMT")) {   // tcgen05 3xTF32
+            static const bool bwd_simt = getenv("LFM_BWD_BATCH_SIMT") != nullptr;   // dev: CUDA-core batched backward
+            if (!p->mac_tc_off && (F == 8 || F == 16) && !bwd_simt) {   // tcgen05 3xTF32
                 if (!p->bmac_F) {   // tensor map over the (backward) transfer matrices, once
                     p->bmac_tc.nkappa = p->geo.nkappa;
                     p->bmac_tc.N2 = N2;
