@@ -27,6 +27,8 @@ constexpr int kMtKC = 32;                 // K floats per chunk (16 complex unit
 constexpr int kMtChain = 4;               // chunks (x 4 K-steps) per drain group
 constexpr int kMtThreads = 448;           // 1 producer + 8 prep + 1 MMA + 4 drainer warps
 constexpr int kMtPrep = 8;
+constexpr int kMtPG = 2;                  // prep groups: group g of kMtPrep / kMtPG warps prepares chunks it % kMtPG == g
+                                          // (each warp's wait -> build -> fence -> arrive chain is serial per chunk)
 constexpr uint32_t kMtATile = kMtM * kMtKC * 4;   // 16 KB
 
 __host__ __device__ inline uint32_t mt_round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             tc::mbar_init(&bar_fullA[i], 1);
-            tc::mbar_init(&bar_ready[i], kMtPrep);
+            tc::mbar_init(&bar_ready[i], kMtPrep / kMtPG);
             tc::mbar_init(&bar_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -93,13 +95,14 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
         }
     } else if (warp <= kMtPrep) {
         // ---- prep warps: A_lo = rna_tf32(a - trunc_tf32(a)); stacked B_hi | B_lo from the frames' G ----
-        constexpr int NP = 32 * kMtPrep;                 // prep threads
+        constexpr int NP = 32 * kMtPrep / kMtPG;         // prep threads per group
         constexpr int NA = (int)(kMtATile / 16) / NP;    // float4 of the A tile per thread
         constexpr int NE = (2 * F * kMtKC) / NP;         // B elements per thread (per stacked half)
-        const int pt = threadIdx.x - 32;
+        const int pt = (threadIdx.x - 32) % NP, grp = (threadIdx.x - 32) / NP;
         int it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
             for (int c = 0; c < nchunks; ++c, ++it) {
+                if (it % kMtPG != grp) continue;
                 const int s = it % S;
                 tc::mbar_wait(&bar_fullA[s], (it / S) & 1);
                 unsigned char* st = smem + (size_t)s * sbytes;
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             tc::mbar_init(&bar_fullA[i], 1);
-            tc::mbar_init(&bar_ready[i], kMtPrep);
+            tc::mbar_init(&bar_ready[i], kMtPrep / kMtPG);
             tc::mbar_init(&bar_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -287,14 +290,15 @@ __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_cons
     } else if (warp <= kMtPrep) {
         // ---- prep warps: A_lo = rna_tf32(a - trunc_tf32(a)); stacked B_hi | B_lo rows (f, re/im) from R (global,
         //      L2-resident: a kappa row of R is 225 x 8 bytes, not a TMA-legal stride) ----
-        constexpr int NP = 32 * kMtPrep;
+        constexpr int NP = 32 * kMtPrep / kMtPG;
         constexpr int NA = (int)(kMtATile / 16) / NP;
         constexpr int NE = (2 * F * kBmKC) / NP;
-        const int pt = threadIdx.x - 32;
+        const int pt = (threadIdx.x - 32) % NP, grp = (threadIdx.x - 32) / NP;
         int it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
             const int kap = item / ntile;
             for (int c = 0; c < nchunks; ++c, ++it) {
+                if (it % kMtPG != grp) continue;
                 const int s = it % S;
                 float2 rv[NE];
 #pragma unroll
