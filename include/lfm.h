@@ -154,6 +154,15 @@ const char* lfm_version(void);
 /* Writes a fresh ncclUniqueId (128 bytes) into id_out (host).  Call on rank 0 only. */
 lfm_status lfm_comm_unique_id(unsigned char* id_out);
 
+/* Host-only: the SM partition the planner picks for one projection direction when its
+ * tensor-core planes take t_tc_ms on the whole GPU and its frequency-path planes stream mac_bytes of transfer
+ * matrices.  direction 0 forward, 1 backward; mac_rate_scale (0 < s <= 1) scales the MAC's per-SM rate (resident
+ * CTAs per SM).  *tc_sms = tensor-core SMs (0: the two halves run one after the other on the whole GPU);
+ * *predicted_ms (nullable) = the model's time of the projection's two halves.  The developer overrides
+ * LFM_TC_SMS_F / LFM_TC_SMS_B are not consulted here.  LFM_EINVAL for negative inputs or num_sms < 32. */
+lfm_status lfm_partition_model(double t_tc_ms, double mac_bytes, int direction, int num_sms, double mac_rate_scale,
+                               int* tc_sms, double* predicted_ms);
+
 /* Host-only: the contiguous unit range [*unit_begin, *unit_end) that `rank` of `world` owns among the
  * nz*N*N units (z-major u = z*N*N + a*N + b); the first (nu mod world) ranks own one extra unit
  * (S:334's even split, refined from planes to (z,a) units). */

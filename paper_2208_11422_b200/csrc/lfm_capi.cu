@@ -1127,6 +1127,21 @@ lfm_status lfm_comm_unique_id(unsigned char* id_out) {
     return LFM_OK;
 }
 
+lfm_status lfm_partition_model(double t_tc_ms, double mac_bytes, int direction, int num_sms, double mac_rate_scale,
+                               int* tc_sms, double* predicted_ms) {
+    g_err[0] = 0;
+    if (!tc_sms) return fail(LFM_EINVAL, "tc_sms is NULL");
+    if (t_tc_ms < 0 || mac_bytes < 0 || num_sms < 32 || (direction != 0 && direction != 1) || !(mac_rate_scale > 0) ||
+        mac_rate_scale > 1)
+        return fail(LFM_EINVAL, "lfm_partition_model: t_tc_ms, mac_bytes >= 0, direction 0/1, num_sms >= 32, "
+                                "0 < mac_rate_scale <= 1");
+    int s = 0;
+    const double t = partition_time(t_tc_ms * 1e-3, mac_bytes, direction, num_sms, &s, mac_rate_scale);
+    *tc_sms = s;
+    if (predicted_ms) *predicted_ms = t * 1e3;
+    return LFM_OK;
+}
+
 lfm_status lfm_shard_units(int nz, int nnum, int world, int rank, int* unit_begin, int* unit_end) {
     g_err[0] = 0;
     if (!unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");

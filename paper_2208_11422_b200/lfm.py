@@ -88,6 +88,7 @@ _lib_policy_default = _sig("lfm_policy_default", lfm_policy, [])
 _lib_last_error = _sig("lfm_last_error", ctypes.c_char_p, [])
 _lib_version = _sig("lfm_version", ctypes.c_char_p, [])
 _lib_shard_units = _sig("lfm_shard_units", _i, [_i, _i, _i, _i, _I, _I])
+_lib_partition_model = _sig("lfm_partition_model", _i, [ctypes.c_double, ctypes.c_double, _i, _i, ctypes.c_double, _I, _D])
 _lib_unique_id = _sig("lfm_comm_unique_id", _i, [ctypes.POINTER(ctypes.c_ubyte)])
 _lib_estimate = _sig("lfm_plan_estimate", _i, [_i, _i, _i, _i, _i, _i, _i, _i, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t])
@@ -126,7 +127,7 @@ _lib_profile_read = _sig("lfm_profile_read", _i, [_P, ctypes.POINTER(lfm_profile
 _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
-EXPORTED = ["lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
+EXPORTED = ["lfm_partition_model", "lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
             "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_set_memory_limit", "lfm_shard_units_balanced", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
@@ -216,6 +217,15 @@ def lfm_shard_units_balanced(psf, nnum, height, width, world, rank, flags=0):
 def lfm_set_memory_limit(nbytes):
     """Cap the device memory later plans may use (0 = free memory); see include/lfm.h."""
     _check(_lib_memlimit(int(nbytes)))
+
+
+def lfm_partition_model(t_tc_ms, mac_bytes, direction, num_sms=148, mac_rate_scale=1.0):
+    """(tensor-core SMs, predicted ms) the planner picks for one projection direction; host-only."""
+    sms = ctypes.c_int(0)
+    ms = ctypes.c_double(0.0)
+    _check(_lib_partition_model(float(t_tc_ms), float(mac_bytes), int(direction), int(num_sms), float(mac_rate_scale),
+                                ctypes.byref(sms), ctypes.byref(ms)))
+    return sms.value, ms.value
 
 
 def lfm_shard_units(nz, nnum, world, rank):
