@@ -3,6 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
     torchrun --nproc-per-node N ... bench.py --gpus N ...      (depth/phase sharding over NCCL)
+    torchrun --nproc-per-node N ... bench.py --config c5 ...   (time-lapse: frame replicas, frame-batched RL)
 
 A step is one RL iteration = every row of SURVEY §8(a) a2..a9 (forward projection, ratio, backward
 projection, multiplicative update, z max-projection, fp64 DCT entropy, stop-rule bookkeeping with the
@@ -46,7 +47,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the oracle's bounded CPU sample (~10-30 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="lfm_plan_create flags (2 = direct path)")
-    ap.add_argument("--frames", type=int, default=8, help="c5: frames per lockstep batch (2/4/8/16)")
+    ap.add_argument("--frames", type=int, default=16, help="c5: frames per GPU per lockstep batch (2/4/8/16)")
     return ap.parse_args()
 
 
@@ -110,11 +111,16 @@ class ClockSampler:
 def oracle_iteration_seconds(cfg, h64, x64, y64, rows):
     """Times the oracle's forward projection on `rows` output rows and its backward projection on the
     same rows of every plane (the two terms of one RL iteration), plus the full-size elementwise RL
-    update and metric, and extrapolates to one full iteration."""
+    update and metric, and extrapolates to one full iteration.  The oracle scans the PSF's per-plane
+    support once per call (a fixed cost a full-size call pays once, not once per row): it is timed on its own
+    (a forward call over zero rows scans every plane) and kept out of the per-row extrapolation."""
     from oracle import lfm_oracle as O
     H = cfg.height
     r0 = max(0, H // 2 - rows // 2)
     r1 = min(H, r0 + rows)
+    t0 = time.perf_counter()
+    O.forward_project(x64, h64, rows=(r0, r0))
+    t_scan = time.perf_counter() - t0
     t0 = time.perf_counter()
     O.forward_project(x64, h64, rows=(r0, r1))
     t_fwd = time.perf_counter() - t0
@@ -137,7 +143,16 @@ def oracle_iteration_seconds(cfg, h64, x64, y64, rows):
     O.ratio_image(y64, y64)
     t_el = time.perf_counter() - t0
     scale = H / (r1 - r0)
-    return (t_fwd + t_bwd) * scale + t_el, dict(t_fwd=t_fwd, t_bwd=t_bwd, t_elementwise=t_el, rows=r1 - r0)
+    # forward: one scan of every plane per call; backward: each per-plane call scans its own plane (all planes
+    # together: one scan of every plane)
+    per_iter = (max(t_fwd - t_scan, 0.0) + max(t_bwd - t_scan, 0.0)) * scale + 2 * t_scan + t_el
+    return per_iter, dict(t_fwd=t_fwd, t_bwd=t_bwd, t_scan=t_scan, t_elementwise=t_el, rows=r1 - r0)
+
+
+def oracle_flops_per_iteration(cfg):
+    """Multiply-adds of the oracle's direct convolution per RL iteration (forward + backward over each plane's
+    non-zero K(z) x K(z) support), 2 flops each: 4 H W sum_z K(z)^2."""
+    return 4.0 * cfg.height * cfg.width * sum(plane_support(cfg, z) ** 2 for z in range(cfg.nz))
 
 
 def cpu_cores():
@@ -159,19 +174,22 @@ def run_reference(args):
     x64 = gen_volume(cfg, 1, np.float64)
     y64 = lf_like(cfg, 7)
     O.build()
-    rows = max(2, min(cfg.height, 12 if cfg.height > 500 else cfg.height))
+    cores = cpu_cores()
+    rows = min(cfg.height, max(2, 4 * cores))   # >= 4 rows per core: every OpenMP thread gets work
     for _ in range(args.warmup):
         oracle_iteration_seconds(cfg, h64, x64, y64, rows)
     ts = [oracle_iteration_seconds(cfg, h64, x64, y64, rows)[0] for _ in range(args.steps)]
     sec = float(np.mean(ts))
     value = 1.0 / sec
     sample = (f"per step: oracle forward on {rows} of {cfg.height} output rows + backward on the same rows of all "
-              f"{cfg.nz} planes + full-size update/metric, extrapolated to one iteration")
+              f"{cfg.nz} planes + full-size update/metric, extrapolated to one iteration (the per-call PSF support "
+              f"scan timed separately and counted once)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg)},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "gflops": oracle_flops_per_iteration(cfg) * value / 1e9},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -299,13 +317,16 @@ def run_ours(args):
     if info.get("tc_planes", 0) > 0:
         pk = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
         ratio = 1.1 / 2.25   # tf32 / bf16 dense nominal (B200_PROFILING.md)
-        tf32_sus = pk.get("bf16_tflops_sustained", 2250.0 * 0.62) * ratio
-        tf32_burst = pk.get("bf16_tflops", 2250.0 * 0.76) * ratio
+        tf32_sus = pk.get("bf16_tflops_sustained", 1400.0) * ratio
+        tf32_burst = pk.get("bf16_tflops", 1590.0) * ratio
+        peak_src_tc = ("MEASURED_PEAKS.json bf16_tflops (burst: measured near the max SM clock this step runs at) x "
+                       "tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32" if "bf16_tflops" in pk else
+                       "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md) x 1.1/2.25, / 3")
         t = {k: kern_ms[k] for k in ("dir_fwd", "dir_bwd")}
         kk = max(t, key=lambda k: t[k])
         ex = info["tc_flops_executed"] / (t[kk] / 1e3) / 1e12
         al = info["tc_flops_algorithmic"] / (t[kk] / 1e3) / 1e12
-        peak3 = tf32_sus / 3.0   # an fp32-accurate contraction on tf32 tensor cores costs 3 products (3xTF32)
+        peak3 = tf32_burst / 3.0   # an fp32-accurate contraction on tf32 tensor cores costs 3 products (3xTF32)
         tc_traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -318,12 +339,14 @@ def run_ours(args):
                    "traffic": tc_traffic, "avg_launch_ms": t[kk],
                    "algorithmic_flops_per_launch": info["tc_flops_algorithmic"],
                    "achieved_is": "algorithmic fp32 flops (SURVEY 8(d): 2*H*W*K(z)^2 non-zero taps per plane) / kernel time",
-                   "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32",
-                   "executed_tensor_tflops": ex, "executed_frac_of_tf32_peak": ex / tf32_sus,
-                   "executed_frac_of_tf32_burst_peak": ex / tf32_burst,
-                   "peak_note": "the sustained bf16 GEMM of MEASURED_PEAKS ran power-capped (median "
-                                f"{pk.get('clocks_under_load', {}).get('sm_mhz_median', 'n/a')} MHz); this step's "
-                                "clocks are in 'clocks' -- compare executed_frac_of_tf32_burst_peak too",
+                   "peak_source": peak_src_tc,
+                   "frac_vs_sustained_peak": al / (tf32_sus / 3.0),
+                   "executed_tensor_tflops": ex, "executed_frac_of_tf32_burst_peak": ex / tf32_burst,
+                   "executed_frac_of_tf32_sustained_peak": ex / tf32_sus,
+                   "peak_note": "primary peak = the burst GEMM (this step runs near the max SM clock, see 'clocks'); "
+                                "the sustained GEMM of MEASURED_PEAKS ran power-capped (median "
+                                f"{pk.get('clocks_under_load', {}).get('sm_mhz_median', 'n/a')} MHz), its fraction "
+                                "is the secondary field",
                    "executed_is": "issued tcgen05 flops (3 TF32 products over the union tap boxes, skipped windows excluded)",
                    "tc_planes": info["tc_planes"], "kernel_ms": t}
     # the dominant kernel (longest average launch) carries the primary roofline
@@ -335,7 +358,7 @@ def run_ours(args):
     # e2e: the public host-buffer call, auto-stop deconvolution of the same measurement
     y_host = torch.from_numpy(y).pin_memory()
     x_host = torch.zeros((nz, H, W), dtype=torch.float32).pin_memory()
-    e2e_iters, e2e_s, auto, call_s = 0, 0.0, None, []
+    e2e_iters, e2e_s, auto, call_s, d2h = 0, 0.0, None, [], 0
     plan.deconvolve_host(y_host.numpy(), x_host.numpy(), L.make_policy(mode="auto", max_iters=50))   # warm-up
     for _ in range(max(1, args.e2e_calls)):
         if dist:
@@ -351,15 +374,21 @@ def run_ours(args):
         call_s.append(round(float(tt.item()), 4))
         e2e_iters += r["stop_iter"]
         auto = r
+        # device -> host bytes of this call: the 8-byte E_k read per iteration, and the volume copy of every
+        # improving iterate (the pinned-mirror host loop copies each new argmax iterate while the next iteration runs)
+        improving = sum(1 for i, e in enumerate(r["series"]) if e > max(r["series"][:i], default=-np.inf))
+        d2h += 8 * r["stop_iter"] + improving * nz * H * W * 4
     s = auto["series"]
     k = auto["stop_iter"]
     margin = min(abs(s[i] - s[i - 1]) / abs(s[i]) for i in range(1, k)) if k > 1 else None
     calls = max(1, args.e2e_calls)
     e2e = {"value": e2e_iters / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(H * W * 4 * calls / e2e_iters),
-           "d2h_bytes_per_step": int((nz * H * W * 4 + 8) * calls / e2e_iters),
-           "step": "one RL iteration of an auto-stop lfm_deconvolve_host call (host y in, host argmax volume out); "
-                   f"{calls} timed call(s) after one warm-up call, {e2e_iters} iterations", "call_s": call_s}
+           "d2h_bytes_per_step": int(d2h / e2e_iters),
+           "step": "one RL iteration of an auto-stop lfm_deconvolve_host call (host y in, host argmax volume out: "
+                   "each improving iterate is copied to the pinned host buffer on a side stream, plus 8 bytes of E_k "
+                   f"per iteration); {calls} timed call(s) after one warm-up call, {e2e_iters} iterations",
+           "call_s": call_s}
 
     out = None
     if rank == 0:
@@ -370,7 +399,10 @@ def run_ours(args):
             cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                    "sample": (f"oracle (fp64 direct conv, OpenMP) forward on {det['rows']} of {H} rows + backward on the "
                               f"same rows of all {nz} planes + full-size update/metric, extrapolated to one iteration "
-                              f"({det['t_fwd'] + det['t_bwd'] + det['t_elementwise']:.1f} s measured)")}
+                              f"({det['t_fwd'] + det['t_bwd'] + det['t_elementwise']:.1f} s measured; the per-call PSF "
+                              f"support scan, {det['t_scan']:.2f} s, counted once per call)"),
+                   "gflops": oracle_flops_per_iteration(cfg) / sec / 1e9,
+                   "gflops_is": "4*H*W*sum_z K(z)^2 direct-convolution flops per iteration / oracle seconds per iteration"}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -397,6 +429,8 @@ def run_ours(args):
             "roofline_mac": roof,
             "roofline_tc": roof_tc,
             "cpu_baseline": cpu,
+            "paper_context": "AutoDeconJ reports 4.4x faster deconvolution than the MATLAB GUI of Prevedel et al. 2014 "
+                             "(P:17, P:33); hardware, image size and iteration count not stated -- context only",
             "e2e": e2e,
             "gpu_launches": prof["launches"],
             "clocks": clk,
@@ -410,61 +444,104 @@ def run_ours(args):
 
 
 def run_c5(args):
-    """c5 (BASELINE configs[4]): time-lapse of c3-geometry frames, frame-batched lockstep RL.
-    value = frame-iterations/s over K lockstep iterations of one batch of F frames (fixed mode)."""
+    """c5 (BASELINE configs[4]): time-lapse of c3-geometry frames, frame-parallel across GPUs (one process per GPU,
+    each rank an independent replica of the plan holding its own slice of the frames; no per-iteration
+    communication -- SURVEY §8(e) "Frame parallelism (c5). Replicas only") and frame-batched lockstep RL within a
+    GPU.  A step = one lockstep iteration of every rank's batch of F frames (fixed mode); value = frame-
+    iterations/s of the whole job (world x F x K / max-over-ranks device time), "scaling": "weak".  After the timed
+    region every rank runs its batch to auto-stop and rank 0 gathers every frame's (stop, best) iterations."""
     import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2208_11422_b200 import lfm as L
     from lfm_inputs import gen_somata
     cfg = CONFIGS["c3"]
     F = args.frames
+    flags = args.flags or L.LFM_PLAN_FFT_ONLY   # DESIGN.md §5.2: batched frames amortise M; tcgen05 planes do not batch
+    side = torch.cuda.Stream()
+    torch.cuda.set_stream(side)
+    stream = torch.cuda.current_stream()
     h = gen_psf(cfg, np.float32)
-    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), flags=args.flags or 4)
+    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), flags=flags)
     info = plan.info()
     del h
     H, W, nz = cfg.height, cfg.width, cfg.nz
     rng = np.random.default_rng(7)
     phase = rng.uniform(0, 2 * np.pi, cfg.n_objects)
+    frames = [rank * F + f for f in range(F)]   # this rank's slice of the time-lapse
     ys = []
-    for f in range(F):   # soma intensities 1 + 0.5 sin(2 pi f / 64 + phi_i) (SURVEY §8(d)), noise seed 1000 + f
-        xt = torch.from_numpy(gen_somata(cfg, 1, np.float32, modulation=1 + 0.5 * np.sin(2 * np.pi * f / 64 + phase))).cuda()
+    for g in frames:   # soma intensities 1 + 0.5 sin(2 pi g / 64 + phi_i) (SURVEY §8(d)), noise seed 1000 + g
+        xt = torch.from_numpy(gen_somata(cfg, 1, np.float32, modulation=1 + 0.5 * np.sin(2 * np.pi * g / 64 + phase))).cuda()
         yh = torch.zeros((H, W), device="cuda")
         plan.forward(xt, yh)
         torch.cuda.synchronize()
-        ys.append(poisson(np.maximum(yh.cpu().numpy().astype(np.float64), 0), 1000 + f).astype(np.float32))
+        ys.append(poisson(np.maximum(yh.cpu().numpy().astype(np.float64), 0), 1000 + g).astype(np.float32))
         del xt
     yb = torch.from_numpy(np.stack(ys)).cuda()
     xb = torch.zeros((F, nz, H, W), device="cuda")
     plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.warmup))
-    plan.profile(True)
-    plan.profile_read(reset=True)
-    clocks = ClockSampler(0)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    if dist:
+        dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    ev0.record(stream)
     plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.steps, init_from_x=True))
-    ev1.record()
+    ev1.record(stream)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # per-stage breakdown: a profiled re-run of the same K iterations
+    plan.profile(True)
+    plan.profile_read(reset=True)
+    plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.steps, init_from_x=True))
     prof = plan.profile_read(reset=True)
     plan.profile(False)
     groups = {"transforms_x": "r2c_x", "fwd_mac_batch": "fwd_mac", "per_frame_forward_rest": "c2r_yhat",
               "bwd_mac_batch": "bwd_mac", "per_frame_update_rest": "c2r_update"}
     stage_ms = {g: prof["ms"][k] / max(1, prof["count"][k]) for g, k in groups.items()}
+    # the time-lapse result: every frame to auto-stop, (stop, best) gathered on rank 0 (volumes stay on their GPU)
     auto = plan.rl_iterate_batch(yb, xb, L.make_policy(mode="auto", max_iters=50))
-    line = {"metric": "frame-iterations/s (c5 time-lapse, frame-batched lockstep RL)", "value": F * args.steps / (ms / 1e3),
-            "unit": "frame-iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"c5: batch of {F} time-lapse frames of the c3 geometry (Nnum=15, 1005x1005, 51 planes)",
-                       "frames_per_batch": F, "plan_flags": args.flags or 4, "fft_units": info["fft_units"],
-                       "auto_stop": {"stop_iter": auto["stop_iter"], "best_iter": auto["best_iter"]},
-                       "batch_stage_avg_ms": stage_ms},
-            "gpu_launches": prof["launches"], "clocks": clk}
-    print(json.dumps(line), flush=True)
+    mine = [(g, auto["stop_iter"][i], auto["best_iter"][i]) for i, g in enumerate(frames)]
+    allf = [None] * world
+    if dist:
+        dist.all_gather_object(allf, mine)
+    else:
+        allf = [mine]
+    if rank == 0:
+        per_frame = sorted(x for part in allf for x in part)
+        line = {"metric": "frame-iterations/s (c5 time-lapse, frame-parallel replicas x frame-batched lockstep RL)",
+                "value": world * F * args.steps / (ms / 1e3), "unit": "frame-iterations/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"c5: time-lapse frames of the c3 geometry (Nnum=15, 1005x1005, 51 planes), "
+                                       f"{F} frames per GPU per lockstep batch, {world * F} frames in the job",
+                           "parallelism": f"frame replicas over {world} GPU(s), no per-iteration communication",
+                           "frames_per_batch": F, "plan_flags": flags, "fft_units": info["fft_units"],
+                           "l2": "inputs larger than L2: every batched pass streams the 58.9 GB transfer matrices",
+                           "auto_stop_per_frame": [{"frame": g, "stop_iter": st, "best_iter": b} for g, st, b in per_frame],
+                           "batch_stage_avg_ms": stage_ms},
+                "gpu_launches": prof["launches"], "clocks": clk}
+        print(json.dumps(line), flush=True)
     plan.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

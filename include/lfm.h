@@ -49,7 +49,8 @@ typedef enum {
     LFM_EINVAL = 1,   /* invalid argument / policy / NULL pointer                         */
     LFM_EDIM = 2,     /* H or W not divisible by N, even kernel or even N, size mismatch */
     LFM_ENEG = 3,     /* negative PSF entry or negative measurement                */
-    LFM_EZERO = 4,    /* all-zero measurement or a PSF that projects nothing             */
+    LFM_EZERO = 4,    /* all-zero measurement, an all-zero PSF plane or a PSF whose
+                         normalizer H^T 1 sums to 0 on this image (it projects nothing)              */
     LFM_ENOMEM = 5,   /* device memory budget exceeded; lfm_last_error names the limiting term */
     LFM_ECUDA = 6,    /* CUDA runtime error                                                        */
     LFM_ENCCL = 7,    /* NCCL error: any rank failure fails the whole run                  */

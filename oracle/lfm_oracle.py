@@ -11,7 +11,7 @@ Contents, in the paper's order:
   * projections  -- direct fp64 spatial convolution in C (lfm_oracle.c): forward H,
                     backward H^T, normalizer H^T 1
   * RL iteration -- classical Richardson-Lucy update (§1 names RL; the update formula is not
-                    printed -> reading C1): x <- x * H^T(y / (max(Hx,0)+eps)) / max(H^T 1, eps)
+                    printed -> reading C1): x <- x * H^T(y / (Hx+eps)) / max(H^T 1, eps)
   * metric       -- z max-projection, orthonormal DCT-II (Eqs. 1-4), Shannon entropy
                     (Eq. 5), cutoff region (Eqs. 6-11), DCT entropy (Eq. 12)
   * stop rule    -- "stop iteration when the DCT entropy value shows a decreasing trend",
@@ -177,9 +177,9 @@ def initial_volume(y, h, nz, H, W):
 
 
 def ratio_image(y, yhat, eps=EPS):
-    """r = y / (max(yhat,0) + eps) (reading C3 for eps; yhat >= 0 exactly here, the clamp
-    only mirrors the GPU's guard against FFT round-off and is a no-op in exact arithmetic)."""
-    return y / (np.maximum(yhat, 0.0) + eps)
+    """r = y / (yhat + eps) (reading C3 for eps).  yhat = H x is a sum of non-negative products
+    here, so it is >= 0 exactly; the GPU's clamp against FFT round-off (reading C19) has no counterpart."""
+    return y / (yhat + eps)
 
 
 def rl_step(x, y, h, norm, eps=EPS):

@@ -15,6 +15,7 @@
 // CTA = (kappa, half of the output phases): M = 128 rows b' in [128 h, 128 h + 128) (rows >= N^2 are TMA zero fill).
 // Warp roles: 0 TMA producer, 1-8 prep (A_lo + B build), 9 MMA issuer (one thread), 10-13 drainers / epilogue.
 #include <algorithm>
+#include <cstdlib>
 
 #include "lfm_internal.cuh"
 #include "tc_sm100.cuh"
@@ -27,22 +28,43 @@ constexpr int kMtKC = 32;                 // K floats per chunk (16 complex unit
 constexpr int kMtChain = 4;               // chunks (x 4 K-steps) per drain group
 constexpr int kMtThreads = 448;           // 1 producer + 8 prep + 1 MMA + 4 drainer warps
 constexpr int kMtPrep = 8;
-constexpr int kMtPG = 2;                  // prep groups: group g of kMtPrep / kMtPG warps prepares chunks it % kMtPG == g
-                                          // (each warp's wait -> build -> fence -> arrive chain is serial per chunk)
+// Prep groups: group g of kMtPrep / PG warps prepares the chunks it with it % PG == g (each warp's wait -> build ->
+// fence -> arrive chain is serial per chunk, so PG groups keep PG chunks in preparation).  The ring depth S is a
+// multiple of PG, so stage s = it % S always belongs to group s % PG: a group finishes chunk it (its fill phase has
+// completed) before it waits for the fill of chunk it + S on the same stage, and the parity (it / S) & 1 it waits on
+// is never a stale phase of another group's chunk.  (With an odd S = 5 the stage alternated between the groups: a
+// group could wait on chunk it + S's parity while chunk it's fill was still in flight, pass on the completed phase of
+// chunk it - S and read a half-written tile -- the fault seen with 4 groups in r01.)
 constexpr uint32_t kMtATile = kMtM * kMtKC * 4;   // 16 KB
+constexpr uint32_t kMtSmemMax = 232448;           // 227 KB per CTA
 
-__host__ __device__ inline uint32_t mt_round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
-__host__ __device__ inline uint32_t mt_btile(int F) { return mt_round1k((uint32_t)(4 * F) * kMtKC * 4); }
-__host__ __device__ inline uint32_t mt_gtile(int F) { return (uint32_t)F * kMtKC * 4; }   // F rows of 128 B
-__host__ __device__ inline uint32_t mt_stage(int F) { return 2 * kMtATile + mt_btile(F) + mt_round1k(mt_gtile(F)); }
-__host__ __device__ inline int mt_stages(int F) { return F >= 32 ? 4 : 5; }
+__host__ __device__ constexpr uint32_t mt_round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
+__host__ __device__ constexpr uint32_t mt_btile(int F) { return mt_round1k((uint32_t)(4 * F) * kMtKC * 4); }
+__host__ __device__ constexpr uint32_t mt_gtile(int F) { return (uint32_t)F * kMtKC * 4; }   // F rows of 128 B
+__host__ __device__ constexpr uint32_t mt_stage(int F) { return 2 * kMtATile + mt_btile(F) + mt_round1k(mt_gtile(F)); }
+// deepest ring that fits next to the 1 KB alignment slack, a multiple of the prep-group count, at most 8 stages
+__host__ __device__ constexpr int ring_depth(uint32_t stage_bytes, int PG) {
+    return (int)((kMtSmemMax - 1024) / stage_bytes) < 8 ? (int)((kMtSmemMax - 1024) / stage_bytes) / PG * PG : 8 / PG * PG;
+}
+__host__ __device__ constexpr int mt_stages(int F, int PG) { return ring_depth(mt_stage(F), PG); }
 }  // namespace
 
-size_t mac_tc_smem_bytes(int F) { return (size_t)mt_stages(F) * mt_stage(F) + 1024; }
+int mac_tc_prep_groups() {
+    static int pg = [] {
+        const char* e = getenv("LFM_MT_PG");
+        const int v = e ? atoi(e) : 2;
+        return v == 4 ? 4 : 2;
+    }();
+    return pg;
+}
 
-template <int F>
+size_t mac_tc_smem_bytes(int F) { return (size_t)mt_stages(F, mac_tc_prep_groups()) * mt_stage(F) + 1024; }
+
+template <int F, int PG>
 __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_constant__ MacTcArgs d) {
-    constexpr int S = F >= 32 ? 4 : 5;
+    constexpr int S = mt_stages(F, PG);
+    constexpr int kMtPG = PG;
+    static_assert(S >= PG && S % PG == 0, "each ring stage must belong to one prep group");
     constexpr int NB = 4 * F;       // rows of the stacked B tile (B_hi: 0..2F-1, B_lo: 2F..4F-1)
     constexpr int NSET = 6 * F;     // TMEM columns per accumulator set: hi*hi | hi*lo | lo*hi
     extern __shared__ unsigned char smem_raw[];
@@ -230,14 +252,18 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
 // ================================================================================================================
 namespace {
 constexpr int kBmKC = 32;                                   // K rows (b') per chunk
-__host__ __device__ inline uint32_t bm_stage(int F) { return 2 * kMtATile + mt_btile(F); }
+__host__ __device__ constexpr uint32_t bm_stage(int F) { return 2 * kMtATile + mt_btile(F); }
 }  // namespace
 
-size_t bmac_tc_smem_bytes(int F) { return (size_t)mt_stages(F) * bm_stage(F) + 1024; }
+__host__ __device__ constexpr int bm_stages(int F, int PG) { return ring_depth(bm_stage(F), PG); }
 
-template <int F>
+size_t bmac_tc_smem_bytes(int F) { return (size_t)bm_stages(F, mac_tc_prep_groups()) * bm_stage(F) + 1024; }
+
+template <int F, int PG>
 __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_constant__ BmacTcArgs d) {
-    constexpr int S = F >= 32 ? 4 : 5;
+    constexpr int S = bm_stages(F, PG);
+    constexpr int kMtPG = PG;
+    static_assert(S >= PG && S % PG == 0, "each ring stage must belong to one prep group");
     constexpr int NB = 4 * F;
     constexpr int NSET = 6 * F;
     extern __shared__ unsigned char smem_raw[];
@@ -467,11 +493,17 @@ cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cuda
     const size_t smem = mac_tc_smem_bytes(F);
     const int grid = std::max(1, std::min(2 * d.nkappa, num_sms));
     cudaError_t e;
-#define LFM_MT(FV)                                                                                           \
-    case FV:                                                                                                 \
-        e = cudaFuncSetAttribute(fmb_tc_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e != cudaSuccess) return e;                                                                      \
-        fmb_tc_kernel<FV><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+#define LFM_MT(FV)                                                                                                  \
+    case FV:                                                                                                        \
+        if (mac_tc_prep_groups() == 4) {                                                                            \
+            e = cudaFuncSetAttribute(fmb_tc_kernel<FV, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e != cudaSuccess) return e;                                                                         \
+            fmb_tc_kernel<FV, 4><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        } else {                                                                                                    \
+            e = cudaFuncSetAttribute(fmb_tc_kernel<FV, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e != cudaSuccess) return e;                                                                         \
+            fmb_tc_kernel<FV, 2><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        }                                                                                                           \
         break;
     switch (F) {
         LFM_MT(8)
@@ -504,11 +536,17 @@ cudaError_t launch_bwd_mac_batch_tc(const BmacTcArgs& d, int F, int num_sms, cud
     const int nitems = d.nkappa * ((2 * d.nu_pad + kMtM - 1) / kMtM);
     const int grid = std::max(1, std::min(nitems, num_sms));
     cudaError_t e;
-#define LFM_BM(FV)                                                                                           \
-    case FV:                                                                                                 \
-        e = cudaFuncSetAttribute(bmb_tc_kernel<FV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e != cudaSuccess) return e;                                                                      \
-        bmb_tc_kernel<FV><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+#define LFM_BM(FV)                                                                                                  \
+    case FV:                                                                                                        \
+        if (mac_tc_prep_groups() == 4) {                                                                            \
+            e = cudaFuncSetAttribute(bmb_tc_kernel<FV, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e != cudaSuccess) return e;                                                                         \
+            bmb_tc_kernel<FV, 4><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        } else {                                                                                                    \
+            e = cudaFuncSetAttribute(bmb_tc_kernel<FV, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e != cudaSuccess) return e;                                                                         \
+            bmb_tc_kernel<FV, 2><<<grid, kMtThreads, smem, s>>>(d);                                                 \
+        }                                                                                                           \
         break;
     switch (F) {
         LFM_BM(8)

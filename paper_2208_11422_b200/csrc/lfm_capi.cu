@@ -1235,6 +1235,15 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->nu_pad = (int)round_up((size_t)(p->nu > 0 ? p->nu : 1), 16);
     // PSF validation over the owned slice
     const size_t kk = (size_t)kh * kw;
+    // "at least one nonzero kernel per z": a plane that projects nothing is rejected (whole stack, so every
+    // rank reaches the same verdict; the scan stops at a plane's first nonzero entry)
+    for (int z = 0; z < nz; ++z) {
+        const float* hz = psf_host + (size_t)z * nnum * nnum * kk;
+        size_t i = 0;
+        const size_t n = (size_t)nnum * nnum * kk;
+        while (i < n && hz[i] == 0.0f) ++i;
+        if (i == n) return guard(fail(LFM_EZERO, "psf plane z=%d is all zero: it projects nothing (S:192)", z));
+    }
     const float* psf_own = psf_host + (size_t)p->u0 * kk;
     for (size_t i = 0, n = (size_t)p->nu * kk; i < n; ++i)
         if (!(psf_own[i] >= 0.0f)) return guard(fail(LFM_ENEG, "psf has a negative (or NaN) entry at unit %zu (S:192)", p->u0 + i / kk));
@@ -1371,14 +1380,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         // tensor-core direct (kernels_tcdir.cu): per direction, CTA pairs over 256-pixel tiles of the padded grid,
         // every tap x K-step = 3 pair MMAs of Ntile/2 cycles (tcgen05 floor), at the measured efficiency
         const int T1 = box1[z].dmax - box1[z].dmin + box1[z].D, T2 = box2[z].dmax - box2[z].dmin + box2[z].D;
-        const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 7) / 8;
-        const int ptiles = (g.nh * (g.nw + T2 - 1) + 255) / 256;
+        const int Ntile = (int)round_up((size_t)N2, 16);
         const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256 && T2 <= 65;
-        // the two edge tap rows are active for about half of the 32-phase chunks (window skipping, §5.3)
-        const double act = T1 >= 3 ? 1.0 - 1.0 / T1 : 1.0;
-        const double pair_cycles = (double)ptiles * T1 * T2 * act * ksteps * 3.0 * (Ntile / 2);
-        static const double tc_eff = getenv("LFM_TC_EFF") ? atof(getenv("LFM_TC_EFF")) : kTcEff;   // dev override
-        (void)pair_cycles;
         const double t_tc = tc_ok ? tc_plane_time(box1[z], box2[z], g, N2, p->num_sms) : 1e30;   // whole plane
         // device bytes per plane on each path (memory-aware planning below)
         pt_fft[z] = t_fft;
@@ -1733,7 +1736,12 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     CKG(cudaMemcpyAsync(p->norm_sum, p->stats, sizeof(double), cudaMemcpyDeviceToDevice, s));
     PG(allreduce(p, p->norm_sum, 1, ncclDouble, ncclSum, s));
     if (p->has_optics) PG(metric_alloc(&p->met, p->region, height, width, s, &p->bytes));
+    CKG(cudaMemcpyAsync(p->host, p->norm_sum, sizeof(double), cudaMemcpyDeviceToHost, s));
     CKG(cudaStreamSynchronize(s));
+    // c0 = sum y / sum H^T 1 (reading C2) needs sum H^T 1 > 0 (LFM_EZERO: "a PSF that projects nothing", lfm.h)
+    if (!(p->host[0] > 0.0) || !std::isfinite(p->host[0]))
+        return guard(fail(LFM_EZERO, "sum of H^T 1 = %g: the PSF projects nothing onto this %dx%d image", p->host[0],
+                          height, width));
     p->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     *out = p;
     return LFM_OK;
@@ -1916,7 +1924,9 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
             for (int i = 0; i < hs.k; ++i) ms_host[i] = ms / hs.k;   // per-iteration average (one graph launch)
         }
         p->pacc.iterations += hs.k;
-        ST(gather_to_image(p, p->xb[2], x, s));
+        // xb[2] holds the argmax iterate once some iteration improved E; if none did (e.g. NaN entropies) return the
+        // last iterate, as the host loop does
+        ST(gather_to_image(p, hs.best_k > 0 ? p->xb[2] : p->xb[(hs.k & 1) ? 1 : 0], x, s));
         CK(cudaStreamSynchronize(s));
         *best_iter = hs.best_k;
         *stop_iter = hs.k;
@@ -1927,6 +1937,14 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
         CK(cudaStreamCreateWithFlags(&p->scopy, cudaStreamNonBlocking));
         for (auto& e : p->evconv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    // every exit path (errors included) drains the side stream first: no queued conversion or copy into the
+    // caller's x / host_mirror may run after this call has returned (lfm.h: nothing is written after a failure)
+    struct DrainOnExit {
+        cudaStream_t st;
+        ~DrainOnExit() {
+            if (st) cudaStreamSynchronize(st);
+        }
+    } drain_guard{mirror ? p->scopy : nullptr};
     bool conv_pending[3] = {false, false, false};
     int mirrored_buf = -1;
     double best_e = -INFINITY, prev = 0.0;

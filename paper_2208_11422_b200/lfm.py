@@ -170,6 +170,14 @@ def _check_dev(t, shape, name):
         raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
 
 
+def _check_host(a, shape, name):
+    """Host buffers cross the ABI as raw pointers: the library reads / writes prod(shape) float32 values."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+        raise TypeError(f"{name} must be a C-contiguous float32 numpy array")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(a.shape)}, expected {tuple(shape)}")
+
+
 def lfm_policy_default():
     return _lib_policy_default()
 
@@ -354,6 +362,10 @@ class Plan:
 
     def deconvolve_host(self, y_host, x_host, policy, want_ms=False, stream=None):
         """End-to-end call with host buffers (numpy float32, ideally pinned torch CPU tensors)."""
+        _check_host(y_host, (self.height, self.width), "y_host")
+        _check_host(x_host, (self.nz, self.height, self.width), "x_host")
+        if not x_host.flags["WRITEABLE"]:
+            raise ValueError("x_host must be writeable")
         cap = max(policy.n_iters, policy.max_iters)
         series = (ctypes.c_double * cap)()
         ms = (ctypes.c_float * cap)() if want_ms else None

@@ -66,3 +66,17 @@ def test_no_cpu_fallback_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dp, f)).read()
                 assert "oracle" not in src.replace("no oracle", ""), f
+
+
+def test_host_buffer_checks():
+    """lfm_deconvolve_host takes raw host pointers: the binding rejects wrong dtype, shape or layout before the call
+    (the library would read H*W and write nz*H*W float32 values)."""
+    import numpy as np
+    from paper_2208_11422_b200 import lfm as L
+    L._check_host(np.zeros((9, 9), np.float32), (9, 9), "y")
+    with pytest.raises(TypeError):
+        L._check_host(np.zeros((9, 9), np.float64), (9, 9), "y")
+    with pytest.raises(ValueError):
+        L._check_host(np.zeros((2, 9, 8), np.float32), (2, 9, 9), "x")
+    with pytest.raises(TypeError):
+        L._check_host(np.zeros((9, 18), np.float32)[:, ::2], (9, 9), "y")

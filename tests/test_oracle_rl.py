@@ -129,3 +129,42 @@ def test_deconvolve_rejects_zero_measurement():
     h = np.ones((1, 3, 3, 3, 3)) / 9
     with pytest.raises(ValueError):
         O.deconvolve(np.zeros((9, 9)), h, O.Optics(nnum=3, **OPTICS), O.Policy())
+
+
+def test_deconvolve_returns_best_snapshot():
+    """S:299 snapshot correctness: the returned volume equals, bit for bit, the iterate obtained by re-running the
+    update best_iter times from the same init (here chained by hand from initial_volume and rl_step, outside the
+    loop's bookkeeping), and it is not the last iterate when the run went on past the best one."""
+    cfg = CONFIGS["tiny"]
+    h = gen_psf(cfg, np.float64)
+    optics = O.Optics(nnum=cfg.nnum, **OPTICS)
+    checked = 0
+    for seed in (1, 2, 3):
+        y = poisson(O.forward_project(gen_volume(cfg, seed), h), 100 + seed)
+        res = O.deconvolve(y, h, optics, O.Policy(mode="auto", max_iters=30))
+        norm = O.compute_normalizer(h, cfg.height, cfg.width)
+        x = O.initial_volume(y, h, cfg.nz, cfg.height, cfg.width)
+        chain = []
+        for _ in range(res.stop_iter):
+            x, _ = O.rl_step(x, y, h, norm)
+            chain.append(x)
+        assert np.array_equal(res.volume, chain[res.best_iter - 1])
+        if res.best_iter < res.stop_iter:
+            assert not np.array_equal(res.volume, chain[-1])
+            checked += 1
+    assert checked > 0
+
+
+def test_isra_start_closed_form():
+    """ISRA starts from x0 = H^T y (reading C23).  Closed form with two planes of delta PSFs of weights 1 and 2
+    (H x = x_0 + 2 x_1, H^T r = (r, 2 r)): x0 = (y, 2y), H x0 = 5y, H^T H x0 = (5y, 10y), so
+    x1 = x0 H^T y / H^T H x0 = (y/5, 2y/5).  A uniform start c would give (y/3, y/3) instead."""
+    rng = np.random.default_rng(7)
+    N, K, H = 3, 3, 12
+    h = np.zeros((2, N, N, K, K))
+    h[0, :, :, 1, 1] = 1.0
+    h[1, :, :, 1, 1] = 2.0
+    y = rng.poisson(20, (H, H)).astype(float) + 1.0
+    res = O.deconvolve(y, h, O.Optics(nnum=N, **OPTICS), O.Policy(mode="fixed", n_iters=1), update="isra")
+    np.testing.assert_allclose(res.volume[0], y / 5, rtol=1e-14)
+    np.testing.assert_allclose(res.volume[1], 2 * y / 5, rtol=1e-14)
