@@ -316,17 +316,17 @@ def run_ours(args):
     roof_tc = None
     if info.get("tc_planes", 0) > 0:
         pk = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
-        ratio = 1.1 / 2.25   # tf32 / bf16 dense nominal (B200_PROFILING.md)
-        tf32_sus = pk.get("bf16_tflops_sustained", 1400.0) * ratio
-        tf32_burst = pk.get("bf16_tflops", 1590.0) * ratio
-        peak_src_tc = ("MEASURED_PEAKS.json bf16_tflops (burst: measured near the max SM clock this step runs at) x "
-                       "tf32/bf16 nominal 1.1/2.25, / 3 for 3xTF32" if "bf16_tflops" in pk else
-                       "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md) x 1.1/2.25, / 3")
+        # the direct path runs kind::f16 MMAs (fp16 operands, fp32 accumulation) at the dense fp16 = bf16 rate
+        f16_sus = pk.get("bf16_tflops_sustained", 1400.0)
+        f16_burst = pk.get("bf16_tflops", 1590.0)
+        peak_src_tc = ("MEASURED_PEAKS.json bf16_tflops (burst, measured near the max SM clock this step runs at; "
+                       "fp16 = bf16 dense rate), / 3 for the 3-product fp16 split" if "bf16_tflops" in pk else
+                       "fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md), / 3")
         t = {k: kern_ms[k] for k in ("dir_fwd", "dir_bwd")}
         kk = max(t, key=lambda k: t[k])
         ex = info["tc_flops_executed"] / (t[kk] / 1e3) / 1e12
         al = info["tc_flops_algorithmic"] / (t[kk] / 1e3) / 1e12
-        peak3 = tf32_burst / 3.0   # an fp32-accurate contraction on tf32 tensor cores costs 3 products (3xTF32)
+        peak3 = f16_burst / 3.0   # an fp32-accurate contraction on fp16 tensor cores costs 3 products (3xFP16)
         tc_traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -340,14 +340,15 @@ def run_ours(args):
                    "algorithmic_flops_per_launch": info["tc_flops_algorithmic"],
                    "achieved_is": "algorithmic fp32 flops (SURVEY 8(d): 2*H*W*K(z)^2 non-zero taps per plane) / kernel time",
                    "peak_source": peak_src_tc,
-                   "frac_vs_sustained_peak": al / (tf32_sus / 3.0),
-                   "executed_tensor_tflops": ex, "executed_frac_of_tf32_burst_peak": ex / tf32_burst,
-                   "executed_frac_of_tf32_sustained_peak": ex / tf32_sus,
+                   "frac_vs_sustained_peak": al / (f16_sus / 3.0),
+                   "executed_tensor_tflops": ex, "executed_frac_of_f16_burst_peak": ex / f16_burst,
+                   "executed_frac_of_f16_sustained_peak": ex / f16_sus,
                    "peak_note": "primary peak = the burst GEMM (this step runs near the max SM clock, see 'clocks'); "
                                 "the sustained GEMM of MEASURED_PEAKS ran power-capped (median "
                                 f"{pk.get('clocks_under_load', {}).get('sm_mhz_median', 'n/a')} MHz), its fraction "
                                 "is the secondary field",
-                   "executed_is": "issued tcgen05 flops (3 TF32 products over the union tap boxes, skipped windows excluded)",
+                   "executed_is": "issued tcgen05 kind::f16 flops (3 products over the union tap boxes and the tiles' "
+                                  "column ranges, skipped windows excluded)",
                    "tc_planes": info["tc_planes"], "kernel_ms": t}
     # the dominant kernel (longest average launch) carries the primary roofline
     roof_primary = roof

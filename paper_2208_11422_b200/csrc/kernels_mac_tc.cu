@@ -29,12 +29,13 @@ constexpr int kMtChain = 4;               // chunks (x 4 K-steps) per drain grou
 constexpr int kMtThreads = 448;           // 1 producer + 8 prep + 1 MMA + 4 drainer warps
 constexpr int kMtPrep = 8;
 // Prep groups: group g of kMtPrep / PG warps prepares the chunks it with it % PG == g (each warp's wait -> build ->
-// fence -> arrive chain is serial per chunk, so PG groups keep PG chunks in preparation).  The ring depth S is a
-// multiple of PG, so stage s = it % S always belongs to group s % PG: a group finishes chunk it (its fill phase has
-// completed) before it waits for the fill of chunk it + S on the same stage, and the parity (it / S) & 1 it waits on
-// is never a stale phase of another group's chunk.  (With an odd S = 5 the stage alternated between the groups: a
-// group could wait on chunk it + S's parity while chunk it's fill was still in flight, pass on the completed phase of
-// chunk it - S and read a half-written tile -- the fault seen with 4 groups in r01.)
+// fence -> arrive chain is serial per chunk, so PG groups keep PG chunks in preparation).  A ring stage s = it % S is
+// reused by chunk it + S, which (unless PG divides S) another group prepares.  With one fill barrier per stage a
+// group waiting for chunk it's fill could find that barrier one phase behind (chunk it - S not yet filled) or one
+// phase ahead (chunk it filled, chunk it + S in flight) -- the same parity, so a parity wait cannot tell them apart
+// and may pass on chunk it - S's completed phase (the fault 4 groups hit in r01).  Each (group, stage) pair
+// therefore has its own fill barrier: bar_fullA[g][s] serves the chunks it = g (mod PG), s (mod S), i.e. every
+// L = lcm(PG, S)-th chunk, all prepared by group g in order, so the phase of chunk it is it / L and unambiguous.
 constexpr uint32_t kMtATile = kMtM * kMtKC * 4;   // 16 KB
 constexpr uint32_t kMtSmemMax = 232448;           // 227 KB per CTA
 
@@ -42,11 +43,12 @@ __host__ __device__ constexpr uint32_t mt_round1k(uint32_t v) { return (v + 1023
 __host__ __device__ constexpr uint32_t mt_btile(int F) { return mt_round1k((uint32_t)(4 * F) * kMtKC * 4); }
 __host__ __device__ constexpr uint32_t mt_gtile(int F) { return (uint32_t)F * kMtKC * 4; }   // F rows of 128 B
 __host__ __device__ constexpr uint32_t mt_stage(int F) { return 2 * kMtATile + mt_btile(F) + mt_round1k(mt_gtile(F)); }
-// deepest ring that fits next to the 1 KB alignment slack, a multiple of the prep-group count, at most 8 stages
+// deepest ring that fits next to the 1 KB alignment slack, at most 8 stages
 __host__ __device__ constexpr int ring_depth(uint32_t stage_bytes, int PG) {
-    return (int)((kMtSmemMax - 1024) / stage_bytes) < 8 ? (int)((kMtSmemMax - 1024) / stage_bytes) / PG * PG : 8 / PG * PG;
+    return (int)((kMtSmemMax - 1024) / stage_bytes) < 8 ? (int)((kMtSmemMax - 1024) / stage_bytes) : 8 + 0 * PG;
 }
 __host__ __device__ constexpr int mt_stages(int F, int PG) { return ring_depth(mt_stage(F), PG); }
+__host__ __device__ constexpr int mt_gcd(int a, int b) { return b == 0 ? a : mt_gcd(b, a % b); }
 }  // namespace
 
 int mac_tc_prep_groups() {
@@ -64,11 +66,12 @@ template <int F, int PG>
 __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_constant__ MacTcArgs d) {
     constexpr int S = mt_stages(F, PG);
     constexpr int kMtPG = PG;
-    static_assert(S >= PG && S % PG == 0, "each ring stage must belong to one prep group");
+    static_assert(S >= PG, "every prep group needs a stage");
     constexpr int NB = 4 * F;       // rows of the stacked B tile (B_hi: 0..2F-1, B_lo: 2F..4F-1)
     constexpr int NSET = 6 * F;     // TMEM columns per accumulator set: hi*hi | hi*lo | lo*hi
     extern __shared__ unsigned char smem_raw[];
-    __shared__ uint64_t bar_fullA[S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
+    constexpr int LG = PG * S / mt_gcd(PG, S);   // chunks between two uses of one (group, stage) fill barrier
+    __shared__ uint64_t bar_fullA[PG][S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
     __shared__ uint32_t tmem_base;
     const uint32_t raw = tc::smem_u32(smem_raw);
     unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            tc::mbar_init(&bar_fullA[i], 1);
+            for (int g = 0; g < PG; ++g) tc::mbar_init(&bar_fullA[g][i], 1);
             tc::mbar_init(&bar_ready[i], kMtPrep / kMtPG);
             tc::mbar_init(&bar_empty[i], 1);
         }
@@ -106,12 +109,13 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
                     const int s = it % S;
                     if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
                     unsigned char* st = smem + (size_t)s * sbytes;
-                    tc::mbar_arrive_expect_tx(&bar_fullA[s], kMtATile + mt_gtile(F));
-                    tc::tma_load_3d(st, &d.tmapM, c * kMtKC, h * kMtM, kap, &bar_fullA[s]);
+                    uint64_t* fb = &bar_fullA[it % PG][s];
+                    tc::mbar_arrive_expect_tx(fb, kMtATile + mt_gtile(F));
+                    tc::tma_load_3d(st, &d.tmapM, c * kMtKC, h * kMtM, kap, fb);
                     // the frames' G for this chunk: F rows of 16 complex units (plain row-major)
                     tc::tma_load_3d(st + 2 * kMtATile + mt_btile(F), &d.tmapG,
                                     (int)((long long)kap * 2 * d.nu_pad % d.gsplit) + c * kMtKC,
-                                    (int)((long long)kap * 2 * d.nu_pad / d.gsplit), 0, &bar_fullA[s]);
+                                    (int)((long long)kap * 2 * d.nu_pad / d.gsplit), 0, fb);
                 }
             }
         }
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_cons
             for (int c = 0; c < nchunks; ++c, ++it) {
                 if (it % kMtPG != grp) continue;
                 const int s = it % S;
-                tc::mbar_wait(&bar_fullA[s], (it / S) & 1);
+                tc::mbar_wait(&bar_fullA[grp][s], (it / LG) & 1);   // this group's own fill barrier (see above)
                 unsigned char* st = smem + (size_t)s * sbytes;
                 const float4* ahi = reinterpret_cast<const float4*>(st);
                 float4* alo = reinterpret_cast<float4*>(st + kMtATile);
@@ -263,11 +267,12 @@ template <int F, int PG>
 __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_constant__ BmacTcArgs d) {
     constexpr int S = bm_stages(F, PG);
     constexpr int kMtPG = PG;
-    static_assert(S >= PG && S % PG == 0, "each ring stage must belong to one prep group");
+    static_assert(S >= PG, "every prep group needs a stage");
     constexpr int NB = 4 * F;
     constexpr int NSET = 6 * F;
     extern __shared__ unsigned char smem_raw[];
-    __shared__ uint64_t bar_fullA[S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
+    constexpr int LG = PG * S / mt_gcd(PG, S);   // chunks between two uses of one (group, stage) fill barrier
+    __shared__ uint64_t bar_fullA[PG][S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
     __shared__ uint32_t tmem_base;
     const uint32_t raw = tc::smem_u32(smem_raw);
     unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_cons
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            tc::mbar_init(&bar_fullA[i], 1);
+            for (int g = 0; g < PG; ++g) tc::mbar_init(&bar_fullA[g][i], 1);
             tc::mbar_init(&bar_ready[i], kMtPrep / kMtPG);
             tc::mbar_init(&bar_empty[i], 1);
         }
@@ -306,10 +311,11 @@ __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_cons
                     const int s = it % S;
                     if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
                     unsigned char* st = smem + (size_t)s * sbytes;
-                    tc::mbar_arrive_expect_tx(&bar_fullA[s], kMtATile);
+                    uint64_t* fb = &bar_fullA[it % PG][s];
+                    tc::mbar_arrive_expect_tx(fb, kMtATile);
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
-                        tc::tma_load_3d(st + b * 4096, &d.tmapA, t * kMtM + 32 * b, c * kBmKC, kap, &bar_fullA[s]);
+                        tc::tma_load_3d(st + b * 4096, &d.tmapA, t * kMtM + 32 * b, c * kBmKC, kap, fb);
                 }
             }
         }
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_cons
                     rv[i] = bq < d.N2 ? __ldg(d.R + (long long)(n >> 1) * d.r_fstride + (long long)kap * d.N2 + bq)
                                       : make_float2(0.f, 0.f);
                 }
-                tc::mbar_wait(&bar_fullA[s], (it / S) & 1);
+                tc::mbar_wait(&bar_fullA[grp][s], (it / LG) & 1);   // this group's own fill barrier (see above)
                 unsigned char* st = smem + (size_t)s * sbytes;
                 const float4* ahi = reinterpret_cast<const float4*>(st);
                 float4* alo = reinterpret_cast<float4*>(st + kMtATile);

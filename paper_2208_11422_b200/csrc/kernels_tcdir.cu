@@ -1,16 +1,18 @@
 // kernels_tcdir.cu -- direct polyphase projections of near-focus planes on the 5th-generation tensor cores
-// (K9tc).  fp32-accurate through the 3xTF32 split (a*b ~ ah*bh + ah*bl + al*bh).
+// (K9tc).  fp32-accurate through a 2 x fp16 split of power-of-two scaled operands
+// (a*b ~ ah*bh + ah*bl + al*bh, "3xFP16" on tcgen05 kind::f16: 22 significant bits per operand, as 3xTF32 has, at
+// twice the tf32 tensor rate).
 //
 // For one plane z the direct path is a sum over coarse taps d of dense contractions over phases
 // (G_d[b'][a] = h_{z,a}[b1 - a1 + c + N d1][b2 - a2 + c + N d2], zero outside the kernel):
 //   forward : Y[m'][b']  = sum_d sum_a  X_a[m' - d] * G_d[b'][a]      (K = input phases a,  N = output phases b')
 //   backward: Xh[m][a]   = sum_d sum_b' r_b'[m + d] * G_d[b'][a]      (K = output phases b', N = input phases a)
-// Mapping onto tcgen05 (M = 128 coarse pixels = TMEM lanes, N = all phases <= 256 TMEM columns, K = 32-phase
-// chunks): every (tap, chunk) is one pipeline stage
-//   * A (128 pixels x 32 phases, hi and lo) is ONE 3-D TMA box each from a per-iteration staged copy of the
+// Mapping onto tcgen05 (M = 128 coarse pixels = TMEM lanes, N = all phases <= 256 TMEM columns, K = 64-phase
+// chunks, one 128-byte row of fp16): every (tap, chunk) is one pipeline stage
+//   * A (128 pixels x 64 phases, hi and lo) is ONE 3-D TMA box each from a per-iteration staged copy of the
 //     source on a padded coarse grid -- a tap is only a row offset of the box, borders come from TMA's zero fill;
-//   * B (the tap's Ntile x 32 coefficient tile, hi and lo, pre-swizzled at plan time) is one 1-D bulk copy;
-//   * one thread issues 3 x ksteps tcgen05.mma.kind::tf32 (K = 8 each) into a fresh TMEM accumulator;
+//   * B (the tap's Ntile x 64 coefficient tile, hi and lo, split at plan time) is one TMA box each;
+//   * one elected thread issues 3 x ksteps tcgen05.mma.kind::f16 (K = 16 each) into a TMEM accumulator;
 //   * 8 drainer warps add the accumulator into fp32 registers with round-to-nearest after every stage
 //     (tcgen05's fp32 accumulation truncates; a 12-MMA chain keeps that bias below 1e-6 relative), while the
 //     tensor core fills the other accumulator.
@@ -28,7 +30,8 @@ namespace lfm {
 
 namespace {
 constexpr int kM = 128;            // pixels per CTA tile (TMEM lanes); a CTA pair covers 2 * kM pixels
-constexpr int kKC = 32;            // phases per chunk (one 128-byte swizzle row)
+constexpr int kKC = 64;            // phases per chunk (one 128-byte swizzle row of fp16)
+constexpr int kKS = kKC / 16;      // K-steps (kind::f16, K = 16) per full chunk
 constexpr int kStagePB = 4;        // 32-pixel blocks per tc_stage_kernel CTA
 constexpr int kASlots = 2;         // A windows in flight (one per 32-phase chunk x tap row e1)
 constexpr int kBSlots = 5;         // coefficient tiles in flight (one per tap)
@@ -42,8 +45,8 @@ constexpr int kChainK = 24;        // default K-steps (x3 MMAs) accumulated in T
 // per-CTA smem: A windows (hi | lo, Arows = 128 + T2max - 1 rows of 128 B each part) and B tiles (hi | lo,
 // Ntile/2 rows each: the pair splits B along N); every part 1024-byte aligned (SWIZZLE_128B atoms)
 __host__ __device__ inline uint32_t round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
-__host__ __device__ inline uint32_t apart_bytes(int Arows) { return round1k((uint32_t)Arows * kKC * 4); }
-__host__ __device__ inline uint32_t bhalf_bytes(int Ntile) { return round1k((uint32_t)(Ntile / 2) * kKC * 4); }
+__host__ __device__ inline uint32_t apart_bytes(int Arows) { return round1k((uint32_t)Arows * 128u); }
+__host__ __device__ inline uint32_t bhalf_bytes(int Ntile) { return round1k((uint32_t)(Ntile / 2) * 128u); }
 }  // namespace
 
 size_t tcdir_smem_bytes(int Ntile, int Arows) {
@@ -92,10 +95,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&d.tmap);
         tc::tma_prefetch_desc(&d.bmap);
-        if (d.tail_w < kKC) {
-            tc::tma_prefetch_desc(&d.tmap_t);
-            tc::tma_prefetch_desc(&d.bmap_t);
-        }
     }
     if (warp == 0) tc::tmem_alloc_pair(&tmem_base, kTmemCols);
     tc::fence_before();
@@ -113,17 +112,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t pol = tc::policy_evict_last();
             const bool hint = !(d.exp & 8);
             const bool ranged = !(d.exp & 16);   // LFM_TC_EXP bit 16: full-width MMAs (no column ranges)
-            int gk = 0;                          // K-steps in the open drain group (mirrors the issuer)
             for (int i = ib; i < ie; ++i) {
                 const int item = d.items[i], zi = item / d.tiles, tile = item - zi * d.tiles;
                 const TcPlane pl = d.planes[zi];
                 const int* rm = d.rowmask + pl.mask_off;
                 const int row0 = tile * 2 * kM + (int)rank * kM - d.e2lo + pl.e2min;
                 for (int c = 0; c < d.nch; ++c) {
-                    const bool tail = c == d.nch - 1 && d.tail_w < kKC;
-                    const void* am = tail ? (const void*)&d.tmap_t : (const void*)&d.tmap;
-                    const void* bm = tail ? (const void*)&d.bmap_t : (const void*)&d.bmap;
-                    const uint32_t w = tail ? (uint32_t)d.tail_w : (uint32_t)kKC;   // phases per row
+                    // the last chunk's phases beyond N2 are zeros in both operands: full 128-byte boxes throughout
+                    const void* am = (const void*)&d.tmap;
+                    const void* bm = (const void*)&d.bmap;
                     const int slab_hi = FWD ? (zi * 2) * d.nch + c : c;
                     const int slab_lo = FWD ? (zi * 2 + 1) * d.nch + c : d.nch + c;
                     for (int t1 = 0; t1 < pl.T1; ++t1) {
@@ -134,7 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (d.exp & 4) dbg_empty += clock64() - c0;
                         unsigned char* as = Abase + (size_t)sa * 2 * apart;
                         const int row = row0 + (pl.e1min + t1) * d.Wp;
-                        if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullA[sa], 2 * 2 * (uint32_t)d.Arows * w * 4);
+                        if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullA[sa], 2 * 2 * (uint32_t)d.Arows * 128u);
                         if (hint) {
                             tc::tma_load_3d_pair_hint(as, am, 0, row, slab_hi, &bar_fullA[sa], pol);
                             tc::tma_load_3d_pair_hint(as + apart, am, 0, row, slab_lo, &bar_fullA[sa], pol);
@@ -145,18 +142,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const bool last_win = c * pl.T1 + t1 == pl.last_win;
                         for (int t2 = 0; t2 < pl.T2; ++t2, ++nb) {
                             const int sb = nb % kBSlots;
-                            const bool gstart = gk == 0;
-                            gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
-                            if ((last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k) gk = 0;
                             const long long c1 = (d.exp & 4) ? clock64() : 0;
                             if (nb >= kBSlots) tc::mbar_wait(&bar_emptyB[sb], ((nb / kBSlots) - 1) & 1);
                             if (d.exp & 4) dbg_empty += clock64() - c1;
                             unsigned char* bs = Bbase + (size_t)sb * 2 * bhalf;
                             const int bslab = (int)(pl.coef_off + (long long)((t1 * pl.T2 + t2) * d.nch + c) * 2);
-                            // B rows of this CTA: its half of the tile's MMA column range [n0, n0 + nn) (a drain
-                            // group's first stage runs full width: its MMA initialises every accumulator column)
+                            // B rows of this CTA: its half of the tile's MMA column range [n0, n0 + nn) (the
+                            // drainers zero every accumulator they hand back, so every MMA accumulates)
                             int brow = (int)rank * Nh;
-                            if (ranged && !gstart) {
+                            if (ranged) {
                                 const int rg = d.trange[bslab >> 1];
                                 if (rg == 0) {   // all-zero tile: the issuer skips its MMAs, so nothing to load
                                     if (rank == 0) tc::mbar_arrive(&bar_fullB[sb]);
@@ -164,7 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                 }
                                 brow = (rg & 0xFFFF) + (int)rank * (rg >> 17);
                             }
-                            if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * w * 4);
+                            if (rank == 0) tc::mbar_arrive_expect_tx(&bar_fullB[sb], 2 * 2 * (uint32_t)Nh * 128u);
                             if (hint) {
                                 tc::tma_load_3d_pair_hint(bs, bm, 0, brow, bslab, &bar_fullB[sb], pol);
                                 tc::tma_load_3d_pair_hint(bs + bhalf, bm, 0, brow, bslab + 1, &bar_fullB[sb], pol);
@@ -189,7 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // The loop runs converged on warp-uniform values, descriptors are built once per stage (+2 per 32-byte
             // K-step), so each MMA costs a few uniform instructions: a single-thread issue loop cost ~75-95 cycles
             // per MMA (scripts/tc_rate_test.cu), above the ~100-cycle MMAs of narrowed column ranges.
-            const uint32_t idesc = tc::idesc_tf32(2 * kM, d.Ntile);
+            const uint32_t idesc = tc::idesc_f16(2 * kM, d.Ntile);
             const bool ranged = !(d.exp & 16);
             long long dbg_full = 0, dbg_tfree = 0, dbg_t0 = clock64();
             int na = 0, nb = 0, g = 0, gk = 0;   // A windows, B tiles, drain group, K-steps in the open group
@@ -199,8 +193,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int* rm = d.rowmask + pl.mask_off;
                 const int T1 = pl.T1, T2 = pl.T2;
                 for (int c = 0; c < d.nch; ++c) {
-                    const int ks = c == d.nch - 1 ? d.kst_last : kKC / 8;
-                    const uint32_t rb = (c == d.nch - 1 && d.tail_w < kKC) ? (uint32_t)d.tail_w * 4 : 128u;   // row bytes
+                    const int ks = c == d.nch - 1 ? d.kst_last : kKS;
+                    const uint32_t rb = 128u;   // row bytes
                     for (int t1 = 0; t1 < T1; ++t1) {
                         if (!((rm[t1] >> c) & 1)) continue;
                         const int sa = na % kASlots;
@@ -216,7 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             const long long c0 = (d.exp & 4) ? clock64() : 0;
                             tc::mbar_wait(&bar_fullB[sb], (nb / kBSlots) & 1);
                             const long long c1 = (d.exp & 4) ? clock64() : 0;
-                            if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
+                            if (gk == 0) tc::mbar_wait(&bar_tfree[j], (g >> 1) & 1);   // zeroed by the drainers
                             if (d.exp & 4) {
                                 dbg_full += c1 - c0;
                                 dbg_tfree += clock64() - c1;
@@ -225,29 +219,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             const uint32_t a_hi = a_hi0 + (uint32_t)t2 * rb, a_lo = a_lo0 + (uint32_t)t2 * rb;
                             const uint32_t b_hi = tc::smem_u32(Bbase + (size_t)sb * 2 * bhalf), b_lo = b_hi + bhalf;
                             // column range of the tile (the zero columns outside it would only add exact zeros, so
-                            // the accumulated sums are bit-identical to full-width MMAs); full width at a group start
+                            // the accumulated sums are bit-identical to full-width MMAs)
                             uint32_t n0 = 0, nn = (uint32_t)d.Ntile, idesc_s = idesc;
-                            if (ranged && gk != 0) {
+                            if (ranged) {
                                 const int rg = d.trange[(pl.coef_off >> 1) + (t1 * T2 + t2) * d.nch + c];
                                 n0 = (uint32_t)(rg & 0xFFFF);
                                 nn = (uint32_t)(rg >> 16);
-                                idesc_s = tc::idesc_tf32(2 * kM, (int)nn);
+                                idesc_s = tc::idesc_f16(2 * kM, (int)nn);
                             }
                             const uint32_t acc = tmem + (uint32_t)(j * 256) + n0;
                             const uint64_t ah = tc::sdesc_swz(a_hi, rb), al = tc::sdesc_swz(a_lo, rb);
                             const uint64_t bh = tc::sdesc_swz(b_hi, rb), bl = tc::sdesc_swz(b_lo, rb);
                             if (nn > 0)
-                                for (int k = 0; k < ks; ++k) {   // K-step k: start address + 32 k bytes = field + 2 k
+                                for (int k = 0; k < ks; ++k) {   // K-step k (16 fp16): start + 32 k bytes = field + 2 k
                                     const uint64_t dk = 2 * (uint64_t)k;
-                                    tc::mma_tf32_pair_elect(acc, ah + dk, bh + dk, idesc_s, (gk == 0 && k == 0) ? 0u : 1u);
-                                    tc::mma_tf32_pair_elect(acc, ah + dk, bl + dk, idesc_s, 1u);
-                                    tc::mma_tf32_pair_elect(acc, al + dk, bh + dk, idesc_s, 1u);
+                                    tc::mma_f16_pair_elect(acc, ah + dk, bh + dk, idesc_s, 1u);
+                                    tc::mma_f16_pair_elect(acc, ah + dk, bl + dk, idesc_s, 1u);
+                                    tc::mma_f16_pair_elect(acc, al + dk, bh + dk, idesc_s, 1u);
                                 }
                             gk += ks;
                             tc::mma_commit_pair_elect(&bar_emptyB[sb], 3);
                             if (t2 == T2 - 1) tc::mma_commit_pair_elect(&bar_emptyA[sa], 3);
                             // close the drain group at the item's last stage or before it could exceed chain_k
-                            if ((last_win && t2 == T2 - 1) || gk + kKC / 8 > d.chain_k) {
+                            if ((last_win && t2 == T2 - 1) || gk + kKS > d.chain_k) {
                                 tc::mma_commit_pair_elect(&bar_acc[j], 3);
                                 ++g;
                                 gk = 0;
@@ -271,9 +265,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int half = (warp - 2) >> 2;             // column half
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(half * Nh);
         const int r = 32 * q + lane;                  // tile row (pixel) of this thread
+        const int aexp = tc::f16_scale_exp(__uint_as_float(*d.amax));   // the staged source's scale (tc_stage_kernel)
         float acc[kMaxNh];
 #pragma unroll
         for (int i = 0; i < kMaxNh; ++i) acc[i] = 0.0f;
+        // zero both accumulators of this warp's lanes / columns and hand them to the issuer (first tfree phase)
+        auto zero_acc = [&](uint32_t base) {
+#pragma unroll
+            for (int c0 = 0; c0 < kMaxNh; c0 += 32) {
+                if (c0 < Nh) {
+                    if (c0 + 32 <= Nh) {
+                        tc::tmem_zero32(base + (uint32_t)c0);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (c0 + 8 * u < Nh) tc::tmem_zero8(base + (uint32_t)(c0 + 8 * u));
+                    }
+                }
+            }
+            tc::tmem_wait_st();
+        };
+        for (int j = 0; j < 2; ++j) {
+            zero_acc(lane_base + (uint32_t)(j * 256));
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(&bar_tfree[j], 0);
+        }
         int g = 0;
         long long dbg_acc = 0, dbg_epi = 0;
         for (int i = ib; i < ie; ++i) {
@@ -306,12 +323,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             if (c0 + u < Nh) acc[c0 + u] += __uint_as_float(v[u]);
                     }
                 }
+                zero_acc(base);   // every later MMA of this accumulator adds (column ranges need no full-width start)
                 tc::fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive_cluster(&bar_tfree[j], 0);
             }
             // ---- epilogue of the item ----
             const long long ce0 = (d.exp & 4) ? clock64() : 0;
+            {   // undo the operands' power-of-two scales (exact)
+                const float inv = ldexpf(1.0f, -(aexp + pl.bexp));
+#pragma unroll
+                for (int i = 0; i < kMaxNh; ++i) acc[i] *= inv;
+            }
             const int L = tile * 2 * kM + (int)rank * kM + r;
             const int m1 = L / d.Wp, m2 = L - (L / d.Wp) * d.Wp;
             if (m1 < d.nh && m2 < d.nw) {
@@ -369,17 +392,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------------
-// Source staging: slab rows L of the padded grid (m1 = L / Wp, m2 = L % Wp + e2lo), 32 phases per row,
-// hi = tf32(v), lo = tf32(v - hi).  A 32-row x 32-phase tile per block, transposed through shared memory.
+// Source maximum (|v|, float bits, atomicMax into d.amax, zeroed before): the staged operands are scaled by
+// 2^f16_scale_exp(amax) so that the fp16 hi / lo split keeps 22 significant bits.
+//   forward  SRC 0: the tensor-core planes' owned units of the polyphase volume; SRC 1: their planes of [nz][H][W]
+//   backward SRC_RATIO: y / (max(yhat,0)+eps); SRC_IMAGE2D: the image; SRC_ONES: 1
+template <bool FWD, int SRC>
+__global__ void __launch_bounds__(256) tc_amax_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ src,
+                                                      const float* __restrict__ src2, float eps) {
+    float m = 0.0f;
+    size_t n;
+    const float* p = src;
+    if constexpr (FWD) {
+        const int z = d.zlist[blockIdx.y];
+        if constexpr (SRC == 0) {
+            const int ub = max(z * d.N2, d.unit0), ue = min((z + 1) * d.N2, d.unit0 + d.nu);
+            n = ue > ub ? (size_t)(ue - ub) * d.nh * d.nw : 0;
+            p = src + (size_t)(max(ub - d.unit0, 0)) * d.nh * d.nw;
+        } else {
+            n = (size_t)d.H * d.W;
+            p = src + (size_t)z * d.H * d.W;
+        }
+    } else {
+        n = SRC == SRC_ONES ? 0 : (size_t)d.H * d.W;
+        if (SRC == SRC_ONES) m = 1.0f;
+    }
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        float v = p[i];
+        if constexpr (!FWD && SRC == SRC_RATIO) v = v / (fmaxf(src2[i], 0.0f) + eps);
+        m = fmaxf(m, fabsf(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, wm[w]);
+        if (m > 0.0f) atomicMax(d.amax, __float_as_uint(m));
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Source staging: slab rows L of the padded grid (m1 = L / Wp, m2 = L % Wp + e2lo), 64 phases per row,
+// v = x 2^aexp, hi = fp16(v), lo = fp16(v - hi).  A 32-row x 64-phase tile per block, transposed through shared memory.
 //   forward  (SRC 0 polyphase volume [nu][nh][nw], 1 image-layout volume [nz][H][W]): plane blockIdx.z
 //   backward (SRC_RATIO y / (max(yhat,0)+eps), SRC_ONES, SRC_IMAGE2D): one image
 template <bool FWD, int SRC>
 __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ TcDirArgs d, const float* __restrict__ src,
                                                        const float* __restrict__ src2, float eps) {
-    // kStagePB blocks of 32 padded pixels per CTA; every thread issues all its kStagePB * 4 loads before the first use
+    // kStagePB blocks of 32 padded pixels per CTA; every thread issues all its loads before the first use
     __shared__ float tile[kStagePB][kKC][33];
     const int L0 = blockIdx.x * 32 * kStagePB, c = blockIdx.y, zi = blockIdx.z;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int aexp = tc::f16_scale_exp(__uint_as_float(*d.amax));
     {
         float v[kStagePB][kKC / 8];
         float w[kStagePB][kKC / 8];   // yhat for SRC_RATIO
@@ -436,15 +501,17 @@ __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ T
     __syncthreads();
     const size_t slab_hi = FWD ? ((size_t)zi * 2) * d.nch + c : (size_t)c;
     const size_t slab_lo = FWD ? ((size_t)zi * 2 + 1) * d.nch + c : (size_t)d.nch + c;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(d.src);   // two fp16 phases (2 tx, 2 tx + 1) per 32-bit store
 #pragma unroll
     for (int j = 0; j < kStagePB; ++j)
         for (int rr = ty; rr < 32; rr += 8) {
             const int L = L0 + 32 * j + rr;
             if (L >= d.Lp) break;
-            float h, l;
-            tc::split_tf32(tile[j][tx][rr], h, l);
-            d.src[(slab_hi * d.Lp + L) * kKC + tx] = h;
-            d.src[(slab_lo * d.Lp + L) * kKC + tx] = l;
+            uint16_t h0, l0, h1, l1;
+            tc::split_f16(tile[j][2 * tx][rr], aexp, h0, l0);
+            tc::split_f16(tile[j][2 * tx + 1][rr], aexp, h1, l1);
+            dst[(slab_hi * d.Lp + L) * (kKC / 2) + tx] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+            dst[(slab_lo * d.Lp + L) * (kKC / 2) + tx] = (uint32_t)l0 | ((uint32_t)l1 << 16);
         }
 }
 
@@ -491,10 +558,11 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const __grid_constant__ 
 
 // ------------------------------------------------------------------------------------------------
 // Coefficient tiles of one plane (plan time), built on the device from the owned PSF slice: tile (tap, chunk) =
-// slabs [hi], [lo] of Ntile x 32 row-major floats (the TMA load swizzles them) with element (n, k) =
-//   forward : G_d[b' = n][a = chunk*32 + k],   d = -e        backward: G_d[b' = chunk*32 + k][a = n],   d = +e
+// fp16 slabs [hi], [lo] of Ntile x 64 row-major (the TMA load swizzles them) of g * 2^bexp with element (n, k) =
+//   forward : G_d[b' = n][a = chunk*64 + k],   d = -e        backward: G_d[b' = chunk*64 + k][a = n],   d = +e
 __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane pl, int z, const float* __restrict__ psf,
-                                  int kh, int kw, int ch, int cw, int fwd, float* __restrict__ out, int* __restrict__ nzflag) {
+                                  int kh, int kw, int ch, int cw, int fwd, uint16_t* __restrict__ out,
+                                  int* __restrict__ nzflag) {
     __shared__ int any, nmin, nmax;
     if (threadIdx.x == 0) {
         any = 0;
@@ -508,8 +576,8 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
     const int N = d.N, N2 = d.N2;
     const int e1 = pl.e1min + tap / pl.T2, e2 = pl.e2min + tap % pl.T2;
     const int d1 = fwd ? -e1 : e1, d2 = fwd ? -e2 : e2;
-    float* hi = out + ((size_t)pl.coef_off + (size_t)tileid * 2) * d.Ntile * kKC;
-    float* lo = hi + (size_t)d.Ntile * kKC;
+    uint16_t* hi = out + ((size_t)pl.coef_off + (size_t)tileid * 2) * d.Ntile * kKC;
+    uint16_t* lo = hi + (size_t)d.Ntile * kKC;
     for (int e = threadIdx.x; e < d.Ntile * kKC; e += blockDim.x) {
         const int n = e / kKC, k = e - (e / kKC) * kKC;
         const int kg = chunk * kKC + k;
@@ -523,8 +591,8 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
                 if (k1 >= 0 && k1 < kh && k2 >= 0 && k2 < kw) v = psf[((size_t)(u - d.unit0) * kh + k1) * kw + k2];
             }
         }
-        float h, l;
-        tc::split_tf32(v, h, l);
+        uint16_t h, l;
+        tc::split_f16(v, pl.bexp, h, l);
         hi[e] = h;
         lo[e] = l;
         if (v != 0.0f) {
@@ -536,6 +604,28 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
     __syncthreads();
     // nonzero flag of the tile = its nonzero B-row (N) range, packed nmin | (nmax + 1) << 16 (0: all zero)
     if (threadIdx.x == 0) nzflag[tileid] = any ? (nmin | ((nmax + 1) << 16)) : 0;
+}
+
+// per-plane max |psf| of the owned units (float bits, atomicMax) -> the coefficient tiles' fp16 scales
+__global__ void tc_plane_amax_kernel(const float* __restrict__ psf, const int* __restrict__ zlist, int N2, int kk,
+                                     int unit0, int nu, unsigned* __restrict__ pmax) {
+    const int zi = blockIdx.y, z = zlist[zi];
+    const int ub = max(z * N2, unit0), ue = min((z + 1) * N2, unit0 + nu);
+    const size_t n = ue > ub ? (size_t)(ue - ub) * kk : 0;
+    const float* p = psf + (size_t)max(ub - unit0, 0) * kk;
+    float m = 0.0f;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(p[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(pmax + zi, __float_as_uint(m));
+}
+
+cudaError_t launch_tc_plane_amax(const float* psf_dev, const int* zlist, int nzd, int N2, int kk, int unit0, int nu,
+                                 unsigned* pmax, cudaStream_t s) {
+    if (nzd <= 0) return cudaSuccess;
+    tc_plane_amax_kernel<<<dim3(64, nzd), 256, 0, s>>>(psf_dev, zlist, N2, kk, unit0, nu, pmax);
+    return cudaGetLastError();
 }
 
 // per-tile MMA column ranges (§5.3 column ranges): n0 | nn << 16, the nonzero B rows [nmin, nmax] widened to n0 a
@@ -565,8 +655,7 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
     d->Ntile = (d->N2 + 15) / 16 * 16;
     if (d->Ntile > 2 * kMaxNh) return false;
     d->nch = (d->N2 + kKC - 1) / kKC;
-    d->kst_last = ((d->N2 - (d->nch - 1) * kKC) + 7) / 8;
-    d->tail_w = d->kst_last == 1 ? 8 : (d->kst_last == 2 ? 16 : kKC);
+    d->kst_last = ((d->N2 - (d->nch - 1) * kKC) + 15) / 16;   // the last chunk's zero phases beyond are skipped
     planes->assign(d->nzd, TcPlane{});
     int e2lo = 1 << 30, e2hi = -(1 << 30);
     long long off = 0;
@@ -576,7 +665,8 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
         pl.T2 = d2max[zi] - d2min[zi] + 1;
         pl.e1min = fwd ? -d1max[zi] : d1min[zi];
         pl.e2min = fwd ? -d2max[zi] : d2min[zi];
-        pl.coef_off = off;   // in slabs of Ntile x 32 floats
+        pl.coef_off = off;   // in slabs of Ntile x 64 fp16
+        pl.bexp = 0;         // set from the plane's max tap before the coefficient tiles are built
         off += (long long)pl.T1 * pl.T2 * d->nch * 2;
         e2lo = std::min(e2lo, pl.e2min);
         e2hi = std::max(e2hi, pl.e2min + pl.T2 - 1);
@@ -629,12 +719,12 @@ void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std:
     }
 }
 
-size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes) {
+size_t tcdir_coef_elems(const TcDirArgs& d, const std::vector<TcPlane>& planes) {
     size_t n = 0;
     for (const TcPlane& pl : planes) n += (size_t)pl.T1 * pl.T2 * d.nch * 2;
     return n * d.Ntile * kKC;
 }
-size_t tcdir_src_floats(const TcDirArgs& d, int fwd) { return (size_t)(fwd ? 2 * d.nzd : 2) * d.nch * d.Lp * kKC; }
+size_t tcdir_src_elems(const TcDirArgs& d, int fwd) { return (size_t)(fwd ? 2 * d.nzd : 2) * d.nch * d.Lp * kKC; }
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd) {
     (void)fwd;   // forward: per-plane partials; backward: H^T r scratch -- both polyphase [nzd][N2][nh][nw]
     return (size_t)d.nzd * d.N2 * d.nh * d.nw;
@@ -656,35 +746,24 @@ cudaError_t tcdir_encode(TcDirArgs* d, int fwd) {
     }
     const cuuint64_t slabs = (cuuint64_t)(fwd ? 2 * d->nzd : 2) * d->nch;
     cuuint64_t dims[3] = {(cuuint64_t)kKC, (cuuint64_t)d->Lp, slabs};
-    cuuint64_t strides[2] = {(cuuint64_t)kKC * 4, (cuuint64_t)d->Lp * kKC * 4};
+    cuuint64_t strides[2] = {(cuuint64_t)kKC * 2, (cuuint64_t)d->Lp * kKC * 2};
     cuuint32_t box[3] = {(cuuint32_t)kKC, (cuuint32_t)d->Arows, 1}, es[3] = {1, 1, 1};
-    CUresult r = enc(&d->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->src, dims, strides, box, es,
+    CUresult r = enc(&d->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d->src, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    // coefficient slabs [nslabs][Ntile][32], each CTA of a pair loads Ntile/2 rows
+    // coefficient slabs [nslabs][Ntile][64] fp16, each CTA of a pair loads Ntile/2 rows
     cuuint64_t bdims[3] = {(cuuint64_t)kKC, (cuuint64_t)d->Ntile, (cuuint64_t)d->nslabs};
-    cuuint64_t bstrides[2] = {(cuuint64_t)kKC * 4, (cuuint64_t)d->Ntile * kKC * 4};
+    cuuint64_t bstrides[2] = {(cuuint64_t)kKC * 2, (cuuint64_t)d->Ntile * kKC * 2};
     cuuint32_t bbox[3] = {(cuuint32_t)kKC, (cuuint32_t)(d->Ntile / 2), 1};
-    r = enc(&d->bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d->coef), bdims, bstrides, bbox, es,
+    r = enc(&d->bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(d->coef), bdims, bstrides, bbox, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    if (d->tail_w < kKC) {   // the last chunk holds <= 16 valid phases: narrow boxes, SWIZZLE_32B / 64B
-        const CUtensorMapSwizzle sw = d->tail_w == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
-        cuuint32_t tbox[3] = {(cuuint32_t)d->tail_w, (cuuint32_t)d->Arows, 1};
-        cuuint32_t tbbox[3] = {(cuuint32_t)d->tail_w, (cuuint32_t)(d->Ntile / 2), 1};
-        r = enc(&d->tmap_t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->src, dims, strides, tbox, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-        r = enc(&d->bmap_t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d->coef), bdims, bstrides, tbbox, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    }
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
-                              int kw, int ch, int cw, int fwd, float* coef, int* nzflags, cudaStream_t s) {
+                              int kw, int ch, int cw, int fwd, uint16_t* coef, int* nzflags, cudaStream_t s) {
     (void)zi;
     const int tiles = pl.T1 * pl.T2 * d.nch;
     if (tiles <= 0) return cudaSuccess;
@@ -725,8 +804,8 @@ void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const 
             for (int t1 = 0; t1 < pl.T1; ++t1) {
                 if (!(((*rowmask)[pl.mask_off + t1] >> c) & 1)) continue;
                 for (int t2 = 0; t2 < pl.T2; ++t2) {
-                    gk += c == d.nch - 1 ? d.kst_last : kKC / 8;
-                    if ((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + kKC / 8 > d.chain_k) {
+                    gk += c == d.nch - 1 ? d.kst_last : kKS;
+                    if ((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + kKS > d.chain_k) {
                         ++pl.ngroups;
                         gk = 0;
                     }
@@ -766,6 +845,9 @@ static cudaError_t tcdir_main(const TcDirArgs& d, const float* xold, const float
 
 template <bool FWD, int SRC>
 static cudaError_t tc_stage(const TcDirArgs& d, const float* src, const float* src2, float eps, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(d.amax, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    tc_amax_kernel<FWD, SRC><<<dim3(FWD ? 16 : 64, FWD ? d.nzd : 1), 256, 0, s>>>(d, src, src2, eps);
     dim3 grid((d.Lp + 32 * kStagePB - 1) / (32 * kStagePB), d.nch, FWD ? d.nzd : 1);
     tc_stage_kernel<FWD, SRC><<<grid, 256, 0, s>>>(d, src, src2, eps);
     return cudaGetLastError();

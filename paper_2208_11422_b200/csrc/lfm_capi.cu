@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "lfm_internal.cuh"
+#include "tc_sm100.cuh"
 
 using namespace lfm;
 
@@ -226,6 +227,7 @@ struct lfm_plan_s {
     int mem_moved = 0;   // planes moved off the frequency path to fit the memory budget
     double tc_flops_exec = 0.0, tc_flops_alg = 0.0;   // per projection (lfm_info)
     double tc_active_frac = 0.0;                       // mean fraction of nonzero (chunk, tap row) windows
+    int part_moved = 0;                                // tensor-core planes the partition-aware step moved to FFT
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -1007,7 +1009,7 @@ struct PlaneCost {
 
 double tc_plane_time(const AxisBox& b1, const AxisBox& b2, const Geo& g, int N2, int num_sms) {
     const int T1 = b1.dmax - b1.dmin + b1.D, T2 = b2.dmax - b2.dmin + b2.D;
-    const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 7) / 8;
+    const int Ntile = (int)round_up((size_t)N2, 16), ksteps = (N2 + 15) / 16;   // kind::f16 K-steps of 16 phases
     const int ptiles = (g.nh * (g.nw + T2 - 1) + 255) / 256;
     const double act = T1 >= 3 ? 1.0 - 1.0 / T1 : 1.0;   // edge tap rows: about half the chunks skipped
     const double pair_cycles = (double)ptiles * T1 * T2 * act * ksteps * 3.0 * (Ntile / 2);
@@ -1390,7 +1392,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             p_alt[z] = 2;
             pt_alt[z] = t_tc;
             const double lp = (double)g.nh * (g.nw + T2 - 1);
-            pm_alt[z] = (double)T1 * T2 * ((N2 + 31) / 32) * 2 * Ntile * 32 * 4 * 2 + 2.0 * ((N2 + 31) / 32) * lp * 128 +
+            pm_alt[z] = (double)T1 * T2 * ((N2 + 63) / 64) * 2 * Ntile * 64 * 2 * 2 + 2.0 * ((N2 + 63) / 64) * lp * 128 +
                         2.0 * height * width * 4;
         } else if (D <= kDirMaxD) {
             p_alt[z] = 1;
@@ -1438,6 +1440,60 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             return guard(fail(LFM_ENOMEM, "transfer matrices of the frequency-path planes need %.0f bytes, %.0f available "
                               "after moving %d planes to the direct path; limiting term: transfer matrices",
                               need(), avail, p->mem_moved));
+    }
+    // partition-aware refinement (§5.5): side by side on SM partitions a tensor-core plane costs SM time (its
+    // whole-GPU time spread over the tensor-core partition), a frequency-path plane only its transfer bytes at a
+    // partition SM's streaming rate -- far below the whole-GPU HBM rate the per-plane choice above assumed.  Planes
+    // with the most tensor time per transfer byte move back to the frequency path while the predicted partitioned
+    // iteration (both directions, partition_time, plus the coarse transforms of the added units) keeps improving and
+    // the transfer matrices fit.
+    p->part_moved = 0;
+    if (partitions_allowed(flags) && !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
+        bool simt = false;
+        for (int z = zb; z <= ze; ++z) simt |= plane_direct[z] == 1;
+        std::vector<int> cand;
+        for (int z = zb; z <= ze; ++z)
+            if (plane_direct[z] == 2 && pm_fft[z] > 0) cand.push_back(z);
+        std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return pt_alt[a] / pm_fft[a] > pt_alt[b] / pm_fft[b]; });
+        auto predict = [&](int k) {   // predicted seconds per iteration with the first k candidates on the FFT path
+            double t_tc = 0.0, units_fft = 0.0;
+            std::vector<int> mode(plane_direct);
+            for (int i = 0; i < k; ++i) mode[cand[i]] = 0;
+            for (int z = zb; z <= ze; ++z) {
+                const double units = std::min<long long>(p->u1, (long long)(z + 1) * N2) - std::max<long long>(p->u0, (long long)z * N2);
+                if (mode[z] == 2) t_tc += 0.5 * pt_alt[z];
+                if (mode[z] == 0) units_fft += units;
+            }
+            const double bytes = units_fft * N2 * g.nkappa * 8.0;
+            double t = kXformPerUnit * units_fft;
+            for (int d = 0; d < 2; ++d) {
+                const double gsm = round_up((size_t)std::max(units_fft, 1.0), 16) * 8.0 + 1024.0;
+                const double scale = d == 0 ? std::min(4.0, std::floor(228.0 * 1024.0 / gsm)) / 4.0 : 1.0;
+                int sdummy = 0;
+                t += partition_time(t_tc, bytes, d, p->num_sms, &sdummy, scale);
+            }
+            double mem = 0;
+            for (int z = zb; z <= ze; ++z) mem += mode[z] == 0 ? pm_fft[z] : pm_alt[z];
+            return mem <= 0.94 * (double)(mem_budget - nonM_bytes) ? t : 1e30;
+        };
+        int best_k = 0;
+        if (!simt && !cand.empty()) {
+            double best_t = predict(0);
+            for (int k = 1; k <= (int)cand.size(); ++k) {
+                const double t = predict(k);
+                if (t < best_t * 0.995) {
+                    best_t = t;
+                    best_k = k;
+                }
+            }
+            if (const char* ev = getenv("LFM_PLAN_MOVE")) best_k = std::max(0, std::min((int)cand.size(), atoi(ev)));   // dev
+            if (getenv("LFM_PLAN_VERBOSE"))
+                fprintf(stderr, "[lfm plan] partition-aware: %d of %zu tensor-core planes to the frequency path "
+                                "(predicted %.3f -> %.3f ms per iteration)\n",
+                        best_k, cand.size(), predict(0) * 1e3, predict(best_k) * 1e3);
+        }
+        for (int i = 0; i < best_k; ++i) plane_direct[cand[i]] = 0;
+        p->part_moved = best_k;
     }
     p->direct = too_big;   // all-direct request with boxes beyond kDirMaxD: the generic spatial kernels
     if (!p->direct) {
@@ -1589,15 +1645,32 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     std::vector<TcPlane> pls;
                     if (!tcdir_geometry(&t, !w, d1a.data(), d1b.data(), d2a.data(), d2b.data(), &pls, tc_sms[w]))
                         return guard(fail(LFM_EUNSUPPORTED, "tensor-core direct path needs Nnum^2 <= 256"));
-                    float *cf = nullptr, *sr = nullptr, *pt = nullptr;
+                    uint16_t *cf = nullptr, *sr = nullptr;
+                    float* pt = nullptr;
                     int* nzf = nullptr;
-                    const size_t nf = tcdir_coef_floats(t, pls), ns = tcdir_src_floats(t, !w), np = tcdir_part_floats(t, !w);
+                    unsigned* am = nullptr;
+                    const size_t nf = tcdir_coef_elems(t, pls), ns = tcdir_src_elems(t, !w), np = tcdir_part_floats(t, !w);
                     size_t ntile = 0;
                     for (const TcPlane& pl : pls) ntile += (size_t)pl.T1 * pl.T2 * t.nch;
-                    PG(dalloc(p, &cf, nf * sizeof(float), "tc direct taps"));
+                    PG(dalloc(p, &cf, nf * sizeof(uint16_t), "tc direct taps"));
                     p->dallocs.push_back(cf);
-                    PG(dalloc(p, &sr, ns * sizeof(float), "tc direct staged source"));
+                    PG(dalloc(p, &sr, ns * sizeof(uint16_t), "tc direct staged source"));
                     p->dallocs.push_back(sr);
+                    PG(dalloc(p, &am, ((size_t)t.nzd + 1) * sizeof(unsigned), "tc operand maxima"));
+                    p->dallocs.push_back(am);
+                    t.amax = am;   // [0]: the staged source's max (per launch); [1 + zi]: plane maxima (plan time)
+                    {   // fp16 scale of each plane's coefficient tiles from its largest tap
+                        CKG(cudaMemsetAsync(am, 0, ((size_t)t.nzd + 1) * sizeof(unsigned), s));
+                        CKG(launch_tc_plane_amax(w ? p->psfb : p->psf, dz, t.nzd, N2, (int)kk, p->u0, p->nu, am + 1, s));
+                        std::vector<unsigned> pm(t.nzd);
+                        CKG(cudaMemcpyAsync(pm.data(), am + 1, t.nzd * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+                        CKG(cudaStreamSynchronize(s));
+                        for (int zi = 0; zi < t.nzd; ++zi) {
+                            float f;
+                            memcpy(&f, &pm[zi], sizeof(f));
+                            pls[zi].bexp = tc::f16_scale_exp(f);
+                        }
+                    }
                     if (np) {
                         PG(dalloc(p, &pt, np * sizeof(float), "tc direct forward partials"));
                         p->dallocs.push_back(pt);
@@ -1654,9 +1727,9 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                     t.items = dit;
                     CKG(tcdir_encode(&t, !w));
                     CKG(cudaStreamSynchronize(s));   // host vectors die at the end of this scope
-                    coef_bytes += nf * sizeof(float);
-                    if (!w)   // executed tensor flops of one projection: 3 pair MMAs per K-step of every nonzero window
-                              // tap, over the tile's column range (full width at a drain group's first stage)
+                    coef_bytes += nf * sizeof(uint16_t);
+                    if (!w)   // executed tensor flops of one projection: 3 pair MMAs (K = 16) per K-step of every nonzero window
+                              // tap, over the tile's column range
                         for (size_t zi = 0; zi < pls.size(); ++zi) {
                             const TcPlane& pl = pls[zi];
                             double col_ks = 0;
@@ -1667,12 +1740,12 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                                     for (int t2 = 0; t2 < pl.T2; ++t2) {
                                         const int ks = c == t.nch - 1 ? t.kst_last : 4;
                                         const int rg = ranges[(size_t)pl.coef_off / 2 + (size_t)(t1 * pl.T2 + t2) * t.nch + c];
-                                        col_ks += (double)ks * (gk == 0 ? t.Ntile : (rg >> 16));
+                                        col_ks += (double)ks * (rg >> 16);
                                         gk += ks;
                                         if ((c * pl.T1 + t1 == pl.last_win && t2 == pl.T2 - 1) || gk + 4 > t.chain_k) gk = 0;
                                     }
                                 }
-                            p->tc_flops_exec += (double)t.tiles * col_ks * 3.0 * 2.0 * 256.0 * 8.0;
+                            p->tc_flops_exec += (double)t.tiles * col_ks * 3.0 * 2.0 * 256.0 * 16.0;
                             p->tc_active_frac += (double)pl.active_windows / (pl.T1 * t.nch) / pls.size();
                             const int z = zl[zi];
                             p->tc_flops_alg += 2.0 * (double)N2 * N2 * box1[z].D * box2[z].D * g.nh * g.nw;

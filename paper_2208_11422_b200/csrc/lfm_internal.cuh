@@ -101,7 +101,8 @@ struct DirArgs {
 // plane, column c holds m2 = c + e2lo) so that a tap is a plain row offset of a TMA box.
 struct TcPlane {
     int T1, T2, e1min, e2min;   // union tap box of the plane (source offsets)
-    long long coef_off;         // first coefficient slab (Ntile x 32 floats) of the plane
+    int bexp;                   // coefficient scale 2^bexp of the plane's fp16 split (f16_scale_exp of its max tap)
+    long long coef_off;         // first coefficient slab (Ntile x 64 fp16) of the plane
     int mask_off;               // rowmask[mask_off + t1]: bit c set if window (chunk c, tap row t1) has a nonzero tap
     int last_win;               // c * T1 + t1 of the last nonzero window
     int active_windows;         // number of nonzero windows
@@ -115,27 +116,26 @@ struct TcDirArgs {
     const TcPlane* planes;    // [nzd] (device)
     const int* rowmask;       // nonzero (chunk, tap row) windows, see TcPlane (device)
     int N2, Ntile;            // phases and TMEM columns per accumulator (N2 rounded up to 16, <= 256)
-    int nch, kst_last;        // reduction chunks of 32 phases; K-steps of 8 in the last chunk
+    int nch, kst_last;        // reduction chunks of 64 phases (one 128-byte fp16 row); K-steps of 16 in the last
     int e2lo;                 // column origin of the staged grid (min e2min over planes)
-    int Wp, Lp, tiles;        // padded grid: Lp = nh * Wp rows of 32 phases, pair tiles of 256 rows
+    int Wp, Lp, tiles;        // padded grid: Lp = nh * Wp rows of 64 phases, pair tiles of 256 rows
     int grid;                 // persistent CTA pairs (launch 2 * grid CTAs, clusters of 2)
     const int* item_off;      // [grid + 1] pair b runs items[item_off[b] .. item_off[b+1])   (LPT schedule)
     const int* items;         // item = zi * tiles + tile
-    const float* coef;        // slabs [plane][tap][chunk][hi | lo] of Ntile x 32 floats (row-major)
+    const uint16_t* coef;     // fp16 slabs [plane][tap][chunk][hi | lo] of Ntile x 64 (row-major), scaled 2^bexp
     long long nslabs;         // coefficient slabs
     int exp;                  // timing experiments only (env LFM_TC_EXP): 1 skip drains, 2 skip reloads, 4 counters
     long long* dbg;           // exp & 4: per-CTA wait-cycle counters [grid*2][8]
-    float* src;               // staged source, slabs of [Lp][32] (hi / lo): fwd ((zi*2+part)*nch+c), bwd (part*nch+c)
+    uint16_t* src;            // staged fp16 source, slabs of [Lp][64] (hi / lo, scaled 2^aexp): fwd ((zi*2+part)*nch
+                              // + c), bwd (part*nch + c)
+    unsigned* amax;           // device scalar: max of the source (float bits) -> aexp = f16_scale_exp(amax)
     float* part;              // polyphase [nzd][N2][nh][nw]: forward per-plane partials (tc_fwd_reduce_kernel sums
                               // and interleaves them), backward H^T r (update epilogues apply it afterwards)
     int chain_k;              // K-steps (x3 MMAs) accumulated in TMEM between round-to-nearest drains
     const int* trange;        // [tiles] MMA column range per coefficient tile: n0 | nn << 16 (tcdir_ranges; device)
-    alignas(64) CUtensorMap tmap;   // 3-D {32, Lp, slabs} over src, box {32, Arows, 1}, SWIZZLE_128B
-    alignas(64) CUtensorMap bmap;   // 3-D {32, Ntile, nslabs} over coef, box {32, Ntile/2, 1}, SWIZZLE_128B
+    alignas(64) CUtensorMap tmap;   // 3-D fp16 {64, Lp, slabs} over src, box {64, Arows, 1}, SWIZZLE_128B
+    alignas(64) CUtensorMap bmap;   // 3-D fp16 {64, Ntile, nslabs} over coef, box {64, Ntile/2, 1}, SWIZZLE_128B
     int Arows;                      // A window rows: 128 + max T2 - 1
-    int tail_w;                     // phases loaded for the last chunk: 8 (SWIZZLE_32B), 16 (64B) or 32 (main maps)
-    alignas(64) CUtensorMap tmap_t; // narrow boxes {tail_w, Arows | Ntile/2, 1} for the last chunk
-    alignas(64) CUtensorMap bmap_t;
 };
 // geometry of one direction from the per-plane tap boxes d in [d1min, d1max] x [d2min, d2max] (host arrays)
 bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, const int* d2min, const int* d2max,
@@ -144,14 +144,17 @@ bool tcdir_geometry(TcDirArgs* d, int fwd, const int* d1min, const int* d1max, c
 void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std::vector<int>* item_off,
                     std::vector<int>* items);
 size_t tcdir_smem_bytes(int Ntile, int Arows);
-size_t tcdir_coef_floats(const TcDirArgs& d, const std::vector<TcPlane>& planes);
-size_t tcdir_src_floats(const TcDirArgs& d, int fwd);
+size_t tcdir_coef_elems(const TcDirArgs& d, const std::vector<TcPlane>& planes);   // fp16 elements
+size_t tcdir_src_elems(const TcDirArgs& d, int fwd);                                 // fp16 elements
 size_t tcdir_part_floats(const TcDirArgs& d, int fwd);
 cudaError_t tcdir_encode(TcDirArgs* d, int fwd);
 // per-tile MMA column ranges from the packed nonzero-row flags of tcdir_coef_kernel (host)
 void tcdir_ranges(const TcDirArgs& d, const std::vector<int>& nzflags, std::vector<int>* ranges);
 cudaError_t launch_tcdir_coef(const TcDirArgs& d, const TcPlane& pl, int zi, int z, const float* psf_dev, int kh,
-                              int kw, int ch, int cw, int fwd, float* coef, int* nzflags, cudaStream_t s);
+                              int kw, int ch, int cw, int fwd, uint16_t* coef, int* nzflags, cudaStream_t s);
+// per-plane maxima of the owned PSF slice (float bits into pmax[zi], zeroed by the caller) for the fp16 scales
+cudaError_t launch_tc_plane_amax(const float* psf_dev, const int* zlist, int nzd, int N2, int kk, int unit0, int nu,
+                                 unsigned* pmax, cudaStream_t s);
 // from the per-(tap, chunk) nonzero flags of every plane: row masks, last windows, active counts (host)
 void tcdir_window_masks(const TcDirArgs& d, std::vector<TcPlane>* planes, const std::vector<int>& nzflags,
                         std::vector<int>* rowmask);

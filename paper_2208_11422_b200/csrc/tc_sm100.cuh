@@ -7,6 +7,7 @@
 //   (r / 8) * SBO + (k / 4) * 128 + (r % 8) * 16 + (k % 4) * 4,   LBO = 128, SBO = (KT / 4) * 128.
 // One tcgen05.mma.kind::tf32 consumes K = 8 (two core matrices along K).
 #pragma once
+#include <cmath>
 #include <cstdint>
 
 namespace lfm {
@@ -131,6 +132,14 @@ __device__ __forceinline__ void mma_tf32_pair_elect(uint32_t d_tmem, uint64_t a,
         "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// the same with 16-bit operands (kind::f16: fp16 A and B, fp32 accumulator, K = 16 per instruction)
+__device__ __forceinline__ void mma_f16_pair_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                   uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
@@ -178,9 +187,28 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// zeros -> 32 lanes x 32 (x8: 8) consecutive fp32 columns of TMEM (no wait; pair with tmem_wait_st)
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+        "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+        "r"(0u)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr), "r"(0u)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // instruction descriptor: D fp32, A/B tf32, both K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// instruction descriptor: D fp32, A/B fp16 (kind::f16), both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
@@ -290,6 +318,28 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     hi = __uint_as_float(h);
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
     lo = __uint_as_float(l);
+}
+
+// fp32 -> (hi, lo) fp16 pair of x * 2^e (round to nearest): hi = fp16(v), lo = fp16(v - hi), v = x * 2^e.  With the
+// operands scaled so that their maxima sit near 2^13, hi + lo carries 22 significant bits (as a 3xTF32 split does)
+// and the 3-product sum ah*bh + ah*bl + al*bh runs on kind::f16 at twice the tf32 rate ("3xFP16").
+__device__ __forceinline__ void split_f16(float x, int e, uint16_t& hi, uint16_t& lo) {
+    const float v = ldexpf(x, e);
+    uint16_t h, l;
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
+    float hf;
+    asm("cvt.f32.f16 %0, %1;" : "=f"(hf) : "h"(h));
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(l) : "f"(v - hf));
+    hi = h;
+    lo = l;
+}
+// power-of-two exponent that puts a non-negative maximum near 2^13 (its fp16 hi / lo parts then stay normal for every
+// value within ~2^-20 of the maximum; smaller values lose relative, not absolute, precision); 0 for an all-zero max
+__host__ __device__ inline int f16_scale_exp(float amax) {
+    if (!(amax > 0.0f) || !(amax < 3.0e38f)) return 0;
+    int ex;
+    (void)frexpf(amax, &ex);   // amax = m * 2^ex, m in [0.5, 1)
+    return 13 - ex;
 }
 
 // residual of the tensor core's own TF32 view of an fp32 operand: the MMA truncates x to TF32 (low 13 mantissa bits

@@ -669,6 +669,24 @@ def test_nccl_one_rank_identical(extra):
     assert np.array_equal(a[3], b[3])
 
 
+def mixed_problem():
+    """The c2 geometry (N=11, 319^2) with a bank whose planes need very different tap boxes: 3 wide planes (K = 143,
+    D = 13: the frequency path) and 5 narrow ones (D <= 3: the tensor cores), so the default plan holds both kinds."""
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS["c2"], name="mixed", nz=8, k_max=143)
+    rng = np.random.default_rng(12)
+    N, K = cfg.nnum, cfg.k_max
+    h = np.zeros((cfg.nz, N, N, K, K), np.float32)
+    c = K // 2
+    for z in range(cfg.nz):
+        half = c if z < 3 else (5 if z < 6 else 16)
+        h[z, :, :, c - half:c + half + 1, c - half:c + half + 1] = rng.uniform(0, 1, (N, N, 2 * half + 1, 2 * half + 1))
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    hd = h.astype(np.float64)
+    y = poisson(O.forward_project(gen_volume(cfg, 1), hd), 77)
+    return cfg, h, hd, y
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("flags", [0, 32], ids=["eager", "graphs"])
 def test_sm_partitions_identical(flags, monkeypatch):
@@ -676,9 +694,10 @@ def test_sm_partitions_identical(flags, monkeypatch):
     contexts, forced here with LFM_TC_SMS_F / _B) every kernel computes the same sums in the same order as the
     one-after-the-other plan (LFM_SERIAL): projections, the RL series and the volumes are bit-identical, eagerly
     and inside captured graphs."""
-    cfg, h, hd, y = tiny_problem("c2", 2)
+    cfg, h, hd, y = mixed_problem()
     x = gen_volume(cfg, 3, np.float32)
     r_img = np.asarray(y, np.float32) / np.float32(max(float(np.max(y)), 1.0)) + np.float32(0.5)
+    monkeypatch.setenv("LFM_PLAN_MOVE", "0")   # the same plane assignment in both modes (no partition-aware moves)
     s = torch.cuda.Stream()
     out = {}
     with torch.cuda.stream(s):
@@ -691,8 +710,7 @@ def test_sm_partitions_identical(flags, monkeypatch):
                 monkeypatch.setenv("LFM_TC_SMS_B", "104")
             with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
                 info = plan.info()
-                if info["tc_planes"] == 0 or info["fft_units"] == 0:
-                    pytest.skip("c2 hybrid plan has no mixed tensor-core / frequency-path planes")
+                assert info["tc_planes"] > 0 and info["fft_units"] > 0, info
                 y_d = torch.zeros((cfg.height, cfg.width), device="cuda")
                 plan.forward(dev(x), y_d, stream=s)
                 xb_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
