@@ -710,10 +710,16 @@ void tcdir_schedule(const TcDirArgs& d, const std::vector<TcPlane>& planes, std:
         load[best] += x.first;
         per[best].push_back(x.second);
     }
+    // Each CTA pair runs its items in the order LPT assigned them, i.e. the global (cost, plane, tile) order: at any
+    // moment all pairs work on neighbouring items of that order -- a few planes -- so a plane's coefficient tiles are
+    // fetched from HBM once and served from L2 to all its pixel tiles (sorting each pair's items by plane instead
+    // spread the pairs over many planes at once: a coefficient working set far beyond L2, re-read from HBM and
+    // competing with the concurrent MAC for bandwidth).  LFM_TC_SCHED=1 (dev): the old per-pair plane sort.
+    static const bool plane_sort = getenv("LFM_TC_SCHED") && atoi(getenv("LFM_TC_SCHED")) == 1;
     item_off->assign(1, 0);
     items->clear();
     for (int b = 0; b < d.grid; ++b) {
-        std::sort(per[b].begin(), per[b].end());   // plane-major within a CTA (L2 locality of the staged source)
+        if (plane_sort) std::sort(per[b].begin(), per[b].end());
         items->insert(items->end(), per[b].begin(), per[b].end());
         item_off->push_back((int)items->size());
     }

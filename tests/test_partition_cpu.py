@@ -50,3 +50,13 @@ def test_invalid_arguments():
         with pytest.raises(lfm.LfmError) as ei:
             lfm.lfm_partition_model(*args, **kw)
         assert ei.value.status == lfm.LFM_EINVAL
+
+
+def test_c3_f16_choice():
+    """r02, direct path on kind::f16: c3's 45 tensor-core planes cost 2.858 ms of tcgen05 work per direction and the 6
+    frequency-path planes stream 6.93 GB; the model gives 120 / 128 tensor-core SMs, the split measured on the box
+    (fwd 3.14 ms tcgen05 on 120 SMs vs MAC 3.14 ms on 28; bwd 3.17 vs 2.79 ms, gpurun_out r2c)."""
+    f, tf = L().lfm_partition_model(2.858, 6.93e9, 0)
+    b, tb = L().lfm_partition_model(2.858, 6.93e9, 1)
+    assert (f, b) == (120, 128)
+    assert 3.0 < tf < 3.6 and 3.0 < tb < 3.6
