@@ -26,8 +26,8 @@ namespace {
 constexpr int kMtM = 128;                 // rows (output phases) per CTA
 constexpr int kMtKC = 32;                 // K floats per chunk (16 complex units, one 128-byte swizzle row)
 constexpr int kMtChain = 4;               // chunks (x 4 K-steps) per drain group
-constexpr int kMtThreads = 448;           // 1 producer + 8 prep + 1 MMA + 4 drainer warps
-constexpr int kMtPrep = 8;
+// warps: 1 producer + NPREP prep + 1 MMA + 4 drainers (NPREP = 8 or 16, template parameter)
+__host__ __device__ constexpr int mt_threads(int NPREP) { return 32 * (NPREP + 6); }
 // Prep groups: group g of kMtPrep / PG warps prepares the chunks it with it % PG == g (each warp's wait -> build ->
 // fence -> arrive chain is serial per chunk, so PG groups keep PG chunks in preparation).  A ring stage s = it % S is
 // reused by chunk it + S, which (unless PG divides S) another group prepares.  With one fill barrier per stage a
@@ -51,21 +51,31 @@ __host__ __device__ constexpr int mt_stages(int F, int PG) { return ring_depth(m
 __host__ __device__ constexpr int mt_gcd(int a, int b) { return b == 0 ? a : mt_gcd(b, a % b); }
 }  // namespace
 
+// prep configuration (warps, groups): (8, 2), (8, 4) default, (16, 4); dev overrides LFM_MT_PREP / LFM_MT_PG
+int mac_tc_prep_warps() {
+    static int np = [] {
+        const char* e = getenv("LFM_MT_PREP");
+        return e && atoi(e) == 16 ? 16 : 8;
+    }();
+    return np;
+}
 int mac_tc_prep_groups() {
     static int pg = [] {
         const char* e = getenv("LFM_MT_PG");
-        const int v = e ? atoi(e) : 2;
-        return v == 4 ? 4 : 2;
+        const int v = e ? atoi(e) : 4;
+        if (mac_tc_prep_warps() == 16) return 4;
+        return v == 2 ? 2 : 4;
     }();
     return pg;
 }
 
 size_t mac_tc_smem_bytes(int F) { return (size_t)mt_stages(F, mac_tc_prep_groups()) * mt_stage(F) + 1024; }
 
-template <int F, int PG>
-__global__ void __launch_bounds__(kMtThreads, 1) fmb_tc_kernel(const __grid_constant__ MacTcArgs d) {
+template <int F, int PG, int NPREP>
+__global__ void __launch_bounds__(mt_threads(NPREP), 1) fmb_tc_kernel(const __grid_constant__ MacTcArgs d) {
     constexpr int S = mt_stages(F, PG);
     constexpr int kMtPG = PG;
+    constexpr int kMtPrep = NPREP;
     static_assert(S >= PG, "every prep group needs a stage");
     constexpr int NB = 4 * F;       // rows of the stacked B tile (B_hi: 0..2F-1, B_lo: 2F..4F-1)
     constexpr int NSET = 6 * F;     // TMEM columns per accumulator set: hi*hi | hi*lo | lo*hi
@@ -263,10 +273,11 @@ __host__ __device__ constexpr int bm_stages(int F, int PG) { return ring_depth(b
 
 size_t bmac_tc_smem_bytes(int F) { return (size_t)bm_stages(F, mac_tc_prep_groups()) * bm_stage(F) + 1024; }
 
-template <int F, int PG>
-__global__ void __launch_bounds__(kMtThreads, 1) bmb_tc_kernel(const __grid_constant__ BmacTcArgs d) {
+template <int F, int PG, int NPREP>
+__global__ void __launch_bounds__(mt_threads(NPREP), 1) bmb_tc_kernel(const __grid_constant__ BmacTcArgs d) {
     constexpr int S = bm_stages(F, PG);
     constexpr int kMtPG = PG;
+    constexpr int kMtPrep = NPREP;
     static_assert(S >= PG, "every prep group needs a stage");
     constexpr int NB = 4 * F;
     constexpr int NSET = 6 * F;
@@ -495,30 +506,29 @@ cudaError_t mac_tc_encode_g(MacTcArgs* d, const float2* G, long long g_fstride, 
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+template <int F, int PG, int NPREP>
+static cudaError_t launch_fmb(const MacTcArgs& d, int grid, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(fmb_tc_kernel<F, PG, NPREP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fmb_tc_kernel<F, PG, NPREP><<<grid, mt_threads(NPREP), smem, s>>>(d);
+    return cudaGetLastError();
+}
+template <int F>
+static cudaError_t launch_fmb_cfg(const MacTcArgs& d, int grid, size_t smem, cudaStream_t s) {
+    const int np = mac_tc_prep_warps(), pg = mac_tc_prep_groups();
+    if (np == 16) return launch_fmb<F, 4, 16>(d, grid, smem, s);
+    return pg == 2 ? launch_fmb<F, 2, 8>(d, grid, smem, s) : launch_fmb<F, 4, 8>(d, grid, smem, s);
+}
+
 cudaError_t launch_fwd_mac_batch_tc(const MacTcArgs& d, int F, int num_sms, cudaStream_t s) {
     const size_t smem = mac_tc_smem_bytes(F);
     const int grid = std::max(1, std::min(2 * d.nkappa, num_sms));
-    cudaError_t e;
-#define LFM_MT(FV)                                                                                                  \
-    case FV:                                                                                                        \
-        if (mac_tc_prep_groups() == 4) {                                                                            \
-            e = cudaFuncSetAttribute(fmb_tc_kernel<FV, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            if (e != cudaSuccess) return e;                                                                         \
-            fmb_tc_kernel<FV, 4><<<grid, kMtThreads, smem, s>>>(d);                                                 \
-        } else {                                                                                                    \
-            e = cudaFuncSetAttribute(fmb_tc_kernel<FV, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            if (e != cudaSuccess) return e;                                                                         \
-            fmb_tc_kernel<FV, 2><<<grid, kMtThreads, smem, s>>>(d);                                                 \
-        }                                                                                                           \
-        break;
     switch (F) {
-        LFM_MT(8)
-        LFM_MT(16)
-        LFM_MT(32)
+        case 8: return launch_fmb_cfg<8>(d, grid, smem, s);
+        case 16: return launch_fmb_cfg<16>(d, grid, smem, s);
+        case 32: return launch_fmb_cfg<32>(d, grid, smem, s);
         default: return cudaErrorInvalidValue;
     }
-#undef LFM_MT
-    return cudaGetLastError();
 }
 
 // A: M as real floats {2 nu_pad (u'), N2 (b'), kappa}, box {32, 32, 1}, SWIZZLE_128B_ATOM_32B (the MN-major tf32
@@ -537,30 +547,29 @@ cudaError_t bmac_tc_encode(BmacTcArgs* d, const float2* M) {
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+template <int F, int PG, int NPREP>
+static cudaError_t launch_bmb(const BmacTcArgs& d, int grid, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(bmb_tc_kernel<F, PG, NPREP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    bmb_tc_kernel<F, PG, NPREP><<<grid, mt_threads(NPREP), smem, s>>>(d);
+    return cudaGetLastError();
+}
+template <int F>
+static cudaError_t launch_bmb_cfg(const BmacTcArgs& d, int grid, size_t smem, cudaStream_t s) {
+    const int np = mac_tc_prep_warps(), pg = mac_tc_prep_groups();
+    if (np == 16) return launch_bmb<F, 4, 16>(d, grid, smem, s);
+    return pg == 2 ? launch_bmb<F, 2, 8>(d, grid, smem, s) : launch_bmb<F, 4, 8>(d, grid, smem, s);
+}
+
 cudaError_t launch_bwd_mac_batch_tc(const BmacTcArgs& d, int F, int num_sms, cudaStream_t s) {
     const size_t smem = bmac_tc_smem_bytes(F);
     const int nitems = d.nkappa * ((2 * d.nu_pad + kMtM - 1) / kMtM);
     const int grid = std::max(1, std::min(nitems, num_sms));
-    cudaError_t e;
-#define LFM_BM(FV)                                                                                                  \
-    case FV:                                                                                                        \
-        if (mac_tc_prep_groups() == 4) {                                                                            \
-            e = cudaFuncSetAttribute(bmb_tc_kernel<FV, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            if (e != cudaSuccess) return e;                                                                         \
-            bmb_tc_kernel<FV, 4><<<grid, kMtThreads, smem, s>>>(d);                                                 \
-        } else {                                                                                                    \
-            e = cudaFuncSetAttribute(bmb_tc_kernel<FV, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            if (e != cudaSuccess) return e;                                                                         \
-            bmb_tc_kernel<FV, 2><<<grid, kMtThreads, smem, s>>>(d);                                                 \
-        }                                                                                                           \
-        break;
     switch (F) {
-        LFM_BM(8)
-        LFM_BM(16)
+        case 8: return launch_bmb_cfg<8>(d, grid, smem, s);
+        case 16: return launch_bmb_cfg<16>(d, grid, smem, s);
         default: return cudaErrorInvalidValue;
     }
-#undef LFM_BM
-    return cudaGetLastError();
 }
 
 }  // namespace lfm

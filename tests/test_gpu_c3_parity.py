@@ -109,18 +109,20 @@ def test_c3g13_1_and_30_iterations(flags, monkeypatch):
     monkeypatch.setenv("LFM_TC_SMS_B", "104")
     sm = g["samples"]
     z, p, q = (np.asarray(sm[k]) for k in ("z", "p", "q"))
-    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L().make_optics(**OPTICS), flags=flags) as plan:
+    st = torch.cuda.Stream()   # graph capture needs a non-default stream
+    with torch.cuda.stream(st), \
+            L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L().make_optics(**OPTICS), flags=flags, stream=st) as plan:
         info = plan.info()
         assert info["tc_planes"] > 0 and info["fft_units"] > 0, info
         assert info["partition_sms"][0][0] == 96 and info["partition_sms"][1][0] == 104
         y_d = dev(y)
         x_d = torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda")
-        r1 = plan.rl_iterate(y_d, x_d, L().make_policy(mode="fixed", n_iters=1))
-        torch.cuda.synchronize()
+        r1 = plan.rl_iterate(y_d, x_d, L().make_policy(mode="fixed", n_iters=1), stream=st)
+        st.synchronize()
         check_volume(x_d.cpu().numpy(), g["x1"], z, p, q, cfg.nnum, 1e-4, 1e-4)
         assert abs(r1["series"][0] - g["series"][0]) <= 1e-4 * abs(g["series"][0])
-        r30 = plan.rl_iterate(y_d, x_d, L().make_policy(mode="fixed", n_iters=30))
-        torch.cuda.synchronize()
+        r30 = plan.rl_iterate(y_d, x_d, L().make_policy(mode="fixed", n_iters=30), stream=st)
+        st.synchronize()
         np.testing.assert_allclose(r30["series"], g["series"], rtol=1e-4)
         assert r30["best_iter"] == g["best_iter"]
         check_volume(x_d.cpu().numpy(), g["x_best"], z, p, q, cfg.nnum, 1e-3, 1e-4)
