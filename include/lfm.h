@@ -104,7 +104,7 @@ enum {
     LFM_PLAN_FFT_ONLY = 4,  /* every plane on the frequency path.  Default (neither flag): hybrid --
                                per plane, the cheapest of frequency / CUDA-core direct / tensor-core
                                direct by the cost model of DESIGN.md §5                               */
-    LFM_PLAN_TC_DIRECT = 16,/* with LFM_PLAN_DIRECT: every plane on the tcgen05 3xTF32 kernel         */
+    LFM_PLAN_TC_DIRECT = 16,/* with LFM_PLAN_DIRECT: every plane on the tcgen05 kernel                */
     LFM_PLAN_GRAPHS = 32,   /* lfm_rl_iterate replays each iteration as one captured CUDA graph (needs a
                                non-default stream; not combined with lfm_profile timing)             */
     LFM_PLAN_NO_TC = 64,    /* hybrid without the tensor-core direct kernel                          */
@@ -112,6 +112,10 @@ enum {
                                every collective of the sharded path runs, over one rank (testing)    */
     LFM_PLAN_EVEN_SHARDS = 256, /* world > 1: split the units evenly (lfm_shard_units) instead of by the
                                cost model (lfm_shard_units_balanced, the default)                     */
+    LFM_PLAN_SYMMETRIC = 1024, /* with a communicator: the forward's partial images live in an NCCL symmetric
+                               window and C1 (their sum over ranks) is our own kernel -- NVLS
+                               multimem.ld_reduce where the NVLink switch supports it, else rank-ordered
+                               peer loads -- instead of ncclAllReduce                 */
     LFM_PLAN_DEVICE_LOOP = 128 /* lfm_rl_iterate runs the whole loop as one CUDA graph: a conditional WHILE
                                node over two unrolled iterations, the stop rule and the argmax snapshot
                                evaluated on the device -- no host round trip per iteration (
@@ -133,14 +137,18 @@ typedef struct {
     double plan_ms;                 /* wall time of lfm_plan_create                                */
     int direct_planes;              /* planes (touching owned units) on the direct path            */
     int fft_units;                  /* owned units on the frequency path                            */
-    int tc_planes;                  /* direct planes on the tcgen05 (3xTF32 tensor-core) kernels    */
-    double tc_flops_executed;       /* per projection: tensor flops the tcgen05 kernel issues (3 TF32
-                                       products, union tap boxes, padded pixel rows)                 */
+    int tc_planes;                  /* direct planes on the tcgen05 (3-product fp16 split) kernels  */
+    double tc_flops_executed;       /* per projection: tensor flops the tcgen05 kernel issues (3 kind::f16
+                                       products, union tap boxes, column ranges, padded pixel rows)   */
     double tc_flops_algorithmic;    /* per projection: 2 * exact taps (D x D per phase pair) * pixels */
     int planes_moved_for_memory;    /* planes the hybrid planner moved off the frequency path so that the
                                        transfer matrices fit the device (memory-aware planning, §5.1)  */
     int partition_sms[2][2];        /* SM partitions of the [forward, backward] projection:
                                        [tensor-core SMs, frequency-path SMs]; 0 = run one after the other */
+    int c1_mode;                    /* the forward's sum over ranks: 0 ncclAllReduce (or none, one rank without
+                                       a communicator), 1 own kernel over symmetric memory with peer loads,
+                                       2 the same with NVLS multimem.ld_reduce (LFM_PLAN_SYMMETRIC, §7)       */
+    int tc_moved_to_fft;            /* tensor-core planes the partition-aware step moved to the frequency path */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */

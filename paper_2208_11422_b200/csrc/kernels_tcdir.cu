@@ -139,7 +139,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             tc::tma_load_3d_pair(as, am, 0, row, slab_hi, &bar_fullA[sa]);
                             tc::tma_load_3d_pair(as + apart, am, 0, row, slab_lo, &bar_fullA[sa]);
                         }
-                        const bool last_win = c * pl.T1 + t1 == pl.last_win;
                         for (int t2 = 0; t2 < pl.T2; ++t2, ++nb) {
                             const int sb = nb % kBSlots;
                             const long long c1 = (d.exp & 4) ? clock64() : 0;
@@ -416,11 +415,29 @@ __global__ void __launch_bounds__(256) tc_amax_kernel(const __grid_constant__ Tc
         n = SRC == SRC_ONES ? 0 : (size_t)d.H * d.W;
         if (SRC == SRC_ONES) m = 1.0f;
     }
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        float v = p[i];
+    // four independent loads in flight per thread (the loop is latency-bound otherwise)
+    const size_t st = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;
+    for (; i + 3 * st < n; i += 4 * st) {
+        float v0 = __ldg(p + i), v1 = __ldg(p + i + st), v2 = __ldg(p + i + 2 * st), v3 = __ldg(p + i + 3 * st);
+        if constexpr (!FWD && SRC == SRC_RATIO) {
+            v0 = v0 / (fmaxf(src2[i], 0.0f) + eps);
+            v1 = v1 / (fmaxf(src2[i + st], 0.0f) + eps);
+            v2 = v2 / (fmaxf(src2[i + 2 * st], 0.0f) + eps);
+            v3 = v3 / (fmaxf(src2[i + 3 * st], 0.0f) + eps);
+        }
+        m = fmaxf(m, fabsf(v0));
+        m1 = fmaxf(m1, fabsf(v1));
+        m2 = fmaxf(m2, fabsf(v2));
+        m3 = fmaxf(m3, fabsf(v3));
+    }
+    for (; i < n; i += st) {
+        float v = __ldg(p + i);
         if constexpr (!FWD && SRC == SRC_RATIO) v = v / (fmaxf(src2[i], 0.0f) + eps);
         m = fmaxf(m, fabsf(v));
     }
+    m = fmaxf(fmaxf(m, m1), fmaxf(m2, m3));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     __shared__ float wm[8];
@@ -853,7 +870,7 @@ template <bool FWD, int SRC>
 static cudaError_t tc_stage(const TcDirArgs& d, const float* src, const float* src2, float eps, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(d.amax, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
-    tc_amax_kernel<FWD, SRC><<<dim3(FWD ? 16 : 64, FWD ? d.nzd : 1), 256, 0, s>>>(d, src, src2, eps);
+    tc_amax_kernel<FWD, SRC><<<dim3(FWD ? 64 : 296, FWD ? d.nzd : 1), 256, 0, s>>>(d, src, src2, eps);
     dim3 grid((d.Lp + 32 * kStagePB - 1) / (32 * kStagePB), d.nch, FWD ? d.nzd : 1);
     tc_stage_kernel<FWD, SRC><<<grid, 256, 0, s>>>(d, src, src2, eps);
     return cudaGetLastError();

@@ -228,6 +228,7 @@ struct lfm_plan_s {
     double tc_flops_exec = 0.0, tc_flops_alg = 0.0;   // per projection (lfm_info)
     double tc_active_frac = 0.0;                       // mean fraction of nonzero (chunk, tap row) windows
     int part_moved = 0;                                // tensor-core planes the partition-aware step moved to FFT
+    SymState* sym = nullptr;                           // LFM_PLAN_SYMMETRIC: C1 over symmetric memory (kernels_sym.cu)
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -457,6 +458,7 @@ void plan_free(lfm_plan p) {
     for (cudaGraphExec_t g : p->lexec) cudaGraphExecDestroy(g);
     cudaFree(p->lstate);
     cudaFree(p->lseries);
+    if (p->sym) sym_destroy(p->sym);
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -556,8 +558,10 @@ lfm_status allreduce(lfm_plan p, void* buf, size_t n, ncclDataType_t t, ncclRedO
 
 // yhat = H x (x polyphase, owned units) summed over ranks
 // yhat = H x summed over ranks; x polyphase (owned units) or image layout [nz][H][W]
-lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, cudaStream_t s) {
+lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
+    // with a symmetric window the producers write this rank's partial image there and C1 sums it into ysum
+    float* yimg = p->sym ? sym_buffer(p->sym) : ysum;
     ST(mark(p, ST_R2C_X, s));
     if (p->direct) {
         const float* xp = x;
@@ -574,15 +578,19 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
         // tensor-core planes: stage the source; FFT units: coarse transforms.  Then the two halves of the projection
         // -- tcgen05 kernel and frequency-path MAC + C2R -- run side by side on the plan's SM partitions (§5.5) or one
         // after the other on `s`; afterwards the direct planes' partial images are added onto the C2R output.
+        // With partitions the staging of the tensor-core source and the coarse R2C run inside their halves (each on
+        // its own partition, overlapping the other half) rather than on the whole GPU before the fork.
         const lfm_plan_s::Part& pt = p->part[0];
         const bool split = pt.stc != nullptr;
-        for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, s, TC_PART_STAGE));
+        static const bool prefork = getenv("LFM_STAGE_PREFORK") != nullptr;   // dev A/B: staging before the fork
+        cudaStream_t st = s, sm = s;
+        if (split && !prefork) ST(fork(p, pt, s, &st, &sm));
+        for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_STAGE));
         if (p->nu_fft > 0)
             CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
-                          r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), s));
+                          r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), sm));
+        if (split && prefork) ST(fork(p, pt, s, &st, &sm));
         ST(mark(p, ST_FWD_MAC, s));
-        cudaStream_t st = s, sm = s;
-        if (split) ST(fork(p, pt, s, &st, &sm));
         if (!p->tcf.empty() && !(part_skip() & 1)) {
             ST(kmark(p, 0, 0, st));
             for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_MAIN));
@@ -624,6 +632,11 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* yimg, c
         if (!acc) CK(cudaMemsetAsync(yimg, 0, (size_t)p->geo.H * p->geo.W * sizeof(float), s));
     }
     ST(mark(p, ST_ALLRED_SUM, s));
+    if (p->sym) {
+        CK(sym_sum(p->sym, ysum, s));
+        p->pacc.launches += 1;
+        return LFM_OK;
+    }
     return allreduce(p, yimg, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclSum, s);
 }
 
@@ -662,12 +675,14 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     // as in the forward (§5.5); the two halves write disjoint units of `out`
     const lfm_plan_s::Part& pt = p->part[1];
     const bool split = pt.stc != nullptr;
-    for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, s, TC_PART_STAGE));
-    if (p->nu_fft > 0)
-        CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), s));
-    ST(mark(p, ST_BWD_MAC, s));
+    static const bool prefork = getenv("LFM_STAGE_PREFORK") != nullptr;
     cudaStream_t st = s, sm = s;
-    if (split) ST(fork(p, pt, s, &st, &sm));
+    if (split && !prefork) ST(fork(p, pt, s, &st, &sm));   // staging / R2C inside the halves, as in the forward
+    for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_STAGE));
+    if (p->nu_fft > 0)
+        CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), sm));
+    if (split && prefork) ST(fork(p, pt, s, &st, &sm));
+    ST(mark(p, ST_BWD_MAC, s));
     if (!p->tcb.empty() && !(part_skip() & 1)) {
         ST(kmark(p, 2, 0, st));
         for (const TcDirArgs& tg : p->tcb) {
@@ -1296,6 +1311,12 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         ncclResult_t r = ncclCommInitRank(&p->nccl, world, id, rank);
         if (r != ncclSuccess) return guard(fail(LFM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
         p->comm = true;
+        if (flags & LFM_PLAN_SYMMETRIC) {   // C1 over an NCCL symmetric window (collective: every rank passes the flag)
+            char e[256];
+            const lfm_status ss = sym_create(p->nccl, (size_t)height * width, getenv("LFM_SYM_NO_MULTIMEM") ? 0 : 1,
+                                             &p->sym, e, sizeof(e));
+            if (ss != LFM_OK) return guard(fail(ss, "LFM_PLAN_SYMMETRIC: %s", e));
+        }
     }
     // geometry for the kernels
     XformGeom& xg = p->xg;
@@ -1887,6 +1908,10 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     for (int d = 0; d < 2; ++d) {
         info->partition_sms[d][0] = p->part[d].sms_tc;
         info->partition_sms[d][1] = p->part[d].sms_mac;
+    }
+    {
+        info->c1_mode = p->sym ? 1 + sym_multimem(p->sym) : 0;
+        info->tc_moved_to_fft = p->part_moved;
     }
     info->tc_flops_algorithmic = p->direct ? 0.0 : p->tc_flops_alg;
     info->transfer_bytes = p->transfer_bytes;

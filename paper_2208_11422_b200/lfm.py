@@ -28,7 +28,7 @@ LFM_MODE_FIXED, LFM_MODE_AUTO = 0, 1
 LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
-LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS, LFM_PLAN_FORCE_COMM = 128, 256, 512
+LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS, LFM_PLAN_FORCE_COMM, LFM_PLAN_SYMMETRIC = 128, 256, 512, 1024
 
 
 class LfmError(RuntimeError):
@@ -62,7 +62,8 @@ class lfm_info(ctypes.Structure):
                 ("direct", ctypes.c_int), ("transfer_bytes", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
                 ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double),
-                ("planes_moved_for_memory", ctypes.c_int), ("partition_sms", (ctypes.c_int * 2) * 2)]
+                ("planes_moved_for_memory", ctypes.c_int), ("partition_sms", (ctypes.c_int * 2) * 2),
+                ("c1_mode", ctypes.c_int), ("tc_moved_to_fft", ctypes.c_int)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

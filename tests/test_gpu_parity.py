@@ -639,7 +639,8 @@ def test_device_loop_identical(name, mode, update):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("extra", [0, 32, 128], ids=["eager", "graphs", "device-loop"])
+@pytest.mark.parametrize("extra", [0, 32, 128, 1024, 1024 | 32], ids=["eager", "graphs", "device-loop", "symmetric",
+                                                                    "symmetric-graphs"])
 def test_nccl_one_rank_identical(extra):
     """The sharded path's collectives executed for real over a one-rank NCCL communicator (LFM_PLAN_FORCE_COMM):
     communicator init from lfm_comm_unique_id, allreduce(sum) of yhat, allreduce(max) of the max-projection, the
@@ -652,8 +653,11 @@ def test_nccl_one_rank_identical(extra):
     out = {}
     with torch.cuda.stream(s):
         for force in (False, True):
-            kw = dict(nccl_id=L_.lfm_comm_unique_id(), flags=extra | L_.LFM_PLAN_FORCE_COMM) if force else dict(flags=extra)
+            kw = dict(nccl_id=L_.lfm_comm_unique_id(), flags=extra | L_.LFM_PLAN_FORCE_COMM) if force else \
+                dict(flags=extra & ~1024)
             with L_.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), stream=s, **kw) as plan:
+                if force:
+                    info_sym = plan.info()
                 x = gen_volume(cfg, 2, np.float32)
                 yh = torch.zeros((cfg.height, cfg.width), device="cuda")
                 plan.forward(dev(x), yh, stream=s)
@@ -664,6 +668,8 @@ def test_nccl_one_rank_identical(extra):
                 s.synchronize()
                 out[force] = (yh.cpu().numpy(), xb.cpu().numpy(), r, x_d.cpu().numpy())
     a, b = out[False], out[True]
+    if extra & 1024:   # C1 through our own kernel over the symmetric window (NVLS multimem where the box offers it)
+        assert info_sym["c1_mode"] in (1, 2), info_sym
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert (a[2]["stop_iter"], a[2]["best_iter"], a[2]["series"]) == (b[2]["stop_iter"], b[2]["best_iter"], b[2]["series"])
     assert np.array_equal(a[3], b[3])
