@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=256, help="rows of the oracle's bounded CPU sample (~10-30 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="lfm_plan_create flags (2 = direct path)")
-    ap.add_argument("--frames", type=int, default=16, help="c5: frames per GPU per lockstep batch (2/4/8/16)")
+    ap.add_argument("--frames", type=int, default=32, help="c5: frames per GPU per lockstep batch (8/16/32 with the default "
+                    "LFM_PLAN_FRAMES plan; 2/4/8/16 with --flags 4)")
     return ap.parse_args()
 
 
@@ -464,26 +465,29 @@ def run_c5(args):
     from lfm_inputs import gen_somata
     cfg = CONFIGS["c3"]
     F = args.frames
-    flags = args.flags or L.LFM_PLAN_FFT_ONLY   # batched frames amortise M; tcgen05 planes do not batch
+    # a plan built for frame batches (all planes on the frequency path, fp16-split transfer matrices)
+    flags = args.flags or L.LFM_PLAN_FRAMES
     side = torch.cuda.Stream()
     torch.cuda.set_stream(side)
     stream = torch.cuda.current_stream()
     h = gen_psf(cfg, np.float32)
-    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), flags=flags)
-    info = plan.info()
-    del h
     H, W, nz = cfg.height, cfg.width, cfg.nz
     rng = np.random.default_rng(7)
     phase = rng.uniform(0, 2 * np.pi, cfg.n_objects)
     frames = [rank * F + f for f in range(F)]   # this rank's slice of the time-lapse
     ys = []
-    for g in frames:   # soma intensities 1 + 0.5 sin(2 pi g / 64 + phi_i), noise seed 1000 + g
-        xt = torch.from_numpy(gen_somata(cfg, 1, np.float32, modulation=1 + 0.5 * np.sin(2 * np.pi * g / 64 + phase))).cuda()
-        yh = torch.zeros((H, W), device="cuda")
-        plan.forward(xt, yh)
-        torch.cuda.synchronize()
-        ys.append(poisson(np.maximum(yh.cpu().numpy().astype(np.float64), 0), 1000 + g).astype(np.float32))
-        del xt
+    with L.Plan(h, cfg.nnum, H, W, optics=L.make_optics(**OPTICS)) as fplan:   # single-frame plan forms the y
+        for g in frames:   # soma intensities 1 + 0.5 sin(2 pi g / 64 + phi_i), noise seed 1000 + g
+            xt = torch.from_numpy(gen_somata(cfg, 1, np.float32, modulation=1 + 0.5 * np.sin(2 * np.pi * g / 64 + phase))).cuda()
+            yh = torch.zeros((H, W), device="cuda")
+            fplan.forward(xt, yh)
+            torch.cuda.synchronize()
+            ys.append(poisson(np.maximum(yh.cpu().numpy().astype(np.float64), 0), 1000 + g).astype(np.float32))
+            del xt
+    torch.cuda.empty_cache()
+    plan = L.Plan(h, cfg.nnum, cfg.height, cfg.width, optics=L.make_optics(**OPTICS), flags=flags)
+    info = plan.info()
+    del h
     yb = torch.from_numpy(np.stack(ys)).cuda()
     xb = torch.zeros((F, nz, H, W), device="cuda")
     plan.rl_iterate_batch(yb, xb, L.make_policy(mode="fixed", n_iters=args.warmup))

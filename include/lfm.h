@@ -112,6 +112,12 @@ enum {
                                every collective of the sharded path runs, over one rank (testing)    */
     LFM_PLAN_EVEN_SHARDS = 256, /* world > 1: split the units evenly (lfm_shard_units) instead of by the
                                cost model (lfm_shard_units_balanced, the default)                     */
+    LFM_PLAN_FRAMES = 2048, /* a plan for time-lapse frame batches (lfm_rl_iterate_batch, F = 8 / 16 / 32): every
+                               plane on the frequency path, the transfer matrices stored split into scaled fp16
+                               hi / lo rows plus a split transposed copy (twice the memory of M) so both batched
+                               passes run as TMA -> tcgen05 kind::f16 pipelines.  The single-frame calls
+                               (lfm_forward / _backward / _rl_step / _rl_iterate / lfm_deconvolve_host) return
+                               LFM_EUNSUPPORTED on such a plan.  Excludes DIRECT, GRAPHS, DEVICE_LOOP.       */
     LFM_PLAN_SYMMETRIC = 1024, /* with a communicator: the forward's partial images live in an NCCL symmetric
                                window and C1 (their sum over ranks) is our own kernel -- NVLS
                                multimem.ld_reduce where the NVLink switch supports it, else rank-ordered

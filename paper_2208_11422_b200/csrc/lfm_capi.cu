@@ -229,6 +229,15 @@ struct lfm_plan_s {
     double tc_active_frac = 0.0;                       // mean fraction of nonzero (chunk, tap row) windows
     int part_moved = 0;                                // tensor-core planes the partition-aware step moved to FFT
     SymState* sym = nullptr;                           // LFM_PLAN_SYMMETRIC: C1 over symmetric memory (kernels_sym.cu)
+    // LFM_PLAN_FRAMES: transfer matrices split into fp16 hi / lo rows (M) plus a split transposed copy (MT, rows u of
+    // bpitch complex) for the fp16 batched MACs (kernels_mac_f16.cu); the single-frame MACs are unavailable
+    bool frames = false;
+    float2* MT = nullptr;
+    int bpitch = 0;
+    MacF16Args mf_fwd{}, mf_bwd{};
+    int* mf_eb = nullptr;                              // [2][32] per-frame source scale exponents (fwd, bwd)
+    const void* mf_src[2] = {nullptr, nullptr};        // encoded source pointers / frame counts of mf_fwd / mf_bwd
+    int mf_F[2] = {0, 0};
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -459,6 +468,8 @@ void plan_free(lfm_plan p) {
     cudaFree(p->lstate);
     cudaFree(p->lseries);
     if (p->sym) sym_destroy(p->sym);
+    cudaFree(p->MT);
+    cudaFree(p->mf_eb);
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -1201,6 +1212,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     if (!out) return fail(LFM_EINVAL, "out is NULL");
     *out = nullptr;
     if (!psf_host) return fail(LFM_EINVAL, "psf_host is NULL");
+    if (flags & LFM_PLAN_FRAMES) {   // built for frame batches: every plane on the frequency path
+        if (flags & (LFM_PLAN_DIRECT | LFM_PLAN_DEVICE_LOOP | LFM_PLAN_GRAPHS))
+            return fail(LFM_EINVAL, "LFM_PLAN_FRAMES excludes LFM_PLAN_DIRECT / _DEVICE_LOOP / _GRAPHS");
+        flags |= LFM_PLAN_FFT_ONLY;
+    }
     Geo g;
     ST(make_geo(nnum, nz, kh, kw, height, width, /*direct=*/false, &g));
     int rank = 0, world = 1;
@@ -1836,6 +1852,24 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     if (!(p->host[0] > 0.0) || !std::isfinite(p->host[0]))
         return guard(fail(LFM_EZERO, "sum of H^T 1 = %g: the PSF projects nothing onto this %dx%d image", p->host[0],
                           height, width));
+    if (flags & LFM_PLAN_FRAMES) {
+        // after every single-frame use of M (the normalizer above): the transposed copy for the backward pass, then
+        // both split in place into scaled fp16 hi / lo rows
+        if (p->nu_fft <= 0 || N2 > 256) return guard(fail(LFM_EUNSUPPORTED, "LFM_PLAN_FRAMES needs frequency-path units and N^2 <= 256"));
+        p->bpitch = (int)round_up((size_t)N2, 4);
+        const size_t mtb = (size_t)g.nkappa * p->nu_fft_pad * p->bpitch * sizeof(float2);
+        PG(dalloc(p, &p->MT, mtb, "transposed transfer matrices (LFM_PLAN_FRAMES)"));
+        p->transfer_bytes += mtb;
+        PG(dalloc(p, &p->mf_eb, 64 * sizeof(int), "frame scales"));
+        CKG(mac_f16_prepare(p->M, p->Mb, p->MT, g.nkappa, N2, p->nu_fft_pad, p->bpitch, &p->mf_fwd, &p->mf_bwd, s));
+        if (p->Mb != p->M) {   // a supplied Ht: its matrices live on only as the transposed copy
+            cudaFree(p->Mb);
+            p->bytes -= (size_t)g.nkappa * N2 * p->nu_fft_pad * sizeof(float2);
+            p->transfer_bytes -= (size_t)g.nkappa * N2 * p->nu_fft_pad * sizeof(float2);
+        }
+        p->Mb = nullptr;
+        p->frames = true;
+    }
     p->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     *out = p;
     return LFM_OK;
@@ -1925,12 +1959,14 @@ void lfm_plan_destroy(lfm_plan p) { plan_free(p); }
 lfm_status lfm_forward(lfm_plan p, const float* x, float* y, void* stream) {
     g_err[0] = 0;
     if (!p || !x || !y) return fail(LFM_EINVAL, "NULL argument");
+    if (p->frames) return fail(LFM_EUNSUPPORTED, "plan built for frame batches (LFM_PLAN_FRAMES): use lfm_rl_iterate_batch");
     return op_forward_src(p, x, /*image=*/true, y, as_stream(stream));
 }
 
 lfm_status lfm_backward(lfm_plan p, const float* y, float* x, void* stream) {
     g_err[0] = 0;
     if (!p || !x || !y) return fail(LFM_EINVAL, "NULL argument");
+    if (p->frames) return fail(LFM_EUNSUPPORTED, "plan built for frame batches (LFM_PLAN_FRAMES): use lfm_rl_iterate_batch");
     return op_backward(p, SRC_IMAGE2D, y, nullptr, 1.0f, DST_VOLIMAGE, x, nullptr, as_stream(stream));
 }
 
@@ -1945,6 +1981,7 @@ lfm_status lfm_rl_step(lfm_plan p, const float* y, const float* x_in, float* x_o
                        float* yhat_out, double* entropy_host, void* stream) {
     g_err[0] = 0;
     if (!p || !y || !x_in || !x_out) return fail(LFM_EINVAL, "NULL argument");
+    if (p->frames) return fail(LFM_EUNSUPPORTED, "plan built for frame batches (LFM_PLAN_FRAMES): use lfm_rl_iterate_batch");
     if (!(eps > 0.0f)) return fail(LFM_EINVAL, "eps must be > 0");
     cudaStream_t s = as_stream(stream);
     CK(launch_image_to_poly(x_in, p->xb[0], p->xall, p->u0, p->nu, s));
@@ -1976,6 +2013,7 @@ lfm_status lfm_rl_iterate(lfm_plan p, const float* y, float* x, const lfm_policy
 lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, int* best_iter, int* stop_iter,
                    double* series_host, float* ms_host, cudaStream_t s, float* host_mirror, bool* mirrored) {
     *mirrored = false;
+    if (p->frames) return fail(LFM_EUNSUPPORTED, "plan built for frame batches (LFM_PLAN_FRAMES): use lfm_rl_iterate_batch");
     ST(check_policy(pol));
     if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the stop rule needs the DCT-entropy metric");
     ST(check_y(p, y, s));
@@ -2196,8 +2234,10 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                                 int* stop_iter, double* series_host, float* ms_host, void* stream) {
     g_err[0] = 0;
     if (!p || !y || !x || !best_iter || !stop_iter || !series_host) return fail(LFM_EINVAL, "NULL argument");
-    if (frames != 2 && frames != 4 && frames != 8 && frames != 16)
-        return fail(LFM_EINVAL, "frames=%d: the batched path takes 2, 4, 8 or 16 frames (one frame: lfm_rl_iterate)", frames);
+    if (p && p->frames ? (frames != 8 && frames != 16 && frames != 32)
+                       : (frames != 2 && frames != 4 && frames != 8 && frames != 16))
+        return fail(LFM_EINVAL, "frames=%d: the batched path takes 2, 4, 8 or 16 frames (LFM_PLAN_FRAMES plans: 8, 16 or "
+                    "32; one frame: lfm_rl_iterate)", frames);
     ST(check_policy(pol));
     if (pol->update != LFM_UPDATE_RL) return fail(LFM_EUNSUPPORTED, "the batched path runs the RL update only");
     if (p->direct) return fail(LFM_EUNSUPPORTED, "the batched path needs a frequency / hybrid plan");
@@ -2208,6 +2248,8 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
     const size_t HW = (size_t)p->geo.H * p->geo.W;
     const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
     const long long sG = (long long)p->geo.nkappa * p->nu_fft_pad, sY = (long long)p->geo.nkappa * N2;
+    const int rld = p->frames ? p->bpitch : N2;             // R row pitch (the fp16 MACs read R through a TMA map)
+    const long long sR = (long long)p->geo.nkappa * rld;
     if (p->bcap < F) {   // (re)allocate the per-frame state
         cudaFree(p->bG); cudaFree(p->bXh); cudaFree(p->bY); cudaFree(p->bR); cudaFree(p->bx); cudaFree(p->byhat);
         cudaFree(p->bmproj); cudaFree(p->bent);
@@ -2221,8 +2263,9 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
             ST(dalloc(p, &p->bG, (size_t)F * sG * sizeof(float2), "batch G spectra"));
             ST(dalloc(p, &p->bXh, (size_t)F * sG * sizeof(float2), "batch Xh spectra"));
             ST(dalloc(p, &p->bY, (size_t)F * sY * sizeof(float2), "batch Y spectra"));
-            ST(dalloc(p, &p->bR, (size_t)F * sY * sizeof(float2), "batch R spectra"));
+            ST(dalloc(p, &p->bR, (size_t)F * sR * sizeof(float2), "batch R spectra"));
             CK(cudaMemsetAsync(p->bG, 0, (size_t)F * sG * sizeof(float2), s));   // padding columns stay zero
+            CK(cudaMemsetAsync(p->bR, 0, (size_t)F * sR * sizeof(float2), s));
         }
         ST(dalloc(p, &p->bx, (size_t)3 * F * vol * sizeof(float), "batch volumes"));
         ST(dalloc(p, &p->byhat, (size_t)F * HW * sizeof(float), "batch yhat"));
@@ -2261,7 +2304,20 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                     CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                                   r2c_args(SRC_POLY, xbuf(f, cur[f]), nullptr, 0.f, p->nu_fft, p->bG + f * sG, p->nu_fft_pad), s));
             ST(mark(p, ST_FWD_MAC, s));
-            if (!p->mac_tc_off && F >= 8 && N2 <= 256) {   // tcgen05 3xTF32 batched MAC
+            if (p->frames) {   // fp16 split transfer matrices, kind::f16 (kernels_mac_f16.cu)
+                CK(launch_frame_scales(p->bG, sG, p->nu_fft_pad, F, p->mf_eb, s));
+                if (p->mf_src[0] != p->bG || p->mf_F[0] != F) {
+                    CK(mac_f16_encode_src(&p->mf_fwd, 1, p->bG, sG, F));
+                    p->mf_src[0] = p->bG;
+                    p->mf_F[0] = F;
+                }
+                p->mf_fwd.bexp = p->mf_eb;
+                p->mf_fwd.out = p->bY;
+                p->mf_fwd.out_fstride = sY;
+                p->mf_fwd.out_ld = N2;
+                ST(kmark(p, 1, 0, s));
+                CK(launch_mac_f16(p->mf_fwd, 1, F, p->num_sms, s));
+            } else if (!p->mac_tc_off && F >= 8 && N2 <= 256) {   // tcgen05 3xTF32 batched MAC
                 if (!p->mac_tc_ready) {
                     p->mac_tc.nkappa = p->geo.nkappa;
                     p->mac_tc.N2 = N2;
@@ -2314,7 +2370,7 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
             ST(allreduce(p, yimg, HW, ncclFloat, ncclSum, s));
             if (p->nu_fft > 0)
                 CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
-                              r2c_args(SRC_RATIO, y + f * HW, yimg, pol->eps, N2, p->bR + f * sY, N2), s));
+                              r2c_args(SRC_RATIO, y + f * HW, yimg, pol->eps, N2, p->bR + f * sR, rld), s));
         }
         // ---- backward: one batched pass over M^H, inverse + update per frame ----
         ST(mark(p, ST_DIR_FWD, s));   // (empty stages: the batch groups above hold their work)
@@ -2324,7 +2380,19 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         if (p->nu_fft > 0) {
             ST(kmark(p, 3, 0, s));
             static const bool bwd_simt = getenv("LFM_BWD_BATCH_SIMT") != nullptr;   // dev: CUDA-core batched backward
-            if (!p->mac_tc_off && (F == 8 || F == 16) && !bwd_simt) {   // tcgen05 3xTF32
+            if (p->frames) {   // fp16 split transposed transfer matrices, kind::f16
+                CK(launch_frame_scales(p->bR, sR, rld, F, p->mf_eb + 32, s));
+                if (p->mf_src[1] != p->bR || p->mf_F[1] != F) {
+                    CK(mac_f16_encode_src(&p->mf_bwd, 0, p->bR, sR, F));
+                    p->mf_src[1] = p->bR;
+                    p->mf_F[1] = F;
+                }
+                p->mf_bwd.bexp = p->mf_eb + 32;
+                p->mf_bwd.out = p->bXh;
+                p->mf_bwd.out_fstride = sG;
+                p->mf_bwd.out_ld = p->nu_fft_pad;
+                CK(launch_mac_f16(p->mf_bwd, 0, F, p->num_sms, s));
+            } else if (!p->mac_tc_off && (F == 8 || F == 16) && !bwd_simt) {   // tcgen05 3xTF32
                 if (!p->bmac_F) {   // tensor map over the (backward) transfer matrices, once
                     p->bmac_tc.nkappa = p->geo.nkappa;
                     p->bmac_tc.N2 = N2;
@@ -2335,10 +2403,10 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
                 p->bmac_tc.Xh = p->bXh;
                 p->bmac_tc.x_fstride = sG;
                 p->bmac_tc.R = p->bR;
-                p->bmac_tc.r_fstride = sY;
+                p->bmac_tc.r_fstride = sR;
                 CK(launch_bwd_mac_batch_tc(p->bmac_tc, F, p->num_sms, s));
             } else {
-                CK(launch_bwd_mac_batch(p->Mb, p->bR, sY, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
+                CK(launch_bwd_mac_batch(p->Mb, p->bR, sR, p->bXh, sG, F, p->geo.nkappa, N2, p->nu_fft_pad, s));
             }
             ST(kmark(p, 3, 1, s));
             p->pacc.launches += 1;

@@ -233,6 +233,25 @@ struct BmacTcArgs {
     long long r_fstride;
     alignas(64) CUtensorMap tmapA;   // M as floats {2 nu_pad, N2, kappa}, box {32, 32, 1}, SWIZZLE_128B_ATOM_32B
 };
+// frame-batched MACs of LFM_PLAN_FRAMES plans: transfer matrices pre-split into scaled fp16 hi / lo rows, kind::f16
+// (kernels_mac_f16.cu).  fwd: A = M rows b', src = G; bwd: A = M^T rows u (row pitch bpitch), src = R (pitch bpitch)
+struct MacF16Args {
+    int nkappa, N2, nu_pad, bpitch;
+    int aexp;                 // the transfer matrices' scale exponent
+    int chain_k;              // K-steps accumulated in TMEM between drains
+    const int* bexp;          // [F] the frames' source scale exponents (device, per call)
+    float2* out;              // fwd: Y [F][kappa][N2]; bwd: Xh [F][kappa][nu_pad]
+    long long out_fstride, out_ld;
+    alignas(64) CUtensorMap tmapAh;   // A hi parts {2n fp16, rows, kappa}, box {64, 128, 1}, SWIZZLE_128B
+    alignas(64) CUtensorMap tmapAl;   // A lo parts (same rows, + 4n bytes)
+    alignas(64) CUtensorMap tmapS;    // the frames' fp32 source {2n floats, kappa, F}, box {64, 1, F}
+};
+cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa, int N2, int nu_pad, int bpitch,
+                            MacF16Args* fwd, MacF16Args* bwd, cudaStream_t s);
+cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F);
+cudaError_t launch_frame_scales(const float2* src, long long fstride, int n, int F, int* eb, cudaStream_t s);
+cudaError_t launch_mac_f16(const MacF16Args& d, int fwd, int F, int num_sms, cudaStream_t s);
+size_t mac_f16_smem_bytes(int F);
 size_t bmac_tc_smem_bytes(int F);
 cudaError_t bmac_tc_encode(BmacTcArgs* d, const float2* M);
 cudaError_t launch_bwd_mac_batch_tc(const BmacTcArgs& d, int F, int num_sms, cudaStream_t s);

@@ -29,6 +29,7 @@ LFM_REGION_TRIANGLE, LFM_REGION_RECTANGLE = 0, 1
 LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
 LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS, LFM_PLAN_FORCE_COMM, LFM_PLAN_SYMMETRIC = 128, 256, 512, 1024
+LFM_PLAN_FRAMES = 2048
 
 
 class LfmError(RuntimeError):

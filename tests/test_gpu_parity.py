@@ -793,3 +793,69 @@ def test_host_call_pinned_mirror(name, mode):
         assert (r1["stop_iter"], r1["best_iter"]) == (r2["stop_iter"], r2["best_iter"])
         assert r1["series"] == r2["series"]
         assert np.array_equal(xh_t.numpy(), x_d.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_batched_tc_macs_repeatable():
+    """Race guard for the frame-batched tcgen05 MACs (compute-sanitizer is closed on this pool): every kernel of the
+    batched path is deterministic, so 12 repetitions of the same F = 16 batch (s15, all planes through the batched
+    forward and backward MACs, ring stages shared by the prep groups) must give bit-identical volumes and series; a
+    prep group reading a half-filled tile (the r01 fault) would show up as a mismatch or a trap."""
+    cfg = CONFIGS["s15"]
+    h = gen_psf(cfg, np.float32)
+    hd = h.astype(np.float64)
+    F = 16
+    ys = [poisson(O.forward_project(gen_volume(cfg, 1 + f % 3), hd) * (1.0 + 0.05 * f), 500 + f) for f in range(F)]
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=L().LFM_PLAN_FFT_ONLY) as plan:
+        yb = dev(np.stack(ys))
+        ref = None
+        for rep in range(12):
+            xb = torch.zeros((F, cfg.nz, cfg.height, cfg.width), device="cuda")
+            r = plan.rl_iterate_batch(yb, xb, L().make_policy(mode="fixed", n_iters=3))
+            torch.cuda.synchronize()
+            got = (xb.cpu().numpy(), r["series"])
+            if ref is None:
+                ref = got
+            else:
+                assert np.array_equal(got[0], ref[0]) and got[1] == ref[1], f"repetition {rep} differs"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,F", [("s15", 8), ("s15", 32), ("c2", 16)])
+def test_frames_plan_matches_oracle(name, F):
+    """LFM_PLAN_FRAMES (f1): the transfer matrices stored split into scaled fp16 hi / lo rows plus a split transposed
+    copy; both batched passes on tcgen05 kind::f16.  Frames 0, 1, F/2, F-1 against the oracle: identical stop / best
+    (C16 margin rule), series within 1e-4, volumes within 1e-3 (fixed 3 and auto); single-frame calls are refused."""
+    cfg = CONFIGS[name]
+    h = gen_psf(cfg, np.float32)
+    hd = h.astype(np.float64)
+    ys = [poisson(O.forward_project(gen_volume(cfg, 1 + f % 3), hd) * (1.0 + 0.05 * f), 700 + f) for f in range(F)]
+    check = [0, 1, F // 2, F - 1]
+    refs = {f: oracle_frame(ys[f], hd, cfg) for f in check}
+    reg = O.cutoff_region(O.Optics(nnum=cfg.nnum, **OPTICS), cfg.height, cfg.width)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=L().LFM_PLAN_FRAMES) as plan:
+        with pytest.raises(L().LfmError) as e:
+            plan.forward(torch.zeros((cfg.nz, cfg.height, cfg.width), device="cuda"),
+                         torch.zeros((cfg.height, cfg.width), device="cuda"))
+        assert e.value.status == L().LFM_EUNSUPPORTED
+        yb = dev(np.stack(ys))
+        for pol in (L().make_policy(mode="fixed", n_iters=3), L().make_policy(mode="auto", max_iters=25)):
+            xb = torch.zeros((F, cfg.nz, cfg.height, cfg.width), device="cuda")
+            rb = plan.rl_iterate_batch(yb, xb, pol)
+            for f in check:
+                ref, its = refs[f]
+                got = xb[f].cpu().numpy()
+                if pol.mode == L().LFM_MODE_FIXED:
+                    es = [O.evaluate_iteration(its[k], reg) for k in range(3)]
+                    np.testing.assert_allclose(rb["series"][f], es, rtol=1e-4)
+                    assert rb["best_iter"][f] == int(np.argmax(es)) + 1
+                    assert rel(got, its[rb["best_iter"][f] - 1]) <= 1e-3
+                    continue
+                n = min(len(ref.series), len(rb["series"][f]))
+                err = max(abs(a - b) / abs(b) for a, b in zip(rb["series"][f][:n], ref.series[:n]))
+                assert err <= 1e-4, (f, err)
+                k = ref.stop_iter
+                margin = min(abs(ref.series[i] - ref.series[i - 1]) / abs(ref.series[i]) for i in range(1, k)) if k > 1 else 1.0
+                if margin > 10 * err:
+                    assert (rb["stop_iter"][f], rb["best_iter"][f]) == (ref.stop_iter, ref.best_iter), f
+                    assert rel(got, ref.volume) <= 1e-3
