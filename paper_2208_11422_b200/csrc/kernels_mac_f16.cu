@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t bar_full[PG][S], bar_ready[S], bar_empty[S], bar_acc[2], bar_tfree[2];
     __shared__ uint32_t tmem_base;
+    __shared__ float s_scale[F], s_inv[F];   // per frame: 2^eB (prep) and 2^-(eA + eB) (epilogue)
     const uint32_t raw = tc::smem_u32(smem_raw);
     unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -84,6 +85,10 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
         tc::tma_prefetch_desc(&d.tmapS);
     }
     if (warp == 0) tc::tmem_alloc(&tmem_base, 2 * NSET <= 256 ? 256 : 512);
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+        s_scale[f] = tc::pow2f(d.bexp[f]);
+        s_inv[f] = ldexpf(1.0f, -(d.aexp + d.bexp[f]));
+    }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -128,26 +133,31 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
                     if (e < F * (kFK / 2)) {
                         const int f = e / (kFK / 2), j = e - f * (kFK / 2);
                         const float2 g = src[f * (kFK / 2) + j];
-                        const int ex = d.bexp[f];
-                        float v0[2], v1[2];   // rows 2f and 2f+1, elements (2j, 2j+1)
-                        if constexpr (FWD) {
-                            v0[0] = g.x; v0[1] = -g.y; v1[0] = g.y; v1[1] = g.x;
-                        } else {
-                            v0[0] = g.x; v0[1] = g.y; v1[0] = g.y; v1[1] = -g.x;
+                        // two splits per complex value; the B entries are +-re / +-im, and -(h + l) = (-h) + (-l)
+                        // is a sign flip of both fp16 halves
+                        uint16_t rh, rl, ih, il;
+                        tc::split_f16(g.x, s_scale[f], rh, rl);
+                        tc::split_f16(g.y, s_scale[f], ih, il);
+                        uint32_t h0, l0, h1, l1;   // rows 2f, 2f+1: (element 2j) | (element 2j+1) << 16
+                        if constexpr (FWD) {       // (re, -im), (im, re)
+                            h0 = (uint32_t)rh | ((uint32_t)(ih ^ 0x8000u) << 16);
+                            l0 = (uint32_t)rl | ((uint32_t)(il ^ 0x8000u) << 16);
+                            h1 = (uint32_t)ih | ((uint32_t)rh << 16);
+                            l1 = (uint32_t)il | ((uint32_t)rl << 16);
+                        } else {                   // (re, im), (im, -re)
+                            h0 = (uint32_t)rh | ((uint32_t)ih << 16);
+                            l0 = (uint32_t)rl | ((uint32_t)il << 16);
+                            h1 = (uint32_t)ih | ((uint32_t)(rh ^ 0x8000u) << 16);
+                            l1 = (uint32_t)il | ((uint32_t)(rl ^ 0x8000u) << 16);
                         }
 #pragma unroll
                         for (int r = 0; r < 2; ++r) {
-                            const float* v = r ? v1 : v0;
-                            uint16_t h0, l0, h1, l1;
-                            tc::split_f16(v[0], ex, h0, l0);
-                            tc::split_f16(v[1], ex, h1, l1);
-                            const int row = 2 * f + r;
+                            const int row = 2 * f + r, rowl = 2 * F + row;
                             // byte offset of elements (row, 2j .. 2j+1) in a K-major SWIZZLE_128B fp16 tile
                             const uint32_t off = (uint32_t)row * 128u + ((((uint32_t)(j >> 2)) ^ (row & 7)) & 7) * 16u + (j & 3) * 4u;
-                            const uint32_t offl = (uint32_t)(2 * F + row) * 128u +
-                                                  ((((uint32_t)(j >> 2)) ^ ((2 * F + row) & 7)) & 7) * 16u + (j & 3) * 4u;
-                            *reinterpret_cast<uint32_t*>(bt + off) = (uint32_t)h0 | ((uint32_t)h1 << 16);
-                            *reinterpret_cast<uint32_t*>(bt + offl) = (uint32_t)l0 | ((uint32_t)l1 << 16);
+                            const uint32_t offl = (uint32_t)rowl * 128u + ((((uint32_t)(j >> 2)) ^ (rowl & 7)) & 7) * 16u + (j & 3) * 4u;
+                            *reinterpret_cast<uint32_t*>(bt + off) = r ? h1 : h0;
+                            *reinterpret_cast<uint32_t*>(bt + offl) = r ? l1 : l0;
                         }
                     }
                 }
@@ -205,14 +215,20 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
                 tc::fence_after();
                 const uint32_t base = lane_base + (uint32_t)(j * NSET);
 #pragma unroll
-                for (int b0 = 0; b0 < 3; ++b0) {
+                for (int b0 = 0; b0 < 3; ++b0) {   // up to 32 columns in flight per wait (not one wait per 8)
 #pragma unroll
-                    for (int c8 = 0; c8 < 2 * F; c8 += 8) {
-                        uint32_t v[8];
-                        tc::tmem_ld8_nowait(base + (uint32_t)(b0 * 2 * F + c8), v);
+                    for (int c8 = 0; c8 < 2 * F; c8 += 32) {
+                        constexpr int W = 2 * F < 32 ? 2 * F : 32;
+                        uint32_t v[W];
+                        if constexpr (W == 32) {
+                            tc::tmem_ld32_nowait(base + (uint32_t)(b0 * 2 * F + c8), v);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < W; c += 8) tc::tmem_ld8_nowait(base + (uint32_t)(b0 * 2 * F + c8 + c), v + c);
+                        }
                         tc::tmem_wait_ld();
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) acc[c8 + u] += __uint_as_float(v[u]);
+                        for (int u = 0; u < W; ++u) acc[c8 + u] += __uint_as_float(v[u]);
                     }
                 }
                 tc::fence_before();
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
             if (row < (FWD ? d.N2 : d.nu_pad)) {
 #pragma unroll
                 for (int f = 0; f < F; ++f) {
-                    const float inv = ldexpf(1.0f, -(d.aexp + d.bexp[f]));
+                    const float inv = s_inv[f];
                     const float2 v = make_float2(acc[2 * f] * inv, acc[2 * f + 1] * inv);
                     d.out[(long long)f * d.out_fstride + (long long)kap * d.out_ld + row] = v;
                 }
@@ -275,10 +291,11 @@ __global__ void mf_split_rows_kernel(float2* __restrict__ rows, int n, int e) {
     __syncthreads();
     uint32_t* hi = reinterpret_cast<uint32_t*>(row);   // n uint32 = 2n fp16
     uint32_t* lo = hi + n;
+    const float sc = tc::pow2f(e);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         uint16_t h0, l0, h1, l1;
-        tc::split_f16(rowbuf[i].x, e, h0, l0);
-        tc::split_f16(rowbuf[i].y, e, h1, l1);
+        tc::split_f16(rowbuf[i].x, sc, h0, l0);
+        tc::split_f16(rowbuf[i].y, sc, h1, l1);
         hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
         lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
     }
@@ -350,7 +367,7 @@ cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa,
         a->nu_pad = nu_pad;
         a->bpitch = bpitch;
         a->aexp = w ? eb : ea;
-        a->chain_k = 24;
+        a->chain_k = getenv("LFM_MF_CHAIN") ? std::max(4, atoi(getenv("LFM_MF_CHAIN"))) : 24;   // dev override
         const int n = w ? bpitch : nu_pad;               // complex per split row
         const int rows = w ? nu_pad : N2;
         unsigned char* base = reinterpret_cast<unsigned char*>(w ? MT : M);

@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ T
     __shared__ float tile[kStagePB][kKC][33];
     const int L0 = blockIdx.x * 32 * kStagePB, c = blockIdx.y, zi = blockIdx.z;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int aexp = tc::f16_scale_exp(__uint_as_float(*d.amax));
+    const float ascale = tc::pow2f(tc::f16_scale_exp(__uint_as_float(*d.amax)));
     {
         float v[kStagePB][kKC / 8];
         float w[kStagePB][kKC / 8];   // yhat for SRC_RATIO
@@ -525,8 +525,8 @@ __global__ void __launch_bounds__(256) tc_stage_kernel(const __grid_constant__ T
             const int L = L0 + 32 * j + rr;
             if (L >= d.Lp) break;
             uint16_t h0, l0, h1, l1;
-            tc::split_f16(tile[j][2 * tx][rr], aexp, h0, l0);
-            tc::split_f16(tile[j][2 * tx + 1][rr], aexp, h1, l1);
+            tc::split_f16(tile[j][2 * tx][rr], ascale, h0, l0);
+            tc::split_f16(tile[j][2 * tx + 1][rr], ascale, h1, l1);
             dst[(slab_hi * d.Lp + L) * (kKC / 2) + tx] = (uint32_t)h0 | ((uint32_t)h1 << 16);
             dst[(slab_lo * d.Lp + L) * (kKC / 2) + tx] = (uint32_t)l0 | ((uint32_t)l1 << 16);
         }
@@ -609,7 +609,7 @@ __global__ void tcdir_coef_kernel(const __grid_constant__ TcDirArgs d, TcPlane p
             }
         }
         uint16_t h, l;
-        tc::split_f16(v, pl.bexp, h, l);
+        tc::split_f16(v, tc::pow2f(pl.bexp), h, l);
         hi[e] = h;
         lo[e] = l;
         if (v != 0.0f) {

@@ -9,6 +9,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 namespace lfm {
 namespace tc {
@@ -326,11 +327,12 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     lo = __uint_as_float(l);
 }
 
-// fp32 -> (hi, lo) fp16 pair of x * 2^e (round to nearest): hi = fp16(v), lo = fp16(v - hi), v = x * 2^e.  With the
+// fp32 -> (hi, lo) fp16 pair of x * 2^e (round to nearest): hi = fp16(v), lo = fp16(v - hi), v = x * 2^e (the caller
+// passes the factor 2^e, computed once: ldexpf per element costs a dozen instructions).  With the
 // operands scaled so that their maxima sit near 2^13, hi + lo carries 22 significant bits (as a 3xTF32 split does)
 // and the 3-product sum ah*bh + ah*bl + al*bh runs on kind::f16 at twice the tf32 rate ("3xFP16").
-__device__ __forceinline__ void split_f16(float x, int e, uint16_t& hi, uint16_t& lo) {
-    const float v = ldexpf(x, e);
+__device__ __forceinline__ void split_f16(float x, float scale2e, uint16_t& hi, uint16_t& lo) {
+    const float v = x * scale2e;   // scale2e = 2^e: exact (a power of two; the scaled values stay normal)
     uint16_t h, l;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
     float hf;
@@ -339,6 +341,15 @@ __device__ __forceinline__ void split_f16(float x, int e, uint16_t& hi, uint16_t
     hi = h;
     lo = l;
 }
+// 2^e exactly, as a float (e in [-126, 127])
+__host__ __device__ inline float pow2f(int e) {
+    e = e < -126 ? -126 : (e > 127 ? 127 : e);
+    const unsigned bits = (unsigned)(e + 127) << 23;
+    float f;
+    memcpy(&f, &bits, sizeof(f));
+    return f;
+}
+
 // power-of-two exponent that puts a non-negative maximum near 2^13 (its fp16 hi / lo parts then stay normal for every
 // value within ~2^-20 of the maximum; smaller values lose relative, not absolute, precision); 0 for an all-zero max
 __host__ __device__ inline int f16_scale_exp(float amax) {
