@@ -12,13 +12,14 @@
 //   * A (128 pixels x 64 phases, hi and lo) is ONE 3-D TMA box each from a per-iteration staged copy of the
 //     source on a padded coarse grid -- a tap is only a row offset of the box, borders come from TMA's zero fill;
 //   * B (the tap's Ntile x 64 coefficient tile, hi and lo, split at plan time) is one TMA box each;
-//   * one elected thread issues 3 x ksteps tcgen05.mma.kind::f16 (K = 16 each) into a TMEM accumulator;
-//   * 8 drainer warps add the accumulator into fp32 registers with round-to-nearest after every stage
-//     (tcgen05's fp32 accumulation truncates; a 12-MMA chain keeps that bias below 1e-6 relative), while the
-//     tensor core fills the other accumulator.
-// One launch per direction covers every tensor-core plane: persistent CTAs walk a static LPT schedule of
+//   * CTA pairs (cta_group::2, M = 256 pixels); the issuer warp runs converged on warp-uniform values and one elected
+//     lane issues 3 tcgen05.mma.kind::f16 (K = 16 each) per K-step, over the tile's nonzero column range;
+//   * 8 drainer warps add the accumulator into fp32 registers with round-to-nearest after every drain group of
+//     <= 24 K-steps (72 MMAs; tcgen05's fp32 accumulation truncates, the chain bounds that bias to ~3e-6 relative),
+//     zero it with tcgen05.st and hand it back while the tensor core fills the other accumulator.
+// One launch per direction covers every tensor-core plane: persistent CTA pairs walk a static LPT schedule of
 // (plane, pixel tile) items; forward items write per-plane partial images (summed over planes in a fixed order
-// afterwards -> deterministic), backward items write the plane's update epilogue directly.
+// afterwards -> deterministic), backward items write H^T r for the update kernel.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

@@ -1485,7 +1485,9 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     // iteration (both directions, partition_time, plus the coarse transforms of the added units) keeps improving and
     // the transfer matrices fit.
     p->part_moved = 0;
-    if (partitions_allowed(flags) && !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
+    // (LFM_PLAN_MOVE, dev: force the number of moved planes -- also without partitions, so that a serial profiling
+    //  run sees the plane assignment of the partitioned plan)
+    if ((partitions_allowed(flags) || getenv("LFM_PLAN_MOVE")) && !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
         bool simt = false;
         for (int z = zb; z <= ze; ++z) simt |= plane_direct[z] == 1;
         std::vector<int> cand;

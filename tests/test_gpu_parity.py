@@ -1,7 +1,7 @@
 """GPU parity (marked gpu): the CUDA path, called through the C ABI, against the fp64 oracle on the
 same seeded inputs.  Tolerances: operators rel-L2 <= 2e-6 and max-abs <= 1e-5 * max|ref| on
 the CUDA-core paths (fp32 FFT + fp32 MAC over nz N^2 terms, measured ~1e-7); <= 1e-5 rel-L2 / 2e-5 max-abs
-when planes run on the tcgen05 3xTF32 path (its fp32 accumulation truncates: measured bias 3e-6..7e-6
+when planes run on the tcgen05 direct path (2xFP16 split, 3 products; its fp32 accumulation truncates: bias up to ~3e-6
 relative over ~250 chained MMAs); RL rel-L2 <= 1e-4 after 1 iteration and
 <= 1e-3 after 30 (BASELINE.json north star); identical stop / best iteration unless the decision margin is
 within 10x the observed entropy error (reading C16)."""
@@ -36,7 +36,7 @@ def optics(nnum):
 
 
 def op_tol(info):
-    """(rel-L2, max-abs/max) operator tolerance: CUDA-core paths 2e-6 / 1e-5; tcgen05 3xTF32 planes 1e-5 / 2e-5."""
+    """(rel-L2, max-abs/max) operator tolerance: CUDA-core paths 2e-6 / 1e-5; tcgen05 planes (2xFP16 split) 1e-5 / 2e-5."""
     return (1e-5, 2e-5) if info.get("tc_planes", 0) > 0 else (2e-6, 1e-5)
 
 
