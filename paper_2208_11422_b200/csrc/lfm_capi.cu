@@ -572,7 +572,7 @@ lfm_status allreduce(lfm_plan p, void* buf, size_t n, ncclDataType_t t, ncclRedO
 lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, cudaStream_t s) {
     const int N2 = p->geo.N * p->geo.N;
     // with a symmetric window the producers write this rank's partial image there and C1 sums it into ysum
-    float* yimg = p->sym ? sym_buffer(p->sym) : ysum;
+    float* yimg = p->sym ? sym_buffer(p->sym, 0) : ysum;
     ST(mark(p, ST_R2C_X, s));
     if (p->direct) {
         const float* xp = x;
@@ -644,7 +644,7 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
     }
     ST(mark(p, ST_ALLRED_SUM, s));
     if (p->sym) {
-        CK(sym_sum(p->sym, ysum, s));
+        CK(sym_reduce(p->sym, 0, ysum, s));
         p->pacc.launches += 1;
         return LFM_OK;
     }
@@ -735,7 +735,12 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
 lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
     if (!p->has_optics) return fail(LFM_EINVAL, "plan was created without optics: the DCT-entropy metric needs them");
     const int ri = region == LFM_REGION_RECTANGLE ? 1 : 0;
-    ST(allreduce(p, p->mproj, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclMax, s));
+    if (p->sym) {   // C2 in our own kernel over the symmetric window: the partial max-projection sits in slot 1
+        CK(sym_reduce(p->sym, 1, p->mproj, s));
+        p->pacc.launches += 1;
+    } else {
+        ST(allreduce(p, p->mproj, (size_t)p->geo.H * p->geo.W, ncclFloat, ncclMax, s));
+    }
     ST(mark(p, ST_METRIC, s));
     CK(launch_metric(p->mproj, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
                      p->met.nmem[ri], p->met.T1, p->met.rowsq, p->met.out, s));
@@ -754,7 +759,8 @@ lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float
         ST(op_backward(p, SRC_IMAGE2D, p->yhat, nullptr, eps, DST_ISRA, xn, xc, s, hty));
     else
         ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
-    CK(launch_max_project_poly(xn, p->mproj, p->xall, s));     // a7: z max-projection, every pixel written
+    // a7: z max-projection, every pixel written (into the symmetric window's slot 1 when C2 runs there)
+    CK(launch_max_project_poly(xn, p->sym ? reinterpret_cast<unsigned*>(sym_buffer(p->sym, 1)) : p->mproj, p->xall, s));
     p->pacc.launches += 1;
     if (metric) ST(op_metric(p, region, s));
     return LFM_OK;
@@ -2194,8 +2200,9 @@ lfm_status lfm_quality(lfm_plan p, const float* x, int region, double* entropy, 
     if (!p || !x || !entropy) return fail(LFM_EINVAL, "NULL argument");
     if (region != LFM_REGION_TRIANGLE && region != LFM_REGION_RECTANGLE) return fail(LFM_EINVAL, "region=%d", region);
     cudaStream_t s = as_stream(stream);
-    CK(cudaMemsetAsync(p->mproj, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
-    CK(launch_max_project(x, p->mproj, p->xall, s));
+    unsigned* mp = p->sym ? reinterpret_cast<unsigned*>(sym_buffer(p->sym, 1)) : p->mproj;   // op_metric's C2 input
+    CK(cudaMemsetAsync(mp, 0, (size_t)p->geo.H * p->geo.W * sizeof(unsigned), s));
+    CK(launch_max_project(x, mp, p->xall, s));
     ST(op_metric(p, region, s));
     CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -170,13 +170,14 @@ cudaError_t launch_dir_fwd(const DirArgs& d, const float* x, int src_image, floa
 cudaError_t launch_dir_bwd(const DirArgs& d, int src, const float* img, const float* img2, float eps, int dst, float* out,
                            const float* xold, const float* norm, cudaStream_t s);
 
-// C1 over NCCL symmetric memory (kernels_sym.cu, LFM_PLAN_SYMMETRIC): each rank writes its partial image into
-// sym_buffer(); sym_sum() leaves the sum over ranks in `out` (NVLS multimem.ld_reduce or rank-ordered peer loads)
+// C1 / C2 over NCCL symmetric memory (kernels_sym.cu, LFM_PLAN_SYMMETRIC): each rank writes its partial image into
+// sym_buffer(st, 0) and its partial max-projection into sym_buffer(st, 1); sym_reduce(st, 0 | 1, out) leaves the sum /
+// max over ranks in `out` (NVLS multimem.ld_reduce or rank-ordered peer loads)
 struct SymState;
 lfm_status sym_create(ncclComm_t comm, size_t n, int want_multimem, SymState** out, char* err, size_t errlen);
-float* sym_buffer(SymState* st);
+float* sym_buffer(SymState* st, int slot);
 int sym_multimem(const SymState* st);
-cudaError_t sym_sum(SymState* st, float* out, cudaStream_t s);
+cudaError_t sym_reduce(SymState* st, int op, void* out, cudaStream_t s);
 void sym_destroy(SymState* st);
 
 // device-resident auto-stop loop state (kernels_misc.cu, LFM_PLAN_DEVICE_LOOP)
