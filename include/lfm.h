@@ -122,6 +122,12 @@ enum {
                                window and C1 (their sum over ranks) is our own kernel -- NVLS
                                multimem.ld_reduce where the NVLink switch supports it, else rank-ordered
                                peer loads -- instead of ncclAllReduce                 */
+    LFM_PLAN_TILES = 4096,  /* the frequency path on overlap-save tiles of the coarse grid: small
+                               transforms whose transfer matrices serve every tile in one tcgen05 kind::f16 pass.
+                               Default (neither TILES nor NO_TILES): chosen by the cost model when the tiles are
+                               cheaper than whole-image transforms.  Not with FRAMES; on such a plan
+                               lfm_rl_iterate_batch runs the frames one after the other.                       */
+    LFM_PLAN_NO_TILES = 8192, /* never tile the frequency path                                               */
     LFM_PLAN_DEVICE_LOOP = 128 /* lfm_rl_iterate runs the whole loop as one CUDA graph: a conditional WHILE
                                node over two unrolled iterations, the stop rule and the argmax snapshot
                                evaluated on the device -- no host round trip per iteration (
@@ -155,6 +161,9 @@ typedef struct {
                                        a communicator), 1 own kernel over symmetric memory with peer loads,
                                        2 the same with NVLS multimem.ld_reduce (LFM_PLAN_SYMMETRIC, §7)       */
     int tc_moved_to_fft;            /* tensor-core planes the partition-aware step moved to the frequency path */
+    int tiles;                      /* overlap-save tiles of the frequency path (0: whole-image transforms); the
+                                       transforms are then fft_h x fft_w windows serving tile_T1 x tile_T2 outputs */
+    int tile_T1, tile_T2;
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblfm.so")
 SOURCES = ["lfm_capi.cu", "kernels_fft.cu", "kernels_fft_fast.cu", "kernels_mac.cu", "kernels_misc.cu", "kernels_direct.cu",
-           "kernels_tcdir.cu", "kernels_mac_tc.cu", "kernels_sym.cu", "kernels_mac_f16.cu"]
-HEADERS = ["lfm_internal.cuh", "fft_smem.cuh", "tc_sm100.cuh"]
+           "kernels_tcdir.cu", "kernels_mac_tc.cu", "kernels_sym.cu", "kernels_mac_f16.cu", "kernels_fft_tile.cu"]
+HEADERS = ["lfm_internal.cuh", "fft_smem.cuh", "fft_warp.cuh", "tc_sm100.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
     }
     if (warp == 0) tc::tmem_alloc(&tmem_base, 2 * NSET <= 256 ? 256 : 512);
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
-        s_scale[f] = tc::pow2f(d.bexp[f]);
-        s_inv[f] = ldexpf(1.0f, -(d.aexp + d.bexp[f]));
+        const int eb = d.bmax ? (f < d.nframes ? tc::f16_scale_exp(__uint_as_float(d.bmax[f])) : 0) : d.bexp[f];
+        s_scale[f] = tc::pow2f(eb);
+        s_inv[f] = ldexpf(1.0f, -(d.aexp + eb));
     }
     tc::fence_before();
     __syncthreads();
@@ -96,10 +97,25 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
 
     if (warp == 0) {
         if (lane == 0) {   // ---- producer: A hi / lo tiles and the frames' fp32 source tile per chunk ----
+            // L2 prefetch of the A tiles d.pf chunks ahead of the loads (across items): the ring of S stages alone
+            // leaves the stream latency-bound at ~40 GB/s per SM
+            int pf_item = blockIdx.x, pf_c = 0;
+            auto pf_next = [&]() {
+                if (pf_item >= nitems) return;
+                const int kp = pf_item / ntile, tp = pf_item - kp * ntile;
+                tc::tma_prefetch_3d(&d.tmapAh, pf_c * kFK, tp * kFM, kp);
+                tc::tma_prefetch_3d(&d.tmapAl, pf_c * kFK, tp * kFM, kp);
+                if (++pf_c == nchunks) {
+                    pf_c = 0;
+                    pf_item += gridDim.x;
+                }
+            };
+            for (int i = 0; i < d.pf; ++i) pf_next();
             int it = 0;
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
                 const int kap = item / ntile, t = item - kap * ntile;
                 for (int c = 0; c < nchunks; ++c, ++it) {
+                    if (d.pf) pf_next();
                     const int s = it % S;
                     if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
                     unsigned char* st = smem + (size_t)s * sbytes;
@@ -239,6 +255,7 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
             if (row < (FWD ? d.N2 : d.nu_pad)) {
 #pragma unroll
                 for (int f = 0; f < F; ++f) {
+                    if (f >= d.nframes) break;
                     const float inv = s_inv[f];
                     const float2 v = make_float2(acc[2 * f] * inv, acc[2 * f + 1] * inv);
                     d.out[(long long)f * d.out_fstride + (long long)kap * d.out_ld + row] = v;
@@ -368,6 +385,7 @@ cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa,
         a->bpitch = bpitch;
         a->aexp = w ? eb : ea;
         a->chain_k = getenv("LFM_MF_CHAIN") ? std::max(4, atoi(getenv("LFM_MF_CHAIN"))) : 24;   // dev override
+        a->pf = getenv("LFM_MF_PF") ? std::max(0, atoi(getenv("LFM_MF_PF"))) : 0;   // dev (measured: L2 prefetch slows it)
         const int n = w ? bpitch : nu_pad;               // complex per split row
         const int rows = w ? nu_pad : N2;
         unsigned char* base = reinterpret_cast<unsigned char*>(w ? MT : M);
@@ -385,11 +403,13 @@ cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa,
 }
 
 // per call: the frames' fp32 source spectra (FWD: G [F][kappa][nu_pad]; BWD: R [F][kappa][bpitch]), F rows of 64 floats
-cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F) {
+cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F, int nframes) {
     MfEncodeFn enc = mf_encoder();
     if (!enc) return cudaErrorSymbolNotFound;
     const int n = fwd ? a->nu_pad : a->bpitch;
-    cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)a->nkappa, (cuuint64_t)F};
+    if (nframes <= 0 || nframes > F) nframes = F;
+    a->nframes = nframes;   // frames nframes .. F-1 of the box are zero-filled by the TMA (out of bounds)
+    cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)a->nkappa, (cuuint64_t)nframes};
     cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)src_fstride * 8};
     cuuint32_t box[3] = {(cuuint32_t)kFK, 1, (cuuint32_t)F}, es[3] = {1, 1, 1};
     CUresult r = enc(&a->tmapS, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(src), dims, strides, box, es,

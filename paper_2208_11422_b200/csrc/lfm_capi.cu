@@ -238,6 +238,13 @@ struct lfm_plan_s {
     int* mf_eb = nullptr;                              // [2][32] per-frame source scale exponents (fwd, bwd)
     const void* mf_src[2] = {nullptr, nullptr};        // encoded source pointers / frame counts of mf_fwd / mf_bwd
     int mf_F[2] = {0, 0};
+    // overlap-save tiled frequency path (LFM_PLAN_TILES): transforms of tg.L points per axis over
+    // tg.ntile tiles; M (forward) and M^T (backward) stored split as in FRAMES plans, both MACs on kind::f16 with the
+    // tiles as the GEMM's N (kernels_mac_f16.cu, F = mf_tF >= ntile)
+    bool tiled = false;
+    TileGeom tg{};
+    int mf_tF = 0;
+    unsigned* tmax = nullptr;   // [2][32] per-tile |source| bounds (float bits) of the forward / backward MAC
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -428,6 +435,12 @@ int part_skip() {
     return v;
 }
 
+// dev A/B LFM_C2R_FULL: tiled plans run their C2R on the whole GPU after the join (default: inside the partition)
+bool c2r_full() {
+    static const bool v = getenv("LFM_C2R_FULL") != nullptr;
+    return v;
+}
+
 // fork the caller's stream s onto the projection's two partition streams (*st tensor cores, *sm MAC)
 lfm_status fork(lfm_plan p, const lfm_plan_s::Part& pt, cudaStream_t s, cudaStream_t* st, cudaStream_t* sm) {
     CK(cudaEventRecord(p->evf, s));
@@ -470,6 +483,7 @@ void plan_free(lfm_plan p) {
     if (p->sym) sym_destroy(p->sym);
     cudaFree(p->MT);
     cudaFree(p->mf_eb);
+    cudaFree(p->tmax);
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -597,9 +611,16 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
         cudaStream_t st = s, sm = s;
         if (split && !prefork) ST(fork(p, pt, s, &st, &sm));
         for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_STAGE));
-        if (p->nu_fft > 0)
+        if (p->nu_fft > 0 && p->tiled) {   // §5.6: window transforms of every (tile, unit), |window| bounds per tile
+            CK(cudaMemsetAsync(p->tmax, 0, 32 * sizeof(unsigned), sm));
+            R2CArgs a = r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->tg.ntile * p->nu_fft, p->G, p->nu_fft_pad);
+            a.cdiv = p->nu_fft;
+            a.cmul = p->xg.nkappa * p->nu_fft_pad;
+            CK(launch_r2c_tile(p->xg, p->tg, p->tw_h, a, 0, p->tmax, sm));
+        } else if (p->nu_fft > 0) {
             CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                           r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), sm));
+        }
         if (split && prefork) ST(fork(p, pt, s, &st, &sm));
         ST(mark(p, ST_FWD_MAC, s));
         if (!p->tcf.empty() && !(part_skip() & 1)) {
@@ -609,13 +630,17 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
         }
         if (p->nu_fft > 0 && !(part_skip() & 2)) {
             ST(kmark(p, 1, 0, sm));
-            CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
-                              split, sm));
+            if (p->tiled)
+                CK(launch_mac_f16(p->mf_fwd, 1, p->mf_tF, split ? pt.sms_mac : p->num_sms, sm));
+            else
+                CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
+                                  split, sm));
             ST(kmark(p, 1, 1, sm));
         }
         // join the MAC partition, then the C2R on the whole GPU (on the small MAC partition it would lengthen the
-        // critical path), then the tensor-core partition
-        if (split) ST(join(p, pt.smac, p->evj2, s));
+        // critical path), then the tensor-core partition.  Tiled plans (§5.6) run their C2R inside the partition.
+        const bool c2r_in = split && p->tiled && !c2r_full();
+        if (split && !c2r_in) ST(join(p, pt.smac, p->evj2, s));
         if (p->nu_fft > 0) {
             C2RArgs c{};
             c.dst = DST_IMAGE;
@@ -623,9 +648,17 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
             c.in_ld = N2;
             c.ntrans = N2;
             c.out = yimg;
-            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+            if (p->tiled) {
+                c.ntrans = p->tg.ntile * N2;
+                c.cdiv = N2;
+                c.cmul = (long long)p->xg.nkappa * N2;
+                CK(launch_c2r_tile(p->xg, p->tg, p->tw_h, c, 0, c2r_in ? sm : s));
+            } else {
+                CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+            }
             p->pacc.launches += 3;
         }
+        if (c2r_in) ST(join(p, pt.smac, p->evj2, s));
         if (split) ST(join(p, pt.stc, p->evj, s));
         ST(mark(p, ST_C2R_YHAT, s));
         ST(mark(p, ST_DIR_FWD, s));
@@ -690,8 +723,15 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     cudaStream_t st = s, sm = s;
     if (split && !prefork) ST(fork(p, pt, s, &st, &sm));   // staging / R2C inside the halves, as in the forward
     for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_STAGE));
-    if (p->nu_fft > 0)
+    if (p->nu_fft > 0 && p->tiled) {   // §5.6: windows of every (tile, output phase), R rows of bpitch
+        CK(cudaMemsetAsync(p->tmax + 32, 0, 32 * sizeof(unsigned), sm));
+        R2CArgs a = r2c_args(src, img, img2, eps, p->tg.ntile * N2, p->R, p->bpitch);
+        a.cdiv = N2;
+        a.cmul = (long long)p->xg.nkappa * p->bpitch;
+        CK(launch_r2c_tile(p->xg, p->tg, p->tw_h, a, 1, p->tmax + 32, sm));
+    } else if (p->nu_fft > 0) {
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), sm));
+    }
     if (split && prefork) ST(fork(p, pt, s, &st, &sm));
     ST(mark(p, ST_BWD_MAC, s));
     if (!p->tcb.empty() && !(part_skip() & 1)) {
@@ -704,10 +744,14 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     }
     if (p->nu_fft > 0 && !(part_skip() & 2)) {
         ST(kmark(p, 3, 0, sm));
-        CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
+        if (p->tiled)
+            CK(launch_mac_f16(p->mf_bwd, 0, p->mf_tF, split ? pt.sms_mac : p->num_sms, sm));
+        else
+            CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
         ST(kmark(p, 3, 1, sm));
     }
-    if (split) ST(join(p, pt.smac, p->evj2, s));   // C2R + update on the whole GPU, as in the forward
+    const bool c2r_in = split && p->tiled && !c2r_full();   // as in the forward
+    if (split && !c2r_in) ST(join(p, pt.smac, p->evj2, s));   // C2R + update on the whole GPU, as in the forward
     if (p->nu_fft > 0) {
         C2RArgs c{};
         c.dst = dst;
@@ -718,9 +762,17 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         c.xold = xold;
         c.norm = aux;
         c.eps = eps;
-        CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+        if (p->tiled) {
+            c.ntrans = p->tg.ntile * p->nu_fft;
+            c.cdiv = p->nu_fft;
+            c.cmul = (long long)p->xg.nkappa * p->nu_fft_pad;
+            CK(launch_c2r_tile(p->xg, p->tg, p->tw_h, c, 1, c2r_in ? sm : s));
+        } else {
+            CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
+        }
         p->pacc.launches += 3;
     }
+    if (c2r_in) ST(join(p, pt.smac, p->evj2, s));
     if (split) ST(join(p, pt.stc, p->evj, s));
     ST(mark(p, ST_C2R_UPD, s));
     ST(mark(p, ST_DIR_BWD, s));
@@ -1011,6 +1063,66 @@ double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s
     return best;
 }
 
+// ---- overlap-save tiles of the frequency path ----
+// Per FFT unit and iteration: the split M (forward) and M^T (backward) streamed once each by the kind::f16 MACs,
+// the tiles' spectra written by the R2C and read by the MAC (and the reverse), and the window transforms.
+constexpr double kMacF16Bps = 5.3e12;        // kind::f16 tile MACs, HBM-bound (r02 c3 tiles: 5.25-5.45 TB/s)
+constexpr double kXformPoint = 6.0e-12;      // whole-image transform seconds per point and direction (r02, L = 75)
+constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms (r02, L = 27: 4.1e-12)
+
+// tile geometry for transform size L (ntile = 0: not possible).  Coarse taps of every phase pair of a kh x kw kernel
+// lie in [dmin, dmax] with N d + b - a + c in [0, k - 1] (reading of S:192's kernel centring).
+TileGeom tile_geometry(const Geo& g, int L) {
+    TileGeom t{};
+    t.L = L;
+    t.dmin1 = ceildiv(-(g.N - 1) - g.ch, g.N);
+    t.dmax1 = floordiv(g.kh - 1 + (g.N - 1) - g.ch, g.N);
+    t.dmin2 = ceildiv(-(g.N - 1) - g.cw, g.N);
+    t.dmax2 = floordiv(g.kw - 1 + (g.N - 1) - g.cw, g.N);
+    t.T1 = L - (t.dmax1 - t.dmin1);
+    t.T2 = L - (t.dmax2 - t.dmin2);
+    if (t.T1 < 1 || t.T2 < 1 || !tile_fft_size(L)) return TileGeom{};
+    t.nty = (g.nh + t.T1 - 1) / t.T1;
+    t.ntx = (g.nw + t.T2 - 1) / t.T2;
+    t.ntile = t.nty * t.ntx;
+    if (t.ntile > 32 || t.ntile < 2) return TileGeom{};
+    return t;
+}
+
+double tile_unit_cost(const TileGeom& t, int N2) {
+    const double nkap = (double)t.L * (t.L / 2 + 1);
+    const double bpitch = (double)round_up((size_t)N2, 4);
+    return nkap * (N2 + bpitch) * 8.0 / kMacF16Bps + 4.0 * t.ntile * nkap * 8.0 / kHbmBps +
+           2.0 * kXformPointTile * t.ntile * t.L * t.L;
+}
+
+double whole_unit_cost(const Geo& g, int N2) {
+    return 2.0 * N2 * (double)g.nkappa * 8.0 / kHbmBps + 2.0 * kXformPoint * g.Lh * g.Lw;
+}
+
+// the cheapest tiling, or ntile = 0 when whole-image transforms are cheaper (LFM_PLAN_TILES: the cheapest tiling
+// whenever one exists; LFM_PLAN_NO_TILES / FRAMES plans: never)
+TileGeom choose_tiles(const Geo& g, int N2, int flags) {
+    if ((flags & (LFM_PLAN_NO_TILES | LFM_PLAN_FRAMES | LFM_PLAN_DIRECT)) || N2 > 256) return TileGeom{};
+    static const int cand[] = {16, 18, 20, 24, 25, 27, 30, 32, 36};
+    TileGeom best{};
+    double best_c = 1e300;
+    const char* ev = getenv("LFM_TILE_L");   // dev override of the transform size
+    for (int L : cand) {
+        if (ev && atoi(ev) != L) continue;
+        const TileGeom t = tile_geometry(g, L);
+        if (t.ntile == 0) continue;
+        const double c = tile_unit_cost(t, N2);
+        if (c < best_c) {
+            best_c = c;
+            best = t;
+        }
+    }
+    if (best.ntile == 0) return best;
+    if (!(flags & LFM_PLAN_TILES) && !(best_c < 0.9 * whole_unit_cost(g, N2))) return TileGeom{};
+    return best;
+}
+
 // SM partitions are used unless the plan runs the device-resident loop (its conditional graph body cannot hold
 // kernels of other contexts), the driver lacks green contexts, or LFM_SERIAL is set (dev)
 bool partitions_allowed(int flags) {
@@ -1073,7 +1185,8 @@ std::vector<PlaneCost> plane_costs(const float* psf, int nnum, const Geo& g, int
         const AxisBox b1 = axis_box(nnum, g.ch, k0, k1), b2 = axis_box(nnum, g.cw, j0, j1);
         const int D = std::max(b1.D, b2.D);
         const int T2 = b2.dmax - b2.dmin + b2.D;
-        const double t_fft = 2.0 * N2 * N2 * (double)g.nkappa * 8.0 / kHbmBps + kXformPerUnit * N2;
+        const TileGeom tl = choose_tiles(g, N2, flags);   // the frequency path as the plan would build it (§5.6)
+        const double t_fft = N2 * (tl.ntile ? tile_unit_cost(tl, N2) : whole_unit_cost(g, N2));
         const double t_dir = D <= kDirMaxD ? 2.0 * N2 * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
         const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && round_up((size_t)N2, 16) <= 256 && T2 <= 65;
         const double t_tc = tc_ok ? tc_plane_time(b1, b2, g, N2, num_sms) : 1e30;
@@ -1395,6 +1508,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     std::vector<int> p_alt(nz, 0);   // best direct alternative per plane (1 CUDA-core, 2 tensor-core, 0 none)
     std::vector<AxisBox> box1(nz), box2(nz);
     const int zb = p->nu > 0 ? p->u0 / N2 : 0, ze = p->nu > 0 ? (p->u1 - 1) / N2 : -1;
+    // frequency path on overlap-save tiles (§5.6) when the cost model prefers them: per-unit time and bytes
+    const TileGeom tiles = choose_tiles(g, N2, flags);
+    const double fft_unit_t = tiles.ntile ? tile_unit_cost(tiles, N2) : whole_unit_cost(g, N2);
+    const double fft_unit_m = tiles.ntile ? (double)tiles.L * (tiles.L / 2 + 1) * (N2 + round_up((size_t)N2, 4)) * 8.0
+                                          : (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
     bool too_big = false;
     for (int z = zb; z <= ze; ++z) {
         int k0 = kh, k1 = -1, j0 = kw, j1 = -1;
@@ -1420,7 +1538,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const int D = std::max(box1[z].D, box2[z].D);
         plane_D[z] = D;
         const double units = ue - ub;
-        const double t_fft = 2.0 * units * N2 * g.nkappa * 8.0 / kHbmBps + kXformPerUnit * units;
+        const double t_fft = units * fft_unit_t;
         const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
         // tensor-core direct (kernels_tcdir.cu): per direction, CTA pairs over 256-pixel tiles of the padded grid,
         // every tap x K-step = 3 pair MMAs of Ntile/2 cycles (tcgen05 floor), at the measured efficiency
@@ -1430,7 +1548,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const double t_tc = tc_ok ? tc_plane_time(box1[z], box2[z], g, N2, p->num_sms) : 1e30;   // whole plane
         // device bytes per plane on each path (memory-aware planning below)
         pt_fft[z] = t_fft;
-        pm_fft[z] = units * (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
+        pm_fft[z] = units * fft_unit_m;
         if (tc_ok && t_tc <= t_dir) {
             p_alt[z] = 2;
             pt_alt[z] = t_tc;
@@ -1493,7 +1611,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->part_moved = 0;
     // (LFM_PLAN_MOVE, dev: force the number of moved planes -- also without partitions, so that a serial profiling
     //  run sees the plane assignment of the partitioned plan)
-    if ((partitions_allowed(flags) || getenv("LFM_PLAN_MOVE")) && !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
+    if ((partitions_allowed(flags) || getenv("LFM_PLAN_MOVE")) && !tiles.ntile &&
+        !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
         bool simt = false;
         for (int z = zb; z <= ze; ++z) simt |= plane_direct[z] == 1;
         std::vector<int> cand;
@@ -1649,7 +1768,20 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 nsimt += plane_direct[z] == 1;
             }
             const double bytes = units_fft * N2 * g.nkappa * 8.0;   // M streamed once per direction
-            for (int d = 0; d < 2 && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
+            // tiled frequency path (§5.6): its MAC (tensor cores, HBM-bound), transforms (SIMT) and the tensor-core
+            // direct planes share the SMs in proportion to their modelled whole-GPU times (r02 c3 sweep: the optimum
+            // 56 of 148 SMs matches the proportional split, +4 % over one after the other)
+            for (int d = 0; d < 2 && tiles.ntile && t_tc > 0 && units_fft > 0 && nsimt == 0; ++d) {
+                const double t_f = 0.5 * units_fft * fft_unit_t;
+                int want = (int)std::lround(p->num_sms * t_tc / (t_tc + t_f) / 8.0) * 8;
+                want = std::max(16, std::min(p->num_sms - 16, want));
+                if (const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F")) want = atoi(ev);   // dev override
+                if (getenv("LFM_PLAN_VERBOSE"))
+                    fprintf(stderr, "[lfm plan] tiles, direction %d: t_tc %.3f ms, t_freq %.3f ms -> %d tc SMs\n", d,
+                            t_tc * 1e3, t_f * 1e3, want);
+                if (want > 0 && green_split(p, dev, want, &p->part[d])) tc_sms[d] = p->part[d].sms_tc;
+            }
+            for (int d = 0; d < 2 && !tiles.ntile && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
                 // the partition's forward MAC keeps four 8-warp CTAs per SM in flight while G[kappa] fits four times in
                 // shared memory; fewer resident CTAs stream proportionally less (c4: 3 CTAs, ~81 GB/s per SM)
                 const double gsm = round_up((size_t)std::max(units_fft, 1.0), 16) * 8.0 + 1024.0;
@@ -1807,19 +1939,36 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         for (const DirArgs& dg : p->dgroups) maxg = std::max(maxg, dg.nzd);
         if (maxg > 0) PG(dalloc(p, &p->dpart, (size_t)maxg * HW * sizeof(float), "direct forward partials"));
         if (p->nu_fft > 0) {
-            if (!fft_factor(g.Lh, &p->fh) || !fft_factor(g.Lw, &p->fw))
-                return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", g.Lh, g.Lw));
-            PG(twiddles(g.Lh, &p->tw_h, p, s));
-            PG(twiddles(g.Lw, &p->tw_w, p, s));
-            const size_t mbytes = (size_t)g.nkappa * N2 * p->nu_fft_pad * sizeof(float2);
+            // whole-image transforms (Lh x Lw) or, on a tiled plan, tg.L x tg.L windows of tg.ntile tiles (§5.6)
+            int Lh = g.Lh, Lw = g.Lw, nkap = g.nkappa, nt = 1;
+            if (tiles.ntile) {
+                CKG(tile_fft_init());
+                p->tiled = true;
+                p->tg = tiles;
+                Lh = Lw = tiles.L;
+                nkap = Lh * (Lw / 2 + 1);
+                nt = tiles.ntile;
+                xg.Lh = Lh;
+                xg.Lw = Lw;
+                xg.nk2 = Lw / 2 + 1;
+                xg.nkappa = nkap;
+                p->bpitch = (int)round_up((size_t)N2, 4);
+            }
+            if (!fft_factor(Lh, &p->fh) || !fft_factor(Lw, &p->fw))
+                return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", Lh, Lw));
+            PG(twiddles(Lh, &p->tw_h, p, s));
+            PG(twiddles(Lw, &p->tw_w, p, s));
+            const size_t mbytes = (size_t)nkap * N2 * p->nu_fft_pad * sizeof(float2);
+            const size_t rpitch = p->tiled ? p->bpitch : N2;
             p->transfer_bytes += mbytes;
             PG(dalloc(p, &p->M, mbytes, "transfer matrices"));
-            PG(dalloc(p, &p->G, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), "G spectra"));
-            PG(dalloc(p, &p->Xh, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
-            PG(dalloc(p, &p->Y, (size_t)g.nkappa * N2 * sizeof(float2), "Y spectra"));
-            PG(dalloc(p, &p->R, (size_t)g.nkappa * N2 * sizeof(float2), "R spectra"));
+            PG(dalloc(p, &p->G, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "G spectra"));
+            PG(dalloc(p, &p->Xh, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
+            PG(dalloc(p, &p->Y, (size_t)nt * nkap * N2 * sizeof(float2), "Y spectra"));
+            PG(dalloc(p, &p->R, (size_t)nt * nkap * rpitch * sizeof(float2), "R spectra"));
             CKG(cudaMemsetAsync(p->M, 0, mbytes, s));      // padding columns stay zero
-            CKG(cudaMemsetAsync(p->G, 0, (size_t)g.nkappa * p->nu_fft_pad * sizeof(float2), s));
+            CKG(cudaMemsetAsync(p->G, 0, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), s));
+            CKG(cudaMemsetAsync(p->R, 0, (size_t)nt * nkap * rpitch * sizeof(float2), s));
             // K1: transfer matrices M[kappa][b'][t] = DFT_{Lh x Lw}(g_{u(t),b'}), g_{u,b'}[d] = h_u[b' - a + c + N d]
             R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * p->nu_fft, p->M, (long long)N2 * p->nu_fft_pad);
             a.cdiv = p->nu_fft;
@@ -1834,6 +1983,33 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 ab.cdiv = p->nu_fft;
                 ab.cmul = p->nu_fft_pad;
                 CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, ab, s));
+            }
+            if (p->tiled) {
+                // M (forward) and M^T (backward) split into scaled fp16 hi / lo rows as for FRAMES plans; the tiles'
+                // spectra G / R are the MACs' frames, their |window| bounds the per-tile scales
+                const size_t mtb = (size_t)nkap * p->nu_fft_pad * p->bpitch * sizeof(float2);
+                PG(dalloc(p, &p->MT, mtb, "transposed transfer matrices (tiles)"));
+                p->transfer_bytes += mtb;
+                PG(dalloc(p, &p->tmax, 64 * sizeof(unsigned), "tile scale bounds"));
+                CKG(cudaMemsetAsync(p->tmax, 0, 64 * sizeof(unsigned), s));
+                CKG(mac_f16_prepare(p->M, p->Mb, p->MT, nkap, N2, p->nu_fft_pad, p->bpitch, &p->mf_fwd, &p->mf_bwd, s));
+                if (p->Mb != p->M) {
+                    cudaFree(p->Mb);
+                    p->bytes -= mbytes;
+                    p->transfer_bytes -= mbytes;
+                }
+                p->Mb = nullptr;
+                p->mf_tF = nt <= 8 ? 8 : (nt <= 16 ? 16 : 32);
+                CKG(mac_f16_encode_src(&p->mf_fwd, 1, p->G, (long long)nkap * p->nu_fft_pad, p->mf_tF, nt));
+                CKG(mac_f16_encode_src(&p->mf_bwd, 0, p->R, (long long)nkap * p->bpitch, p->mf_tF, nt));
+                p->mf_fwd.bmax = p->tmax;
+                p->mf_fwd.out = p->Y;
+                p->mf_fwd.out_fstride = (long long)nkap * N2;
+                p->mf_fwd.out_ld = N2;
+                p->mf_bwd.bmax = p->tmax + 32;
+                p->mf_bwd.out = p->Xh;
+                p->mf_bwd.out_fstride = (long long)nkap * p->nu_fft_pad;
+                p->mf_bwd.out_ld = p->nu_fft_pad;
             }
         }
         CKG(cudaStreamSynchronize(s));
@@ -1933,11 +2109,14 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->width = p->geo.W;
     info->unit_begin = p->u0;
     info->unit_end = p->u1;
-    info->fft_h = p->geo.Lh;
-    info->fft_w = p->geo.Lw;
+    info->fft_h = p->tiled ? p->tg.L : p->geo.Lh;
+    info->fft_w = p->tiled ? p->tg.L : p->geo.Lw;
     info->lc_min_h = p->geo.lcmin_h;
     info->lc_min_w = p->geo.lcmin_w;
-    info->n_kappa = p->geo.nkappa;
+    info->n_kappa = p->tiled ? p->xg.nkappa : p->geo.nkappa;
+    info->tiles = p->tiled ? p->tg.ntile : 0;
+    info->tile_T1 = p->tiled ? p->tg.T1 : 0;
+    info->tile_T2 = p->tiled ? p->tg.T2 : 0;
     info->units_padded = p->nu_fft_pad;
     info->x_s = p->region.xs;
     info->y_s = p->region.ys;
@@ -2255,6 +2434,22 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
     cudaStream_t s = as_stream(stream);
     const int F = frames, N2 = p->geo.N * p->geo.N;
     const size_t HW = (size_t)p->geo.H * p->geo.W;
+    if (p->tiled) {
+        // a tiled plan (§5.6) already batches its tiles through the kind::f16 MACs: the frames run one after the other
+        // through the single-frame loop (identical results to lfm_rl_iterate per frame); ms_host sums the frames'
+        // k-th iterations
+        const int sstride = std::max(pol->n_iters, pol->max_iters);
+        std::vector<float> msf(ms_host ? sstride : 0, 0.0f);
+        if (ms_host) std::fill(ms_host, ms_host + sstride, 0.0f);
+        for (int f = 0; f < F; ++f) {
+            bool mirrored = false;
+            ST(rl_loop(p, y + f * HW, x + (size_t)f * p->geo.nz * HW, pol, best_iter + f, stop_iter + f,
+                       series_host + (size_t)f * sstride, ms_host ? msf.data() : nullptr, s, nullptr, &mirrored));
+            if (ms_host)
+                for (int i = 0; i < stop_iter[f] && i < sstride; ++i) ms_host[i] += msf[i];
+        }
+        return LFM_OK;
+    }
     const size_t vol = (size_t)p->nu * p->geo.nh * p->geo.nw;
     const long long sG = (long long)p->geo.nkappa * p->nu_fft_pad, sY = (long long)p->geo.nkappa * N2;
     const int rld = p->frames ? p->bpitch : N2;             // R row pitch (the fp16 MACs read R through a TMA map)

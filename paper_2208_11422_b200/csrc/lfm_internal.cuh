@@ -80,6 +80,18 @@ struct C2RArgs {
     const float* xold;      // DST_UPDATE
     const float* norm;      // DST_UPDATE: H^T 1; DST_ISRA: H^T y
     float eps;
+    int cdiv;               // overlap-save tiles (launch_c2r_tile): transform t = tile * cdiv + item reads column
+    long long cmul;         //   tile * cmul + item of in[kappa * in_ld + .]
+};
+
+// overlap-save tiles of the coarse grid: a square transform of L points per axis serves T1 x T2
+// output coarse pixels; the coarse taps of every (phase pair, plane) lie in [dmin1, dmax1] x [dmin2, dmax2], so
+// L >= T + dmax - dmin.  Forward windows start at tile * T - dmax (valid outputs at dmax ..), backward windows at
+// tile * T + dmin (valid outputs at -dmin ..).
+struct TileGeom {
+    int L;
+    int T1, T2, nty, ntx, ntile;
+    int dmin1, dmax1, dmin2, dmax2;
 };
 
 // hybrid-plan direct part (kernels_direct.cu)
@@ -200,6 +212,17 @@ cudaError_t launch_c2r(const XformGeom& g, const FftDesc& fh, const FftDesc& fw,
 bool fast_fft_size(int Lh, int Lw);
 cudaError_t launch_r2c_fast(const XformGeom& g, const float2* tw, const R2CArgs& a, cudaStream_t s);
 cudaError_t launch_c2r_fast(const XformGeom& g, const float2* tw, const C2RArgs& a, cudaStream_t s);
+// (kernels_fft_tile.cu) overlap-save tile transforms.  R2C: transform t = tile * a.cdiv + item (item = FFT unit or
+// output phase as in the whole-image modes), window of the item's coarse image at the tile's origin (dir 0: forward
+// source, dir 1: backward source), spectrum to out[kappa * out_ld + tile * cmul + item]; with amax != nullptr the sum
+// of |window| of every transform is max-reduced into amax[tile] (float bits; the fp16 scale bound of the tile MACs).
+// C2R: the tile's valid T1 x T2 outputs (dir 0: forward image, dir 1: backward volume) into the C2RDst destination.
+bool tile_fft_size(int L);
+cudaError_t tile_fft_init();   // twiddle table of the tile kernels (once per process, plan time)
+cudaError_t launch_r2c_tile(const XformGeom& g, const TileGeom& tg, const float2* tw, const R2CArgs& a, int dir,
+                            unsigned* amax, cudaStream_t s);
+cudaError_t launch_c2r_tile(const XformGeom& g, const TileGeom& tg, const float2* tw, const C2RArgs& a, int dir,
+                            cudaStream_t s);
 void set_fast_fft_enabled(bool on);
 // (kernels_mac.cu)
 cudaError_t launch_fwd_mac(const float2* M, const float2* G, float2* Y, int nkappa, int N2, int nu_pad, int num_sms,
@@ -240,7 +263,10 @@ struct MacF16Args {
     int nkappa, N2, nu_pad, bpitch;
     int aexp;                 // the transfer matrices' scale exponent
     int chain_k;              // K-steps accumulated in TMEM between drains
+    int pf;                   // A chunks prefetched into L2 ahead of the TMA loads (0: none)
     const int* bexp;          // [F] the frames' source scale exponents (device, per call)
+    const unsigned* bmax;     // or (non-null): [F] bounds of the frames' |source| (float bits), exponents derived in-kernel
+    int nframes;              // frames actually present (<= F; the TMA zero-fills the rest, no output for them)
     float2* out;              // fwd: Y [F][kappa][N2]; bwd: Xh [F][kappa][nu_pad]
     long long out_fstride, out_ld;
     alignas(64) CUtensorMap tmapAh;   // A hi parts {2n fp16, rows, kappa}, box {64, 128, 1}, SWIZZLE_128B
@@ -249,7 +275,7 @@ struct MacF16Args {
 };
 cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa, int N2, int nu_pad, int bpitch,
                             MacF16Args* fwd, MacF16Args* bwd, cudaStream_t s);
-cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F);
+cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F, int nframes = 0);
 cudaError_t launch_frame_scales(const float2* src, long long fstride, int n, int F, int* eb, cudaStream_t s);
 cudaError_t launch_mac_f16(const MacF16Args& d, int fwd, int F, int num_sms, cudaStream_t s);
 size_t mac_f16_smem_bytes(int F);

@@ -30,6 +30,7 @@ LFM_UPDATE_RL, LFM_UPDATE_ISRA = 0, 1
 LFM_PLAN_NO_COMM, LFM_PLAN_DIRECT, LFM_PLAN_FFT_ONLY, LFM_PLAN_TC_DIRECT, LFM_PLAN_GRAPHS, LFM_PLAN_NO_TC = 1, 2, 4, 16, 32, 64
 LFM_PLAN_DEVICE_LOOP, LFM_PLAN_EVEN_SHARDS, LFM_PLAN_FORCE_COMM, LFM_PLAN_SYMMETRIC = 128, 256, 512, 1024
 LFM_PLAN_FRAMES = 2048
+LFM_PLAN_TILES, LFM_PLAN_NO_TILES = 4096, 8192
 
 
 class LfmError(RuntimeError):
@@ -64,7 +65,8 @@ class lfm_info(ctypes.Structure):
                 ("plan_ms", ctypes.c_double), ("direct_planes", ctypes.c_int), ("fft_units", ctypes.c_int),
                 ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double),
                 ("planes_moved_for_memory", ctypes.c_int), ("partition_sms", (ctypes.c_int * 2) * 2),
-                ("c1_mode", ctypes.c_int), ("tc_moved_to_fft", ctypes.c_int)]
+                ("c1_mode", ctypes.c_int), ("tc_moved_to_fft", ctypes.c_int), ("tiles", ctypes.c_int),
+                ("tile_T1", ctypes.c_int), ("tile_T2", ctypes.c_int)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

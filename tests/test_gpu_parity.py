@@ -549,7 +549,8 @@ def test_batched_frames_match_single_and_oracle(name, F, flags):
     ys = [poisson(O.forward_project(gen_volume(cfg, 1 + f % 3), hd) * (1.0 + 0.1 * f), 300 + f) for f in range(F)]
     check = list(range(F)) if not (name == "c2" and F > 4) else [0, 1, F // 2, F - 1]
     refs = {f: oracle_frame(ys[f], hd, cfg) for f in check}
-    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags) as plan:
+    # (whole-image transforms: the lockstep batched MACs; tiled plans batch frame by frame, test_gpu_tiles.py)
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=flags | L().LFM_PLAN_NO_TILES) as plan:
         for pol in (L().make_policy(mode="fixed", n_iters=3), L().make_policy(mode="auto", max_iters=25)):
             yb = dev(np.stack(ys))
             xb = torch.zeros((F, cfg.nz, cfg.height, cfg.width), device="cuda")
@@ -806,7 +807,8 @@ def test_batched_tc_macs_repeatable():
     hd = h.astype(np.float64)
     F = 16
     ys = [poisson(O.forward_project(gen_volume(cfg, 1 + f % 3), hd) * (1.0 + 0.05 * f), 500 + f) for f in range(F)]
-    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum), flags=L().LFM_PLAN_FFT_ONLY) as plan:
+    with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum),
+                  flags=L().LFM_PLAN_FFT_ONLY | L().LFM_PLAN_NO_TILES) as plan:
         yb = dev(np.stack(ys))
         ref = None
         for rep in range(12):
@@ -859,3 +861,30 @@ def test_frames_plan_matches_oracle(name, F):
                 if margin > 10 * err:
                     assert (rb["stop_iter"][f], rb["best_iter"][f]) == (ref.stop_iter, ref.best_iter), f
                     assert rel(got, ref.volume) <= 1e-3
+
+
+@pytest.mark.gpu
+def test_frames_plan_with_supplied_ht():
+    """LFM_PLAN_FRAMES with a supplied transposed PSF (f3): the transposed split copy is built from the Ht matrices, so
+    the batched frames equal the single-frame plan with the same Ht (itself oracle-tested, test_supplied_ht) within
+    the fp32 / 2xFP16 re-association bound."""
+    h, x, r = rand_case(31, 3, 3, 27, 33, 9, 9)
+    rng = np.random.default_rng(32)
+    ht = rng.uniform(0, 1, h.shape).astype(np.float32)
+    F = 8
+    ys = [np.ascontiguousarray(rng.uniform(5, 50, (27, 33)).astype(np.float32)) for _ in range(F)]
+    pol = L().make_policy(mode="fixed", n_iters=4)
+    with L().Plan(h, 3, 27, 33, optics=optics(3), flags=L().LFM_PLAN_FFT_ONLY, psf_t=ht) as p1:
+        singles = []
+        for f in range(F):
+            x1 = torch.zeros((3, 27, 33), device="cuda")
+            r1 = p1.rl_iterate(dev(ys[f]), x1, pol)
+            singles.append((r1, x1.cpu().numpy()))
+    with L().Plan(h, 3, 27, 33, optics=optics(3), flags=L().LFM_PLAN_FRAMES, psf_t=ht) as pf:
+        xb = torch.zeros((F, 3, 27, 33), device="cuda")
+        rb = pf.rl_iterate_batch(dev(np.stack(ys)), xb, pol)
+    for f in range(F):
+        r1, x1 = singles[f]
+        assert rb["best_iter"][f] == r1["best_iter"]
+        np.testing.assert_allclose(rb["series"][f], r1["series"], rtol=1e-5)
+        assert rel(xb[f].cpu().numpy(), x1.astype(np.float64)) <= 1e-4
