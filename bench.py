@@ -291,6 +291,13 @@ def run_ours(args):
         "fwd_mac": kap_min * N2 * nu * 8 + kap_min * nu * 8 + kap_min * N2 * 8,   # M + G + Y
         "bwd_mac": kap_min * N2 * nu * 8 + kap_min * N2 * 8 + kap_min * nu * 8,   # M + R + Xh
     }
+    ntile = info.get("tiles", 0)
+    if ntile:   # tiled frequency path: L x (L/2+1) frequencies per window, every tile per pass
+        kt = info["n_kappa"]
+        alg = {
+            "fwd_mac": kt * N2 * nu * 8 + ntile * kt * nu * 8 + ntile * kt * N2 * 8,   # M + G (all tiles) + Y
+            "bwd_mac": kt * N2 * nu * 8 + ntile * kt * N2 * 8 + ntile * kt * nu * 8,   # M^T + R + Xh
+        }
     if info["fft_units"] == 0:
         dom = max(("dir_fwd", "dir_bwd"), key=lambda k: stage_ms[k])
         roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
@@ -303,9 +310,10 @@ def run_ours(args):
         if os.path.exists(tpath):
             tj = json.load(open(tpath))
             for key, ent in tj.items():   # a capture of the same config and plan (frequency-path unit count)
-                if key.split("_")[0] == cfg.name and ent.get("fft_units") == nu:
+                if key.split("_")[0] == cfg.name and ent.get("fft_units") == nu and ent.get("tiles", 0) == ntile:
                     traffic = ent.get(dom)
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        roof = {"bound": "hbm", "kernel": (dom + " (mac_f16_kernel, tiles)") if ntile else dom,
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": kern_ms[dom],
                 "sms": mac_sms[dom],
@@ -332,7 +340,8 @@ def run_ours(args):
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             for key, ent in json.load(open(tpath)).items():
-                if key.split("_")[0] == cfg.name and ent.get("fft_units") == info["fft_units"]:
+                if (key.split("_")[0] == cfg.name and ent.get("fft_units") == info["fft_units"]
+                        and ent.get("tiles", 0) == ntile):
                     tc_traffic = ent.get("tcdir_" + kk.split("_")[1])
         roof_tc = {"bound": "tensor", "kernel": "tcdir_kernel (" + kk.split("_")[1] + ")",
                    "achieved": al, "peak": peak3, "unit": "TFLOP/s", "frac": al / peak3,
@@ -351,10 +360,14 @@ def run_ours(args):
                    "executed_is": "issued tcgen05 kind::f16 flops (3 products over the union tap boxes and the tiles' "
                                   "column ranges, skipped windows excluded)",
                    "tc_planes": info["tc_planes"], "kernel_ms": t}
-    # the dominant kernel (longest average launch) carries the primary roofline
+    # the dominant kernel carries the primary roofline: the largest SM-time (launch time x SMs of its partition) per
+    # iteration -- with SM partitions the longest launch can be the one on the smaller partition
     roof_primary = roof
-    if roof_tc is not None and (info["fft_units"] == 0 or max(roof_tc["kernel_ms"].values()) > kern_ms[dom]):
-        roof_primary = roof_tc
+    if roof_tc is not None:
+        sm_t_tc = sum(kern_ms[k] * tc_sms[k] for k in ("dir_fwd", "dir_bwd"))
+        sm_t_mac = sum(kern_ms[k] * mac_sms[k] for k in ("fwd_mac", "bwd_mac")) if info["fft_units"] else 0.0
+        if sm_t_tc > sm_t_mac:
+            roof_primary = roof_tc
     share = {k: prof["ms"][k] / max(1e-9, sum(prof["ms"].values())) for k in prof["ms"]}
 
     # e2e: the public host-buffer call, auto-stop deconvolution of the same measurement
@@ -413,7 +426,10 @@ def run_ours(args):
                 "workload": workload_desc(cfg),
                 "parallelism": f"depth/phase (z,a)-unit sharding over {world} GPU(s), NCCL allreduce sum+max per iteration"
                 if world > 1 else "single GPU",
-                "transform": f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})"
+                "transform": (f"overlap-save tiles: {info['tiles']} windows of {info['fft_h']}x{info['fft_w']} coarse "
+                              f"pixels, {info['tile_T1']}x{info['tile_T2']} valid outputs each (whole-image alias-free "
+                              f"minimum {info['lc_min_h']})" if info.get("tiles") else
+                              f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})")
                 if not info["direct"] else "direct spatial",
                 "transfer_matrix_gb_per_gpu": info["transfer_bytes"] / 1e9,
                 "hybrid": {"direct_planes": info["direct_planes"], "tc_planes": info["tc_planes"], "fft_units": info["fft_units"], "planes_moved_for_memory": info["planes_moved_for_memory"]},

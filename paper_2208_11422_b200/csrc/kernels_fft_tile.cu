@@ -519,6 +519,11 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         float2 z[L];
 #pragma unroll
         for (int i = 0; i < L; ++i) z[i] = in[(long long)i * NK2 * a.in_ld];
+        for (int sp = 1; sp < a.nsum; ++sp) {   // split-K partial spectra, summed in split order
+            const float2* ins = in + sp * a.in_sstride;
+#pragma unroll
+            for (int i = 0; i < L; ++i) z[i] = c_add(z[i], ins[(long long)i * NK2 * a.in_ld]);
+        }
         reg_fft_stages<L, 0, 1, true>(z);
         float2* col = sp + (size_t)ui * RG::CIMG + k;
 #pragma unroll
@@ -667,7 +672,7 @@ cudaError_t r2c_tile_L(const XformGeom& g, const TileGeom& tg, const float2* tw,
 template <int L>
 cudaError_t c2r_tile_L(const XformGeom& g, const TileGeom& tg, const float2* tw, const C2RArgs& a, int j1, int j2,
                        cudaStream_t s) {
-    if (!tile_warp_kernels()) {
+    if (!tile_warp_kernels() || a.nsum > 1) {
         switch (a.dst) {
             case DST_IMAGE: return c2r_tile_reg_go<L, DST_IMAGE>(g, tg, a, j1, j2, s);
             case DST_POLY: return c2r_tile_reg_go<L, DST_POLY>(g, tg, a, j1, j2, s);

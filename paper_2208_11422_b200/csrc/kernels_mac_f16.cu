@@ -64,8 +64,18 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sbytes = f_stage(F);
     const int ntile = FWD ? 2 : (d.nu_pad + kFM - 1) / kFM;
-    const int nitems = d.nkappa * ntile;
+    const int ksp = d.ksplit > 1 ? d.ksplit : 1;   // K splits per (kappa, tile): partial outputs ksp apart
+    const int nitems = d.nkappa * ntile * ksp;
     const int nchunks = FWD ? (2 * d.nu_pad + kFK - 1) / kFK : (2 * d.bpitch + kFK - 1) / kFK;
+    // item -> kappa, row tile, K split and its chunk range [c_lo, c_hi)
+    auto decode = [&](int item, int& kap, int& t, int& sp, int& c_lo, int& c_hi) {
+        kap = item / (ntile * ksp);
+        const int rem = item - kap * ntile * ksp;
+        t = rem / ksp;
+        sp = rem - t * ksp;
+        c_lo = (int)((long long)sp * nchunks / ksp);
+        c_hi = (int)((long long)(sp + 1) * nchunks / ksp);
+    };
     const int kvalid_last = (FWD ? 2 * d.nu_pad : 2 * d.N2) - (nchunks - 1) * kFK;   // real K elements, last chunk
     const int ks_last = (kvalid_last + 15) / 16;
 
@@ -97,25 +107,11 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
 
     if (warp == 0) {
         if (lane == 0) {   // ---- producer: A hi / lo tiles and the frames' fp32 source tile per chunk ----
-            // L2 prefetch of the A tiles d.pf chunks ahead of the loads (across items): the ring of S stages alone
-            // leaves the stream latency-bound at ~40 GB/s per SM
-            int pf_item = blockIdx.x, pf_c = 0;
-            auto pf_next = [&]() {
-                if (pf_item >= nitems) return;
-                const int kp = pf_item / ntile, tp = pf_item - kp * ntile;
-                tc::tma_prefetch_3d(&d.tmapAh, pf_c * kFK, tp * kFM, kp);
-                tc::tma_prefetch_3d(&d.tmapAl, pf_c * kFK, tp * kFM, kp);
-                if (++pf_c == nchunks) {
-                    pf_c = 0;
-                    pf_item += gridDim.x;
-                }
-            };
-            for (int i = 0; i < d.pf; ++i) pf_next();
             int it = 0;
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int kap = item / ntile, t = item - kap * ntile;
-                for (int c = 0; c < nchunks; ++c, ++it) {
-                    if (d.pf) pf_next();
+                int kap, t, sp, c_lo, c_hi;
+                decode(item, kap, t, sp, c_lo, c_hi);
+                for (int c = c_lo; c < c_hi; ++c, ++it) {
                     const int s = it % S;
                     if (it >= S) tc::mbar_wait(&bar_empty[s], ((it / S) - 1) & 1);
                     unsigned char* st = smem + (size_t)s * sbytes;
@@ -136,7 +132,9 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
         const int pt = (threadIdx.x - 32) % NP, grp = (threadIdx.x - 32) / NP;
         int it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-            for (int c = 0; c < nchunks; ++c, ++it) {
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo; c < c_hi; ++c, ++it) {
                 if (it % PG != grp) continue;
                 const int s = it % S;
                 tc::mbar_wait(&bar_full[grp][s], (it / LG) & 1);
@@ -187,7 +185,9 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
         const uint32_t id1 = tc::idesc_f16(kFM, NB), id2 = tc::idesc_f16(kFM, 2 * F);
         int it = 0, g = 0, gk = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-            for (int c = 0; c < nchunks; ++c, ++it) {
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo; c < c_hi; ++c, ++it) {
                 const int s = it % S, j = g & 1;
                 tc::mbar_wait(&bar_ready[s], (it / S) & 1);
                 if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
                 }
                 tc::mma_commit_elect(&bar_empty[s]);
                 gk += ks;
-                if (gk + kFKS > d.chain_k || c == nchunks - 1) {
+                if (gk + kFKS > d.chain_k || c == c_hi - 1) {
                     tc::mma_commit_elect(&bar_acc[j]);
                     ++g;
                     gk = 0;
@@ -220,10 +220,11 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
         for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
         int g = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-            const int kap = item / ntile, t = item - kap * ntile;
-            for (int c = 0, gk = 0; c < nchunks; ++c) {   // the issuer's drain groups
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo, gk = 0; c < c_hi; ++c) {   // the issuer's drain groups
                 gk += c == nchunks - 1 ? ks_last : kFKS;
-                if (!(gk + kFKS > d.chain_k || c == nchunks - 1)) continue;
+                if (!(gk + kFKS > d.chain_k || c == c_hi - 1)) continue;
                 gk = 0;
                 const int j = g & 1;
                 tc::mbar_wait(&bar_acc[j], (g >> 1) & 1);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
                     if (f >= d.nframes) break;
                     const float inv = s_inv[f];
                     const float2 v = make_float2(acc[2 * f] * inv, acc[2 * f + 1] * inv);
-                    d.out[(long long)f * d.out_fstride + (long long)kap * d.out_ld + row] = v;
+                    d.out[(long long)sp * d.out_sstride + (long long)f * d.out_fstride + (long long)kap * d.out_ld + row] = v;
                 }
             }
 #pragma unroll
@@ -385,7 +386,6 @@ cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa,
         a->bpitch = bpitch;
         a->aexp = w ? eb : ea;
         a->chain_k = getenv("LFM_MF_CHAIN") ? std::max(4, atoi(getenv("LFM_MF_CHAIN"))) : 24;   // dev override
-        a->pf = getenv("LFM_MF_PF") ? std::max(0, atoi(getenv("LFM_MF_PF"))) : 0;   // dev (measured: L2 prefetch slows it)
         const int n = w ? bpitch : nu_pad;               // complex per split row
         const int rows = w ? nu_pad : N2;
         unsigned char* base = reinterpret_cast<unsigned char*>(w ? MT : M);
@@ -429,7 +429,7 @@ static cudaError_t launch_mf(const MacF16Args& d, int num_sms, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(mac_f16_kernel<F, 4, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ntile = FWD ? 2 : (d.nu_pad + kFM - 1) / kFM;
-    const int grid = std::max(1, std::min(d.nkappa * ntile, num_sms));
+    const int grid = std::max(1, std::min(d.nkappa * ntile * std::max(1, d.ksplit), num_sms));
     mac_f16_kernel<F, 4, FWD><<<grid, kFThreads, smem, s>>>(d);
     return cudaGetLastError();
 }

@@ -652,6 +652,8 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
                 c.ntrans = p->tg.ntile * N2;
                 c.cdiv = N2;
                 c.cmul = (long long)p->xg.nkappa * N2;
+                c.nsum = p->mf_fwd.ksplit;
+                c.in_sstride = p->mf_fwd.out_sstride;
                 CK(launch_c2r_tile(p->xg, p->tg, p->tw_h, c, 0, c2r_in ? sm : s));
             } else {
                 CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
@@ -1964,7 +1966,10 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             PG(dalloc(p, &p->M, mbytes, "transfer matrices"));
             PG(dalloc(p, &p->G, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "G spectra"));
             PG(dalloc(p, &p->Xh, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
-            PG(dalloc(p, &p->Y, (size_t)nt * nkap * N2 * sizeof(float2), "Y spectra"));
+            // tiled forward MAC: K split so that every SM gets >= 16 (kappa, half, split) items (load balance); the
+            // partial spectra are summed in split order by the C2R
+            const int ksplit = tiles.ntile ? std::max(1, std::min(8, (16 * p->num_sms + 2 * nkap - 1) / (2 * nkap))) : 1;
+            PG(dalloc(p, &p->Y, (size_t)ksplit * nt * nkap * N2 * sizeof(float2), "Y spectra"));
             PG(dalloc(p, &p->R, (size_t)nt * nkap * rpitch * sizeof(float2), "R spectra"));
             CKG(cudaMemsetAsync(p->M, 0, mbytes, s));      // padding columns stay zero
             CKG(cudaMemsetAsync(p->G, 0, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), s));
@@ -2006,6 +2011,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 p->mf_fwd.out = p->Y;
                 p->mf_fwd.out_fstride = (long long)nkap * N2;
                 p->mf_fwd.out_ld = N2;
+                p->mf_fwd.ksplit = ksplit;
+                p->mf_fwd.out_sstride = (long long)nt * nkap * N2;
                 p->mf_bwd.bmax = p->tmax + 32;
                 p->mf_bwd.out = p->Xh;
                 p->mf_bwd.out_fstride = (long long)nkap * p->nu_fft_pad;

@@ -82,6 +82,8 @@ struct C2RArgs {
     float eps;
     int cdiv;               // overlap-save tiles (launch_c2r_tile): transform t = tile * cdiv + item reads column
     long long cmul;         //   tile * cmul + item of in[kappa * in_ld + .]
+    int nsum;               //   summed over nsum partial inputs in_sstride apart (split-K MAC outputs; 0 / 1: one)
+    long long in_sstride;
 };
 
 // overlap-save tiles of the coarse grid: a square transform of L points per axis serves T1 x T2
@@ -263,7 +265,8 @@ struct MacF16Args {
     int nkappa, N2, nu_pad, bpitch;
     int aexp;                 // the transfer matrices' scale exponent
     int chain_k;              // K-steps accumulated in TMEM between drains
-    int pf;                   // A chunks prefetched into L2 ahead of the TMA loads (0: none)
+    int ksplit;               // K splits per (kappa, row tile) (0 / 1: none): split sp writes out + sp * out_sstride
+    long long out_sstride;
     const int* bexp;          // [F] the frames' source scale exponents (device, per call)
     const unsigned* bmax;     // or (non-null): [F] bounds of the frames' |source| (float bits), exponents derived in-kernel
     int nframes;              // frames actually present (<= F; the TMA zero-fills the rest, no output for them)

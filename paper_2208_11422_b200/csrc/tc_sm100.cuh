@@ -73,13 +73,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, in
         : "memory");
 }
 
-// L2 prefetch of a 3-D tensor-map box (no shared-memory destination, no completion): keeps more HBM requests in flight
-// than the shared-memory ring holds; the later tma_load_3d of the same box then hits L2
-__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tmap), "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
-}
-
 // CTA-pair (cta_group::2) variant: issued by each CTA of the pair for its own smem; the completion bytes are
 // counted on the LEADER CTA's mbarrier (peer bit of the shared::cluster address cleared)
 __device__ __forceinline__ void tma_load_3d_pair(void* dst_smem, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
