@@ -225,7 +225,14 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_tile_kernel(XformGeom g
         if (ui >= nt) continue;
         const int k1 = kap / NK2;
         const int k2 = kap - k1 * NK2;
-        cp_async8(&buf[ui * S + k1 * RHO + k2], &a.in[(long long)kap * a.in_ld + s_col[ui]]);
+        const float2* src = &a.in[(long long)kap * a.in_ld + s_col[ui]];
+        if (a.nsum > 1) {   // split-K partial spectra, summed in split order
+            float2 v = src[0];
+            for (int sp = 1; sp < a.nsum; ++sp) v = c_add(v, src[sp * a.in_sstride]);
+            buf[ui * S + k1 * RHO + k2] = v;
+        } else {
+            cp_async8(&buf[ui * S + k1 * RHO + k2], src);
+        }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -339,6 +346,7 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_tile_kernel(XformGeom g
 // destination epilogue over the valid T1 x T2 outputs, consecutive threads on consecutive columns.
 // ================================================================================================================
 constexpr int kTwTotal = 228;
+constexpr int kRegMaxL = 36;               // larger windows (c4: 45) run the warp-per-transform kernels above
 __constant__ float2 c_tile_tw[kTwTotal];   // W_L^e = exp(-2 pi i e / L) for every L of tile_fft_size, fp64-rounded
 
 __host__ __device__ constexpr int tw_off(int L) {
@@ -628,28 +636,36 @@ bool tile_warp_kernels() {
 template <int L, int SRC>
 cudaError_t r2c_tile_reg_go(const XformGeom& g, const TileGeom& tg, const R2CArgs& a, int o1, int o2, unsigned* amax,
                             cudaStream_t s) {
+    if constexpr (L > kRegMaxL) {
+        return cudaErrorInvalidValue;
+    } else {
     using RG = RegGeom<L>;
     const size_t smem = RG::smem_r2c();
     cudaError_t e = cudaFuncSetAttribute(r2c_tile_reg_kernel<L, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     r2c_tile_reg_kernel<L, SRC><<<(unsigned)((a.ntrans + RG::UB - 1) / RG::UB), RG::NT, smem, s>>>(g, tg, a, o1, o2, amax);
     return cudaGetLastError();
+    }
 }
 
 template <int L, int DST>
 cudaError_t c2r_tile_reg_go(const XformGeom& g, const TileGeom& tg, const C2RArgs& a, int j1, int j2, cudaStream_t s) {
+    if constexpr (L > kRegMaxL) {
+        return cudaErrorInvalidValue;
+    } else {
     using RG = RegGeom<L>;
     const size_t smem = RG::smem_c2r(tg.T1, tg.T2);
     cudaError_t e = cudaFuncSetAttribute(c2r_tile_reg_kernel<L, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     c2r_tile_reg_kernel<L, DST><<<(unsigned)((a.ntrans + RG::UB - 1) / RG::UB), RG::NT, smem, s>>>(g, tg, a, j1, j2);
     return cudaGetLastError();
+    }
 }
 
 template <int L>
 cudaError_t r2c_tile_L(const XformGeom& g, const TileGeom& tg, const float2* tw, const R2CArgs& a, int o1, int o2,
                        unsigned* amax, cudaStream_t s) {
-    if (!tile_warp_kernels()) {
+    if (!tile_warp_kernels() && L <= kRegMaxL) {
         switch (a.src) {
             case SRC_POLY: return r2c_tile_reg_go<L, SRC_POLY>(g, tg, a, o1, o2, amax, s);
             case SRC_IMAGE: return r2c_tile_reg_go<L, SRC_IMAGE>(g, tg, a, o1, o2, amax, s);
@@ -672,7 +688,7 @@ cudaError_t r2c_tile_L(const XformGeom& g, const TileGeom& tg, const float2* tw,
 template <int L>
 cudaError_t c2r_tile_L(const XformGeom& g, const TileGeom& tg, const float2* tw, const C2RArgs& a, int j1, int j2,
                        cudaStream_t s) {
-    if (!tile_warp_kernels() || a.nsum > 1) {
+    if (!tile_warp_kernels() && L <= kRegMaxL) {
         switch (a.dst) {
             case DST_IMAGE: return c2r_tile_reg_go<L, DST_IMAGE>(g, tg, a, j1, j2, s);
             case DST_POLY: return c2r_tile_reg_go<L, DST_POLY>(g, tg, a, j1, j2, s);
@@ -712,9 +728,12 @@ cudaError_t tile_fft_init() {
 }
 
 // transform sizes with compiled tile kernels (5-smooth, radix-2/3/4/5 stages)
-bool tile_fft_size(int L) { return L == 16 || L == 18 || L == 20 || L == 24 || L == 25 || L == 27 || L == 30 || L == 32 || L == 36; }
+bool tile_fft_size(int L) {
+    return L == 16 || L == 18 || L == 20 || L == 24 || L == 25 || L == 27 || L == 30 || L == 32 || L == 36 || L == 40 ||
+           L == 45 || L == 48;
+}
 
-#define LFM_TILE_SIZES(X) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32) X(36)
+#define LFM_TILE_SIZES(X) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32) X(36) X(40) X(45) X(48)
 
 cudaError_t launch_r2c_tile(const XformGeom& g, const TileGeom& tg, const float2* tw, const R2CArgs& a, int dir,
                             unsigned* amax, cudaStream_t s) {

@@ -1070,7 +1070,8 @@ double partition_time(double t_tc, double bytes, int d, int num_sms, int* best_s
 // the tiles' spectra written by the R2C and read by the MAC (and the reverse), and the window transforms.
 constexpr double kMacF16Bps = 5.3e12;        // kind::f16 tile MACs, HBM-bound (r02 c3 tiles: 5.25-5.45 TB/s)
 constexpr double kXformPoint = 6.0e-12;      // whole-image transform seconds per point and direction (r02, L = 75)
-constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms (r02, L = 27: 4.1e-12)
+constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms, L <= 36 (r02, L = 27: 4.1e-12)
+constexpr double kXformPointTileW = 7.5e-12; // warp-per-transform tile kernels, L > 36 (r02, L = 27: 7.5e-12)
 
 // tile geometry for transform size L (ntile = 0: not possible).  Coarse taps of every phase pair of a kh x kw kernel
 // lie in [dmin, dmax] with N d + b - a + c in [0, k - 1] (reading of S:192's kernel centring).
@@ -1095,7 +1096,7 @@ double tile_unit_cost(const TileGeom& t, int N2) {
     const double nkap = (double)t.L * (t.L / 2 + 1);
     const double bpitch = (double)round_up((size_t)N2, 4);
     return nkap * (N2 + bpitch) * 8.0 / kMacF16Bps + 4.0 * t.ntile * nkap * 8.0 / kHbmBps +
-           2.0 * kXformPointTile * t.ntile * t.L * t.L;
+           2.0 * (t.L <= 36 ? kXformPointTile : kXformPointTileW) * t.ntile * t.L * t.L;
 }
 
 double whole_unit_cost(const Geo& g, int N2) {
@@ -1106,7 +1107,7 @@ double whole_unit_cost(const Geo& g, int N2) {
 // whenever one exists; LFM_PLAN_NO_TILES / FRAMES plans: never)
 TileGeom choose_tiles(const Geo& g, int N2, int flags) {
     if ((flags & (LFM_PLAN_NO_TILES | LFM_PLAN_FRAMES | LFM_PLAN_DIRECT)) || N2 > 256) return TileGeom{};
-    static const int cand[] = {16, 18, 20, 24, 25, 27, 30, 32, 36};
+    static const int cand[] = {16, 18, 20, 24, 25, 27, 30, 32, 36, 40, 45, 48};
     TileGeom best{};
     double best_c = 1e300;
     const char* ev = getenv("LFM_TILE_L");   // dev override of the transform size

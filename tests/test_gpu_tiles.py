@@ -70,6 +70,29 @@ def test_tiled_projections_match_oracle(case, flags):
         assert np.abs(g - ref).max() <= 2e-5 * np.abs(ref).max(), info
 
 
+@pytest.mark.parametrize("L", [45, 20], ids=["warp-kernels", "register-kernels"])
+def test_tiled_window_sizes(L, monkeypatch):
+    """Forced window sizes (LFM_TILE_L, dev): L = 45 runs the warp-per-transform tile kernels (c4's size), L = 20 the
+    register-resident ones, on the same problem; both match the oracle."""
+    monkeypatch.setenv("LFM_TILE_L", str(L))
+    h, x, r = rand_case(97, 2, 3, 120, 99, 27, 21)
+    hd = h.astype(np.float64)
+    with L_().Plan(h, 3, 120, 99, flags=L_().LFM_PLAN_TILES | L_().LFM_PLAN_FFT_ONLY) as plan:
+        info = plan.info()
+        assert info["tiles"] >= 2 and info["fft_h"] == L, info
+        y_d = torch.zeros((120, 99), device="cuda")
+        plan.forward(dev(x), y_d)
+        xb_d = torch.zeros((2, 120, 99), device="cuda")
+        plan.backward(dev(r), xb_d)
+        torch.cuda.synchronize()
+    assert rel(y_d.cpu().numpy(), O.forward_project(x.astype(np.float64), hd)) <= 1e-5
+    assert rel(xb_d.cpu().numpy(), O.backward_project(r.astype(np.float64), hd)) <= 1e-5
+
+
+def L_():
+    return L()
+
+
 def test_tiled_signed_inputs():
     """lfm_forward / lfm_backward of sign-changing inputs: the per-tile fp16 scale is bounded by sum |window|, not by
     the (non-negative-source) DC term."""
