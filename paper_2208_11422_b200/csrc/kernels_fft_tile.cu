@@ -527,8 +527,8 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         float2 z[L];
 #pragma unroll
         for (int i = 0; i < L; ++i) z[i] = in[(long long)i * NK2 * a.in_ld];
-        for (int sp = 1; sp < a.nsum; ++sp) {   // split-K partial spectra, summed in split order
-            const float2* ins = in + sp * a.in_sstride;
+        for (int ks = 1; ks < a.nsum; ++ks) {   // split-K partial spectra, summed in split order
+            const float2* ins = in + ks * a.in_sstride;
 #pragma unroll
             for (int i = 0; i < L; ++i) z[i] = c_add(z[i], ins[(long long)i * NK2 * a.in_ld]);
         }
