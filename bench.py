@@ -292,12 +292,9 @@ def run_ours(args):
         "bwd_mac": kap_min * N2 * nu * 8 + kap_min * N2 * 8 + kap_min * nu * 8,   # M + R + Xh
     }
     ntile = info.get("tiles", 0)
-    if ntile:   # tiled frequency path: L x (L/2+1) frequencies per window, every tile per pass
-        kt = info["n_kappa"]
-        alg = {
-            "fwd_mac": kt * N2 * nu * 8 + ntile * kt * nu * 8 + ntile * kt * N2 * 8,   # M + G (all tiles) + Y
-            "bwd_mac": kt * N2 * nu * 8 + ntile * kt * N2 * 8 + ntile * kt * nu * 8,   # M^T + R + Xh
-        }
+    if ntile:   # tiled frequency path: per tile group L x (L/2+1) frequencies per window, every tile
+        # per pass -- M (or M^T) of the group's units + the tiles' spectra in and out, summed over groups (lfm_info)
+        alg = {"fwd_mac": info["fft_bytes"], "bwd_mac": info["fft_bytes"]}
     if info["fft_units"] == 0:
         dom = max(("dir_fwd", "dir_bwd"), key=lambda k: stage_ms[k])
         roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
@@ -426,9 +423,10 @@ def run_ours(args):
                 "workload": workload_desc(cfg),
                 "parallelism": f"depth/phase (z,a)-unit sharding over {world} GPU(s), NCCL allreduce sum+max per iteration"
                 if world > 1 else "single GPU",
-                "transform": (f"overlap-save tiles: {info['tiles']} windows of {info['fft_h']}x{info['fft_w']} coarse "
-                              f"pixels, {info['tile_T1']}x{info['tile_T2']} valid outputs each (whole-image alias-free "
-                              f"minimum {info['lc_min_h']})" if info.get("tiles") else
+                "transform": (f"overlap-save tiles in {info['tile_groups']} group(s) (one window geometry per coarse-tap "
+                              f"range; first: {info['tiles']} windows of {info['fft_h']}x{info['fft_w']} coarse pixels, "
+                              f"{info['tile_T1']}x{info['tile_T2']} valid outputs each; whole-image alias-free minimum "
+                              f"{info['lc_min_h']})" if info.get("tiles") else
                               f"coarse {info['fft_h']}x{info['fft_w']} (alias-free minimum {info['lc_min_h']})")
                 if not info["direct"] else "direct spatial",
                 "transfer_matrix_gb_per_gpu": info["transfer_bytes"] / 1e9,

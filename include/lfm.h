@@ -162,8 +162,12 @@ typedef struct {
                                        2 the same with NVLS multimem.ld_reduce (LFM_PLAN_SYMMETRIC, §7)       */
     int tc_moved_to_fft;            /* tensor-core planes the partition-aware step moved to the frequency path */
     int tiles;                      /* overlap-save tiles of the frequency path (0: whole-image transforms); the
-                                       transforms are then fft_h x fft_w windows serving tile_T1 x tile_T2 outputs */
+                                       transforms are then fft_h x fft_w windows serving tile_T1 x tile_T2 outputs
+                                       (of the first tile group when several coarse-tap ranges have their own)      */
     int tile_T1, tile_T2;
+    int tile_groups;                /* tile groups (one window geometry per coarse-tap range of the planes)        */
+    double fft_bytes;               /* per projection: algorithmic bytes of the frequency-path MAC(s) -- transfer
+                                       matrices of the owned frequency-path units + the spectra they read / write */
 } lfm_info;
 
 /* Default policy: auto, max 50, min 2, patience 1, eps 1e-6, triangle, uniform init, RL. */

@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_tile_kernel(XformGeom g
                     const int item = s_item[ui];
                     if constexpr (DST == DST_IMAGE) {
                         const int b1 = item / g.N, b2 = item % g.N;
-                        a.out[(size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2] = v;
+                        float* o = a.out + (size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
+                        *o = a.accum ? *o + v : v;
                     } else if constexpr (DST == DST_VOLIMAGE) {
                         const int u = g.unit0 + (g.umap ? g.umap[item] : item);
                         const int N2 = g.N * g.N;
@@ -586,7 +587,8 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         const int item = s_item[ui];
         if constexpr (DST == DST_IMAGE) {
             const int b1 = item / g.N, b2 = item % g.N;
-            a.out[(size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2] = v;
+            float* o = a.out + (size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
+            *o = a.accum ? *o + v : v;
         } else if constexpr (DST == DST_VOLIMAGE) {
             const int u = g.unit0 + (g.umap ? g.umap[item] : item);
             const int N2 = g.N * g.N;

@@ -238,13 +238,24 @@ struct lfm_plan_s {
     int* mf_eb = nullptr;                              // [2][32] per-frame source scale exponents (fwd, bwd)
     const void* mf_src[2] = {nullptr, nullptr};        // encoded source pointers / frame counts of mf_fwd / mf_bwd
     int mf_F[2] = {0, 0};
-    // overlap-save tiled frequency path (LFM_PLAN_TILES): transforms of tg.L points per axis over
-    // tg.ntile tiles; M (forward) and M^T (backward) stored split as in FRAMES plans, both MACs on kind::f16 with the
-    // tiles as the GEMM's N (kernels_mac_f16.cu, F = mf_tF >= ntile)
+    // overlap-save tiled frequency path (LFM_PLAN_TILES): one group per coarse-tap range of the
+    // frequency-path planes, each with transforms of tg.L points per axis over tg.ntile tiles; M (forward) and M^T
+    // (backward) stored split as in FRAMES plans, both MACs on kind::f16 with the tiles as the GEMM's N
+    // (kernels_mac_f16.cu, F >= ntile)
+    struct TileGroup {
+        TileGeom tg{};
+        XformGeom xg{};            // the group's windows (L x L) and units (umap, nu, nu_pad)
+        FftDesc fd{};
+        float2* tw = nullptr;      // twiddles of L (warp kernels, M build)
+        int* umap = nullptr;       // [nu] local unit index of the group's transform t
+        float2 *M = nullptr, *MT = nullptr, *G = nullptr, *Xh = nullptr, *Y = nullptr, *R = nullptr;
+        unsigned* tmax = nullptr;  // [2][32] per-tile |source| bounds (float bits) of the forward / backward MAC
+        MacF16Args fwd{}, bwd{};
+        int F = 0;
+    };
     bool tiled = false;
-    TileGeom tg{};
-    int mf_tF = 0;
-    unsigned* tmax = nullptr;   // [2][32] per-tile |source| bounds (float bits) of the forward / backward MAC
+    std::vector<TileGroup> tgs;
+    double fft_alg_bytes = 0.0;   // per projection: algorithmic bytes of the frequency path's MAC (lfm_info)
     std::vector<void*> dallocs;     // device arrays owned by the direct groups
     int n_direct_planes = 0;
     float* dpart = nullptr;         // [max group planes][H][W] per-plane forward partials
@@ -483,7 +494,11 @@ void plan_free(lfm_plan p) {
     if (p->sym) sym_destroy(p->sym);
     cudaFree(p->MT);
     cudaFree(p->mf_eb);
-    cudaFree(p->tmax);
+    for (auto& gr : p->tgs) {
+        for (void* q : {(void*)gr.tw, (void*)gr.umap, (void*)gr.M, (void*)gr.MT, (void*)gr.G, (void*)gr.Xh, (void*)gr.Y,
+                        (void*)gr.R, (void*)gr.tmax})
+            cudaFree(q);
+    }
     if (p->nccl) ncclCommDestroy(p->nccl);
     cudaFree(p->tw_h);
     cudaFree(p->tw_w);
@@ -612,11 +627,13 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
         if (split && !prefork) ST(fork(p, pt, s, &st, &sm));
         for (const TcDirArgs& tg : p->tcf) CK(launch_tcdir_fwd(tg, x, image ? 1 : 0, yimg, 0, st, TC_PART_STAGE));
         if (p->nu_fft > 0 && p->tiled) {   // §5.6: window transforms of every (tile, unit), |window| bounds per tile
-            CK(cudaMemsetAsync(p->tmax, 0, 32 * sizeof(unsigned), sm));
-            R2CArgs a = r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->tg.ntile * p->nu_fft, p->G, p->nu_fft_pad);
-            a.cdiv = p->nu_fft;
-            a.cmul = p->xg.nkappa * p->nu_fft_pad;
-            CK(launch_r2c_tile(p->xg, p->tg, p->tw_h, a, 0, p->tmax, sm));
+            for (auto& gr : p->tgs) {
+                CK(cudaMemsetAsync(gr.tmax, 0, 32 * sizeof(unsigned), sm));
+                R2CArgs a = r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, gr.tg.ntile * gr.xg.nu, gr.G, gr.xg.nu_pad);
+                a.cdiv = gr.xg.nu;
+                a.cmul = (long long)gr.xg.nkappa * gr.xg.nu_pad;
+                CK(launch_r2c_tile(gr.xg, gr.tg, gr.tw, a, 0, gr.tmax, sm));
+            }
         } else if (p->nu_fft > 0) {
             CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w,
                           r2c_args(image ? SRC_IMAGE : SRC_POLY, x, nullptr, 0.f, p->nu_fft, p->G, p->nu_fft_pad), sm));
@@ -631,7 +648,7 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
         if (p->nu_fft > 0 && !(part_skip() & 2)) {
             ST(kmark(p, 1, 0, sm));
             if (p->tiled)
-                CK(launch_mac_f16(p->mf_fwd, 1, p->mf_tF, split ? pt.sms_mac : p->num_sms, sm));
+                for (auto& gr : p->tgs) CK(launch_mac_f16(gr.fwd, 1, gr.F, split ? pt.sms_mac : p->num_sms, sm));
             else
                 CK(launch_fwd_mac(p->M, p->G, p->Y, p->geo.nkappa, N2, p->nu_fft_pad, split ? pt.sms_mac : p->num_sms,
                                   split, sm));
@@ -649,12 +666,17 @@ lfm_status op_forward_src(lfm_plan p, const float* x, bool image, float* ysum, c
             c.ntrans = N2;
             c.out = yimg;
             if (p->tiled) {
-                c.ntrans = p->tg.ntile * N2;
-                c.cdiv = N2;
-                c.cmul = (long long)p->xg.nkappa * N2;
-                c.nsum = p->mf_fwd.ksplit;
-                c.in_sstride = p->mf_fwd.out_sstride;
-                CK(launch_c2r_tile(p->xg, p->tg, p->tw_h, c, 0, c2r_in ? sm : s));
+                for (size_t gi = 0; gi < p->tgs.size(); ++gi) {   // the groups' images summed in group order
+                    const auto& gr = p->tgs[gi];
+                    c.in = gr.Y;
+                    c.ntrans = gr.tg.ntile * N2;
+                    c.cdiv = N2;
+                    c.cmul = (long long)gr.xg.nkappa * N2;
+                    c.nsum = gr.fwd.ksplit;
+                    c.in_sstride = gr.fwd.out_sstride;
+                    c.accum = gi > 0;
+                    CK(launch_c2r_tile(gr.xg, gr.tg, gr.tw, c, 0, c2r_in ? sm : s));
+                }
             } else {
                 CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
             }
@@ -726,11 +748,13 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     if (split && !prefork) ST(fork(p, pt, s, &st, &sm));   // staging / R2C inside the halves, as in the forward
     for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_STAGE));
     if (p->nu_fft > 0 && p->tiled) {   // §5.6: windows of every (tile, output phase), R rows of bpitch
-        CK(cudaMemsetAsync(p->tmax + 32, 0, 32 * sizeof(unsigned), sm));
-        R2CArgs a = r2c_args(src, img, img2, eps, p->tg.ntile * N2, p->R, p->bpitch);
-        a.cdiv = N2;
-        a.cmul = (long long)p->xg.nkappa * p->bpitch;
-        CK(launch_r2c_tile(p->xg, p->tg, p->tw_h, a, 1, p->tmax + 32, sm));
+        for (auto& gr : p->tgs) {
+            CK(cudaMemsetAsync(gr.tmax + 32, 0, 32 * sizeof(unsigned), sm));
+            R2CArgs a = r2c_args(src, img, img2, eps, gr.tg.ntile * N2, gr.R, p->bpitch);
+            a.cdiv = N2;
+            a.cmul = (long long)gr.xg.nkappa * p->bpitch;
+            CK(launch_r2c_tile(gr.xg, gr.tg, gr.tw, a, 1, gr.tmax + 32, sm));
+        }
     } else if (p->nu_fft > 0) {
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), sm));
     }
@@ -747,7 +771,7 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     if (p->nu_fft > 0 && !(part_skip() & 2)) {
         ST(kmark(p, 3, 0, sm));
         if (p->tiled)
-            CK(launch_mac_f16(p->mf_bwd, 0, p->mf_tF, split ? pt.sms_mac : p->num_sms, sm));
+            for (auto& gr : p->tgs) CK(launch_mac_f16(gr.bwd, 0, gr.F, split ? pt.sms_mac : p->num_sms, sm));
         else
             CK(launch_bwd_mac(p->Mb, p->R, p->Xh, p->geo.nkappa, N2, p->nu_fft_pad, sm));
         ST(kmark(p, 3, 1, sm));
@@ -765,10 +789,14 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
         c.norm = aux;
         c.eps = eps;
         if (p->tiled) {
-            c.ntrans = p->tg.ntile * p->nu_fft;
-            c.cdiv = p->nu_fft;
-            c.cmul = (long long)p->xg.nkappa * p->nu_fft_pad;
-            CK(launch_c2r_tile(p->xg, p->tg, p->tw_h, c, 1, c2r_in ? sm : s));
+            for (const auto& gr : p->tgs) {   // disjoint units
+                c.in = gr.Xh;
+                c.in_ld = gr.xg.nu_pad;
+                c.ntrans = gr.tg.ntile * gr.xg.nu;
+                c.cdiv = gr.xg.nu;
+                c.cmul = (long long)gr.xg.nkappa * gr.xg.nu_pad;
+                CK(launch_c2r_tile(gr.xg, gr.tg, gr.tw, c, 1, c2r_in ? sm : s));
+            }
         } else {
             CK(launch_c2r(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, c, s));
         }
@@ -1073,15 +1101,14 @@ constexpr double kXformPoint = 6.0e-12;      // whole-image transform seconds pe
 constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms, L <= 36 (r02, L = 27: 4.1e-12)
 constexpr double kXformPointTileW = 7.5e-12; // warp-per-transform tile kernels, L > 36 (r02, L = 27: 7.5e-12)
 
-// tile geometry for transform size L (ntile = 0: not possible).  Coarse taps of every phase pair of a kh x kw kernel
-// lie in [dmin, dmax] with N d + b - a + c in [0, k - 1] (reading of S:192's kernel centring).
-TileGeom tile_geometry(const Geo& g, int L) {
+// tile geometry for transform size L (ntile = 0: not possible) over coarse taps in [d1a, d1b] x [d2a, d2b]
+TileGeom tile_geometry(const Geo& g, int L, int d1a, int d1b, int d2a, int d2b) {
     TileGeom t{};
     t.L = L;
-    t.dmin1 = ceildiv(-(g.N - 1) - g.ch, g.N);
-    t.dmax1 = floordiv(g.kh - 1 + (g.N - 1) - g.ch, g.N);
-    t.dmin2 = ceildiv(-(g.N - 1) - g.cw, g.N);
-    t.dmax2 = floordiv(g.kw - 1 + (g.N - 1) - g.cw, g.N);
+    t.dmin1 = d1a;
+    t.dmax1 = d1b;
+    t.dmin2 = d2a;
+    t.dmax2 = d2b;
     t.T1 = L - (t.dmax1 - t.dmin1);
     t.T2 = L - (t.dmax2 - t.dmin2);
     if (t.T1 < 1 || t.T2 < 1 || !tile_fft_size(L)) return TileGeom{};
@@ -1103,9 +1130,9 @@ double whole_unit_cost(const Geo& g, int N2) {
     return 2.0 * N2 * (double)g.nkappa * 8.0 / kHbmBps + 2.0 * kXformPoint * g.Lh * g.Lw;
 }
 
-// the cheapest tiling, or ntile = 0 when whole-image transforms are cheaper (LFM_PLAN_TILES: the cheapest tiling
-// whenever one exists; LFM_PLAN_NO_TILES / FRAMES plans: never)
-TileGeom choose_tiles(const Geo& g, int N2, int flags) {
+// the cheapest tiling of coarse taps in [d1a, d1b] x [d2a, d2b] (ntile = 0: none possible, or LFM_PLAN_NO_TILES /
+// FRAMES / DIRECT plans)
+TileGeom choose_tiles(const Geo& g, int N2, int flags, int d1a, int d1b, int d2a, int d2b) {
     if ((flags & (LFM_PLAN_NO_TILES | LFM_PLAN_FRAMES | LFM_PLAN_DIRECT)) || N2 > 256) return TileGeom{};
     static const int cand[] = {16, 18, 20, 24, 25, 27, 30, 32, 36, 40, 45, 48};
     TileGeom best{};
@@ -1113,7 +1140,7 @@ TileGeom choose_tiles(const Geo& g, int N2, int flags) {
     const char* ev = getenv("LFM_TILE_L");   // dev override of the transform size
     for (int L : cand) {
         if (ev && atoi(ev) != L) continue;
-        const TileGeom t = tile_geometry(g, L);
+        const TileGeom t = tile_geometry(g, L, d1a, d1b, d2a, d2b);
         if (t.ntile == 0) continue;
         const double c = tile_unit_cost(t, N2);
         if (c < best_c) {
@@ -1121,9 +1148,17 @@ TileGeom choose_tiles(const Geo& g, int N2, int flags) {
             best = t;
         }
     }
-    if (best.ntile == 0) return best;
-    if (!(flags & LFM_PLAN_TILES) && !(best_c < 0.9 * whole_unit_cost(g, N2))) return TileGeom{};
     return best;
+}
+
+// the same for a whole kh x kw kernel: coarse taps of every phase pair lie in [dmin, dmax] with N d + b - a + c in
+// [0, k - 1] (reading of S:192's kernel centring); ntile = 0 also when whole-image transforms are
+// cheaper by the cost model (the sharding model's view of the frequency path)
+TileGeom choose_tiles(const Geo& g, int N2, int flags) {
+    const TileGeom t = choose_tiles(g, N2, flags, ceildiv(-(g.N - 1) - g.ch, g.N), floordiv(g.kh - 1 + (g.N - 1) - g.ch, g.N),
+                                    ceildiv(-(g.N - 1) - g.cw, g.N), floordiv(g.kw - 1 + (g.N - 1) - g.cw, g.N));
+    if (t.ntile && !(flags & LFM_PLAN_TILES) && !(tile_unit_cost(t, N2) < 0.9 * whole_unit_cost(g, N2))) return TileGeom{};
+    return t;
 }
 
 // SM partitions are used unless the plan runs the device-resident loop (its conditional graph body cannot hold
@@ -1243,6 +1278,91 @@ double range_cost(const std::vector<PlaneCost>& pc, int N2, int b, int e) {
         t += pc[z].atomic ? pc[z].t : pc[z].t * (hi - lo) / N2;
     }
     return t;
+}
+
+// §5.6: one tile group: window geometry tg over the local units `units`; builds its transfer matrices on the L x L
+// grid (K1 on the window size), the split M / M^T of the kind::f16 MACs, its spectra buffers and MAC arguments
+lfm_status build_tile_group(lfm_plan p, lfm_plan_s::TileGroup& gr, const TileGeom& tg, const std::vector<int>& units,
+                            const XformGeom& xg_plan, bool has_ht, cudaStream_t s) {
+    const int N2 = p->geo.N * p->geo.N;
+    const int L = tg.L, nkap = L * (L / 2 + 1), nt = tg.ntile;
+    const int nu = (int)units.size(), nu_pad = (int)round_up((size_t)nu, 16);
+    gr.tg = tg;
+    gr.xg = xg_plan;
+    gr.xg.Lh = gr.xg.Lw = L;
+    gr.xg.nk2 = L / 2 + 1;
+    gr.xg.nkappa = nkap;
+    gr.xg.nu = nu;
+    gr.xg.nu_pad = nu_pad;
+    if (!fft_factor(L, &gr.fd)) return fail(LFM_EUNSUPPORTED, "tile window %d is not 5-smooth", L);
+    {
+        std::vector<float2> t(L);
+        for (int k = 0; k < L; ++k) {
+            const double ang = -2.0 * 3.14159265358979323846 * k / L;
+            t[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        }
+        ST(dalloc(p, &gr.tw, L * sizeof(float2), "tile twiddles"));
+        CK(cudaMemcpy(gr.tw, t.data(), L * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+    ST(dalloc(p, &gr.umap, nu * sizeof(int), "tile group unit map"));
+    CK(cudaMemcpy(gr.umap, units.data(), nu * sizeof(int), cudaMemcpyHostToDevice));
+    gr.xg.umap = gr.umap;
+    const size_t mbytes = (size_t)nkap * N2 * nu_pad * sizeof(float2);
+    const size_t mtb = (size_t)nkap * nu_pad * p->bpitch * sizeof(float2);
+    const size_t gbytes = (size_t)nt * nkap * nu_pad * sizeof(float2);
+    // forward MAC split along K so that every SM gets >= 16 (kappa, half, split) items (load balance); the partial
+    // spectra are summed in split order by the C2R
+    const int ksplit = std::max(1, std::min(8, (16 * p->num_sms + 2 * nkap - 1) / (2 * nkap)));
+    ST(dalloc(p, &gr.M, mbytes, "transfer matrices (tiles)"));
+    ST(dalloc(p, &gr.MT, mtb, "transposed transfer matrices (tiles)"));
+    ST(dalloc(p, &gr.G, gbytes, "G spectra (tiles)"));
+    ST(dalloc(p, &gr.Xh, gbytes, "Xh spectra (tiles)"));
+    ST(dalloc(p, &gr.Y, (size_t)ksplit * nt * nkap * N2 * sizeof(float2), "Y spectra (tiles)"));
+    ST(dalloc(p, &gr.R, (size_t)nt * nkap * p->bpitch * sizeof(float2), "R spectra (tiles)"));
+    ST(dalloc(p, &gr.tmax, 64 * sizeof(unsigned), "tile scale bounds"));
+    p->transfer_bytes += mbytes + mtb;
+    CK(cudaMemsetAsync(gr.M, 0, mbytes, s));   // padding columns stay zero
+    CK(cudaMemsetAsync(gr.G, 0, gbytes, s));
+    CK(cudaMemsetAsync(gr.R, 0, (size_t)nt * nkap * p->bpitch * sizeof(float2), s));
+    CK(cudaMemsetAsync(gr.tmax, 0, 64 * sizeof(unsigned), s));
+    // K1 on the window grid: M[kappa][b'][t] = DFT_{L x L}(g_{u(t),b'}) (taps within the group's range: no wrap)
+    R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * nu, gr.M, (long long)N2 * nu_pad);
+    a.cdiv = nu;
+    a.cmul = nu_pad;
+    CK(launch_r2c(gr.xg, gr.fd, gr.fd, gr.tw, gr.tw, a, s));
+    float2* Mb = gr.M;
+    if (has_ht) {   // rot180(Ht): only its transposed split copy is kept
+        ST(dalloc(p, &Mb, mbytes, "backward transfer matrices (tiles, temporary)"));
+        CK(cudaMemsetAsync(Mb, 0, mbytes, s));
+        R2CArgs ab = r2c_args(SRC_KERNEL, p->psfb, nullptr, 0.f, N2 * nu, Mb, (long long)N2 * nu_pad);
+        ab.cdiv = nu;
+        ab.cmul = nu_pad;
+        CK(launch_r2c(gr.xg, gr.fd, gr.fd, gr.tw, gr.tw, ab, s));
+    }
+    // M (forward) and M^T (backward) split into scaled fp16 hi / lo rows as for FRAMES plans; the tiles' spectra G / R
+    // are the MACs' frames, their |window| bounds the per-tile scales
+    CK(mac_f16_prepare(gr.M, Mb, gr.MT, nkap, N2, nu_pad, p->bpitch, &gr.fwd, &gr.bwd, s));
+    if (Mb != gr.M) {
+        CK(cudaStreamSynchronize(s));
+        cudaFree(Mb);
+        p->bytes -= mbytes;
+    }
+    gr.F = nt <= 8 ? 8 : (nt <= 16 ? 16 : 32);
+    CK(mac_f16_encode_src(&gr.fwd, 1, gr.G, (long long)nkap * nu_pad, gr.F, nt));
+    CK(mac_f16_encode_src(&gr.bwd, 0, gr.R, (long long)nkap * p->bpitch, gr.F, nt));
+    gr.fwd.bmax = gr.tmax;
+    gr.fwd.out = gr.Y;
+    gr.fwd.out_fstride = (long long)nkap * N2;
+    gr.fwd.out_ld = N2;
+    gr.fwd.ksplit = ksplit;
+    gr.fwd.out_sstride = (long long)nt * nkap * N2;
+    gr.bwd.bmax = gr.tmax + 32;
+    gr.bwd.out = gr.Xh;
+    gr.bwd.out_fstride = (long long)nkap * nu_pad;
+    gr.bwd.out_ld = nu_pad;
+    // algorithmic bytes of one projection's MAC (M or M^T of the real units + the tiles' spectra in and out)
+    p->fft_alg_bytes += (double)nkap * N2 * nu * 8.0 + (double)nt * nkap * (nu + N2) * 8.0;
+    return LFM_OK;
 }
 
 }  // namespace
@@ -1511,11 +1631,12 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     std::vector<int> p_alt(nz, 0);   // best direct alternative per plane (1 CUDA-core, 2 tensor-core, 0 none)
     std::vector<AxisBox> box1(nz), box2(nz);
     const int zb = p->nu > 0 ? p->u0 / N2 : 0, ze = p->nu > 0 ? (p->u1 - 1) / N2 : -1;
-    // frequency path on overlap-save tiles (§5.6) when the cost model prefers them: per-unit time and bytes
-    const TileGeom tiles = choose_tiles(g, N2, flags);
-    const double fft_unit_t = tiles.ntile ? tile_unit_cost(tiles, N2) : whole_unit_cost(g, N2);
-    const double fft_unit_m = tiles.ntile ? (double)tiles.L * (tiles.L / 2 + 1) * (N2 + round_up((size_t)N2, 4)) * 8.0
-                                          : (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
+    // frequency path: whole-image transforms, or overlap-save tiles (§5.6) with the window geometry of each plane's own
+    // coarse-tap range (planes with equal ranges share a tile group)
+    std::vector<TileGeom> ptile(nz);
+    std::vector<double> pt_whole(nz, 0.0), pm_whole(nz, 0.0), pt_tile(nz, 0.0), pm_tile(nz, 0.0), pt_dir(nz, 1e30),
+        pt_tc(nz, 1e30);
+    std::vector<int> ptc_ok(nz, 0);
     bool too_big = false;
     for (int z = zb; z <= ze; ++z) {
         int k0 = kh, k1 = -1, j0 = kw, j1 = -1;
@@ -1541,7 +1662,14 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const int D = std::max(box1[z].D, box2[z].D);
         plane_D[z] = D;
         const double units = ue - ub;
-        const double t_fft = units * fft_unit_t;
+        pt_whole[z] = units * whole_unit_cost(g, N2);
+        pm_whole[z] = units * (double)g.nkappa * N2 * sizeof(float2) * (psf_t_host ? 2 : 1);
+        ptile[z] = choose_tiles(g, N2, flags, box1[z].dmin, box1[z].dmax + box1[z].D - 1, box2[z].dmin,
+                                box2[z].dmax + box2[z].D - 1);
+        if (ptile[z].ntile) {
+            pt_tile[z] = units * tile_unit_cost(ptile[z], N2);
+            pm_tile[z] = units * (double)ptile[z].L * (ptile[z].L / 2 + 1) * (N2 + round_up((size_t)N2, 4)) * 8.0;
+        }
         const double t_dir = D <= kDirMaxD ? 2.0 * units * N2 * D * D * (double)g.nh * g.nw * 2.0 / kDirFlops[D] : 1e30;
         // tensor-core direct (kernels_tcdir.cu): per direction, CTA pairs over 256-pixel tiles of the padded grid,
         // every tap x K-step = 3 pair MMAs of Ntile/2 cycles (tcgen05 floor), at the measured efficiency
@@ -1549,9 +1677,10 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         const int Ntile = (int)round_up((size_t)N2, 16);
         const bool tc_ok = !(flags & LFM_PLAN_NO_TC) && Ntile <= 256 && T2 <= 65;
         const double t_tc = tc_ok ? tc_plane_time(box1[z], box2[z], g, N2, p->num_sms) : 1e30;   // whole plane
+        pt_dir[z] = t_dir;
+        pt_tc[z] = t_tc;
+        ptc_ok[z] = tc_ok;
         // device bytes per plane on each path (memory-aware planning below)
-        pt_fft[z] = t_fft;
-        pm_fft[z] = units * fft_unit_m;
         if (tc_ok && t_tc <= t_dir) {
             p_alt[z] = 2;
             pt_alt[z] = t_tc;
@@ -1563,17 +1692,33 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             pt_alt[z] = t_dir;
             pm_alt[z] = 2.0 * units * D * D * N2 * 4 + (double)height * width * 4;
         }
+    }
+    // tiles when every owned plane has a tiling and (LFM_PLAN_TILES, or the tiles beat whole-image transforms by 10 %
+    // over the owned planes)
+    bool use_tiles = zb <= ze;
+    {
+        double sw = 0.0, st = 0.0;
+        for (int z = zb; z <= ze; ++z) {
+            use_tiles &= ptile[z].ntile > 0;
+            sw += pt_whole[z];
+            st += pt_tile[z];
+        }
+        if (use_tiles && !(flags & LFM_PLAN_TILES) && !(st < 0.9 * sw)) use_tiles = false;
+    }
+    for (int z = zb; z <= ze; ++z) {
+        pt_fft[z] = use_tiles ? pt_tile[z] : pt_whole[z];
+        pm_fft[z] = use_tiles ? pm_tile[z] : pm_whole[z];
         int mode = 0;                            // 0 FFT, 1 SIMT direct, 2 tensor-core direct
         if (flags & LFM_PLAN_FFT_ONLY) {
             mode = 0;
         } else if (flags & LFM_PLAN_DIRECT) {
-            mode = (flags & LFM_PLAN_TC_DIRECT) && tc_ok ? 2 : 1;
+            mode = (flags & LFM_PLAN_TC_DIRECT) && ptc_ok[z] ? 2 : 1;
         } else {
-            const double best = std::min(t_fft, std::min(t_dir, t_tc));
-            mode = best == t_fft ? 0 : (best == t_tc ? 2 : 1);
+            const double best = std::min(pt_fft[z], std::min(pt_dir[z], pt_tc[z]));
+            mode = best == pt_fft[z] ? 0 : (best == pt_tc[z] ? 2 : 1);
         }
         plane_direct[z] = mode;
-        if (mode == 1 && D > kDirMaxD) too_big = true;
+        if (mode == 1 && plane_D[z] > kDirMaxD) too_big = true;
     }
     // memory-aware planning: while the frequency-path planes' transfer matrices do not fit, move the plane whose
     // direct alternative costs the least extra time per byte saved
@@ -1614,7 +1759,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
     p->part_moved = 0;
     // (LFM_PLAN_MOVE, dev: force the number of moved planes -- also without partitions, so that a serial profiling
     //  run sees the plane assignment of the partitioned plan)
-    if ((partitions_allowed(flags) || getenv("LFM_PLAN_MOVE")) && !tiles.ntile &&
+    if ((partitions_allowed(flags) || getenv("LFM_PLAN_MOVE")) && !use_tiles &&
         !(flags & (LFM_PLAN_FFT_ONLY | LFM_PLAN_DIRECT | LFM_PLAN_NO_TC))) {
         bool simt = false;
         for (int z = zb; z <= ze; ++z) simt |= plane_direct[z] == 1;
@@ -1774,8 +1919,10 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             // tiled frequency path (§5.6): its MAC (tensor cores, HBM-bound), transforms (SIMT) and the tensor-core
             // direct planes share the SMs in proportion to their modelled whole-GPU times (r02 c3 sweep: the optimum
             // 56 of 148 SMs matches the proportional split, +4 % over one after the other)
-            for (int d = 0; d < 2 && tiles.ntile && t_tc > 0 && units_fft > 0 && nsimt == 0; ++d) {
-                const double t_f = 0.5 * units_fft * fft_unit_t;
+            double t_f = 0.0;   // per direction, the tiled frequency-path planes
+            for (int z = zb; z <= ze; ++z)
+                if (plane_direct[z] == 0) t_f += 0.5 * pt_fft[z];
+            for (int d = 0; d < 2 && use_tiles && t_tc > 0 && units_fft > 0 && nsimt == 0; ++d) {
                 int want = (int)std::lround(p->num_sms * t_tc / (t_tc + t_f) / 8.0) * 8;
                 want = std::max(16, std::min(p->num_sms - 16, want));
                 if (const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F")) want = atoi(ev);   // dev override
@@ -1784,7 +1931,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                             t_tc * 1e3, t_f * 1e3, want);
                 if (want > 0 && green_split(p, dev, want, &p->part[d])) tc_sms[d] = p->part[d].sms_tc;
             }
-            for (int d = 0; d < 2 && !tiles.ntile && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
+            for (int d = 0; d < 2 && !use_tiles && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
                 // the partition's forward MAC keeps four 8-warp CTAs per SM in flight while G[kappa] fits four times in
                 // shared memory; fewer resident CTAs stream proportionally less (c4: 3 CTAs, ~81 GB/s per SM)
                 const double gsm = round_up((size_t)std::max(units_fft, 1.0), 16) * 8.0 + 1024.0;
@@ -1941,40 +2088,47 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
         int maxg = 0;
         for (const DirArgs& dg : p->dgroups) maxg = std::max(maxg, dg.nzd);
         if (maxg > 0) PG(dalloc(p, &p->dpart, (size_t)maxg * HW * sizeof(float), "direct forward partials"));
-        if (p->nu_fft > 0) {
-            // whole-image transforms (Lh x Lw) or, on a tiled plan, tg.L x tg.L windows of tg.ntile tiles (§5.6)
-            int Lh = g.Lh, Lw = g.Lw, nkap = g.nkappa, nt = 1;
-            if (tiles.ntile) {
-                CKG(tile_fft_init());
-                p->tiled = true;
-                p->tg = tiles;
-                Lh = Lw = tiles.L;
-                nkap = Lh * (Lw / 2 + 1);
-                nt = tiles.ntile;
-                xg.Lh = Lh;
-                xg.Lw = Lw;
-                xg.nk2 = Lw / 2 + 1;
-                xg.nkappa = nkap;
-                p->bpitch = (int)round_up((size_t)N2, 4);
+        if (p->nu_fft > 0 && use_tiles) {
+            // §5.6: one tile group per coarse-tap range of the frequency-path planes (z order kept inside a group)
+            CKG(tile_fft_init());
+            p->tiled = true;
+            p->bpitch = (int)round_up((size_t)N2, 4);
+            const std::vector<int>& umap_h = umap;   // the host unit map (the device copy may still be in flight on s)
+            std::vector<int> gz;                 // first plane of each group (its tile geometry)
+            std::vector<std::vector<int>> gunits;
+            for (int t = 0; t < p->nu_fft; ++t) {
+                const int z = (p->u0 + umap_h[t]) / N2;
+                size_t gi = 0;
+                for (; gi < gz.size(); ++gi) {
+                    const TileGeom& a = ptile[gz[gi]];
+                    const TileGeom& b = ptile[z];
+                    if (a.dmin1 == b.dmin1 && a.dmax1 == b.dmax1 && a.dmin2 == b.dmin2 && a.dmax2 == b.dmax2) break;
+                }
+                if (gi == gz.size()) {
+                    gz.push_back(z);
+                    gunits.emplace_back();
+                }
+                gunits[gi].push_back(umap_h[t]);
             }
+            p->tgs.resize(gz.size());
+            for (size_t gi = 0; gi < gz.size(); ++gi)
+                PG(build_tile_group(p, p->tgs[gi], ptile[gz[gi]], gunits[gi], xg, psf_t_host != nullptr, s));
+        } else if (p->nu_fft > 0) {
+            // whole-image transforms (Lh x Lw)
+            const int Lh = g.Lh, Lw = g.Lw, nkap = g.nkappa;
             if (!fft_factor(Lh, &p->fh) || !fft_factor(Lw, &p->fw))
                 return guard(fail(LFM_EUNSUPPORTED, "coarse transform sizes %dx%d are not 5-smooth", Lh, Lw));
             PG(twiddles(Lh, &p->tw_h, p, s));
             PG(twiddles(Lw, &p->tw_w, p, s));
             const size_t mbytes = (size_t)nkap * N2 * p->nu_fft_pad * sizeof(float2);
-            const size_t rpitch = p->tiled ? p->bpitch : N2;
             p->transfer_bytes += mbytes;
             PG(dalloc(p, &p->M, mbytes, "transfer matrices"));
-            PG(dalloc(p, &p->G, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "G spectra"));
-            PG(dalloc(p, &p->Xh, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
-            // tiled forward MAC: K split so that every SM gets >= 16 (kappa, half, split) items (load balance); the
-            // partial spectra are summed in split order by the C2R
-            const int ksplit = tiles.ntile ? std::max(1, std::min(8, (16 * p->num_sms + 2 * nkap - 1) / (2 * nkap))) : 1;
-            PG(dalloc(p, &p->Y, (size_t)ksplit * nt * nkap * N2 * sizeof(float2), "Y spectra"));
-            PG(dalloc(p, &p->R, (size_t)nt * nkap * rpitch * sizeof(float2), "R spectra"));
+            PG(dalloc(p, &p->G, (size_t)nkap * p->nu_fft_pad * sizeof(float2), "G spectra"));
+            PG(dalloc(p, &p->Xh, (size_t)nkap * p->nu_fft_pad * sizeof(float2), "Xh spectra"));
+            PG(dalloc(p, &p->Y, (size_t)nkap * N2 * sizeof(float2), "Y spectra"));
+            PG(dalloc(p, &p->R, (size_t)nkap * N2 * sizeof(float2), "R spectra"));
             CKG(cudaMemsetAsync(p->M, 0, mbytes, s));      // padding columns stay zero
-            CKG(cudaMemsetAsync(p->G, 0, (size_t)nt * nkap * p->nu_fft_pad * sizeof(float2), s));
-            CKG(cudaMemsetAsync(p->R, 0, (size_t)nt * nkap * rpitch * sizeof(float2), s));
+            CKG(cudaMemsetAsync(p->G, 0, (size_t)nkap * p->nu_fft_pad * sizeof(float2), s));
             // K1: transfer matrices M[kappa][b'][t] = DFT_{Lh x Lw}(g_{u(t),b'}), g_{u,b'}[d] = h_u[b' - a + c + N d]
             R2CArgs a = r2c_args(SRC_KERNEL, p->psf, nullptr, 0.f, N2 * p->nu_fft, p->M, (long long)N2 * p->nu_fft_pad);
             a.cdiv = p->nu_fft;
@@ -1990,35 +2144,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 ab.cmul = p->nu_fft_pad;
                 CKG(launch_r2c(xg, p->fh, p->fw, p->tw_h, p->tw_w, ab, s));
             }
-            if (p->tiled) {
-                // M (forward) and M^T (backward) split into scaled fp16 hi / lo rows as for FRAMES plans; the tiles'
-                // spectra G / R are the MACs' frames, their |window| bounds the per-tile scales
-                const size_t mtb = (size_t)nkap * p->nu_fft_pad * p->bpitch * sizeof(float2);
-                PG(dalloc(p, &p->MT, mtb, "transposed transfer matrices (tiles)"));
-                p->transfer_bytes += mtb;
-                PG(dalloc(p, &p->tmax, 64 * sizeof(unsigned), "tile scale bounds"));
-                CKG(cudaMemsetAsync(p->tmax, 0, 64 * sizeof(unsigned), s));
-                CKG(mac_f16_prepare(p->M, p->Mb, p->MT, nkap, N2, p->nu_fft_pad, p->bpitch, &p->mf_fwd, &p->mf_bwd, s));
-                if (p->Mb != p->M) {
-                    cudaFree(p->Mb);
-                    p->bytes -= mbytes;
-                    p->transfer_bytes -= mbytes;
-                }
-                p->Mb = nullptr;
-                p->mf_tF = nt <= 8 ? 8 : (nt <= 16 ? 16 : 32);
-                CKG(mac_f16_encode_src(&p->mf_fwd, 1, p->G, (long long)nkap * p->nu_fft_pad, p->mf_tF, nt));
-                CKG(mac_f16_encode_src(&p->mf_bwd, 0, p->R, (long long)nkap * p->bpitch, p->mf_tF, nt));
-                p->mf_fwd.bmax = p->tmax;
-                p->mf_fwd.out = p->Y;
-                p->mf_fwd.out_fstride = (long long)nkap * N2;
-                p->mf_fwd.out_ld = N2;
-                p->mf_fwd.ksplit = ksplit;
-                p->mf_fwd.out_sstride = (long long)nt * nkap * N2;
-                p->mf_bwd.bmax = p->tmax + 32;
-                p->mf_bwd.out = p->Xh;
-                p->mf_bwd.out_fstride = (long long)nkap * p->nu_fft_pad;
-                p->mf_bwd.out_ld = p->nu_fft_pad;
-            }
+            p->fft_alg_bytes = (double)g.nkappa * N2 * p->nu_fft * 8.0 + (double)g.nkappa * (p->nu_fft + N2) * 8.0;
         }
         CKG(cudaStreamSynchronize(s));
         if (p->psfb != p->psf) {
@@ -2117,14 +2243,17 @@ lfm_status lfm_plan_info(lfm_plan p, lfm_info* info) {
     info->width = p->geo.W;
     info->unit_begin = p->u0;
     info->unit_end = p->u1;
-    info->fft_h = p->tiled ? p->tg.L : p->geo.Lh;
-    info->fft_w = p->tiled ? p->tg.L : p->geo.Lw;
+    const lfm_plan_s::TileGroup* g0 = p->tiled ? &p->tgs[0] : nullptr;   // (tiled plans: the first group)
+    info->fft_h = g0 ? g0->tg.L : p->geo.Lh;
+    info->fft_w = g0 ? g0->tg.L : p->geo.Lw;
     info->lc_min_h = p->geo.lcmin_h;
     info->lc_min_w = p->geo.lcmin_w;
-    info->n_kappa = p->tiled ? p->xg.nkappa : p->geo.nkappa;
-    info->tiles = p->tiled ? p->tg.ntile : 0;
-    info->tile_T1 = p->tiled ? p->tg.T1 : 0;
-    info->tile_T2 = p->tiled ? p->tg.T2 : 0;
+    info->n_kappa = g0 ? g0->xg.nkappa : p->geo.nkappa;
+    info->tiles = g0 ? g0->tg.ntile : 0;
+    info->tile_T1 = g0 ? g0->tg.T1 : 0;
+    info->tile_T2 = g0 ? g0->tg.T2 : 0;
+    info->tile_groups = (int)p->tgs.size();
+    info->fft_bytes = p->fft_alg_bytes;
     info->units_padded = p->nu_fft_pad;
     info->x_s = p->region.xs;
     info->y_s = p->region.ys;

@@ -84,6 +84,7 @@ struct C2RArgs {
     long long cmul;         //   tile * cmul + item of in[kappa * in_ld + .]
     int nsum;               //   summed over nsum partial inputs in_sstride apart (split-K MAC outputs; 0 / 1: one)
     long long in_sstride;
+    int accum;              //   DST_IMAGE: add onto out instead of writing it (tile groups after the first)
 };
 
 // overlap-save tiles of the coarse grid: a square transform of L points per axis serves T1 x T2

@@ -66,7 +66,8 @@ class lfm_info(ctypes.Structure):
                 ("tc_planes", ctypes.c_int), ("tc_flops_executed", ctypes.c_double), ("tc_flops_algorithmic", ctypes.c_double),
                 ("planes_moved_for_memory", ctypes.c_int), ("partition_sms", (ctypes.c_int * 2) * 2),
                 ("c1_mode", ctypes.c_int), ("tc_moved_to_fft", ctypes.c_int), ("tiles", ctypes.c_int),
-                ("tile_T1", ctypes.c_int), ("tile_T2", ctypes.c_int)]
+                ("tile_T1", ctypes.c_int), ("tile_T2", ctypes.c_int), ("tile_groups", ctypes.c_int),
+                ("fft_bytes", ctypes.c_double)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

@@ -139,14 +139,15 @@ def test_memory_aware_planning():
     h[2:, :, :, c - 5:c + 6, c - 5:c + 6] = rng.uniform(0, 1, (2, N, N, 11, 11))
     h /= h.sum(axis=(3, 4), keepdims=True)
     x = rng.uniform(0, 1, (4, H, W)).astype(np.float32)
+    nt = L_.LFM_PLAN_NO_TILES   # whole-image transfer matrices (the estimate's model; tiles need far less memory)
     try:
-        with L_.Plan(h, N, H, W, optics=optics(N)) as free:
+        with L_.Plan(h, N, H, W, optics=optics(N), flags=nt) as free:
             assert free.info()["fft_units"] > 0
-        with L_.Plan(h, N, H, W, optics=optics(N), flags=L_.LFM_PLAN_FFT_ONLY) as full:
+        with L_.Plan(h, N, H, W, optics=optics(N), flags=L_.LFM_PLAN_FFT_ONLY | nt) as full:
             m_all = full.info()["transfer_bytes"]
         est, _ = L_.lfm_plan_estimate(N, 4, K, K, H, W)   # all-frequency-path estimate: transfer + the rest
         L_.lfm_set_memory_limit(int(est - m_all + 0.45 * m_all))   # fits only after moving the wide planes
-        with L_.Plan(h, N, H, W, optics=optics(N)) as plan:
+        with L_.Plan(h, N, H, W, optics=optics(N), flags=nt) as plan:
             info = plan.info()
             assert info["planes_moved_for_memory"] > 0
             tol = op_tol(info)[0]
