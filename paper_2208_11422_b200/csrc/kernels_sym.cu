@@ -135,6 +135,7 @@ lfm_status sym_create(ncclComm_t comm, size_t n, int want_multimem, SymState** o
         return LFM_ENCCL;
     }
     cudaMemset(st->buf, 0, st->bytes);
+    cudaDeviceSynchronize();   // the plan's streams may be non-blocking: the zeroed window must be visible to them
     *out = st;
     return LFM_OK;
 }
