@@ -889,3 +889,44 @@ def test_frames_plan_with_supplied_ht():
         assert rb["best_iter"][f] == r1["best_iter"]
         np.testing.assert_allclose(rb["series"][f], r1["series"], rtol=1e-5)
         assert rel(xb[f].cpu().numpy(), x1.astype(np.float64)) <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [4, 2048], ids=["fft", "frames"])
+def test_whole_image_75_point_transforms(flags):
+    """Whole-image coarse transforms of 75 points (the c3 / c5 size, kernels_fft_fast.cu) at a small geometry: N = 3,
+    213 x 213 (71 coarse pixels, kernel 13: alias-free minimum 73 -> 75).  Operators against the oracle (fft plan) and
+    batched RL frames against the oracle's iterations (frames plan)."""
+    h, x, r = rand_case(75, 2, 3, 213, 213, 13, 13)
+    hd = h.astype(np.float64)
+    if flags == 4:
+        with L().Plan(h, 3, 213, 213, optics=optics(3), flags=4 | L().LFM_PLAN_NO_TILES) as plan:
+            assert plan.info()["fft_h"] == 75 and plan.info()["tiles"] == 0
+            y_d = torch.zeros((213, 213), device="cuda")
+            plan.forward(dev(x), y_d)
+            xb_d = torch.zeros((2, 213, 213), device="cuda")
+            plan.backward(dev(r), xb_d)
+            nrm_d = torch.zeros((2, 213, 213), device="cuda")
+            plan.normalizer(nrm_d)
+            torch.cuda.synchronize()
+        for got, ref in [(y_d, O.forward_project(x.astype(np.float64), hd)),
+                         (xb_d, O.backward_project(r.astype(np.float64), hd)),
+                         (nrm_d, O.compute_normalizer(hd, 213, 213))]:
+            g = got.cpu().numpy()
+            assert rel(g, ref) <= 2e-6, rel(g, ref)
+            assert np.abs(g - ref).max() <= 1e-5 * np.abs(ref).max()
+        return
+    rng = np.random.default_rng(76)
+    F = 8
+    ys = [np.maximum(O.forward_project(rng.uniform(0, 1, (2, 213, 213)), hd), 0.0) + 1.0 for _ in range(F)]
+    opt = O.Optics(nnum=3, **OPTICS)
+    with L().Plan(h, 3, 213, 213, optics=optics(3), flags=L().LFM_PLAN_FRAMES) as plan:
+        assert plan.info()["fft_h"] == 75
+        xb = torch.zeros((F, 2, 213, 213), device="cuda")
+        rb = plan.rl_iterate_batch(dev(np.stack(ys).astype(np.float32)), xb, L().make_policy(mode="fixed", n_iters=2))
+        torch.cuda.synchronize()
+    for f in (0, F - 1):
+        ref = O.deconvolve(ys[f], hd, opt, O.Policy(mode="fixed", n_iters=2), keep_iterates=True)
+        got = xb[f].cpu().numpy()
+        assert rel(got, ref.iterates[rb["best_iter"][f] - 1]) <= 1e-4
+        np.testing.assert_allclose(rb["series"][f], ref.series, rtol=1e-4)
