@@ -195,3 +195,61 @@ def test_tiled_plan_batches_frame_by_frame():
             assert (rb["best_iter"][f], rb["stop_iter"][f]) == (r1["best_iter"], r1["stop_iter"])
             assert np.array_equal(np.asarray(rb["series"][f]), np.asarray(r1["series"]))
             assert torch.equal(xb[f], x1)
+
+
+def test_tiled_virtual_shards():
+    """Depth / phase sharding on tiled plans: NO_COMM plans of rank r / world own contiguous unit ranges (a
+    rank may hold part of a plane: its tile groups hold only its units); partial forwards sum to the oracle's forward,
+    the backwards cover disjoint units."""
+    h, x, r = rand_case(98, 3, 3, 99, 99, 9, 9)
+    h[2] = 0.0
+    h[2, :, :, 3:6, 3:6] = np.random.default_rng(99).uniform(0, 1, (3, 3, 3, 3))   # a narrower plane: 2 tile groups
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    hd = h.astype(np.float64)
+    y_ref = O.forward_project(x.astype(np.float64), hd)
+    xb_ref = O.backward_project(r.astype(np.float64), hd)
+    for world in (2, 3):
+        tot = np.zeros_like(y_ref)
+        cover = np.zeros((3, 99, 99))
+        xb_acc = np.zeros_like(xb_ref)
+        for rank in range(world):
+            with L().Plan(h, 3, 99, 99, rank=rank, world=world,
+                          flags=L().LFM_PLAN_NO_COMM | L().LFM_PLAN_TILES | L().LFM_PLAN_FFT_ONLY) as plan:
+                assert plan.info()["tiles"] >= 2
+                y_d = torch.zeros((99, 99), device="cuda")
+                plan.forward(dev(x), y_d)
+                xb_d = torch.full((3, 99, 99), -1.0, device="cuda")
+                plan.backward(dev(r), xb_d)
+                torch.cuda.synchronize()
+                tot += y_d.cpu().numpy()
+                xb = xb_d.cpu().numpy()
+                own = xb != -1.0
+                cover += own
+                xb_acc[own] = xb[own]
+        assert rel(tot, y_ref) <= 1e-5
+        assert (cover == 1).all()
+        assert rel(xb_acc, xb_ref) <= 1e-5
+
+
+def test_tiled_isra_and_groups():
+    """ISRA (f3) on a tiled plan whose planes need two window geometries (tile groups): 1 and 5 iterations against
+    the oracle's ISRA."""
+    h, _, _ = rand_case(100, 3, 3, 99, 99, 9, 9)
+    h[0] = 0.0
+    h[0, :, :, 3:6, 3:6] = np.random.default_rng(101).uniform(0, 1, (3, 3, 3, 3))
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    hd = h.astype(np.float64)
+    y = O.forward_project(np.random.default_rng(102).uniform(0, 1, (3, 99, 99)), hd) + 0.5
+    opt = O.Optics(nnum=3, **OPTICS)
+    with L().Plan(h, 3, 99, 99, optics=L().make_optics(**OPTICS),
+                  flags=L().LFM_PLAN_TILES | L().LFM_PLAN_FFT_ONLY) as plan:
+        info = plan.info()
+        assert info["tile_groups"] == 2, info
+        for n, tol in [(1, 1e-4), (5, 1e-3)]:
+            ref = O.deconvolve(y, hd, opt, O.Policy(mode="fixed", n_iters=n), update="isra", keep_iterates=True)
+            x_d = torch.zeros((3, 99, 99), device="cuda")
+            res = plan.rl_iterate(dev(y), x_d, L().make_policy(mode="fixed", n_iters=n, update="isra"))
+            torch.cuda.synchronize()
+            assert res["best_iter"] == ref.best_iter
+            assert rel(x_d.cpu().numpy(), ref.iterates[res["best_iter"] - 1]) <= tol
+            np.testing.assert_allclose(res["series"], ref.series, rtol=1e-4)
