@@ -282,10 +282,10 @@ lfm_status lfm_rl_iterate_batch(lfm_plan plan, int frames, const float* y, float
                                 int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
 /* End-to-end call with HOST buffers: copies y in (H2D), runs lfm_rl_iterate, copies the argmax-E
- * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best).
- * When x_host is page-locked (cudaHostAlloc / pinned) and the plan has a single rank, every improving iterate is
- * copied into x_host on a side stream while the next iteration runs, so x_host holds intermediate iterates during
- * the call and x_best when it returns (no final copy); pageable memory gets the single final copy. */
+ * volume out (D2H, once, after the loop).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best).
+ * (Developer switch LFM_HOST_MIRROR, single rank, page-locked x_host: every improving iterate is copied into x_host
+ * on a side stream while the next iteration runs, skipping iterates while the previous copy is on the link --
+ * measured slower at c3 than the single final copy: the copies take HBM bandwidth from the iteration.) */
 lfm_status lfm_deconvolve_host(lfm_plan plan, const float* y_host, float* x_host, const lfm_policy* policy,
                                int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
@@ -314,6 +314,8 @@ typedef struct {
                                          partition) that runs them: tcgen05 forward, forward MAC, tcgen05
                                          backward (+ its update), backward MAC                           */
     long long kern_count[4];
+    long long d2h_bytes;              /* device -> host bytes of lfm_rl_iterate / lfm_deconvolve_host so far: the
+                                         8-byte E_k reads, the argmax mirror copies and final volume copies      */
 } lfm_profile_t;
 
 /* enable != 0 turns per-stage event timing on.  Counters keep accumulating until read with reset. */

@@ -282,6 +282,7 @@ struct lfm_plan_s {
     // next iteration runs, so the call returns without a final 0.2-1.7 GB device-to-host copy
     cudaStream_t scopy = nullptr;
     cudaEvent_t evconv[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t evcopy = nullptr;   // end of the last mirror copy (a new one is skipped while it is in flight)
     // CUDA-graph replay of one iteration (LFM_PLAN_GRAPHS): one graph per (cur, next) buffer pair,
     // keyed also by the measurement pointer and the policy scalars baked into the captured launches
     bool graphs = false;
@@ -537,6 +538,7 @@ void plan_free(lfm_plan p) {
     if (p->host) cudaFreeHost(p->host);
     green_free(p);
     if (p->scopy) cudaStreamDestroy(p->scopy);
+    if (p->evcopy) cudaEventDestroy(p->evcopy);
     for (cudaEvent_t e : p->evconv)
         if (e) cudaEventDestroy(e);
     if (p->ev0) cudaEventDestroy(p->ev0);
@@ -2396,6 +2398,7 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
     if (mirror && !p->scopy) {
         CK(cudaStreamCreateWithFlags(&p->scopy, cudaStreamNonBlocking));
         for (auto& e : p->evconv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->evcopy, cudaEventDisableTiming));
     }
     // every exit path (errors included) drains the side stream first: no queued conversion or copy into the
     // caller's x / host_mirror may run after this call has returned (lfm.h: nothing is written after a failure)
@@ -2424,6 +2427,7 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
             ST(op_step(p, y, p->xb[cur], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty));
             CK(cudaMemcpyAsync(p->host, p->met.out, sizeof(double), cudaMemcpyDeviceToHost, s));
         }
+        p->pacc.d2h_bytes += sizeof(double);
         if (ms_host) CK(cudaEventRecord(p->ev1, s));
         CK(cudaStreamSynchronize(s));
         const double e = p->host[0];
@@ -2453,12 +2457,27 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
             best_e = e;
             best_k = k;
             best = nxt;
-            if (mirror) {   // iteration k is complete (synchronised above): convert + copy it on the side stream
+            // iteration k is complete (synchronised above): convert + copy it on the side stream -- unless the previous
+            // mirror copy is still in flight (the host link is slower than an iteration): then this iterate is skipped
+            // and a later one (or the final copy after the loop) brings x_best
+            bool link_busy = false;
+            if (mirror && mirrored_buf >= 0) {
+                const cudaError_t q = cudaEventQuery(p->evcopy);
+                if (q == cudaErrorNotReady) {
+                    link_busy = true;
+                    cudaGetLastError();   // (not an error)
+                } else if (q != cudaSuccess) {
+                    return fail(LFM_ECUDA, "mirror copy: %s", cudaGetErrorString(q));
+                }
+            }
+            if (mirror && !link_busy) {
                 ST(gather_to_image(p, p->xb[nxt], x, p->scopy));
                 CK(cudaEventRecord(p->evconv[nxt], p->scopy));
                 conv_pending[nxt] = true;
                 CK(cudaMemcpyAsync(host_mirror, x, (size_t)p->geo.nz * p->geo.H * p->geo.W * sizeof(float),
                                    cudaMemcpyDeviceToHost, p->scopy));
+                CK(cudaEventRecord(p->evcopy, p->scopy));
+                p->pacc.d2h_bytes += (long long)p->geo.nz * p->geo.H * p->geo.W * sizeof(float);
                 mirrored_buf = nxt;
                 p->pacc.launches += 1;
             }
@@ -2505,8 +2524,11 @@ lfm_status lfm_deconvolve_host(lfm_plan p, const float* y_host, float* x_host, c
     cudaGetLastError();   // clear a possible error of the query
     bool mirrored = false;
     ST(rl_loop(p, p->y_stage, p->x_stage, pol, best_iter, stop_iter, series_host, ms_host, s,
-               (p->dloop || !pinned) ? nullptr : x_host, &mirrored));
-    if (!mirrored) CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
+               (p->dloop || !pinned || !getenv("LFM_HOST_MIRROR")) ? nullptr : x_host, &mirrored));
+    if (!mirrored) {
+        CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
+        p->pacc.d2h_bytes += (long long)V * sizeof(float);
+    }
     CK(cudaStreamSynchronize(s));
     return LFM_OK;
 }

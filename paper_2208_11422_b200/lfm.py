@@ -122,7 +122,7 @@ LFM_N_STAGES = 11
 class lfm_profile_t(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * LFM_N_STAGES), ("count", ctypes.c_longlong * LFM_N_STAGES),
                 ("launches", ctypes.c_longlong), ("iterations", ctypes.c_longlong),
-                ("kern_ms", ctypes.c_double * 4), ("kern_count", ctypes.c_longlong * 4)]
+                ("kern_ms", ctypes.c_double * 4), ("kern_count", ctypes.c_longlong * 4), ("d2h_bytes", ctypes.c_longlong)]
 
 KERNEL_NAMES = ["tc_fwd", "mac_fwd", "tc_bwd", "mac_bwd"]
 
@@ -393,7 +393,7 @@ class Plan:
                     count={STAGE_NAMES[i]: pr.count[i] for i in range(LFM_N_STAGES)},
                     launches=pr.launches, iterations=pr.iterations,
                     kern_ms={KERNEL_NAMES[i]: pr.kern_ms[i] for i in range(4)},
-                    kern_count={KERNEL_NAMES[i]: pr.kern_count[i] for i in range(4)})
+                    kern_count={KERNEL_NAMES[i]: pr.kern_count[i] for i in range(4)}, d2h_bytes=pr.d2h_bytes)
 
     def quality(self, x, region=LFM_REGION_TRIANGLE, stream=None):
         _check_dev(x, (self.nz, self.height, self.width), "x")

@@ -779,11 +779,14 @@ def test_tc_column_ranges_bit_identical(name, flags, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mirror", [0, 1], ids=["final-copy", "mirror"])
 @pytest.mark.parametrize("name,mode", [("tiny", "auto"), ("c2", "auto"), ("s15", "fixed")])
-def test_host_call_pinned_mirror(name, mode):
-    """lfm_deconvolve_host into page-locked memory: each improving iterate is converted and copied to the host on a
-    side stream while the next iteration runs, and the call skips its final copy.  The returned volume, series and
-    stop / best iterations equal the device call's."""
+def test_host_call_pinned_mirror(name, mode, mirror, monkeypatch):
+    """lfm_deconvolve_host into page-locked memory, with the single final copy (default) and with LFM_HOST_MIRROR
+    (improving iterates converted and copied on a side stream while the next iteration runs; the call then skips its
+    final copy).  The returned volume, series and stop / best iterations equal the device call's."""
+    if mirror:
+        monkeypatch.setenv("LFM_HOST_MIRROR", "1")
     cfg, h, hd, y = tiny_problem(name, 5)
     pol = L().make_policy(mode=mode, max_iters=30, n_iters=6)
     with L().Plan(h, cfg.nnum, cfg.height, cfg.width, optics=optics(cfg.nnum)) as plan:
