@@ -276,13 +276,17 @@ struct lfm_plan_s {
     unsigned* mproj = nullptr;
     double* partials = nullptr; // 3 * kParts
     double* stats = nullptr;    // 3
-    double* host = nullptr;     // pinned 8 doubles
+    double* host = nullptr;     // pinned 16 doubles (8, 9: the pipelined fixed loop's E_k slots)
     float *y_stage = nullptr, *x_stage = nullptr;   // lfm_deconvolve_host staging
     // lfm_deconvolve_host: every improving iterate is converted and copied to the host on a side stream while the
     // next iteration runs, so the call returns without a final 0.2-1.7 GB device-to-host copy
     cudaStream_t scopy = nullptr;
     cudaEvent_t evconv[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t evcopy = nullptr;   // end of the last mirror copy (a new one is skipped while it is in flight)
+    // fixed-iteration host loop pipelined one iteration deep: the max-projection and the metric of iteration k run on
+    // stream smet while iteration k + 1 runs on the caller's stream (rl_loop)
+    cudaStream_t smet = nullptr;
+    cudaEvent_t evupd[2] = {nullptr, nullptr}, evmet[2] = {nullptr, nullptr};
     // CUDA-graph replay of one iteration (LFM_PLAN_GRAPHS): one graph per (cur, next) buffer pair,
     // keyed also by the measurement pointer and the policy scalars baked into the captured launches
     bool graphs = false;
@@ -539,6 +543,9 @@ void plan_free(lfm_plan p) {
     green_free(p);
     if (p->scopy) cudaStreamDestroy(p->scopy);
     if (p->evcopy) cudaEventDestroy(p->evcopy);
+    if (p->smet) cudaStreamDestroy(p->smet);
+    for (cudaEvent_t e : {p->evupd[0], p->evupd[1], p->evmet[0], p->evmet[1]})
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->evconv)
         if (e) cudaEventDestroy(e);
     if (p->ev0) cudaEventDestroy(p->ev0);
@@ -836,17 +843,23 @@ lfm_status op_metric(lfm_plan p, int region, cudaStream_t s) {
 // one iteration on polyphase volumes, then the z max-projection and (optionally) the metric -> met.out[0]
 //   RL   (C1): xn = xc * H^T(y/(max(H xc,0)+eps)) / max(H^T 1, eps)
 //   ISRA (f3): xn = xc * H^T y / max(H^T H xc, eps)           (hty = H^T y, polyphase)
+// a7 z max-projection of the new iterate, every pixel written (into the symmetric window's slot 1 when C2
+// runs there), and optionally the metric (a8)
+lfm_status op_tail(lfm_plan p, const float* xn, int region, bool metric, cudaStream_t s) {
+    CK(launch_max_project_poly(xn, p->sym ? reinterpret_cast<unsigned*>(sym_buffer(p->sym, 1)) : p->mproj, p->xall, s));
+    p->pacc.launches += 1;
+    if (metric) ST(op_metric(p, region, s));
+    return LFM_OK;
+}
+
 lfm_status op_step(lfm_plan p, const float* y, const float* xc, float* xn, float eps, int region, bool metric,
-                   cudaStream_t s, int update = LFM_UPDATE_RL, const float* hty = nullptr) {
+                   cudaStream_t s, int update = LFM_UPDATE_RL, const float* hty = nullptr, bool tail = true) {
     ST(op_forward_poly(p, xc, p->yhat, s));
     if (update == LFM_UPDATE_ISRA)
         ST(op_backward(p, SRC_IMAGE2D, p->yhat, nullptr, eps, DST_ISRA, xn, xc, s, hty));
     else
         ST(op_backward(p, SRC_RATIO, y, p->yhat, eps, DST_UPDATE, xn, xc, s));
-    // a7: z max-projection, every pixel written (into the symmetric window's slot 1 when C2 runs there)
-    CK(launch_max_project_poly(xn, p->sym ? reinterpret_cast<unsigned*>(sym_buffer(p->sym, 1)) : p->mproj, p->xall, s));
-    p->pacc.launches += 1;
-    if (metric) ST(op_metric(p, region, s));
+    if (tail) ST(op_tail(p, xn, region, metric, s));
     return LFM_OK;
 }
 
@@ -2392,6 +2405,64 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
         CK(cudaStreamSynchronize(s));
         *best_iter = hs.best_k;
         *stop_iter = hs.k;
+        return LFM_OK;
+    }
+    // fixed-iteration mode, one rank, no graphs / profiling / mirror: pipeline the host loop one iteration deep.
+    // Iteration k + 1 is issued before E_k is read; its output buffer avoids x_k's and best_{k-1}'s, so whichever of
+    // them E_k makes the argmax survives (three volume buffers suffice).  The max-projection and the metric of
+    // iteration k run on p->smet beside iteration k + 1 (they only read x_k, which iteration k + 1 also only reads,
+    // and x_k's buffer is rewritten at k + 2 at the earliest, after E_k -- hence its max-projection -- was waited for).
+    static const bool no_pipe = getenv("LFM_NO_PIPELINE") != nullptr;   // dev A/B
+    if (pol->mode == LFM_MODE_FIXED && !p->graphs && !p->prof && !p->comm && !host_mirror && !no_pipe) {
+        if (!p->smet) {
+            CK(cudaStreamCreateWithFlags(&p->smet, cudaStreamNonBlocking));
+            for (auto* e : {&p->evupd[0], &p->evupd[1], &p->evmet[0], &p->evmet[1]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        double best_e = -INFINITY;
+        int best_k = 0, xk = cur;   // xk: the buffer of the newest iterate
+        auto take = [&](int kk, int buf) -> lfm_status {   // E_kk of the iterate in buf: argmax bookkeeping
+            CK(cudaEventSynchronize(p->evmet[kk & 1]));
+            const double e = p->host[8 + (kk & 1)];
+            series_host[kk - 1] = e;
+            p->pacc.iterations += 1;
+            if (e > best_e) {
+                best_e = e;
+                best_k = kk;
+                best = buf;
+            }
+            return LFM_OK;
+        };
+        if (ms_host) CK(cudaEventRecord(p->ev0, s));
+        int prev_buf = -1;
+        for (int kk = 1; kk <= pol->n_iters; ++kk) {
+            int nxt = 0;
+            while (nxt == xk || nxt == best) ++nxt;
+            ST(op_step(p, y, p->xb[xk], p->xb[nxt], pol->eps, pol->region, true, s, pol->update, p->hty, false));
+            CK(cudaEventRecord(p->evupd[kk & 1], s));
+            CK(cudaStreamWaitEvent(p->smet, p->evupd[kk & 1], 0));
+            ST(op_tail(p, p->xb[nxt], pol->region, true, p->smet));
+            CK(cudaMemcpyAsync(p->host + 8 + (kk & 1), p->met.out, sizeof(double), cudaMemcpyDeviceToHost, p->smet));
+            CK(cudaEventRecord(p->evmet[kk & 1], p->smet));
+            p->pacc.d2h_bytes += sizeof(double);
+            if (kk > 1) ST(take(kk - 1, prev_buf));
+            prev_buf = nxt;
+            xk = nxt;
+        }
+        ST(take(pol->n_iters, prev_buf));
+        CK(cudaStreamWaitEvent(s, p->evmet[pol->n_iters & 1], 0));   // the caller's stream sees the whole loop
+        if (ms_host) {
+            CK(cudaEventRecord(p->ev1, s));
+            CK(cudaEventSynchronize(p->ev1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            for (int i = 0; i < pol->n_iters; ++i) ms_host[i] = ms / pol->n_iters;   // per-iteration average
+        }
+        if (best < 0) best = xk;
+        ST(gather_to_image(p, p->xb[best], x, s));
+        CK(cudaStreamSynchronize(s));
+        *best_iter = best_k;
+        *stop_iter = pol->n_iters;
         return LFM_OK;
     }
     const bool mirror = host_mirror && !p->comm;
