@@ -191,6 +191,16 @@ lfm_status lfm_comm_unique_id(unsigned char* id_out);
 lfm_status lfm_partition_model(double t_tc_ms, double mac_bytes, int direction, int num_sms, double mac_rate_scale,
                                int* tc_sms, double* predicted_ms);
 
+/* Host-only: the overlap-save tiling the planner picks for frequency-path planes of an nnum-phase
+ * height x width image whose coarse taps lie in [d1a, d1b] x [d2a, d2b] (flags: LFM_PLAN_NO_TILES etc. as for
+ * lfm_plan_create).  *L = window size (0: no tiling possible: fewer than 2 or more than 32 tiles for every compiled
+ * window size), *T1 x *T2 = valid outputs per window, *ntile = tiles; *cost_unit (nullable) = the cost model's
+ * seconds per frequency-path unit and iteration (both projections) on these tiles, *cost_whole (nullable) = the
+ * same on whole-image transforms of the alias-free size for a kernel of side kh = kw = nnum * (2 max(|d|) + 1).
+ * LFM_EINVAL for nnum < 1, image sides not multiples of nnum, or d1a > d1b / d2a > d2b. */
+lfm_status lfm_tile_model(int nnum, int height, int width, int d1a, int d1b, int d2a, int d2b, int flags, int* L,
+                          int* T1, int* T2, int* ntile, double* cost_unit, double* cost_whole);
+
 /* Host-only: the contiguous unit range [*unit_begin, *unit_end) that `rank` of `world` owns among the
  * nz*N*N units (z-major u = z*N*N + a*N + b); the first (nu mod world) ranks own one extra unit
  * (S:334's even split, refined from planes to (z,a) units). */

@@ -1427,6 +1427,24 @@ lfm_status lfm_partition_model(double t_tc_ms, double mac_bytes, int direction, 
     return LFM_OK;
 }
 
+lfm_status lfm_tile_model(int nnum, int height, int width, int d1a, int d1b, int d2a, int d2b, int flags, int* L,
+                          int* T1, int* T2, int* ntile, double* cost_unit, double* cost_whole) {
+    g_err[0] = 0;
+    if (!L || !T1 || !T2 || !ntile) return fail(LFM_EINVAL, "NULL argument");
+    if (d1a > d1b || d2a > d2b) return fail(LFM_EINVAL, "tap ranges [%d, %d] x [%d, %d]", d1a, d1b, d2a, d2b);
+    const int r = std::max(std::max(-d1a, d1b), std::max(-d2a, d2b));
+    Geo g;
+    ST(make_geo(nnum, 1, nnum * (2 * r + 1), nnum * (2 * r + 1), height, width, false, &g));
+    const TileGeom t = choose_tiles(g, nnum * nnum, flags, d1a, d1b, d2a, d2b);
+    *L = t.ntile ? t.L : 0;
+    *T1 = t.ntile ? t.T1 : 0;
+    *T2 = t.ntile ? t.T2 : 0;
+    *ntile = t.ntile;
+    if (cost_unit) *cost_unit = t.ntile ? tile_unit_cost(t, nnum * nnum) : 0.0;
+    if (cost_whole) *cost_whole = whole_unit_cost(g, nnum * nnum);
+    return LFM_OK;
+}
+
 lfm_status lfm_shard_units(int nz, int nnum, int world, int rank, int* unit_begin, int* unit_end) {
     g_err[0] = 0;
     if (!unit_begin || !unit_end) return fail(LFM_EINVAL, "NULL argument");

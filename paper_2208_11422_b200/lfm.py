@@ -94,6 +94,7 @@ _lib_last_error = _sig("lfm_last_error", ctypes.c_char_p, [])
 _lib_version = _sig("lfm_version", ctypes.c_char_p, [])
 _lib_shard_units = _sig("lfm_shard_units", _i, [_i, _i, _i, _i, _I, _I])
 _lib_partition_model = _sig("lfm_partition_model", _i, [ctypes.c_double, ctypes.c_double, _i, _i, ctypes.c_double, _I, _D])
+_lib_tile_model = _sig("lfm_tile_model", _i, [_i, _i, _i, _i, _i, _i, _i, _i, _I, _I, _I, _I, _D, _D])
 _lib_unique_id = _sig("lfm_comm_unique_id", _i, [ctypes.POINTER(ctypes.c_ubyte)])
 _lib_estimate = _sig("lfm_plan_estimate", _i, [_i, _i, _i, _i, _i, _i, _i, _i, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p, ctypes.c_size_t])
@@ -132,7 +133,7 @@ _lib_profile_read = _sig("lfm_profile_read", _i, [_P, ctypes.POINTER(lfm_profile
 _lib_stage_name = _sig("lfm_profile_stage_name", ctypes.c_char_p, [_i])
 STAGE_NAMES = [_lib_stage_name(i).decode() for i in range(LFM_N_STAGES)]
 
-EXPORTED = ["lfm_partition_model", "lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
+EXPORTED = ["lfm_partition_model", "lfm_tile_model", "lfm_shard_units", "lfm_policy_default", "lfm_last_error", "lfm_version", "lfm_comm_unique_id", "lfm_plan_estimate",
             "lfm_plan_create", "lfm_plan_info", "lfm_plan_owned", "lfm_set_memory_limit", "lfm_shard_units_balanced", "lfm_plan_destroy", "lfm_forward", "lfm_backward", "lfm_normalizer",
             "lfm_rl_step", "lfm_rl_iterate", "lfm_deconvolve_host", "lfm_quality", "lfm_dct_entropy",
             "lfm_profile", "lfm_profile_read", "lfm_profile_stage_name", "lfm_rl_iterate_batch"]
@@ -239,6 +240,16 @@ def lfm_partition_model(t_tc_ms, mac_bytes, direction, num_sms=148, mac_rate_sca
     _check(_lib_partition_model(float(t_tc_ms), float(mac_bytes), int(direction), int(num_sms), float(mac_rate_scale),
                                 ctypes.byref(sms), ctypes.byref(ms)))
     return sms.value, ms.value
+
+
+def lfm_tile_model(nnum, height, width, d1a, d1b, d2a, d2b, flags=0):
+    """The planner's overlap-save tiling for coarse taps in [d1a, d1b] x [d2a, d2b]: dict with L (0:
+    none), T1, T2, ntile, cost_unit, cost_whole (seconds per frequency-path unit and iteration); host-only."""
+    v = [ctypes.c_int(0) for _ in range(4)]
+    cu, cw = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(_lib_tile_model(int(nnum), int(height), int(width), int(d1a), int(d1b), int(d2a), int(d2b), int(flags),
+                           *[ctypes.byref(x) for x in v], ctypes.byref(cu), ctypes.byref(cw)))
+    return dict(L=v[0].value, T1=v[1].value, T2=v[2].value, ntile=v[3].value, cost_unit=cu.value, cost_whole=cw.value)
 
 
 def lfm_shard_units(nz, nnum, world, rank):

@@ -85,3 +85,39 @@ def test_c3_tap_range_and_window():
     assert tap_range(15, 165) == (-6, 6)
     T = 27 - 12
     assert T == 15 and -(-67 // T) == 5
+
+
+def _lib():
+    from paper_2208_11422_b200 import lfm
+    return lfm
+
+
+@pytest.mark.parametrize("args,expect", [
+    ((15, 1005, 1005, -6, 6, -6, 6), (27, 15, 15, 25)),     # c3, r = 5 planes (taps +-6)
+    ((15, 1005, 1005, -3, 3, -3, 3), (20, 14, 14, 25)),     # c3, r = 2 planes
+    ((15, 2025, 2025, -8, 8, -8, 8), (45, 29, 29, 25)),     # c4, the widest planes
+    ((11, 319, 319, -5, 5, -5, 5), (20, 10, 10, 9)),        # c2
+    ((3, 33, 33, -2, 2, -2, 2), (0, 0, 0, 0)),              # tiny: a single window would cover the image
+])
+def test_tile_model_choices(args, expect):
+    """lfm_tile_model is the planner's own choice (host-only, no GPU): window size, valid outputs and tile count at
+    the BASELINE geometries; the window spans the taps (L = T + d1b - d1a) and 2-32 tiles cover the coarse image."""
+    m = _lib().lfm_tile_model(*args)
+    assert (m["L"], m["T1"], m["T2"], m["ntile"]) == expect
+    if m["L"]:
+        nnum, h, w, d1a, d1b, d2a, d2b = args
+        assert m["L"] == m["T1"] + d1b - d1a == m["T2"] + d2b - d2a
+        assert 2 <= m["ntile"] == -(-(h // nnum) // m["T1"]) * -(-(w // nnum) // m["T2"]) <= 32
+        assert 0 < m["cost_unit"] < m["cost_whole"]
+
+
+def test_tile_model_flags_and_errors():
+    L = _lib()
+    assert L.lfm_tile_model(15, 1005, 1005, -6, 6, -6, 6, flags=L.LFM_PLAN_NO_TILES)["L"] == 0
+    assert L.lfm_tile_model(15, 1005, 1005, -6, 6, -6, 6, flags=L.LFM_PLAN_FRAMES)["L"] == 0
+    with pytest.raises(L.LfmError) as e:
+        L.lfm_tile_model(15, 1005, 1005, 6, -6, -6, 6)
+    assert e.value.status == L.LFM_EINVAL
+    with pytest.raises(L.LfmError) as e:
+        L.lfm_tile_model(15, 1000, 1005, -6, 6, -6, 6)   # 1000 is not a multiple of N = 15
+    assert e.value.status == L.LFM_EDIM
