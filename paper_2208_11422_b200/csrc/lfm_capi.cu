@@ -1956,8 +1956,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             for (int z = zb; z <= ze; ++z)
                 if (plane_direct[z] == 0) t_f += 0.5 * pt_fft[z];
             for (int d = 0; d < 2 && use_tiles && t_tc > 0 && units_fft > 0 && nsimt == 0; ++d) {
-                int want = (int)std::lround(p->num_sms * t_tc / (t_tc + t_f) / 8.0) * 8;
-                want = std::max(16, std::min(p->num_sms - 16, want));
+                const double raw = p->num_sms * t_tc / (t_tc + t_f);
+                // a tensor-core share below a dozen SMs is not worth a partition (c4: 38.4 it/s one after the other vs
+                // 36.0 on a forced 16-SM partition)
+                int want = raw < 12.0 ? 0 : (int)std::lround(raw / 8.0) * 8;
+                if (want) want = std::max(16, std::min(p->num_sms - 16, want));
                 if (const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F")) want = atoi(ev);   // dev override
                 if (getenv("LFM_PLAN_VERBOSE"))
                     fprintf(stderr, "[lfm plan] tiles, direction %d: t_tc %.3f ms, t_freq %.3f ms -> %d tc SMs\n", d,
