@@ -392,30 +392,33 @@ __device__ __forceinline__ void reg_fft_stages(float2 (&a)[L]) {
     }
 }
 
+// Shared memory per window: one block of BLK floats per packed row pair pr, used in place -- first the two real
+// window rows 2pr (floats 0 .. L-1) and 2pr+1 (L .. 2L-1), then (the thread that transformed them overwrites its own
+// block) the two Hermitian-half spectrum rows (complex 0 .. NK2-1 and CP .. CP+NK2-1), and in the C2R the two output
+// rows again.  Half the shared memory of separate real and spectrum planes, so four CTAs of 16 windows fit an SM.
+// BLK / 2 and the window stride IMG / 2 are odd (64-bit accesses of consecutive blocks / windows hit distinct banks).
 template <int L>
 struct RegGeom {
     static constexpr int NK2 = L / 2 + 1;
     static constexpr int P = (L + 1) / 2;
-    static constexpr int RP = (L % 2) ? L : L + 1;            // real row pitch (floats), odd
-    static constexpr int RPL = P * RP;                        // floats per real plane
-    static constexpr int RIMG = 2 * RPL;                      // floats per image (real planes)
-    static constexpr int CP = (NK2 % 2) ? NK2 : NK2 + 1;      // spectrum row pitch (complex), odd
-    static constexpr int CPL = P * CP;                        // complex per spectrum plane
-    static constexpr int CIMG = 2 * CPL + 1;                  // complex per image (spectrum planes), odd
-    static constexpr int UB = 16;                             // images per CTA
+    static constexpr int CP = (NK2 % 2) ? NK2 : NK2 + 1;      // spectrum row pitch within a block (complex)
+    static constexpr int BLK0 = (2 * L > 4 * CP ? 2 * L : 4 * CP);
+    static constexpr int BLK = ((BLK0 + 1) / 2 % 2) ? (BLK0 + 1) / 2 * 2 : (BLK0 + 1) / 2 * 2 + 2;   // floats, BLK/2 odd
+    static constexpr int IMG0 = P * BLK;
+    static constexpr int IMG = (IMG0 / 2 % 2) ? IMG0 : IMG0 + 2;   // floats per window, IMG/2 odd
+    static constexpr int UB = 16;                                 // windows per CTA
     static constexpr int NT = ((P > NK2 ? P : NK2) * UB + 31) / 32 * 32;
-    static constexpr size_t smem_r2c() { return (size_t)UB * RIMG * 4 + (size_t)UB * CIMG * 8; }
-    static constexpr size_t smem_c2r(int T1, int T2) { return (size_t)UB * CIMG * 8 + (size_t)UB * T1 * T2 * 4; }
+    static constexpr int MINB = L <= 27 ? 4 : 2;                  // resident CTAs per SM (registers, shared memory)
+    static constexpr size_t smem() { return (size_t)UB * IMG * 4; }
 };
 
 template <int L, int SRC>
-__global__ void __launch_bounds__(RegGeom<L>::NT) r2c_tile_reg_kernel(XformGeom g, TileGeom tg, R2CArgs a, int o1, int o2,
+__global__ void __launch_bounds__(RegGeom<L>::NT, RegGeom<L>::MINB) r2c_tile_reg_kernel(XformGeom g, TileGeom tg, R2CArgs a, int o1, int o2,
                                                                       unsigned* __restrict__ amax) {
     using RG = RegGeom<L>;
-    constexpr int NK2 = RG::NK2, P = RG::P, UB = RG::UB;
+    constexpr int NK2 = RG::NK2, P = RG::P, UB = RG::UB, BLK = RG::BLK, IMG = RG::IMG, CP = RG::CP;
     extern __shared__ float4 smr[];
-    float* re = reinterpret_cast<float*>(smr);                               // [UB][2][P][RP]
-    float2* sp = reinterpret_cast<float2*>(re + (size_t)UB * RG::RIMG);      // [UB][CIMG]: [2][P][CP]
+    float* sm = reinterpret_cast<float*>(smr);   // [UB][P][BLK]
     const int t0 = blockIdx.x * UB;
     const int nt = min(UB, a.ntrans - t0);
     __shared__ long long s_base[UB], s_col[UB];
@@ -434,14 +437,14 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) r2c_tile_reg_kernel(XformGeom 
     __syncthreads();
     const long long rp = (SRC == SRC_POLY) ? (long long)g.nw : (long long)g.N * g.W;
     const int cs = (SRC == SRC_POLY) ? 1 : g.N;
-    // A. window rows 0 .. 2P-1 (row L of an odd L: zeros) -> real planes
-    for (int idx = threadIdx.x; idx < nt * 2 * P * L; idx += blockDim.x) {
-        const int ui = idx / (2 * P * L);
-        const int rem = idx - ui * 2 * P * L;
+    // A. window rows 0 .. L-1 -> their blocks (zero outside the coarse image)
+    for (int idx = threadIdx.x; idx < nt * L * L; idx += blockDim.x) {
+        const int ui = idx / (L * L);
+        const int rem = idx - ui * L * L;
         const int i = rem / L, c = rem - i * L;
-        float* dst = re + (size_t)ui * RG::RIMG + (i & 1) * RG::RPL + (i >> 1) * RG::RP + c;
+        float* dst = sm + (size_t)ui * IMG + (i >> 1) * BLK + (i & 1) * L + c;
         const int gr = s_r0[ui] + i, gc = s_c0[ui] + c;
-        const bool v = i < L && gr >= 0 && gr < g.nh && gc >= 0 && gc < g.nw;
+        const bool v = gr >= 0 && gr < g.nh && gc >= 0 && gc < g.nw;
         const long long q = s_base[ui] + (long long)gr * rp + (long long)gc * cs;
         if constexpr (SRC == SRC_ONES) {
             *dst = v ? 1.0f : 0.0f;
@@ -453,28 +456,27 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) r2c_tile_reg_kernel(XformGeom 
     }
     cp_async_wait_all();
     __syncthreads();
-    // B. row FFTs of the packed pairs, Hermitian split, |x| sums
+    // B. per thread: its packed row pair x[2pr] + i x[2pr+1], row FFT, Hermitian split back into its own block
     for (int task = threadIdx.x; task < nt * P; task += blockDim.x) {
         const int ui = task / P, pr = task - ui * P;
-        const float* r0 = re + (size_t)ui * RG::RIMG + pr * RG::RP;
-        const float* r1 = r0 + RG::RPL;
+        float* blk = sm + (size_t)ui * IMG + pr * BLK;
+        const bool has1 = 2 * pr + 1 < L;
         float2 z[L];
         float sacc = 0.0f;
 #pragma unroll
         for (int c = 0; c < L; ++c) {
-            z[c] = make_float2(r0[c], r1[c]);
+            z[c] = make_float2(blk[c], has1 ? blk[L + c] : 0.0f);
             sacc += fabsf(z[c].x) + fabsf(z[c].y);
         }
         s_rsum[ui][pr] = sacc;
         reg_fft_stages<L, 0, 1, false>(z);
-        float2* o0 = sp + (size_t)ui * RG::CIMG + pr * RG::CP;
-        float2* o1 = o0 + RG::CPL;
+        float2* o = reinterpret_cast<float2*>(blk);
 #pragma unroll
         for (int k = 0; k < NK2; ++k) {
             const float2 zk = z[k], zm = z[k == 0 ? 0 : L - k];
             const float2 q = make_float2(zm.x, -zm.y);   // conj(Z[-k])
-            o0[k] = make_float2(0.5f * (zk.x + q.x), 0.5f * (zk.y + q.y));
-            o1[k] = make_float2(0.5f * (zk.y - q.y), -0.5f * (zk.x - q.x));
+            o[k] = make_float2(0.5f * (zk.x + q.x), 0.5f * (zk.y + q.y));
+            o[CP + k] = make_float2(0.5f * (zk.y - q.y), -0.5f * (zk.x - q.x));
         }
     }
     __syncthreads();
@@ -483,14 +485,14 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) r2c_tile_reg_kernel(XformGeom 
         for (int pr = 0; pr < P; ++pr) sum += s_rsum[threadIdx.x][pr];
         atomicMax(amax + s_tile[threadIdx.x], __float_as_uint(sum));
     }
-    // C. column FFTs, stored kappa-major (kappa = k1 * NK2 + k2)
+    // C. column FFTs, stored kappa-major (kappa = k1 * NK2 + k2); row i of column k: block i >> 1, plane i & 1
     for (int task = threadIdx.x; task < NK2 * UB; task += blockDim.x) {
         const int k = task / UB, ui = task - k * UB;
         if (ui >= nt) continue;
-        const float2* col = sp + (size_t)ui * RG::CIMG + k;
+        const float2* col = reinterpret_cast<const float2*>(sm + (size_t)ui * IMG) + k;
         float2 z[L];
 #pragma unroll
-        for (int i = 0; i < L; ++i) z[i] = col[(i & 1) * RG::CPL + (i >> 1) * RG::CP];
+        for (int i = 0; i < L; ++i) z[i] = col[(i >> 1) * (BLK / 2) + (i & 1) * CP];
         reg_fft_stages<L, 0, 1, false>(z);
         float2* out = a.out + s_col[ui] + (long long)k * a.out_ld;
 #pragma unroll
@@ -499,12 +501,11 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) r2c_tile_reg_kernel(XformGeom 
 }
 
 template <int L, int DST>
-__global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom g, TileGeom tg, C2RArgs a, int j1, int j2) {
+__global__ void __launch_bounds__(RegGeom<L>::NT, RegGeom<L>::MINB) c2r_tile_reg_kernel(XformGeom g, TileGeom tg, C2RArgs a, int j1, int j2) {
     using RG = RegGeom<L>;
-    constexpr int NK2 = RG::NK2, UB = RG::UB;
+    constexpr int NK2 = RG::NK2, UB = RG::UB, BLK = RG::BLK, IMG = RG::IMG, CP = RG::CP;
     extern __shared__ float4 smr[];
-    float2* sp = reinterpret_cast<float2*>(smr);                                // [UB][CIMG]
-    float* ob = reinterpret_cast<float*>(sp + (size_t)UB * RG::CIMG);           // [UB][T1][T2]
+    float* sm = reinterpret_cast<float*>(smr);   // [UB][P][BLK]
     const int T1 = tg.T1, T2 = tg.T2;
     const int t0 = blockIdx.x * UB;
     const int nt = min(UB, a.ntrans - t0);
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         s_m2[threadIdx.x] = tx * T2;
     }
     __syncthreads();
-    // A. inverse column FFTs straight from global (consecutive threads: consecutive images of one column)
+    // A. inverse column FFTs straight from global (consecutive threads: consecutive windows of one column)
     for (int task = threadIdx.x; task < NK2 * UB; task += blockDim.x) {
         const int k = task / UB, ui = task - k * UB;
         if (ui >= nt) continue;
@@ -534,18 +535,20 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
             for (int i = 0; i < L; ++i) z[i] = c_add(z[i], ins[(long long)i * NK2 * a.in_ld]);
         }
         reg_fft_stages<L, 0, 1, true>(z);
-        float2* col = sp + (size_t)ui * RG::CIMG + k;
+        float2* col = reinterpret_cast<float2*>(sm + (size_t)ui * IMG) + k;
 #pragma unroll
-        for (int i = 0; i < L; ++i) col[(i & 1) * RG::CPL + (i >> 1) * RG::CP] = z[i];
+        for (int i = 0; i < L; ++i) col[(i >> 1) * (BLK / 2) + (i & 1) * CP] = z[i];
     }
     __syncthreads();
-    // B. the packed row pairs holding valid rows j1 .. j1 + T1 - 1: Hermitian rebuild, inverse row FFT
+    // B. the packed row pairs holding valid rows j1 .. j1 + T1 - 1: Hermitian rebuild, inverse row FFT, the two
+    //    output rows back into the pair's own block (scaled)
     const int pr_lo = j1 >> 1, npr = ((j1 + T1 - 1) >> 1) - pr_lo + 1;
     const float scale = 1.0f / (float)(L * L);
     for (int task = threadIdx.x; task < nt * npr; task += blockDim.x) {
         const int ui = task / npr, pr = pr_lo + task - ui * npr;
-        const float2* s0 = sp + (size_t)ui * RG::CIMG + pr * RG::CP;
-        const float2* s1 = s0 + RG::CPL;
+        float* blk = sm + (size_t)ui * IMG + pr * BLK;
+        const float2* s0 = reinterpret_cast<const float2*>(blk);
+        const float2* s1 = s0 + CP;
         const bool has1 = 2 * pr + 1 < L;
         float2 z[L];
 #pragma unroll
@@ -566,13 +569,9 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         }
         reg_fft_stages<L, 0, 1, true>(z);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int i = 2 * pr + h;
-            if (i < j1 || i >= j1 + T1) continue;
-            float* orow = ob + ((size_t)ui * T1 + (i - j1)) * T2;
-#pragma unroll
-            for (int c = 0; c < L; ++c)
-                if (c >= j2 && c < j2 + T2) orow[c - j2] = (h ? z[c].y : z[c].x) * scale;
+        for (int c = 0; c < L; ++c) {
+            blk[c] = z[c].x * scale;
+            if (has1) blk[L + c] = z[c].y * scale;
         }
     }
     __syncthreads();
@@ -583,7 +582,8 @@ __global__ void __launch_bounds__(RegGeom<L>::NT) c2r_tile_reg_kernel(XformGeom 
         const int ii = rem / T2, cc = rem - ii * T2;
         const int m1 = s_m1[ui] + ii, m2 = s_m2[ui] + cc;
         if (m1 >= g.nh || m2 >= g.nw) continue;
-        const float v = ob[idx];
+        const int i = j1 + ii;   // window row
+        const float v = sm[(size_t)ui * IMG + (i >> 1) * BLK + (i & 1) * L + j2 + cc];
         const int item = s_item[ui];
         if constexpr (DST == DST_IMAGE) {
             const int b1 = item / g.N, b2 = item % g.N;
@@ -642,7 +642,7 @@ cudaError_t r2c_tile_reg_go(const XformGeom& g, const TileGeom& tg, const R2CArg
         return cudaErrorInvalidValue;
     } else {
     using RG = RegGeom<L>;
-    const size_t smem = RG::smem_r2c();
+    const size_t smem = RG::smem();
     cudaError_t e = cudaFuncSetAttribute(r2c_tile_reg_kernel<L, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     r2c_tile_reg_kernel<L, SRC><<<(unsigned)((a.ntrans + RG::UB - 1) / RG::UB), RG::NT, smem, s>>>(g, tg, a, o1, o2, amax);
@@ -656,7 +656,7 @@ cudaError_t c2r_tile_reg_go(const XformGeom& g, const TileGeom& tg, const C2RArg
         return cudaErrorInvalidValue;
     } else {
     using RG = RegGeom<L>;
-    const size_t smem = RG::smem_c2r(tg.T1, tg.T2);
+    const size_t smem = RG::smem();
     cudaError_t e = cudaFuncSetAttribute(c2r_tile_reg_kernel<L, DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     c2r_tile_reg_kernel<L, DST><<<(unsigned)((a.ntrans + RG::UB - 1) / RG::UB), RG::NT, smem, s>>>(g, tg, a, j1, j2);
