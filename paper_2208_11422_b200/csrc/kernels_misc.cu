@@ -325,6 +325,24 @@ cudaError_t launch_ratio(const float* y, const float* yhat, float* r, size_t n, 
     return cudaGetLastError();
 }
 
+// ---- image -> output-phase planes for the tiled path's image-side transforms: out[b'][i][j] = v(b1 + N i, b2 + N j),
+//      v = y / (max(yhat, 0) + eps) (yhat != nullptr) or y; computed once per projection instead of once per tile group
+__global__ void image_phase_planes_kernel(const float* __restrict__ y, const float* __restrict__ yhat, float eps,
+                                          float* __restrict__ out, int N, int H, int W, int nh, int nw) {
+    const size_t n = (size_t)H * W;
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(p / W), c = (int)(p - (size_t)r * W);
+        const float v = yhat ? y[p] / (fmaxf(yhat[p], 0.0f) + eps) : y[p];
+        out[((size_t)((r % N) * N + c % N) * nh + r / N) * nw + c / N] = v;
+    }
+}
+
+cudaError_t launch_image_phase_planes(const float* y, const float* yhat, float eps, float* out, int N, int H, int W,
+                                      cudaStream_t s) {
+    image_phase_planes_kernel<<<1184, 256, 0, s>>>(y, yhat, eps, out, N, H, W, H / N, W / N);
+    return cudaGetLastError();
+}
+
 // ---- device-resident auto-stop loop (LFM_PLAN_DEVICE_LOOP) ----
 // The stop rule of lfm_rl_iterate (reading C15) evaluated on the device after each iteration: appends E_k to the
 // series, counts strict decreases, tracks the argmax (ties -> smallest k) and sets the WHILE / IF conditions of the

@@ -757,12 +757,24 @@ lfm_status op_backward(lfm_plan p, int src, const float* img, const float* img2,
     if (split && !prefork) ST(fork(p, pt, s, &st, &sm));   // staging / R2C inside the halves, as in the forward
     for (const TcDirArgs& tg : p->tcb) CK(launch_tcdir_bwd(tg, src, img, img2, eps, dst, out, xold, aux, st, TC_PART_STAGE));
     if (p->nu_fft > 0 && p->tiled) {   // §5.6: windows of every (tile, output phase), R rows of bpitch
+        // the ratio (or the plain image) once into output-phase planes, read row-contiguously by every tile group
+        int gsrc = src;
+        const float* gimg = img;
+        if (src == SRC_RATIO || src == SRC_IMAGE2D) {
+            CK(launch_image_phase_planes(img, src == SRC_RATIO ? img2 : nullptr, eps, p->rimg, p->geo.N, p->geo.H,
+                                         p->geo.W, sm));
+            p->pacc.launches += 1;
+            gsrc = SRC_POLY;
+            gimg = p->rimg;
+        }
         for (auto& gr : p->tgs) {
             CK(cudaMemsetAsync(gr.tmax + 32, 0, 32 * sizeof(unsigned), sm));
-            R2CArgs a = r2c_args(src, img, img2, eps, gr.tg.ntile * N2, gr.R, p->bpitch);
+            XformGeom gx = gr.xg;
+            if (gsrc == SRC_POLY) gx.umap = nullptr;   // item = output phase b' -> plane b' of rimg
+            R2CArgs a = r2c_args(gsrc, gimg, img2, eps, gr.tg.ntile * N2, gr.R, p->bpitch);
             a.cdiv = N2;
             a.cmul = (long long)gr.xg.nkappa * p->bpitch;
-            CK(launch_r2c_tile(gr.xg, gr.tg, gr.tw, a, 1, gr.tmax + 32, sm));
+            CK(launch_r2c_tile(gx, gr.tg, gr.tw, a, 1, gr.tmax + 32, sm));
         }
     } else if (p->nu_fft > 0) {
         CK(launch_r2c(p->xg, p->fh, p->fw, p->tw_h, p->tw_w, r2c_args(src, img, img2, eps, N2, p->R, N2), sm));

@@ -304,5 +304,7 @@ cudaError_t launch_direct_fwd(const float* xp, const float* psf, float* yimg, co
 cudaError_t launch_direct_bwd(const float* rimg, const float* psf, float* out, int dst, const float* xold,
                               const float* norm, unsigned* mproj, float eps, const XformGeom& g, cudaStream_t s);
 cudaError_t launch_ratio(const float* y, const float* yhat, float* r, size_t n, float eps, cudaStream_t s);
+cudaError_t launch_image_phase_planes(const float* y, const float* yhat, float eps, float* out, int N, int H, int W,
+                                      cudaStream_t s);
 
 }  // namespace lfm
