@@ -176,7 +176,8 @@ def run_reference(args):
     y64 = lf_like(cfg, 7)
     O.build()
     cores = cpu_cores()
-    rows = min(cfg.height, max(2, 4 * cores))   # >= 4 rows per core: every OpenMP thread gets work
+    rows = min(cfg.height, max(2, 8 * cores))   # 8 rows per core: every OpenMP thread gets work, per-call overheads
+    # stay small against the extrapolated rows (4 per core measured 0.015-0.026 it/s across boxes)
     for _ in range(args.warmup):
         oracle_iteration_seconds(cfg, h64, x64, y64, rows)
     ts = [oracle_iteration_seconds(cfg, h64, x64, y64, rows)[0] for _ in range(args.steps)]
