@@ -389,7 +389,7 @@ def run_ours(args):
         e2e_iters += r["stop_iter"]
         auto = r
     # device -> host bytes of the timed calls as the library counted them: the 8-byte E_k read per iteration and the
-    # final volume copy (or, with the LFM_HOST_MIRROR switch, the improving iterates copied while the loop runs)
+    # volume copies (improving iterates once the E curve flattens, copied while the loop runs, or the final copy)
     d2h = plan.profile_read(reset=True)["d2h_bytes"]
     s = auto["series"]
     k = auto["stop_iter"]
@@ -398,8 +398,9 @@ def run_ours(args):
     e2e = {"value": e2e_iters / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(H * W * 4 * calls / e2e_iters),
            "d2h_bytes_per_step": int(d2h / e2e_iters),
-           "step": "one RL iteration of an auto-stop lfm_deconvolve_host call (host y in, host argmax volume out once "
-                   "after the loop, plus 8 bytes of E_k per iteration; d2h counted by the library); "
+           "step": "one RL iteration of an auto-stop lfm_deconvolve_host call (host y in, host argmax volume out: "
+                   "improving iterates after the E curve flattens (gain < 1 %) copied while the next iteration runs, "
+                   "else once after the loop; plus 8 bytes of E_k per iteration; d2h counted by the library); "
                    f"{calls} timed call(s) after one warm-up call, {e2e_iters} iterations",
            "call_s": call_s}
 

@@ -292,10 +292,13 @@ lfm_status lfm_rl_iterate_batch(lfm_plan plan, int frames, const float* y, float
                                 int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 
 /* End-to-end call with HOST buffers: copies y in (H2D), runs lfm_rl_iterate, copies the argmax-E
- * volume out (D2H, once, after the loop).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best).
- * (Developer switch LFM_HOST_MIRROR, single rank, page-locked x_host: every improving iterate is copied into x_host
- * on a side stream while the next iteration runs, skipping iterates while the previous copy is on the link --
- * measured slower at c3 than the single final copy: the copies take HBM bandwidth from the iteration.) */
+ * volume out (D2H).  y_host [H][W], x_host [nz][H][W] (in: x0 if init_from_x; out: x_best).
+ * With a page-locked x_host on a single rank in auto mode, an improving iterate whose E gain over the previous one is
+ * below 1 % (the curve flattening before the stop) is copied into x_host on a side stream while the next iteration
+ * runs (skipped while a previous copy is still on the link), so the argmax is usually on the host when the loop stops
+ * and the final copy is skipped; x_host may hold such an intermediate iterate during the call and holds x_best when
+ * it returns.  Otherwise x_best is copied once after the loop.  (Developer switch LFM_HOST_MIRROR: every improving
+ * iterate -- measured slower at c3: the copies take HBM bandwidth from the iteration.) */
 lfm_status lfm_deconvolve_host(lfm_plan plan, const float* y_host, float* x_host, const lfm_policy* policy,
                                int* best_iter, int* stop_iter, double* series_host, float* ms_host, void* stream);
 

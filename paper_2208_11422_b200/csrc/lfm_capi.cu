@@ -2552,6 +2552,8 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
             ms_host[k - 1] = ms;
         }
         // stop rule (reading C15): strict decreases counted, argmax with ties -> smallest k
+        // (relative gain of E_k over E_{k-1}: the auto-stop curve flattening before its peak, see the mirror below)
+        const double gain = k > 1 ? (e - prev) / std::max(std::fabs(e), 1e-300) : 1.0;
         if (k > 1 && e < prev)
             ++decreases;
         else
@@ -2564,8 +2566,14 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
             // iteration k is complete (synchronised above): convert + copy it on the side stream -- unless the previous
             // mirror copy is still in flight (the host link is slower than an iteration): then this iterate is skipped
             // and a later one (or the final copy after the loop) brings x_best
+            // Which improving iterates are mirrored: in auto mode those after the curve has flattened (gain below
+            // kMirrorGain: the stop is near, and the iterate the stop keeps is then usually on the host already when
+            // the loop ends); every one with LFM_HOST_MIRROR (dev); none in fixed mode (x_best is copied after the loop)
+            static const bool mirror_all = getenv("LFM_HOST_MIRROR") != nullptr;
+            constexpr double kMirrorGain = 1e-2;
+            const bool want = mirror && (mirror_all || (pol->mode != LFM_MODE_FIXED && gain < kMirrorGain));
             bool link_busy = false;
-            if (mirror && mirrored_buf >= 0) {
+            if (want && mirrored_buf >= 0) {
                 const cudaError_t q = cudaEventQuery(p->evcopy);
                 if (q == cudaErrorNotReady) {
                     link_busy = true;
@@ -2574,7 +2582,7 @@ lfm_status rl_loop(lfm_plan p, const float* y, float* x, const lfm_policy* pol, 
                     return fail(LFM_ECUDA, "mirror copy: %s", cudaGetErrorString(q));
                 }
             }
-            if (mirror && !link_busy) {
+            if (want && !link_busy) {
                 ST(gather_to_image(p, p->xb[nxt], x, p->scopy));
                 CK(cudaEventRecord(p->evconv[nxt], p->scopy));
                 conv_pending[nxt] = true;
@@ -2628,7 +2636,7 @@ lfm_status lfm_deconvolve_host(lfm_plan p, const float* y_host, float* x_host, c
     cudaGetLastError();   // clear a possible error of the query
     bool mirrored = false;
     ST(rl_loop(p, p->y_stage, p->x_stage, pol, best_iter, stop_iter, series_host, ms_host, s,
-               (p->dloop || !pinned || !getenv("LFM_HOST_MIRROR")) ? nullptr : x_host, &mirrored));
+               (p->dloop || !pinned) ? nullptr : x_host, &mirrored));
     if (!mirrored) {
         CK(cudaMemcpyAsync(x_host, p->x_stage, V * sizeof(float), cudaMemcpyDeviceToHost, s));
         p->pacc.d2h_bytes += (long long)V * sizeof(float);
