@@ -126,6 +126,38 @@ __global__ void max_project_poly_kernel(const float* __restrict__ xp, unsigned* 
     }
 }
 
+// F frames: frame f reads base + (f * 3 + sel.b[f]) * vol (its current triple-buffer slot) into mproj + f H W
+__global__ void max_project_poly_batch_kernel(const float* __restrict__ base, size_t vol, FrameSel sel,
+                                              unsigned* __restrict__ mproj, XformGeom g) {
+    const int f = blockIdx.y;
+    const float* xp = base + ((size_t)f * 3 + sel.b[f]) * vol;
+    unsigned* mp = mproj + (size_t)f * g.H * g.W;
+    const int N = g.N, N2 = N * N;
+    const int per = g.nh * g.nw;
+    const size_t total = (size_t)N2 * per;
+    const int zb = g.unit0 / N2, ze = (g.unit0 + g.nu - 1) / N2;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e / per);
+        const int m = (int)(e - (size_t)a * per);
+        float v = 0.0f;
+        for (int z = zb; z <= ze; ++z) {
+            const int u = z * N2 + a;
+            if (u >= g.unit0 && u < g.unit0 + g.nu) v = fmaxf(v, xp[(size_t)(u - g.unit0) * per + m]);
+        }
+        const int m1 = m / g.nw, m2 = m - m1 * g.nw;
+        const int a1 = a / N, a2 = a - a1 * N;
+        mp[(size_t)(a1 + N * m1) * g.W + a2 + N * m2] = __float_as_uint(v);
+    }
+}
+
+cudaError_t launch_max_project_poly_batch(const float* base, size_t vol, const FrameSel& sel, int F, unsigned* mproj,
+                                          const XformGeom& g, cudaStream_t s) {
+    const size_t total = (size_t)g.N * g.N * g.nh * g.nw;
+    const unsigned blocks = (unsigned)((total + 255) / 256 < 1184 ? (total + 255) / 256 : 1184);
+    max_project_poly_batch_kernel<<<dim3(blocks, F), 256, 0, s>>>(base, vol, sel, mproj, g);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_max_project_poly(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s) {
     const size_t total = (size_t)g.N * g.N * g.nh * g.nw;
     const unsigned blocks = (unsigned)((total + 255) / 256 < 4736 ? (total + 255) / 256 : 4736);
@@ -199,8 +231,11 @@ constexpr int kMetricRows = 4;
 // T1[v][i] = sum_j m[i][j] Cw[v][j] (v < xs) and rowsq[i] = sum_j m[i][j]^2, fp64, kMetricRows rows per CTA
 __global__ void __launch_bounds__(256) metric_rows_kernel(const unsigned* __restrict__ mbits, int H, int W, int xs,
                                                           const double* __restrict__ Cw, double* __restrict__ T1,
-                                                          double* __restrict__ rowsq) {
+                                                          double* __restrict__ rowsq, size_t fs_m, size_t fs_t1) {
     extern __shared__ double mrow[];
+    mbits += blockIdx.y * fs_m;   // frame blockIdx.y of a batch (fs_* = per-frame strides; 0 for one frame)
+    T1 += blockIdx.y * fs_t1;
+    rowsq += blockIdx.y * (size_t)H;
     const int i0 = blockIdx.x * kMetricRows;
     const int nr = min(kMetricRows, H - i0);
     for (int e = threadIdx.x; e < nr * W; e += blockDim.x)
@@ -259,8 +294,13 @@ __global__ void __launch_bounds__(256) metric_member_kernel(int H, const double*
                                                             const double* __restrict__ T1,
                                                             const double* __restrict__ rowsq,
                                                             const int2* __restrict__ mem, int nmem,
-                                                            double* __restrict__ term, double* __restrict__ out) {
+                                                            double* __restrict__ term, double* __restrict__ out,
+                                                            size_t fs_t1, int fs_out) {
     __shared__ double red[32];
+    T1 += blockIdx.y * fs_t1;
+    term += blockIdx.y * fs_t1;
+    rowsq += blockIdx.y * (size_t)H;
+    out += blockIdx.y * fs_out;
     const double L = metric_norm(rowsq, H, red);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -284,8 +324,10 @@ __global__ void __launch_bounds__(256) metric_member_kernel(int H, const double*
 
 // E = 2 / (xs ys) * sum_k term[k] in a fixed order (one CTA)
 __global__ void __launch_bounds__(1024) metric_sum_kernel(int xs, int ys, const double* __restrict__ term, int nmem,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, size_t fs_t1, int fs_out) {
     __shared__ double red[32];
+    term += blockIdx.x * fs_t1;   // one CTA per frame
+    out += blockIdx.x * fs_out;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     double t = 0.0;
     for (int k = threadIdx.x; k < nmem; k += blockDim.x) t += term[k];
@@ -305,11 +347,29 @@ cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int 
     const size_t smem = (size_t)kMetricRows * W * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(metric_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    metric_rows_kernel<<<(H + kMetricRows - 1) / kMetricRows, 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq);
+    metric_rows_kernel<<<(H + kMetricRows - 1) / kMetricRows, 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq, 0, 0);
     // the per-member terms follow T1 ([xs][H] doubles) in the same allocation (MetricDev)
     double* term = T1 + (size_t)xs * H;
-    metric_member_kernel<<<(nmem + 7) / 8, 256, 0, s>>>(H, Cr, T1, rowsq, members, nmem, term, out);
-    metric_sum_kernel<<<1, 1024, 0, s>>>(xs, ys, term, nmem, out);
+    metric_member_kernel<<<(nmem + 7) / 8, 256, 0, s>>>(H, Cr, T1, rowsq, members, nmem, term, out, 0, 0);
+    metric_sum_kernel<<<1, 1024, 0, s>>>(xs, ys, term, nmem, out, 0, 0);
+    return cudaGetLastError();
+}
+
+// the metric of F frames in three launches: frame f reads mproj_bits + f H W and writes out[2 f] (E) / out[2 f + 1]
+// (its norm); T1 / rowsq hold F per-frame workspaces (T1: xs H + nmem doubles each, rowsq: H each).  Same arithmetic
+// and reduction order per frame as launch_metric.
+cudaError_t launch_metric_batch(const unsigned* mproj_bits, int F, int H, int W, int xs, int ys, const double* Cr,
+                                const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
+                                double* out, cudaStream_t s) {
+    const size_t smem = (size_t)kMetricRows * W * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(metric_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const size_t fs_t1 = (size_t)xs * H + nmem;
+    metric_rows_kernel<<<dim3((H + kMetricRows - 1) / kMetricRows, F), 256, smem, s>>>(mproj_bits, H, W, xs, Cw, T1, rowsq,
+                                                                                       (size_t)H * W, fs_t1);
+    double* term = T1 + (size_t)xs * H;
+    metric_member_kernel<<<dim3((nmem + 7) / 8, F), 256, 0, s>>>(H, Cr, T1, rowsq, members, nmem, term, out, fs_t1, 2);
+    metric_sum_kernel<<<F, 1024, 0, s>>>(xs, ys, term, nmem, out, fs_t1, 2);
     return cudaGetLastError();
 }
 

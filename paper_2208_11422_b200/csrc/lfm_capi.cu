@@ -323,6 +323,7 @@ struct lfm_plan_s {
     float *bx = nullptr, *byhat = nullptr;
     unsigned* bmproj = nullptr;
     double *bent = nullptr, *bhost = nullptr;
+    double *bmT1 = nullptr, *bmrs = nullptr;   // per-frame metric workspaces (launch_metric_batch)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // co-resident projections: the tensor-core direct kernel on a high-priority side stream, the
     // frequency-path MAC beside it on the caller's stream, one fork / join per projection
@@ -538,6 +539,8 @@ void plan_free(lfm_plan p) {
     cudaFree(p->byhat);
     cudaFree(p->bmproj);
     cudaFree(p->bent);
+    cudaFree(p->bmT1);
+    cudaFree(p->bmrs);
     if (p->bhost) cudaFreeHost(p->bhost);
     if (p->host) cudaFreeHost(p->host);
     green_free(p);
@@ -2727,12 +2730,13 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
     const long long sR = (long long)p->geo.nkappa * rld;
     if (p->bcap < F) {   // (re)allocate the per-frame state
         cudaFree(p->bG); cudaFree(p->bXh); cudaFree(p->bY); cudaFree(p->bR); cudaFree(p->bx); cudaFree(p->byhat);
-        cudaFree(p->bmproj); cudaFree(p->bent);
+        cudaFree(p->bmproj); cudaFree(p->bent); cudaFree(p->bmT1); cudaFree(p->bmrs);
         if (p->bhost) cudaFreeHost(p->bhost);
         p->bG = p->bXh = p->bY = p->bR = nullptr;
         p->bx = p->byhat = nullptr;
         p->bmproj = nullptr;
         p->bent = p->bhost = nullptr;
+        p->bmT1 = p->bmrs = nullptr;
         p->bcap = 0;
         if (p->nu_fft > 0) {
             ST(dalloc(p, &p->bG, (size_t)F * sG * sizeof(float2), "batch G spectra"));
@@ -2746,6 +2750,11 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
         ST(dalloc(p, &p->byhat, (size_t)F * HW * sizeof(float), "batch yhat"));
         ST(dalloc(p, &p->bmproj, (size_t)F * HW * sizeof(unsigned), "batch max projections"));
         ST(dalloc(p, &p->bent, (size_t)2 * F * sizeof(double), "batch entropies"));
+        {
+            const int nmem = std::max(p->met.nmem[0], p->met.nmem[1]);
+            ST(dalloc(p, &p->bmT1, (size_t)F * ((size_t)p->met.xs * p->geo.H + nmem) * sizeof(double), "batch metric T1"));
+            ST(dalloc(p, &p->bmrs, (size_t)F * p->geo.H * sizeof(double), "batch metric rows"));
+        }
         CK(cudaMallocHost(&p->bhost, (size_t)2 * F * sizeof(double)));
         p->bcap = F;
     }
@@ -2909,12 +2918,17 @@ lfm_status lfm_rl_iterate_batch(lfm_plan p, int frames, const float* y, float* x
             }
             for (const DirArgs& dg : p->dgroups)
                 CK(launch_dir_bwd(dg, SRC_RATIO, y + f * HW, p->byhat + f * HW, pol->eps, DST_UPDATE, xn, xo, p->norm, s));
-            unsigned* mp = p->bmproj + f * HW;
-            CK(launch_max_project_poly(xn, mp, p->xall, s));
-            ST(allreduce(p, mp, HW, ncclFloat, ncclMax, s));
+        }
+        // a7 / C2 / a8 of every frame in one launch each: the max-projections (frame f from its new slot; a stopped
+        // frame's slot is re-projected and ignored), one collective over all frames, the batched metric
+        {
+            FrameSel sel{};
+            for (int f = 0; f < F; ++f) sel.b[f] = stopped[f] ? cur[f] : nxt[f];
+            CK(launch_max_project_poly_batch(p->bx, vol, sel, F, p->bmproj, p->xall, s));
+            ST(allreduce(p, p->bmproj, (size_t)F * HW, ncclFloat, ncclMax, s));
             const int ri = pol->region == LFM_REGION_RECTANGLE ? 1 : 0;
-            CK(launch_metric(mp, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw, p->met.mem[ri],
-                             p->met.nmem[ri], p->met.T1, p->met.rowsq, p->bent + 2 * f, s));
+            CK(launch_metric_batch(p->bmproj, F, p->geo.H, p->geo.W, p->met.xs, p->met.ys, p->met.Cr, p->met.Cw,
+                                   p->met.mem[ri], p->met.nmem[ri], p->bmT1, p->bmrs, p->bent, s));
             p->pacc.launches += 4;
         }
         ST(mark(p, ST_DIR_BWD, s));

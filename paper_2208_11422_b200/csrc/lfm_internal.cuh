@@ -295,6 +295,14 @@ cudaError_t launch_image_to_poly(const float* x, float* xp, const XformGeom& g, 
                                  cudaStream_t s);
 cudaError_t launch_max_project(const float* x, unsigned* mproj, const XformGeom& g, cudaStream_t s);
 cudaError_t launch_max_project_poly(const float* xp, unsigned* mproj, const XformGeom& g, cudaStream_t s);
+struct FrameSel {
+    int b[32];   // per frame of a batch: the triple-buffer slot holding its current iterate
+};
+cudaError_t launch_max_project_poly_batch(const float* base, size_t vol, const FrameSel& sel, int F, unsigned* mproj,
+                                          const XformGeom& g, cudaStream_t s);
+cudaError_t launch_metric_batch(const unsigned* mproj_bits, int F, int H, int W, int xs, int ys, const double* Cr,
+                                const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
+                                double* out, cudaStream_t s);
 cudaError_t launch_sum_stats(const float* p, size_t n, double* partials, int nparts, double* out3, cudaStream_t s);
 cudaError_t launch_metric(const unsigned* mproj_bits, int H, int W, int xs, int ys, const double* Cr,
                           const double* Cw, const int2* members, int nmem, double* T1, double* rowsq,
