@@ -1164,6 +1164,12 @@ double whole_unit_cost(const Geo& g, int N2) {
 // FRAMES / DIRECT plans)
 TileGeom choose_tiles(const Geo& g, int N2, int flags, int d1a, int d1b, int d2a, int d2b) {
     if ((flags & (LFM_PLAN_NO_TILES | LFM_PLAN_FRAMES | LFM_PLAN_DIRECT)) || N2 > 256) return TileGeom{};
+    // the window offsets (forward outputs at dmax, backward at -dmin) need 0 in the tap range: a one-sided support
+    // (an off-centre PSF) widens its range to the centre
+    d1a = std::min(d1a, 0);
+    d2a = std::min(d2a, 0);
+    d1b = std::max(d1b, 0);
+    d2b = std::max(d2b, 0);
     static const int cand[] = {16, 18, 20, 24, 25, 27, 30, 32, 36, 40, 45, 48};
     TileGeom best{};
     double best_c = 1e300;

@@ -93,6 +93,28 @@ def L_():
     return L()
 
 
+def test_tiled_off_centre_psf():
+    """A PSF whose support lies on one side of the kernel centre (coarse taps not straddling 0): the tile windows
+    keep the centre in their tap range; forward and backward match the oracle."""
+    rng = np.random.default_rng(103)
+    h = np.zeros((2, 3, 3, 15, 15), np.float32)
+    h[:, :, :, 12:15, 11:15] = rng.uniform(0, 1, (2, 3, 3, 3, 4))   # rows / columns >= 4 right of the centre (7):
+    # every coarse tap d >= 1 on both axes
+    h /= h.sum(axis=(3, 4), keepdims=True)
+    x = rng.uniform(0, 1, (2, 120, 99)).astype(np.float32)
+    r = rng.uniform(0.5, 1.5, (120, 99)).astype(np.float32)
+    hd = h.astype(np.float64)
+    with L().Plan(h, 3, 120, 99, flags=L().LFM_PLAN_TILES | L().LFM_PLAN_FFT_ONLY) as plan:
+        assert plan.info()["tiles"] >= 2
+        y_d = torch.zeros((120, 99), device="cuda")
+        plan.forward(dev(x), y_d)
+        xb_d = torch.zeros((2, 120, 99), device="cuda")
+        plan.backward(dev(r), xb_d)
+        torch.cuda.synchronize()
+    assert rel(y_d.cpu().numpy(), O.forward_project(x.astype(np.float64), hd)) <= 1e-5
+    assert rel(xb_d.cpu().numpy(), O.backward_project(r.astype(np.float64), hd)) <= 1e-5
+
+
 def test_tiled_signed_inputs():
     """lfm_forward / lfm_backward of sign-changing inputs: the per-tile fp16 scale is bounded by sum |window|, not by
     the (non-negative-source) DC term."""
