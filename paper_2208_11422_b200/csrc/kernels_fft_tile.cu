@@ -437,21 +437,45 @@ __global__ void __launch_bounds__(RegGeom<L>::NT, RegGeom<L>::MINB) r2c_tile_reg
     __syncthreads();
     const long long rp = (SRC == SRC_POLY) ? (long long)g.nw : (long long)g.N * g.W;
     const int cs = (SRC == SRC_POLY) ? 1 : g.N;
-    // A. window rows 0 .. L-1 -> their blocks (zero outside the coarse image)
-    for (int idx = threadIdx.x; idx < nt * L * L; idx += blockDim.x) {
-        const int ui = idx / (L * L);
-        const int rem = idx - ui * L * L;
-        const int i = rem / L, c = rem - i * L;
-        float* dst = sm + (size_t)ui * IMG + (i >> 1) * BLK + (i & 1) * L + c;
-        const int gr = s_r0[ui] + i, gc = s_c0[ui] + c;
-        const bool v = gr >= 0 && gr < g.nh && gc >= 0 && gc < g.nw;
-        const long long q = s_base[ui] + (long long)gr * rp + (long long)gc * cs;
-        if constexpr (SRC == SRC_ONES) {
-            *dst = v ? 1.0f : 0.0f;
-        } else if constexpr (SRC == SRC_RATIO) {
-            *dst = v ? a.in[q] / (fmaxf(a.in2[q], 0.0f) + a.eps) : 0.0f;
-        } else {
-            cp_async4_zfill(dst, a.in + (v ? q : 0), v);
+    // A. window rows 0 .. L-1 -> their blocks (zero outside the coarse image): one warp per window row (ui, i), the
+    //    lanes over its columns.  Per lane the column's validity, source pointer and shared-memory offset are set once
+    //    per window and then stepped by NW rows (the flat element loop spent a third of this kernel's instructions on
+    //    divisions and three shared-memory lookups per element, ncu r02)
+    {
+        constexpr int NW = RG::NT / 32;
+        static_assert(NW <= L, "one wrap of the window-row counter per step");
+        const int lane = threadIdx.x & 31;
+        const long long rstep = (long long)NW * rp;
+        for (int c = lane; c < L; c += 32) {
+            int ui = 0, i = threadIdx.x >> 5;
+            int gr = s_r0[0] + i;
+            int gc = s_c0[0] + c;
+            bool cv = gc >= 0 && gc < g.nw;
+            long long q = s_base[0] + (long long)gr * rp + (long long)gc * cs;
+            float* dwin = sm + c;
+            for (;;) {
+                float* dst = dwin + (i >> 1) * BLK + (i & 1) * L;
+                const bool v = cv && (unsigned)gr < (unsigned)g.nh;
+                if constexpr (SRC == SRC_ONES) {
+                    *dst = v ? 1.0f : 0.0f;
+                } else if constexpr (SRC == SRC_RATIO) {
+                    *dst = v ? a.in[q] / (fmaxf(a.in2[q], 0.0f) + a.eps) : 0.0f;
+                } else {
+                    cp_async4_zfill(dst, a.in + (v ? q : 0), v);
+                }
+                i += NW;
+                gr += NW;
+                q += rstep;
+                if (i >= L) {
+                    i -= L;
+                    if (++ui >= nt) break;
+                    gr = s_r0[ui] + i;
+                    gc = s_c0[ui] + c;
+                    cv = gc >= 0 && gc < g.nw;
+                    q = s_base[ui] + (long long)gr * rp + (long long)gc * cs;
+                    dwin += IMG;
+                }
+            }
         }
     }
     cp_async_wait_all();
@@ -509,16 +533,29 @@ __global__ void __launch_bounds__(RegGeom<L>::NT, RegGeom<L>::MINB) c2r_tile_reg
     const int T1 = tg.T1, T2 = tg.T2;
     const int t0 = blockIdx.x * UB;
     const int nt = min(UB, a.ntrans - t0);
-    __shared__ long long s_col[UB];
-    __shared__ int s_item[UB], s_m1[UB], s_m2[UB];
+    __shared__ long long s_col[UB], s_ob[UB];
+    __shared__ int s_m1[UB], s_m2[UB];
     if (threadIdx.x < nt) {
         const int t = t0 + threadIdx.x;
         const int tile = t / a.cdiv, item = t - tile * a.cdiv;
         const int ty = tile / tg.ntx, tx = tile - ty * tg.ntx;
+        const int m1 = ty * T1, m2 = tx * T2;
         s_col[threadIdx.x] = (long long)tile * a.cmul + item;
-        s_item[threadIdx.x] = item;
-        s_m1[threadIdx.x] = ty * T1;
-        s_m2[threadIdx.x] = tx * T2;
+        s_m1[threadIdx.x] = m1;
+        s_m2[threadIdx.x] = m2;
+        // destination offset of the window's first valid output (m1, m2); the others follow at ii * rs + cc * cs
+        if constexpr (DST == DST_IMAGE) {
+            const int b1 = item / g.N, b2 = item - (item / g.N) * g.N;
+            s_ob[threadIdx.x] = (long long)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
+        } else if constexpr (DST == DST_VOLIMAGE) {
+            const int u = g.unit0 + (g.umap ? g.umap[item] : item);
+            const int N2 = g.N * g.N;
+            const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+            s_ob[threadIdx.x] = ((long long)z * g.H + a1 + g.N * m1) * g.W + a2 + g.N * m2;
+        } else {
+            const int lu = g.umap ? g.umap[item] : item;
+            s_ob[threadIdx.x] = ((long long)lu * g.nh + m1) * g.nw + m2;
+        }
     }
     __syncthreads();
     // A. inverse column FFTs straight from global (consecutive threads: consecutive windows of one column)
@@ -575,32 +612,74 @@ __global__ void __launch_bounds__(RegGeom<L>::NT, RegGeom<L>::MINB) c2r_tile_reg
         }
     }
     __syncthreads();
-    // C. epilogue over the valid outputs (consecutive threads: consecutive columns)
-    for (int idx = threadIdx.x; idx < nt * T1 * T2; idx += blockDim.x) {
-        const int ui = idx / (T1 * T2);
-        const int rem = idx - ui * T1 * T2;
-        const int ii = rem / T2, cc = rem - ii * T2;
-        const int m1 = s_m1[ui] + ii, m2 = s_m2[ui] + cc;
-        if (m1 >= g.nh || m2 >= g.nw) continue;
-        const int i = j1 + ii;   // window row
-        const float v = sm[(size_t)ui * IMG + (i >> 1) * BLK + (i & 1) * L + j2 + cc];
-        const int item = s_item[ui];
-        if constexpr (DST == DST_IMAGE) {
-            const int b1 = item / g.N, b2 = item % g.N;
-            float* o = a.out + (size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
-            *o = a.accum ? *o + v : v;
-        } else if constexpr (DST == DST_VOLIMAGE) {
-            const int u = g.unit0 + (g.umap ? g.umap[item] : item);
-            const int N2 = g.N * g.N;
-            const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
-            a.out[((size_t)z * g.H + a1 + g.N * m1) * g.W + a2 + g.N * m2] = v;
-        } else {
-            const int lu = g.umap ? g.umap[item] : item;
-            const size_t q = ((size_t)lu * g.nh + m1) * g.nw + m2;
-            if constexpr (DST == DST_POLY)
-                a.out[q] = v;
-            else
-                a.out[q] = update_value<DST>(a.xold[q], a.norm[q], v, a.eps);
+    // C. epilogue over the valid outputs: LR lanes per output row (consecutive lanes: consecutive columns), 32 / LR rows
+    //    per warp and step, each warp over a contiguous chunk of the CTA's (window, row) list; every lane handles two
+    //    of its rows per pass with all global loads issued before the stores (the update's x_old / normaliser loads
+    //    were the kernel's top stall, ncu r02), (ui, ii) advance incrementally (no per-element divisions)
+    {
+        constexpr int NW = RG::NT / 32;
+        const int LR = T2 <= 16 ? 16 : 32;
+        const int RPW = 32 / LR;
+        const int lane = threadIdx.x & 31;
+        const int nrows = nt * T1;
+        const int chunk = ((nrows + NW - 1) / NW + RPW - 1) / RPW * RPW;
+        const int rbeg = (threadIdx.x >> 5) * chunk + lane / LR;
+        const int rend = min(nrows, (threadIdx.x >> 5) * chunk + chunk);
+        const long long rs = (DST == DST_IMAGE || DST == DST_VOLIMAGE) ? (long long)g.N * g.W : (long long)g.nw;
+        const int cst = (DST == DST_IMAGE || DST == DST_VOLIMAGE) ? g.N : 1;
+        // output (ui, ii, c): false if outside the image, else its destination offset and value
+        auto elem = [&](int ui, int ii, int c, long long& q, float& v) -> bool {
+            if (s_m1[ui] + ii >= g.nh || s_m2[ui] + c >= g.nw) return false;
+            const int i = j1 + ii;   // window row
+            v = sm[(size_t)ui * IMG + (i >> 1) * BLK + (i & 1) * L + j2 + c];
+            q = s_ob[ui] + (long long)ii * rs + (long long)c * cst;
+            return true;
+        };
+        for (int c = lane & (LR - 1); c < T2; c += LR) {   // one pass unless T2 > 32
+            int r = rbeg;
+            int ui = r / T1, ii = r - (r / T1) * T1;
+            while (r < rend) {
+                int ui2 = ui, ii2 = ii + RPW;   // the lane's next row
+                while (ii2 >= T1) {
+                    ii2 -= T1;
+                    ++ui2;
+                }
+                long long qa = 0, qb = 0;
+                float va = 0.0f, vb = 0.0f;
+                const bool oka = elem(ui, ii, c, qa, va);
+                const bool okb = r + RPW < rend && elem(ui2, ii2, c, qb, vb);
+                if constexpr (DST == DST_UPDATE || DST == DST_ISRA) {
+                    float xa = 0.0f, na = 0.0f, xb = 0.0f, nb = 0.0f;
+                    if (oka) {
+                        xa = a.xold[qa];
+                        na = a.norm[qa];
+                    }
+                    if (okb) {
+                        xb = a.xold[qb];
+                        nb = a.norm[qb];
+                    }
+                    if (oka) a.out[qa] = update_value<DST>(xa, na, va, a.eps);
+                    if (okb) a.out[qb] = update_value<DST>(xb, nb, vb, a.eps);
+                } else if constexpr (DST == DST_IMAGE) {
+                    float oa = 0.0f, ob = 0.0f;
+                    if (a.accum) {
+                        if (oka) oa = a.out[qa];
+                        if (okb) ob = a.out[qb];
+                    }
+                    if (oka) a.out[qa] = a.accum ? oa + va : va;
+                    if (okb) a.out[qb] = a.accum ? ob + vb : vb;
+                } else {
+                    if (oka) a.out[qa] = va;
+                    if (okb) a.out[qb] = vb;
+                }
+                r += 2 * RPW;
+                ui = ui2;
+                ii = ii2 + RPW;
+                while (ii >= T1) {
+                    ii -= T1;
+                    ++ui;
+                }
+            }
         }
     }
 }

@@ -70,16 +70,19 @@ def test_tiled_projections_match_oracle(case, flags):
         assert np.abs(g - ref).max() <= 2e-5 * np.abs(ref).max(), info
 
 
-@pytest.mark.parametrize("L", [45, 20], ids=["warp-kernels", "register-kernels"])
+@pytest.mark.parametrize("L", [45, 20, 32], ids=["warp-kernels", "register-kernels", "register-wide-tiles"])
 def test_tiled_window_sizes(L, monkeypatch):
     """Forced window sizes (LFM_TILE_L, dev): L = 45 runs the warp-per-transform tile kernels (c4's size), L = 20 the
-    register-resident ones, on the same problem; both match the oracle."""
+    register-resident ones, L = 32 the register kernels with tiles wider than 16 outputs (the C2R epilogue's one-row-
+    per-warp lane mapping); all match the oracle."""
     monkeypatch.setenv("LFM_TILE_L", str(L))
     h, x, r = rand_case(97, 2, 3, 120, 99, 27, 21)
     hd = h.astype(np.float64)
     with L_().Plan(h, 3, 120, 99, flags=L_().LFM_PLAN_TILES | L_().LFM_PLAN_FFT_ONLY) as plan:
         info = plan.info()
         assert info["tiles"] >= 2 and info["fft_h"] == L, info
+        if L == 32:
+            assert info["tile_T2"] > 16, info
         y_d = torch.zeros((120, 99), device="cuda")
         plan.forward(dev(x), y_d)
         xb_d = torch.zeros((2, 120, 99), device="cuda")
