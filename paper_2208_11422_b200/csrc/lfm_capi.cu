@@ -1130,6 +1130,7 @@ constexpr double kMacF16Bps = 5.3e12;        // kind::f16 tile MACs, HBM-bound (
 constexpr double kXformPoint = 6.0e-12;      // whole-image transform seconds per point and direction (r02, L = 75)
 constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms, L <= 36 (r02, L = 27: 4.1e-12)
 constexpr double kXformPointTileW = 7.5e-12; // warp-per-transform tile kernels, L > 36 (r02, L = 27: 7.5e-12)
+constexpr double kTcBwdLive = 1.25;         // tcgen05 backward / forward time live beside the tile half (r02: c3 1.23, c2 1.39)
 
 // tile geometry for transform size L (ntile = 0: not possible) over coarse taps in [d1a, d1b] x [d2a, d2b]
 TileGeom tile_geometry(const Geo& g, int L, int d1a, int d1b, int d2a, int d2b) {
@@ -1977,7 +1978,12 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             for (int z = zb; z <= ze; ++z)
                 if (plane_direct[z] == 0) t_f += 0.5 * pt_fft[z];
             for (int d = 0; d < 2 && use_tiles && t_tc > 0 && units_fft > 0 && nsimt == 0; ++d) {
-                const double raw = p->num_sms * t_tc / (t_tc + t_f);
+                // live beside the backward tile half (MAC + C2R / update) the tcgen05 backward runs slower than its
+                // forward twin, which the whole-GPU model does not see (r02, c3 on 24 SMs: 1.70 vs 1.38 ms; c2 on 32:
+                // 0.098 vs 0.070 ms; serialised on the whole GPU both 0.24 ms): weight its share accordingly (c3: the
+                // backward partition 24 -> 32 SMs, 281 -> 288 it/s on one box)
+                const double ttc = d ? kTcBwdLive * t_tc : t_tc;
+                const double raw = p->num_sms * ttc / (ttc + t_f);
                 // a tensor-core share below a dozen SMs is not worth a partition (c4: 38.4 it/s one after the other vs
                 // 36.0 on a forced 16-SM partition)
                 int want = raw < 12.0 ? 0 : (int)std::lround(raw / 8.0) * 8;
@@ -1985,7 +1991,7 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 if (const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F")) want = atoi(ev);   // dev override
                 if (getenv("LFM_PLAN_VERBOSE"))
                     fprintf(stderr, "[lfm plan] tiles, direction %d: t_tc %.3f ms, t_freq %.3f ms -> %d tc SMs\n", d,
-                            t_tc * 1e3, t_f * 1e3, want);
+                            ttc * 1e3, t_f * 1e3, want);
                 if (want > 0 && green_split(p, dev, want, &p->part[d])) tc_sms[d] = p->part[d].sms_tc;
             }
             for (int d = 0; d < 2 && !use_tiles && t_tc > 0 && bytes > 0 && nsimt == 0; ++d) {
