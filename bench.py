@@ -180,7 +180,11 @@ def run_reference(args):
     # stay small against the extrapolated rows (4 per core measured 0.015-0.026 it/s across boxes)
     for _ in range(args.warmup):
         oracle_iteration_seconds(cfg, h64, x64, y64, rows)
-    ts = [oracle_iteration_seconds(cfg, h64, x64, y64, rows)[0] for _ in range(args.steps)]
+    ts, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ts.append(oracle_iteration_seconds(cfg, h64, x64, y64, rows)[0])
+        walls.append(time.perf_counter() - t0)
     sec = float(np.mean(ts))
     value = 1.0 / sec
     sample = (f"per step: oracle forward on {rows} of {cfg.height} output rows + backward on the same rows of all "
@@ -192,6 +196,8 @@ def run_reference(args):
             "config": {"workload": workload_desc(cfg)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "gflops": oracle_flops_per_iteration(cfg) * value / 1e9},
+            # ms_per_step is the extrapolated full iteration; the sample a step actually runs takes wall_s_per_step
+            "wall_s_per_step": float(np.mean(walls)), "sample_rows": rows,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
