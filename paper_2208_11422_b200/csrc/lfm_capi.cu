@@ -1972,8 +1972,8 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
             }
             const double bytes = units_fft * N2 * g.nkappa * 8.0;   // M streamed once per direction
             // tiled frequency path (§5.6): its MAC (tensor cores, HBM-bound), transforms (SIMT) and the tensor-core
-            // direct planes share the SMs in proportion to their modelled whole-GPU times (r02 c3 sweep: the optimum
-            // 56 of 148 SMs matches the proportional split, +4 % over one after the other)
+            // direct planes share the SMs in proportion to their modelled whole-GPU times (r02 c3 sweeps: the
+            // proportional split, rounded to the driver's 8-SM steps, was the best step)
             double t_f = 0.0;   // per direction, the tiled frequency-path planes
             for (int z = zb; z <= ze; ++z)
                 if (plane_direct[z] == 0) t_f += 0.5 * pt_fft[z];
