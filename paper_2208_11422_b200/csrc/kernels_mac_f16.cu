@@ -33,23 +33,39 @@ constexpr uint32_t kFSmemMax = 232448;
 
 __host__ __device__ constexpr uint32_t f_round1k(uint32_t v) { return (v + 1023u) & ~1023u; }
 __host__ __device__ constexpr uint32_t f_btile(int F) { return f_round1k((uint32_t)(4 * F) * 128u); }   // 4F fp16 rows
+constexpr uint32_t kFAStage = 2 * kFATile;     // A hi + lo per chunk
+// the two-ring kernel (F = 32): four prep groups of two warps, four B slots (>= the groups, see its prep warps)
+__host__ __device__ constexpr int f_pg(int F) { return F >= 32 ? 4 : 8; }
+__host__ __device__ constexpr int f_bslots(int F) { return f_pg(F); }
+// the one-ring kernel (F <= 16): A hi + lo, B tile and fp32 source tile per stage
 __host__ __device__ constexpr uint32_t f_stile(int F) { return f_round1k((uint32_t)F * kFK * 4u); }     // F fp32 rows
 __host__ __device__ constexpr uint32_t f_stage(int F) { return 2 * kFATile + f_btile(F) + f_stile(F); }
 __host__ __device__ constexpr int f_depth(int F) {
     return (int)((kFSmemMax - 1024) / f_stage(F)) < 8 ? (int)((kFSmemMax - 1024) / f_stage(F)) : 8;
 }
 __host__ __device__ constexpr int f_gcd(int a, int b) { return b == 0 ? a : f_gcd(b, a % b); }
+// A ring depth: what shared memory holds beside the B ring (F = 32: 5 x 32 KB; the A bytes in flight per SM bound
+// the MAC's streaming rate)
+__host__ __device__ constexpr int f_adepth(int F) {
+    return (int)((kFSmemMax - 1024 - f_bslots(F) * f_btile(F)) / kFAStage) < 8
+               ? (int)((kFSmemMax - 1024 - f_bslots(F) * f_btile(F)) / kFAStage)
+               : 8;
+}
 }  // namespace
 
-size_t mac_f16_smem_bytes(int F) { return (size_t)f_depth(F) * f_stage(F) + 1024; }
+size_t mac_f16_smem_bytes(int F) {
+    return F >= 32 ? (size_t)f_adepth(F) * kFAStage + (size_t)f_bslots(F) * f_btile(F) + 1024
+                   : (size_t)f_depth(F) * f_stage(F) + 1024;
+}
 
 // ---------------------------------------------------------------------------------------------------------------
-// FWD: item = (kappa, half h of the output phases): D[b'][n] over all K chunks of the kappa row.
-// BWD: item = (kappa, tile t of 128 units):        D[u][n] over the 8 K chunks of (b', re/im).
-// Warps: 0 TMA producer, 1..8 prep (PG groups, alternate chunks; one fill barrier per (group, stage), see
-// kernels_mac_tc.cu), 9 MMA issuer, 10..13 drainers (lane quarters 2, 3, 0, 1).
+// F <= 16 variant: one ring whose stages hold A hi + lo, the B tile and the frames' fp32 source tile (TMA, loaded with
+// A).  Items as in mac_f16_kernel below.  Warps: 0 TMA producer, 1..8 prep (PG groups, alternate chunks; one fill
+// barrier per (group, stage), see kernels_mac_tc.cu), 9 MMA issuer, 10..13 drainers (lane quarters 2, 3, 0, 1).
+// At F <= 16 the stages are small enough to run five or six deep, and the TMA-staged source measured faster than the
+// prep warps' L2 reads of the two-ring kernel (c2, F = 8: forward MAC 0.143 vs 0.160 ms).
 template <int F, int PG, bool FWD>
-__global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_constant__ MacF16Args d) {
+__global__ void __launch_bounds__(kFThreads, 1) mac_f16_tma_kernel(const __grid_constant__ MacF16Args d) {
     constexpr int S = f_depth(F);
     constexpr int LG = PG * S / f_gcd(PG, S);
     constexpr int NB = 4 * F;      // stacked B rows: hi 0..2F-1, lo 2F..4F-1
@@ -271,6 +287,252 @@ __global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_cons
     if (warp == 0) tc::tmem_dealloc(tmem, 2 * NSET <= 256 ? 256 : 512);
 }
 
+// FWD: item = (kappa, half h of the output phases): D[b'][n] over all K chunks of the kappa row.
+// BWD: item = (kappa, tile t of 128 units):        D[u][n] over the 8 K chunks of (b', re/im).
+// Warps: 0 TMA producer (A only), 1..8 prep (PG groups, alternate chunks), 9 MMA issuer, 10..13 drainers (lane
+// quarters 2, 3, 0, 1).  Two rings: A (hi + lo tiles, SA deep, TMA) and the stacked B tiles (f_bslots(F), written by the
+// prep warps from the fp32 source read through L2).  Keeping the B tiles and the source out of the A stages lets the
+// A ring run five deep at F = 32 instead of four (the F = 32 MAC streamed 5.5-5.8 TB/s with four, the F = 16 one 6.4
+// with five, r02 ncu).  Used at F = 32; F <= 16 runs mac_f16_tma_kernel above.
+template <int F, int PG, bool FWD>
+__global__ void __launch_bounds__(kFThreads, 1) mac_f16_kernel(const __grid_constant__ MacF16Args d) {
+    constexpr int SA = f_adepth(F);
+    constexpr int SB = f_bslots(F);
+    constexpr int NB = 4 * F;      // stacked B rows: hi 0..2F-1, lo 2F..4F-1
+    constexpr int NSET = 6 * F;    // accumulator columns: hi*hi | hi*lo | lo*hi
+    // a prep group waits for the MMA to release B slot (it % SB) from chunk it - SB; its own previous chunk (it - PG)
+    // already waited for chunk it - PG - SB, so with PG <= SB the slot's earlier use it - 2 SB is released and the
+    // parity wait cannot pass on a stale phase
+    static_assert(SB >= PG, "B ring at least as deep as the prep groups");
+    static_assert(SA >= 2, "A ring");
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar_afull[SA], bar_aempty[SA], bar_bready[SB], bar_bempty[SB], bar_acc[2], bar_tfree[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float s_scale[F], s_inv[F];   // per frame: 2^eB (prep) and 2^-(eA + eB) (epilogue)
+    const uint32_t raw = tc::smem_u32(smem_raw);
+    unsigned char* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    unsigned char* bring = smem + (size_t)SA * kFAStage;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntile = FWD ? 2 : (d.nu_pad + kFM - 1) / kFM;
+    const int ksp = d.ksplit > 1 ? d.ksplit : 1;   // K splits per (kappa, tile): partial outputs ksp apart
+    const int nitems = d.nkappa * ntile * ksp;
+    const int nchunks = FWD ? (2 * d.nu_pad + kFK - 1) / kFK : (2 * d.bpitch + kFK - 1) / kFK;
+    // item -> kappa, row tile, K split and its chunk range [c_lo, c_hi)
+    auto decode = [&](int item, int& kap, int& t, int& sp, int& c_lo, int& c_hi) {
+        kap = item / (ntile * ksp);
+        const int rem = item - kap * ntile * ksp;
+        t = rem / ksp;
+        sp = rem - t * ksp;
+        c_lo = (int)((long long)sp * nchunks / ksp);
+        c_hi = (int)((long long)(sp + 1) * nchunks / ksp);
+    };
+    const int kvalid_last = (FWD ? 2 * d.nu_pad : 2 * d.N2) - (nchunks - 1) * kFK;   // real K elements, last chunk
+    const int ks_last = (kvalid_last + 15) / 16;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < SA; ++i) {
+            tc::mbar_init(&bar_afull[i], 1);
+            tc::mbar_init(&bar_aempty[i], 1);
+        }
+        for (int i = 0; i < SB; ++i) {
+            tc::mbar_init(&bar_bready[i], kFPrep / PG);
+            tc::mbar_init(&bar_bempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bar_acc[i], 1);
+            tc::mbar_init(&bar_tfree[i], 4);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&d.tmapAh);
+        tc::tma_prefetch_desc(&d.tmapAl);
+    }
+    if (warp == 0) tc::tmem_alloc(&tmem_base, 2 * NSET <= 256 ? 256 : 512);
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+        const int eb = d.bmax ? (f < d.nframes ? tc::f16_scale_exp(__uint_as_float(d.bmax[f])) : 0) : d.bexp[f];
+        s_scale[f] = tc::pow2f(eb);
+        s_inv[f] = ldexpf(1.0f, -(d.aexp + eb));
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- producer: A hi / lo tiles per chunk ----
+            int it = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int kap, t, sp, c_lo, c_hi;
+                decode(item, kap, t, sp, c_lo, c_hi);
+                for (int c = c_lo; c < c_hi; ++c, ++it) {
+                    const int s = it % SA;
+                    if (it >= SA) tc::mbar_wait(&bar_aempty[s], ((it / SA) - 1) & 1);
+                    unsigned char* st = smem + (size_t)s * kFAStage;
+                    tc::mbar_arrive_expect_tx(&bar_afull[s], kFAStage);
+                    tc::tma_load_3d(st, &d.tmapAh, c * kFK, t * kFM, kap, &bar_afull[s]);
+                    tc::tma_load_3d(st + kFATile, &d.tmapAl, c * kFK, t * kFM, kap, &bar_afull[s]);
+                }
+            }
+        }
+    } else if (warp <= kFPrep) {
+        // ---- prep: stacked B rows from the fp32 source [F][32 complex] of the chunk (read through L2), scaled by
+        //      2^eB[f], split hi | lo ----
+        //   FWD  row 2f: (Gr, -Gi), row 2f+1: (Gi, Gr)   -> D[b'][2f] = Re Y_f, D[b'][2f+1] = Im Y_f
+        //   BWD  row 2f: (Rr,  Ri), row 2f+1: (Ri, -Rr)  -> D[u][2f]  = Re Xh_f, D[u][2f+1] = Im Xh_f (conj(M) R)
+        constexpr int NP = 32 * kFPrep / PG;
+        constexpr int NE = (F * (kFK / 2) + NP - 1) / NP;   // complex source values per thread
+        const int pt = (threadIdx.x - 32) % NP, grp = (threadIdx.x - 32) / NP;
+        int it = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo; c < c_hi; ++c, ++it) {
+                if (it % PG != grp) continue;
+                // the source values first (independent of the slot; L2 / DRAM), then wait for the slot
+                const float2* gsrc = d.src + (long long)kap * d.src_n + (long long)c * (kFK / 2);
+                float2 gv[NE];
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                    const int e = pt + NP * i;
+                    const int f = e / (kFK / 2), j = e - f * (kFK / 2);
+                    gv[i] = (e < F * (kFK / 2) && f < d.nframes && c * (kFK / 2) + j < d.src_n)
+                                ? __ldg(gsrc + (long long)f * d.src_fstride + j)
+                                : make_float2(0.0f, 0.0f);
+                }
+                const int b = it % SB;
+                if (it >= SB) tc::mbar_wait(&bar_bempty[b], ((it / SB) - 1) & 1);
+                unsigned char* bt = bring + (size_t)b * f_btile(F);
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                    const int e = pt + NP * i;
+                    if (e < F * (kFK / 2)) {
+                        const int f = e / (kFK / 2), j = e - f * (kFK / 2);
+                        const float2 g = gv[i];
+                        // two splits per complex value; the B entries are +-re / +-im, and -(h + l) = (-h) + (-l)
+                        // is a sign flip of both fp16 halves
+                        uint16_t rh, rl, ih, il;
+                        tc::split_f16(g.x, s_scale[f], rh, rl);
+                        tc::split_f16(g.y, s_scale[f], ih, il);
+                        uint32_t h0, l0, h1, l1;   // rows 2f, 2f+1: (element 2j) | (element 2j+1) << 16
+                        if constexpr (FWD) {       // (re, -im), (im, re)
+                            h0 = (uint32_t)rh | ((uint32_t)(ih ^ 0x8000u) << 16);
+                            l0 = (uint32_t)rl | ((uint32_t)(il ^ 0x8000u) << 16);
+                            h1 = (uint32_t)ih | ((uint32_t)rh << 16);
+                            l1 = (uint32_t)il | ((uint32_t)rl << 16);
+                        } else {                   // (re, im), (im, -re)
+                            h0 = (uint32_t)rh | ((uint32_t)ih << 16);
+                            l0 = (uint32_t)rl | ((uint32_t)il << 16);
+                            h1 = (uint32_t)ih | ((uint32_t)(rh ^ 0x8000u) << 16);
+                            l1 = (uint32_t)il | ((uint32_t)(rl ^ 0x8000u) << 16);
+                        }
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const int row = 2 * f + r, rowl = 2 * F + row;
+                            // byte offset of elements (row, 2j .. 2j+1) in a K-major SWIZZLE_128B fp16 tile
+                            const uint32_t off = (uint32_t)row * 128u + ((((uint32_t)(j >> 2)) ^ (row & 7)) & 7) * 16u + (j & 3) * 4u;
+                            const uint32_t offl = (uint32_t)rowl * 128u + ((((uint32_t)(j >> 2)) ^ (rowl & 7)) & 7) * 16u + (j & 3) * 4u;
+                            *reinterpret_cast<uint32_t*>(bt + off) = r ? h1 : h0;
+                            *reinterpret_cast<uint32_t*>(bt + offl) = r ? l1 : l0;
+                        }
+                    }
+                }
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_bready[b]);
+            }
+        }
+    } else if (warp == kFPrep + 1) {
+        // ---- MMA issuer (whole warp, uniform values, one elected lane issues) ----
+        const uint32_t id1 = tc::idesc_f16(kFM, NB), id2 = tc::idesc_f16(kFM, 2 * F);
+        int it = 0, g = 0, gk = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo; c < c_hi; ++c, ++it) {
+                const int s = it % SA, b = it % SB, j = g & 1;
+                tc::mbar_wait(&bar_afull[s], (it / SA) & 1);
+                tc::mbar_wait(&bar_bready[b], (it / SB) & 1);
+                if (gk == 0 && g >= 2) tc::mbar_wait(&bar_tfree[j], ((g >> 1) - 1) & 1);
+                tc::fence_after();
+                const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * kFAStage), a_lo = a_hi + kFATile;
+                const uint32_t bsm = tc::smem_u32(bring + (size_t)b * f_btile(F));
+                const uint32_t acc = tmem + (uint32_t)(j * NSET);
+                const uint64_t ah0 = tc::sdesc_sw128(a_hi), al0 = tc::sdesc_sw128(a_lo), bd0 = tc::sdesc_sw128(bsm);
+                const int ks = c == nchunks - 1 ? ks_last : kFKS;
+                for (int k = 0; k < ks; ++k) {   // K-step k (16 fp16 = 32 bytes): descriptor address + 2 k
+                    const uint64_t dk = 2 * (uint64_t)k;
+                    tc::mma_f16_elect(acc, ah0 + dk, bd0 + dk, id1, (gk == 0 && k == 0) ? 0u : 1u);           // hi*hi | hi*lo
+                    tc::mma_f16_elect(acc + 4 * F, al0 + dk, bd0 + dk, id2, (gk == 0 && k == 0) ? 0u : 1u);   // lo*hi
+                }
+                tc::mma_commit_elect(&bar_aempty[s]);
+                tc::mma_commit_elect(&bar_bempty[b]);
+                gk += ks;
+                if (gk + kFKS > d.chain_k || c == c_hi - 1) {
+                    tc::mma_commit_elect(&bar_acc[j]);
+                    ++g;
+                    gk = 0;
+                }
+            }
+        }
+    } else {
+        // ---- drainers: TMEM -> fp32 running sums (2F per thread), unscale per frame, store ----
+        const int q = warp & 3;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+        float acc[2 * F];
+#pragma unroll
+        for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        int g = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int kap, t, sp, c_lo, c_hi;
+            decode(item, kap, t, sp, c_lo, c_hi);
+            for (int c = c_lo, gk = 0; c < c_hi; ++c) {   // the issuer's drain groups
+                gk += c == nchunks - 1 ? ks_last : kFKS;
+                if (!(gk + kFKS > d.chain_k || c == c_hi - 1)) continue;
+                gk = 0;
+                const int j = g & 1;
+                tc::mbar_wait(&bar_acc[j], (g >> 1) & 1);
+                ++g;
+                tc::fence_after();
+                const uint32_t base = lane_base + (uint32_t)(j * NSET);
+#pragma unroll
+                for (int b0 = 0; b0 < 3; ++b0) {   // up to 32 columns in flight per wait (not one wait per 8)
+#pragma unroll
+                    for (int c8 = 0; c8 < 2 * F; c8 += 32) {
+                        constexpr int W = 2 * F < 32 ? 2 * F : 32;
+                        uint32_t v[W];
+                        if constexpr (W == 32) {
+                            tc::tmem_ld32_nowait(base + (uint32_t)(b0 * 2 * F + c8), v);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < W; c += 8) tc::tmem_ld8_nowait(base + (uint32_t)(b0 * 2 * F + c8 + c), v + c);
+                        }
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < W; ++u) acc[c8 + u] += __uint_as_float(v[u]);
+                    }
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_tfree[j]);
+            }
+            const int row = t * kFM + 32 * q + lane;
+            if (row < (FWD ? d.N2 : d.nu_pad)) {
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    if (f >= d.nframes) break;
+                    const float inv = s_inv[f];
+                    const float2 v = make_float2(acc[2 * f] * inv, acc[2 * f + 1] * inv);
+                    d.out[(long long)sp * d.out_sstride + (long long)f * d.out_fstride + (long long)kap * d.out_ld + row] = v;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 2 * F; ++i) acc[i] = 0.0f;
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * NSET <= 256 ? 256 : 512);
+}
+
 // ---------------------------------------------------------------------------------------------------------------
 // plan time: max |M| (float bits), transposed copy M^T, in-place split of complex64 rows into [hi | lo] fp16 rows
 
@@ -402,13 +664,18 @@ cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa,
     return cudaSuccess;
 }
 
-// per call: the frames' fp32 source spectra (FWD: G [F][kappa][nu_pad]; BWD: R [F][kappa][bpitch]), F rows of 64 floats
+// per call: the frames' fp32 source spectra (FWD: G [F][kappa][nu_pad]; BWD: R [F][kappa][bpitch]), read by the prep
+// warps (frames nframes .. F-1 and the K tail read as zeros)
 cudaError_t mac_f16_encode_src(MacF16Args* a, int fwd, const float2* src, long long src_fstride, int F, int nframes) {
+    if (nframes <= 0 || nframes > F) nframes = F;
+    const int n = fwd ? a->nu_pad : a->bpitch;
+    a->nframes = nframes;   // frames nframes .. F-1 read as zeros (TMA out of bounds / the prep warps' bounds check)
+    a->src = src;
+    a->src_fstride = src_fstride;
+    a->src_n = n;
+    if (F >= 32) return cudaSuccess;   // the two-ring kernel reads the source directly
     MfEncodeFn enc = mf_encoder();
     if (!enc) return cudaErrorSymbolNotFound;
-    const int n = fwd ? a->nu_pad : a->bpitch;
-    if (nframes <= 0 || nframes > F) nframes = F;
-    a->nframes = nframes;   // frames nframes .. F-1 of the box are zero-filled by the TMA (out of bounds)
     cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)a->nkappa, (cuuint64_t)nframes};
     cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)src_fstride * 8};
     cuuint32_t box[3] = {(cuuint32_t)kFK, 1, (cuuint32_t)F}, es[3] = {1, 1, 1};
@@ -426,11 +693,17 @@ cudaError_t launch_frame_scales(const float2* src, long long fstride, int n, int
 template <int F, bool FWD>
 static cudaError_t launch_mf(const MacF16Args& d, int num_sms, cudaStream_t s) {
     const size_t smem = mac_f16_smem_bytes(F);
-    cudaError_t e = cudaFuncSetAttribute(mac_f16_kernel<F, 4, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     const int ntile = FWD ? 2 : (d.nu_pad + kFM - 1) / kFM;
     const int grid = std::max(1, std::min(d.nkappa * ntile * std::max(1, d.ksplit), num_sms));
-    mac_f16_kernel<F, 4, FWD><<<grid, kFThreads, smem, s>>>(d);
+    if constexpr (F >= 32) {
+        cudaError_t e = cudaFuncSetAttribute(mac_f16_kernel<F, f_pg(F), FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        mac_f16_kernel<F, f_pg(F), FWD><<<grid, kFThreads, smem, s>>>(d);
+    } else {
+        cudaError_t e = cudaFuncSetAttribute(mac_f16_tma_kernel<F, 4, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        mac_f16_tma_kernel<F, 4, FWD><<<grid, kFThreads, smem, s>>>(d);
+    }
     return cudaGetLastError();
 }
 

@@ -270,12 +270,15 @@ struct MacF16Args {
     long long out_sstride;
     const int* bexp;          // [F] the frames' source scale exponents (device, per call)
     const unsigned* bmax;     // or (non-null): [F] bounds of the frames' |source| (float bits), exponents derived in-kernel
-    int nframes;              // frames actually present (<= F; the TMA zero-fills the rest, no output for them)
+    int nframes;              // frames actually present (<= F; the rest read as zeros, no output for them)
     float2* out;              // fwd: Y [F][kappa][N2]; bwd: Xh [F][kappa][nu_pad]
     long long out_fstride, out_ld;
+    const float2* src;        // the frames' fp32 source spectra [nframes][kappa][src_n] (frame stride src_fstride),
+    long long src_fstride;    //   read by the F = 32 kernel's prep warps (L2) into the stacked B tiles
+    int src_n;
     alignas(64) CUtensorMap tmapAh;   // A hi parts {2n fp16, rows, kappa}, box {64, 128, 1}, SWIZZLE_128B
     alignas(64) CUtensorMap tmapAl;   // A lo parts (same rows, + 4n bytes)
-    alignas(64) CUtensorMap tmapS;    // the frames' fp32 source {2n floats, kappa, F}, box {64, 1, F}
+    alignas(64) CUtensorMap tmapS;    // F <= 16: the frames' fp32 source {2n floats, kappa, F}, box {64, 1, F}
 };
 cudaError_t mac_f16_prepare(float2* M, const float2* Mb, float2* MT, int nkappa, int N2, int nu_pad, int bpitch,
                             MacF16Args* fwd, MacF16Args* bwd, cudaStream_t s);
