@@ -206,18 +206,33 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_tile_kernel(XformGeom g
     const int nt = min(UB, a.ntrans - t0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     constexpr int NKAP = L * NK2;
-    __shared__ long long s_col[UB];
-    __shared__ int s_item[UB], s_m1[UB], s_m2[UB];
+    __shared__ long long s_col[UB], s_ob[UB];
+    __shared__ int s_m1[UB], s_m2[UB];
     if (threadIdx.x < nt) {
         const int t = t0 + threadIdx.x;
         const int tile = t / a.cdiv, item = t - tile * a.cdiv;
         const int ty = tile / tg.ntx, tx = tile - ty * tg.ntx;
+        const int m1 = ty * tg.T1, m2 = tx * tg.T2;
         s_col[threadIdx.x] = (long long)tile * a.cmul + item;
-        s_item[threadIdx.x] = item;
-        s_m1[threadIdx.x] = ty * tg.T1;
-        s_m2[threadIdx.x] = tx * tg.T2;
+        s_m1[threadIdx.x] = m1;
+        s_m2[threadIdx.x] = m2;
+        // destination offset of the window's first valid output (m1, m2), as the register kernel's prologue
+        if constexpr (DST == DST_IMAGE) {
+            const int b1 = item / g.N, b2 = item - (item / g.N) * g.N;
+            s_ob[threadIdx.x] = (long long)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
+        } else if constexpr (DST == DST_VOLIMAGE) {
+            const int u = g.unit0 + (g.umap ? g.umap[item] : item);
+            const int N2 = g.N * g.N;
+            const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
+            s_ob[threadIdx.x] = ((long long)z * g.H + a1 + g.N * m1) * g.W + a2 + g.N * m2;
+        } else {
+            const int lu = g.umap ? g.umap[item] : item;
+            s_ob[threadIdx.x] = ((long long)lu * g.nh + m1) * g.nw + m2;
+        }
     }
     __syncthreads();
+    const long long ors = (DST == DST_IMAGE || DST == DST_VOLIMAGE) ? (long long)g.N * g.W : (long long)g.nw;
+    const int ocs = (DST == DST_IMAGE || DST == DST_VOLIMAGE) ? g.N : 1;
     // 1. gather spectra into rows k1 (stride RHO)
     for (int idx = threadIdx.x; idx < NKAP * UB; idx += blockDim.x) {
         const int kap = idx / UB;
@@ -307,23 +322,14 @@ __global__ void __launch_bounds__(512, LFM_FFT_MINB) c2r_tile_kernel(XformGeom g
                     const int m1 = s_m1[ui] + i - j1;
                     if (m1 >= g.nh) continue;
                     const float v = (h ? zz.y : zz.x) * scale;
-                    const int item = s_item[ui];
+                    const long long q = s_ob[ui] + (long long)(i - j1) * ors + (long long)c * ocs;
                     if constexpr (DST == DST_IMAGE) {
-                        const int b1 = item / g.N, b2 = item % g.N;
-                        float* o = a.out + (size_t)(b1 + g.N * m1) * g.W + b2 + g.N * m2;
+                        float* o = a.out + q;
                         *o = a.accum ? *o + v : v;
-                    } else if constexpr (DST == DST_VOLIMAGE) {
-                        const int u = g.unit0 + (g.umap ? g.umap[item] : item);
-                        const int N2 = g.N * g.N;
-                        const int z = u / N2, a1 = (u / g.N) % g.N, a2 = u % g.N;
-                        a.out[((size_t)z * g.H + a1 + g.N * m1) * g.W + a2 + g.N * m2] = v;
+                    } else if constexpr (DST == DST_VOLIMAGE || DST == DST_POLY) {
+                        a.out[q] = v;
                     } else {
-                        const int lu = g.umap ? g.umap[item] : item;
-                        const size_t q = ((size_t)lu * g.nh + m1) * g.nw + m2;
-                        if constexpr (DST == DST_POLY)
-                            a.out[q] = v;
-                        else
-                            a.out[q] = update_value<DST>(a.xold[q], a.norm[q], v, a.eps);
+                        a.out[q] = update_value<DST>(a.xold[q], a.norm[q], v, a.eps);
                     }
                 }
             }
