@@ -412,9 +412,9 @@ struct RegGeom {
     static constexpr int BLK = ((BLK0 + 1) / 2 % 2) ? (BLK0 + 1) / 2 * 2 : (BLK0 + 1) / 2 * 2 + 2;   // floats, BLK/2 odd
     static constexpr int IMG0 = P * BLK;
     static constexpr int IMG = (IMG0 / 2 % 2) ? IMG0 : IMG0 + 2;   // floats per window, IMG/2 odd
-    static constexpr int UB = 16;                                 // windows per CTA
+    static constexpr int UB = 8;                                  // windows per CTA
     static constexpr int NT = ((P > NK2 ? P : NK2) * UB + 31) / 32 * 32;
-    static constexpr int MINB = L <= 27 ? 4 : 2;                  // resident CTAs per SM (registers, shared memory)
+    static constexpr int MINB = L <= 27 ? 7 : 4;                  // resident CTAs per SM (registers, shared memory)
     static constexpr size_t smem() { return (size_t)UB * IMG * 4; }
 };
 

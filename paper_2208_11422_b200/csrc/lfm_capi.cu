@@ -1130,6 +1130,7 @@ constexpr double kMacF16Bps = 5.3e12;        // kind::f16 tile MACs, HBM-bound (
 constexpr double kXformPoint = 6.0e-12;      // whole-image transform seconds per point and direction (r02, L = 75)
 constexpr double kXformPointTile = 4.5e-12;  // register-resident tile transforms, L <= 36 (r02, L = 27: 4.1e-12)
 constexpr double kXformPointTileW = 7.5e-12; // warp-per-transform tile kernels, L > 36 (r02, L = 27: 7.5e-12)
+constexpr double kPartMinShare = 0.18;     // smallest tensor-core share of a tiled projection that gets an SM partition
 constexpr double kTcBwdLive = 1.25;         // tcgen05 backward / forward time live beside the tile half (r02: c3 1.23, c2 1.39)
 
 // tile geometry for transform size L (ntile = 0: not possible) over coarse taps in [d1a, d1b] x [d2a, d2b]
@@ -1984,9 +1985,11 @@ lfm_status lfm_plan_create(lfm_plan* out, const float* psf_host, const float* ps
                 // backward partition 24 -> 32 SMs, 281 -> 288 it/s on one box)
                 const double ttc = d ? kTcBwdLive * t_tc : t_tc;
                 const double raw = p->num_sms * ttc / (ttc + t_f);
-                // a tensor-core share below a dozen SMs is not worth a partition (c4: 38.4 it/s one after the other vs
-                // 36.0 on a forced 16-SM partition)
-                int want = raw < 12.0 ? 0 : (int)std::lround(raw / 8.0) * 8;
+                // a small tensor-core share is not worth a partition: the tile half then loses more on its fewer SMs
+                // than the overlap gains (c4, share 0.02: 38.4 it/s one after the other vs 36.0 on a forced 16-SM
+                // partition; c3 forward, share 0.16: 298.5 it/s one after the other vs 291.4 partitioned, with the
+                // backward (0.20) partitioned in both; c2, shares 0.22 / 0.26: 2163 partitioned vs 1841 not)
+                int want = raw < kPartMinShare * p->num_sms ? 0 : (int)std::lround(raw / 8.0) * 8;
                 if (want) want = std::max(16, std::min(p->num_sms - 16, want));
                 if (const char* ev = getenv(d ? "LFM_TC_SMS_B" : "LFM_TC_SMS_F")) want = atoi(ev);   // dev override
                 if (getenv("LFM_PLAN_VERBOSE"))
